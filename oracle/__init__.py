@@ -1,0 +1,1 @@
+"""Parity oracle package (test infrastructure only; see oracle/oracle.py)."""
