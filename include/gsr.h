@@ -1,0 +1,161 @@
+/*
+ * gsr.h -- C ABI of the B200-native per-pose Gaussian-splat render path.
+ *
+ * Drop-in boundary for splatstream's renderer API.  The reference's boundary
+ * is a Python function API with no FFI layer; each entry point
+ * below replaces one reference function, cited as path:line under
+ * /root/reference/pkg/src/splatstream/.  The Python shim
+ * (paper_2605_08699_b200/render.py, metrics.py) binds these through ctypes and
+ * re-exposes the reference's exact Python signatures; INTEGRATION.md shows
+ * the stub a maintainer adds to splatstream.
+ *
+ * Conventions: plain pointers and sizes, no torch types; every function
+ * returns an int status (GSR_OK or a negative GSR_E_* code, never throws);
+ * gsr_last_error() returns a thread-local message for the last failure.
+ * Scenes are immutable and may be shared by any number of contexts; a
+ * context (stream + workspace) must be used by one thread at a time.
+ * Host arrays may be pageable or pinned.
+ */
+#ifndef GSR_H
+#define GSR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSR_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define GSR_API __attribute__((visibility("default")))
+#else
+#define GSR_API
+#endif
+
+/* status codes; the Python shim maps them to the reference's exceptions */
+#define GSR_OK 0
+#define GSR_E_INVALID (-1)        /* ValueError (camera.py:64-70, render.py:131-132) */
+#define GSR_E_CUDA (-2)           /* RenderError (render.py:52-53) */
+#define GSR_E_OOM (-3)            /* RenderError */
+#define GSR_E_DIM_MISMATCH (-4)   /* metrics.DimensionMismatch (metrics.py:85-86) */
+#define GSR_E_TOO_SMALL (-5)      /* metrics.TooSmall (metrics.py:87-88) */
+#define GSR_E_NO_DEVICE (-6)      /* RenderError: no CUDA device */
+
+typedef struct gsr_scene gsr_scene;
+typedef struct gsr_ctx gsr_ctx;
+
+/* Camera of one render call.  The Python shim fills it with the reference's
+ * own host math: w2c = world_to_camera(pose)[:3, :] (camera.py:101-108),
+ * campos = -R @ w2c[:3, 3] (render.py:276), intrinsics after
+ * scale_intrinsics for ladder rungs (camera.py:146-154, render.py:537). */
+typedef struct gsr_camera {
+    double w2c[12];     /* row-major 3x4 */
+    double campos[3];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} gsr_camera;
+
+/* RenderStats (render.py:103-107) plus per-stage device timings. */
+typedef struct gsr_stats {
+    int64_t splats_drawn;     /* K: kept splats */
+    int64_t splats_culled;    /* N - K */
+    int64_t tile_keys;        /* D: (tile, splat) pairs under the tile-list contract */
+    int32_t depth_passes;     /* radix passes of the f64 depth sort */
+    int32_t retries;          /* re-renders after growing the tile-key buffer */
+    float ms_device;          /* CUDA-event time of the whole device pipeline */
+    float ms_preprocess, ms_depth_sort, ms_binning, ms_tile_sort, ms_blend;
+} gsr_stats;
+
+GSR_API int gsr_abi_version(void);
+GSR_API const char *gsr_last_error(void);
+GSR_API int gsr_device_count(int *out_count);
+
+/* ---- scenes: replaces the registry's ActivatedPrimitives residency
+ * (model.py:89-102, 311-421); upload on load, free on evict ---------------
+ * means (N,3), scales (N,3), rotations (N,4) wxyz, opacities (N,),
+ * colors_dc (N,3): f64 row-major host arrays as in ActivatedPrimitives.
+ * sh_coeffs (N,16,3) f64 or NULL (degree-0 only scene).  rsq (N,) is the
+ * view-independent cutoff radius^2 of render.py:476-481, computed by the shim
+ * with the reference's numpy expression; NULL computes it on the device
+ * (IEEE log, may differ from numpy by 1 ulp).  SH coefficients are stored as
+ * f32 when that is lossless (PLY-loaded scenes), else f64. */
+GSR_API int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means,
+                     const double *scales, const double *rotations,
+                     const double *opacities, const double *colors_dc,
+                     const double *sh_coeffs, const double *rsq);
+GSR_API int gsr_scene_destroy(gsr_scene *scene);
+GSR_API int64_t gsr_scene_count(const gsr_scene *scene);
+GSR_API int64_t gsr_scene_device_bytes(const gsr_scene *scene);
+GSR_API int gsr_scene_sh_is_f32(const gsr_scene *scene);
+
+/* ---- contexts: one CUDA stream + workspace (one per serving thread,
+ * server.py:99-100) ------------------------------------------------------- */
+GSR_API int gsr_ctx_create(gsr_ctx **out, int device);
+GSR_API int gsr_ctx_destroy(gsr_ctx *ctx);
+GSR_API int64_t gsr_ctx_device_bytes(const gsr_ctx *ctx);
+/* device pointer of the ctx's last u8 frame (H,W,3), valid until next render */
+GSR_API const uint8_t *gsr_ctx_frame_u8(const gsr_ctx *ctx);
+
+/* ---- the hot path: render_framebuffer (render.py:516-524) ----------------
+ * project (render.py:163-290) -> stable f64 depth sort (293-302) -> tile
+ * binning -> tile sort -> 16x16 front-to-back blend (430-473) -> u8
+ * (484-485).  Outputs are optional host buffers:
+ *   out_u8   (H,W,3) u8   = framebuffer_to_u8(fb)
+ *   out_rgb  (H,W,3) f32  = rgb before the reference's clip (render.py:470)
+ *   out_T    (H,W)   f32  = transmittance (alpha = 1 - T)
+ * Synchronous: returns after the frame (and copies) completed. */
+GSR_API int gsr_render(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+               const float background[3], int sh_degree, int frustum_cull,
+               uint8_t *out_u8, float *out_rgb, float *out_T, gsr_stats *stats);
+
+/* Asynchronous variant: enqueues the frame on the ctx stream and returns.
+ * gsr_ctx_finish() waits, re-renders once if the tile-key buffer overflowed,
+ * copies the u8 frame to out_u8 (nullable) and fills stats (nullable). */
+GSR_API int gsr_render_async(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+                     const float background[3], int sh_degree, int frustum_cull);
+GSR_API int gsr_ctx_finish(gsr_ctx *ctx, uint8_t *out_u8, gsr_stats *stats);
+
+/* ---- stage entry points for parity tests (same kernels as gsr_render) ---
+ * out_keep (N,) u8; out_order (K,) i64 original indices in depth order
+ * (kept[argsort(z[kept], stable)], render.py:279-302); out_packed (K,11) f32
+ * in depth order (render.py:448-453); counts are returned in stats. */
+GSR_API int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+                         int sh_degree, int frustum_cull, uint8_t *out_keep,
+                         int64_t *out_order, float *out_packed, gsr_stats *stats);
+/* Tile lists of the last render on ctx: out_tiles/out_ranks (D,) sorted by
+ * (tile, depth rank); out_ranges (n_tiles, 2) [start, end).  Pass NULL to
+ * query sizes through stats->tile_keys. */
+GSR_API int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_ranks,
+                         int32_t *out_ranges, gsr_stats *stats);
+
+/* ---- ladder resample: metrics.upscale_to (metrics.py:125-130), Pillow
+ * BILINEAR bit-exact.  Host (h,w,3) u8 in, host (H,W,3) u8 out. ---------- */
+GSR_API int gsr_resample_bilinear_u8(gsr_ctx *ctx, const uint8_t *src, int src_w, int src_h,
+                             uint8_t *dst, int dst_w, int dst_h);
+
+/* ---- SSIM hook: metrics.ssim (metrics.py:76-114).  Two host (H,W,3) u8. -- */
+GSR_API int gsr_ssim_u8(gsr_ctx *ctx, const uint8_t *a, const uint8_t *b, int width, int height,
+                double *out_ssim);
+/* Same on precomputed f64 luma planes (H,W) (metrics.py:69-73 for inputs that
+ * are not RGB u8, e.g. grayscale or float images). */
+GSR_API int gsr_ssim_luma_f64(gsr_ctx *ctx, const double *x, const double *y, int width,
+                              int height, double *out_ssim);
+
+/* ---- pinned host memory for end-to-end frame readback ------------------- */
+GSR_API int gsr_host_alloc(void **out, size_t bytes);
+GSR_API int gsr_host_free(void *ptr);
+
+/* ---- fused ladder evaluation (render_view per rung, render.py:527-541,
+ * + upscale_to + ssim vs the base render, metrics.py:205-211), all on
+ * device: renders base, then each rung (w[i],h[i]) with rescaled
+ * intrinsics, upsamples to base and scores SSIM.  out_ssim[n_rungs]. ---- */
+GSR_API int gsr_ladder_ssim(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *base_cam,
+                    const float background[3], int sh_degree, int n_rungs,
+                    const gsr_camera *rung_cams, double *out_ssim, gsr_stats *base_stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSR_H */

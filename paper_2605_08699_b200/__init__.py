@@ -1,0 +1,23 @@
+"""B200-native per-pose Gaussian-splat render path (TIGAS backend, arXiv 2605.08699).
+
+Drop-in for splatstream's renderer API (render_framebuffer / render_view and
+the SSIM hook ssim / upscale_to); the hot path runs in libgsr.so, hand-written
+CUDA for sm_100a behind the C ABI in include/gsr.h.  See DESIGN.md.
+"""
+
+__version__ = "0.1.0"
+
+from .camera import CameraPose, Intrinsics, pose_from_degrees, scale_intrinsics, world_to_camera
+from .metrics import DimensionMismatch, TooSmall, ladder_ssim, psnr, ssim, upscale_to
+from .render import (DeviceScene, EncodeFailure, Framebuffer, RenderError, RenderStats,
+                     decode_image, device_scene, encode_jpeg, encode_png, evict,
+                     framebuffer_to_u8, render_framebuffer, render_u8, render_view, set_device)
+from .synth import ActivatedPrimitives
+
+__all__ = [
+    "ActivatedPrimitives", "CameraPose", "DeviceScene", "DimensionMismatch", "EncodeFailure",
+    "Framebuffer", "Intrinsics", "RenderError", "RenderStats", "TooSmall", "decode_image",
+    "device_scene", "encode_jpeg", "encode_png", "evict", "framebuffer_to_u8", "ladder_ssim",
+    "pose_from_degrees", "psnr", "render_framebuffer", "render_u8", "render_view",
+    "scale_intrinsics", "set_device", "ssim", "upscale_to", "world_to_camera",
+]

@@ -1,0 +1,187 @@
+"""ctypes binding of the C ABI (include/gsr.h) -> _build/libgsr.so.
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every render/metric call raises RenderError (loudly), it never
+silently computes on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "_build" / "libgsr.so"
+HEADER = PKG.parent / "include" / "gsr.h"
+
+GSR_OK = 0
+GSR_E_INVALID = -1
+GSR_E_CUDA = -2
+GSR_E_OOM = -3
+GSR_E_DIM_MISMATCH = -4
+GSR_E_TOO_SMALL = -5
+GSR_E_NO_DEVICE = -6
+
+
+class RenderError(Exception):
+    """render.py:52-53."""
+
+
+class GsrCamera(ctypes.Structure):
+    _fields_ = [("w2c", ctypes.c_double * 12), ("campos", ctypes.c_double * 3),
+                ("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double),
+                ("cy", ctypes.c_double), ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class GsrStats(ctypes.Structure):
+    _fields_ = [("splats_drawn", ctypes.c_int64), ("splats_culled", ctypes.c_int64),
+                ("tile_keys", ctypes.c_int64), ("depth_passes", ctypes.c_int32),
+                ("retries", ctypes.c_int32), ("ms_device", ctypes.c_float),
+                ("ms_preprocess", ctypes.c_float), ("ms_depth_sort", ctypes.c_float),
+                ("ms_binning", ctypes.c_float), ("ms_tile_sort", ctypes.c_float),
+                ("ms_blend", ctypes.c_float)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+# (name, restype, argtypes); every symbol declared in include/gsr.h
+_vp, _i32, _i64, _dbl, _sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+_P = ctypes.POINTER
+SIGNATURES = [
+    ("gsr_abi_version", _i32, []),
+    ("gsr_last_error", ctypes.c_char_p, []),
+    ("gsr_device_count", _i32, [_P(_i32)]),
+    ("gsr_scene_create", _i32, [_P(_vp), _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("gsr_scene_destroy", _i32, [_vp]),
+    ("gsr_scene_count", _i64, [_vp]),
+    ("gsr_scene_device_bytes", _i64, [_vp]),
+    ("gsr_scene_sh_is_f32", _i32, [_vp]),
+    ("gsr_ctx_create", _i32, [_P(_vp), _i32]),
+    ("gsr_ctx_destroy", _i32, [_vp]),
+    ("gsr_ctx_device_bytes", _i64, [_vp]),
+    ("gsr_ctx_frame_u8", _vp, [_vp]),
+    ("gsr_render", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32, _vp, _vp, _vp, _P(GsrStats)]),
+    ("gsr_render_async", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32]),
+    ("gsr_ctx_finish", _i32, [_vp, _vp, _P(GsrStats)]),
+    ("gsr_debug_preprocess", _i32, [_vp, _vp, _P(GsrCamera), _i32, _i32, _vp, _vp, _vp,
+                                    _P(GsrStats)]),
+    ("gsr_debug_tile_lists", _i32, [_vp, _vp, _vp, _vp, _P(GsrStats)]),
+    ("gsr_resample_bilinear_u8", _i32, [_vp, _vp, _i32, _i32, _vp, _i32, _i32]),
+    ("gsr_ssim_u8", _i32, [_vp, _vp, _vp, _i32, _i32, _P(_dbl)]),
+    ("gsr_ssim_luma_f64", _i32, [_vp, _vp, _vp, _i32, _i32, _P(_dbl)]),
+    ("gsr_host_alloc", _i32, [_P(_vp), _sz]),
+    ("gsr_host_free", _i32, [_vp]),
+    ("gsr_ladder_ssim", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32, _P(GsrCamera),
+                               _P(_dbl), _P(GsrStats)]),
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libgsr.so (raises RenderError if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RenderError(f"CUDA library {LIB_PATH} is not built; run "
+                                  "`python -m paper_2605_08699_b200.build` (no CPU fallback)")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, res, args in SIGNATURES:
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().gsr_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map GSR_E_* to the reference's exception types."""
+    if rc == GSR_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == GSR_E_INVALID:
+        raise ValueError(msg)
+    if rc == GSR_E_DIM_MISMATCH:
+        from .metrics import DimensionMismatch
+        raise DimensionMismatch(msg)
+    if rc == GSR_E_TOO_SMALL:
+        from .metrics import TooSmall
+        raise TooSmall(msg)
+    raise RenderError(msg or f"gsr error {rc}")
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    load().gsr_device_count(ctypes.byref(n))
+    return int(n.value)
+
+
+def ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class Context:
+    """One gsr_ctx: a CUDA stream + workspace, owned by one thread."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        self.device = device
+        h = ctypes.c_void_p()
+        check(self.lib.gsr_ctx_create(ctypes.byref(h), int(device)), "gsr_ctx_create")
+        self.handle = h
+        self._pinned = {}
+
+    def pinned(self, key: str, shape, dtype) -> np.ndarray:
+        """A page-locked host array (reused per key) for fast readback."""
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        cur = self._pinned.get(key)
+        if cur is None or cur[1] < nbytes:
+            if cur is not None:
+                self.lib.gsr_host_free(cur[0])
+            p = ctypes.c_void_p()
+            check(self.lib.gsr_host_alloc(ctypes.byref(p), max(nbytes, 1)), "gsr_host_alloc")
+            cur = (p, max(nbytes, 1))
+            self._pinned[key] = cur
+        buf = (ctypes.c_uint8 * cur[1]).from_address(cur[0].value)
+        return np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
+
+    def close(self):
+        if getattr(self, "handle", None) is not None:
+            for p, _ in self._pinned.values():
+                self.lib.gsr_host_free(p)
+            self._pinned = {}
+            self.lib.gsr_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def context(device: int = 0) -> Context:
+    """The calling thread's context for `device` (server.py:99-100 threads)."""
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    c = ctxs.get(device)
+    if c is None:
+        c = ctxs[device] = Context(device)
+    return c

@@ -1,0 +1,852 @@
+// gsr_api.cu -- the C ABI (include/gsr.h): scene residency, per-thread
+// contexts, frame orchestration and the ladder/SSIM entry points.
+//
+// A frame is enqueued on the context's stream with no host synchronisation:
+// item counts (K kept splats, D tile keys, depth-sort pass count) live in a
+// device FrameCounters struct and every kernel reads them from there, with
+// grids sized from capacities.  The only host round trip is at completion,
+// where the tile-key count is checked against the buffer capacity (on
+// overflow the buffer grows and the frame is re-rendered once).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/gsr.h"
+#include "kernels.cuh"
+
+namespace gsr {
+
+thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int fail_cuda(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();  // clear sticky-free errors
+    return e == cudaErrorMemoryAllocation ? GSR_E_OOM : GSR_E_CUDA;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T *as() const {
+        return reinterpret_cast<T *>(p);
+    }
+};
+
+static int ensure(DevBuf &b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return GSR_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    GSR_CUDA_OK(cudaMalloc(&b.p, bytes));
+    b.bytes = bytes;
+    return GSR_OK;
+}
+
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace gsr
+
+using namespace gsr;
+
+struct gsr_scene {
+    int device = 0;
+    int64_t n = 0;
+    int64_t stride = 0;
+    int sh_f32 = 1;
+    int has_sh = 0;
+    DevBuf block;
+    SceneView view{};
+};
+
+struct SavedCall {
+    const gsr_scene *scene = nullptr;
+    gsr_camera cam{};
+    float bg[3] = {0, 0, 0};
+    int sh_degree = 0;
+    int cull = 1;
+    bool want_rgb = false;
+    bool want_keep = false;
+};
+
+struct gsr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t cap_n = 0, cap_d = 0;
+    DevBuf keys[2], vals[2], rec, srec, counts, offsets, keep;
+    DevBuf hist, partials;
+    DevBuf tkeys[2], tvals[2];
+    DevBuf ranges;
+    DevBuf frame_u8, frame_rgb, frame_t;
+    DevBuf ctr;
+    FrameCounters *hctr = nullptr;
+    cudaEvent_t ev[8] = {};
+    // ladder / resample / ssim scratch
+    DevBuf base_u8, up_u8, tmp_u8, src_u8, dst_u8, coefs, ssim_part, ssim_misc, ssim_w;
+    double *hssim = nullptr;
+    // last frame
+    int W = 0, H = 0, ntiles = 0;
+    const uint32_t *final_tkeys = nullptr, *final_tvals = nullptr;
+    SavedCall saved;
+    bool pending = false;
+    int retries = 0;
+    int64_t bytes() const {
+        int64_t s = 0;
+        const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &rec, &srec, &counts,
+                               &offsets, &keep, &hist, &partials, &tkeys[0], &tkeys[1],
+                               &tvals[0], &tvals[1], &ranges, &frame_u8, &frame_rgb, &frame_t,
+                               &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
+                               &ssim_part, &ssim_misc, &ssim_w};
+        for (auto *b : all) s += (int64_t)b->bytes;
+        return s;
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+__global__ void rsq_kernel(const float *op32, const double *op64, int64_t n, double *rsq) {
+    // device fallback of render.py:476-481 (IEEE log; numpy may differ by 1 ulp)
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double floor_ = 1.0 / (255.0 * 32.0);
+    double o = op64[i];
+    o = o > floor_ ? o : floor_;
+    double r = 2.0 * log(o / floor_);
+    rsq[i] = r < 20.25 ? r : 20.25;
+    (void)op32;
+}
+
+int check_camera(const gsr_camera *cam) {
+    if (!cam) return fail(GSR_E_INVALID, "camera is null");
+    if (cam->width <= 0 || cam->height <= 0)
+        return fail(GSR_E_INVALID, "image dimensions must be positive");
+    if (cam->width > 32768 || cam->height > 32768)
+        return fail(GSR_E_INVALID, "image dimensions above 32768 are not supported");
+    if (!(cam->fx > 0) || !(cam->fy > 0)) return fail(GSR_E_INVALID, "focal lengths must be positive");
+    return GSR_OK;
+}
+
+CameraArgs camera_args(const gsr_camera *cam) {
+    CameraArgs a;
+    for (int r = 0; r < 3; r++) {
+        for (int c = 0; c < 3; c++) a.r[r * 3 + c] = cam->w2c[r * 4 + c];
+        a.t[r] = cam->w2c[r * 4 + 3];
+        a.campos[r] = cam->campos[r];
+    }
+    a.fx = cam->fx;
+    a.fy = cam->fy;
+    a.cx = cam->cx;
+    a.cy = cam->cy;
+    a.width = (double)cam->width;
+    a.height = (double)cam->height;
+    a.iwidth = cam->width;
+    a.iheight = cam->height;
+    return a;
+}
+
+int tile_sort_passes(int ntiles) {
+    int bits = 0;
+    while ((1 << bits) < ntiles) bits++;
+    return (bits + 7) / 8;
+}
+
+int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool want_keep) {
+    int rc;
+    if (n > c->cap_n) {
+        const int64_t cap = round_up(n + n / 8 + 1024, 4096);
+        for (int i = 0; i < 2; i++) {
+            if ((rc = ensure(c->keys[i], sizeof(unsigned long long) * cap))) return rc;
+            if ((rc = ensure(c->vals[i], sizeof(uint32_t) * cap))) return rc;
+        }
+        if ((rc = ensure(c->rec, sizeof(SplatRec) * cap))) return rc;
+        if ((rc = ensure(c->srec, sizeof(SplatRec) * cap))) return rc;
+        if ((rc = ensure(c->counts, sizeof(uint32_t) * cap))) return rc;
+        if ((rc = ensure(c->offsets, sizeof(uint32_t) * cap))) return rc;
+        c->cap_n = cap;
+    }
+    if (want_keep && (rc = ensure(c->keep, (size_t)c->cap_n))) return rc;
+    if (c->cap_d == 0) c->cap_d = round_up(std::max<int64_t>(int64_t(1) << 22, 12 * n), 4096);
+    for (int i = 0; i < 2; i++) {
+        if ((rc = ensure(c->tkeys[i], sizeof(uint32_t) * c->cap_d))) return rc;
+        if ((rc = ensure(c->tvals[i], sizeof(uint32_t) * c->cap_d))) return rc;
+    }
+    const int64_t big = std::max(c->cap_n, c->cap_d);
+    const int64_t hist_n = 256 * radix_tiles(big);
+    if ((rc = ensure(c->hist, sizeof(uint32_t) * hist_n))) return rc;
+    if ((rc = ensure(c->partials, sizeof(uint32_t) * scan_partials_needed(std::max(hist_n, big)))))
+        return rc;
+    const int ntiles = ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+    if ((rc = ensure(c->ranges, sizeof(uint2) * (size_t)ntiles))) return rc;
+    const int64_t px = (int64_t)W * H;
+    if ((rc = ensure(c->frame_u8, (size_t)px * 3))) return rc;
+    if (want_rgb) {
+        if ((rc = ensure(c->frame_rgb, sizeof(float) * (size_t)px * 3))) return rc;
+        if ((rc = ensure(c->frame_t, sizeof(float) * (size_t)px))) return rc;
+    }
+    return GSR_OK;
+}
+
+// Enqueue one full frame on c->stream (no host synchronisation).
+int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const float bg[3],
+                  int sh_degree, int cull, bool want_rgb, bool want_keep) {
+    int rc;
+    if ((rc = check_camera(cam))) return rc;
+    if (!sc) return fail(GSR_E_INVALID, "scene is null");
+    if (sh_degree < 0 || sh_degree > 3) return fail(GSR_E_INVALID, "SH degree must be in 0..3");
+    if (sh_degree > 0 && !sc->has_sh)
+        return fail(GSR_E_INVALID, "scene was created without SH coefficients");
+    if (sc->device != c->device) return fail(GSR_E_INVALID, "scene and context are on different devices");
+    const int W = cam->width, H = cam->height;
+    const int64_t n = sc->n;
+    if ((rc = ensure_capacity(c, n, W, H, want_rgb, want_keep))) return rc;
+    cudaStream_t s = c->stream;
+    FrameCounters *ctr = c->ctr.as<FrameCounters>();
+    const CameraArgs ca = camera_args(cam);
+    ScanWorkspace ws{c->partials.as<uint32_t>(), (int64_t)(c->partials.bytes / 4)};
+    c->W = W;
+    c->H = H;
+    c->ntiles = ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+
+    cudaEventRecord(c->ev[0], s);
+    launch_frame_init(ctr, s);
+    if (n > 0) {
+        launch_preprocess(sc->view, ca, sh_degree, cull, c->keys[0].as<unsigned long long>(),
+                          c->rec.as<SplatRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr, ctr,
+                          s);
+        launch_depth_passes(ctr, s);
+    }
+    cudaEventRecord(c->ev[1], s);
+    if (n > 0) {
+        for (int p = 0; p < 8; p++) {
+            launch_radix_pass<unsigned long long>(
+                c->keys[p & 1].as<unsigned long long>(), p == 0 ? nullptr : c->vals[p & 1].as<uint32_t>(),
+                c->keys[(p + 1) & 1].as<unsigned long long>(), c->vals[(p + 1) & 1].as<uint32_t>(),
+                p == 0 ? nullptr : &ctr->K, n, 8 * p, &ctr->kmin, &ctr->npass, p, p == 0,
+                c->hist.as<uint32_t>(), ws, s);
+        }
+    }
+    cudaEventRecord(c->ev[2], s);
+    if (n > 0) {
+        launch_bin_count(c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), c->rec.as<SplatRec>(),
+                         c->srec.as<SplatRec>(), c->counts.as<uint32_t>(), n, ctr, W, H, s);
+        launch_scan_exclusive(c->counts.as<uint32_t>(), c->offsets.as<uint32_t>(), n, &ctr->D, ws, s);
+        launch_bin_write(c->srec.as<SplatRec>(), c->offsets.as<uint32_t>(), n, ctr, W, H,
+                         c->tkeys[0].as<uint32_t>(), c->tvals[0].as<uint32_t>(), c->cap_d, s);
+    }
+    cudaEventRecord(c->ev[3], s);
+    const int tp = tile_sort_passes(c->ntiles);
+    if (n > 0) {
+        for (int p = 0; p < tp; p++) {
+            launch_radix_pass<uint32_t>(c->tkeys[p & 1].as<uint32_t>(), c->tvals[p & 1].as<uint32_t>(),
+                                        c->tkeys[(p + 1) & 1].as<uint32_t>(),
+                                        c->tvals[(p + 1) & 1].as<uint32_t>(), &ctr->D, c->cap_d,
+                                        8 * p, nullptr, nullptr, p, false, c->hist.as<uint32_t>(),
+                                        ws, s);
+        }
+    }
+    c->final_tkeys = c->tkeys[tp & 1].as<uint32_t>();
+    c->final_tvals = c->tvals[tp & 1].as<uint32_t>();
+    if (n > 0) {
+        launch_tile_ranges(c->final_tkeys, ctr, c->cap_d, c->ranges.as<uint2>(), c->ntiles, s);
+    } else {
+        cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
+    }
+    cudaEventRecord(c->ev[4], s);
+    BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
+                 want_rgb ? c->frame_t.as<float>() : nullptr};
+    launch_blend(c->srec.as<SplatRec>(), c->final_tvals, c->ranges.as<uint2>(), W, H, bg[0], bg[1],
+                 bg[2], out, s);
+    cudaEventRecord(c->ev[5], s);
+    cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s);
+    GSR_CUDA_OK(cudaGetLastError());
+    c->saved.scene = sc;
+    c->saved.cam = *cam;
+    for (int i = 0; i < 3; i++) c->saved.bg[i] = bg[i];
+    c->saved.sh_degree = sh_degree;
+    c->saved.cull = cull;
+    c->saved.want_rgb = want_rgb;
+    c->saved.want_keep = want_keep;
+    c->pending = true;
+    return GSR_OK;
+}
+
+// Wait for the pending frame; on tile-key overflow grow and re-render once.
+int complete_frame(gsr_ctx *c) {
+    if (!c->pending) return GSR_OK;
+    GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
+    c->pending = false;
+    c->retries = 0;
+    if ((int64_t)c->hctr->D > c->cap_d) {
+        c->cap_d = round_up((int64_t)c->hctr->D + (int64_t)c->hctr->D / 4 + (1 << 20), 4096);
+        SavedCall sv = c->saved;
+        int rc = enqueue_frame(c, sv.scene, &sv.cam, sv.bg, sv.sh_degree, sv.cull, sv.want_rgb,
+                               sv.want_keep);
+        if (rc) return rc;
+        GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
+        c->pending = false;
+        c->retries = 1;
+        if ((int64_t)c->hctr->D > c->cap_d) return fail(GSR_E_OOM, "tile-key buffer overflow");
+    }
+    return GSR_OK;
+}
+
+void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
+    if (!st) return;
+    st->splats_drawn = c->hctr->K;
+    st->splats_culled = sc ? sc->n - (int64_t)c->hctr->K : 0;
+    st->tile_keys = c->hctr->D;
+    st->depth_passes = (int32_t)c->hctr->npass;
+    st->retries = c->retries;
+    float t[6] = {0, 0, 0, 0, 0, 0};
+    cudaEventElapsedTime(&t[0], c->ev[0], c->ev[5]);
+    cudaEventElapsedTime(&t[1], c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&t[2], c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&t[3], c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&t[4], c->ev[3], c->ev[4]);
+    cudaEventElapsedTime(&t[5], c->ev[4], c->ev[5]);
+    st->ms_device = t[0];
+    st->ms_preprocess = t[1];
+    st->ms_depth_sort = t[2];
+    st->ms_binning = t[3];
+    st->ms_tile_sort = t[4];
+    st->ms_blend = t[5];
+}
+
+// ---- Pillow BILINEAR coefficients (Resample.c precompute_coeffs +
+// normalize_coeffs_8bpc), host double arithmetic, no FMA contraction ----
+int pillow_coeffs(int in_size, int out_size, std::vector<int32_t> &bounds,
+                  std::vector<int32_t> &kk) {
+    const double scale = (double)((float)in_size - 0.0f) / out_size;
+    const double filterscale = scale < 1.0 ? 1.0 : scale;
+    const double support = 1.0 * filterscale;
+    const int ksize = (int)std::ceil(support) * 2 + 1;
+    bounds.assign((size_t)out_size * 2, 0);
+    kk.assign((size_t)out_size * ksize, 0);
+    std::vector<double> k((size_t)ksize);
+    for (int xx = 0; xx < out_size; xx++) {
+        const double center = 0.0 + (xx + 0.5) * scale;
+        double ww = 0.0;
+        const double ss = 1.0 / filterscale;
+        int xmin = (int)(center - support + 0.5);
+        if (xmin < 0) xmin = 0;
+        int xmax = (int)(center + support + 0.5);
+        if (xmax > in_size) xmax = in_size;
+        xmax -= xmin;
+        int x;
+        for (x = 0; x < xmax; x++) {
+            double t = (x + xmin - center + 0.5) * ss;
+            if (t < 0.0) t = -t;
+            const double w = t < 1.0 ? 1.0 - t : 0.0;
+            k[x] = w;
+            ww += w;
+        }
+        for (x = 0; x < xmax; x++)
+            if (ww != 0.0) k[x] /= ww;
+        for (; x < ksize; x++) k[x] = 0;
+        for (x = 0; x < ksize; x++) {
+            const double v = k[x];
+            kk[(size_t)xx * ksize + x] = v < 0 ? (int32_t)(-0.5 + v * (1 << 22))
+                                               : (int32_t)(0.5 + v * (1 << 22));
+        }
+        bounds[2 * xx] = xmin;
+        bounds[2 * xx + 1] = xmax;
+    }
+    return ksize;
+}
+
+// device-to-device resample on c->stream (dst may not alias src)
+int resample_device(gsr_ctx *c, const uint8_t *src, int sw, int sh, uint8_t *dst, int dw, int dh) {
+    cudaStream_t s = c->stream;
+    if (sw == dw && sh == dh) {
+        GSR_CUDA_OK(cudaMemcpyAsync(dst, src, (size_t)sw * sh * 3, cudaMemcpyDeviceToDevice, s));
+        return GSR_OK;
+    }
+    std::vector<int32_t> bh, kh, bv, kv;
+    const int ksh = pillow_coeffs(sw, dw, bh, kh);
+    const int ksv = pillow_coeffs(sh, dh, bv, kv);
+    const bool need_h = dw != sw, need_v = dh != sh;
+    const int ybox_first = bv[0];
+    const int ybox_last = bv[(size_t)dh * 2 - 2] + bv[(size_t)dh * 2 - 1];
+    if (need_h)
+        for (int i = 0; i < dh; i++) bv[2 * i] -= ybox_first;
+    // one upload: [bh | kh | bv | kv]
+    std::vector<int32_t> blob;
+    blob.reserve(bh.size() + kh.size() + bv.size() + kv.size());
+    blob.insert(blob.end(), bh.begin(), bh.end());
+    blob.insert(blob.end(), kh.begin(), kh.end());
+    blob.insert(blob.end(), bv.begin(), bv.end());
+    blob.insert(blob.end(), kv.begin(), kv.end());
+    int rc;
+    if ((rc = ensure(c->coefs, blob.size() * sizeof(int32_t)))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(c->coefs.p, blob.data(), blob.size() * sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+    // the host vector must outlive the async copy
+    GSR_CUDA_OK(cudaStreamSynchronize(s));
+    const int32_t *d = c->coefs.as<int32_t>();
+    ResampleAxis axh{d, d + bh.size(), ksh};
+    ResampleAxis axv{d + bh.size() + kh.size(), d + bh.size() + kh.size() + bv.size(), ksv};
+    const uint8_t *cur = src;
+    int cw = sw;
+    if (need_h) {
+        const int rows = ybox_last - ybox_first;
+        if ((rc = ensure(c->tmp_u8, (size_t)dw * rows * 3))) return rc;
+        uint8_t *tgt = need_v ? c->tmp_u8.as<uint8_t>() : dst;
+        launch_resample_h(src, sw, ybox_first, tgt, dw, rows, axh, s);
+        cur = tgt;
+        cw = dw;
+    }
+    if (need_v) launch_resample_v(cur, cw, dst, dh, axv, s);
+    GSR_CUDA_OK(cudaGetLastError());
+    return GSR_OK;
+}
+
+int ssim_device(gsr_ctx *c, const SsimInput &in, int W, int H, double *dev_out) {
+    int rc;
+    if ((rc = ensure(c->ssim_part, sizeof(double) * (size_t)ssim_partials_needed(W, H)))) return rc;
+    launch_ssim(in, W, H, c->ssim_w.as<double>(), c->ssim_part.as<double>(),
+                c->ssim_misc.as<uint32_t>(), dev_out, c->stream);
+    GSR_CUDA_OK(cudaGetLastError());
+    return GSR_OK;
+}
+
+}  // namespace
+
+// =========================================================== C ABI =========
+extern "C" {
+
+int gsr_abi_version(void) { return GSR_ABI_VERSION; }
+
+const char *gsr_last_error(void) { return g_err.c_str(); }
+
+int gsr_device_count(int *out_count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    if (out_count) *out_count = n;
+    return GSR_OK;
+}
+
+int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means,
+                     const double *scales, const double *rotations, const double *opacities,
+                     const double *colors_dc, const double *sh_coeffs, const double *rsq) {
+    if (!out) return fail(GSR_E_INVALID, "out is null");
+    *out = nullptr;
+    if (n < 0 || n >= (int64_t(1) << 31)) return fail(GSR_E_INVALID, "invalid Gaussian count");
+    if (n > 0 && (!means || !scales || !rotations || !opacities || !colors_dc))
+        return fail(GSR_E_INVALID, "null attribute array");
+    int ndev = 0;
+    gsr_device_count(&ndev);
+    if (ndev == 0) return fail(GSR_E_NO_DEVICE, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(GSR_E_INVALID, "device index out of range");
+    DeviceGuard g(device);
+    gsr_scene *sc = new (std::nothrow) gsr_scene();
+    if (!sc) return fail(GSR_E_OOM, "host allocation failed");
+    sc->device = device;
+    sc->n = n;
+    sc->stride = round_up(std::max<int64_t>(n, 1), 32);
+    sc->has_sh = sh_coeffs != nullptr;
+    // f32 SH storage when lossless (PLY scenes are f32 on disk, model.py:188)
+    bool f32ok = true;
+    if (sh_coeffs)
+        for (int64_t i = 0; i < n * 48 && f32ok; i++)
+            f32ok = (double)(float)sh_coeffs[i] == sh_coeffs[i];
+    sc->sh_f32 = f32ok ? 1 : 0;
+    const int64_t st = sc->stride;
+    const size_t sh_elem = sc->sh_f32 ? 4 : 8;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += round_up((int64_t)bytes, 256);
+        return o;
+    };
+    const size_t o_mean = take(3 * st * 8), o_scale = take(3 * st * 8), o_rot = take(4 * st * 8),
+                 o_rsq = take(st * 8), o_opac = take(st * 4), o_dc = take(3 * st * 4),
+                 o_op64 = take(st * 8),
+                 o_sh = take(sc->has_sh ? 48 * st * sh_elem : 16);
+    int rc = ensure(sc->block, off);
+    if (rc) {
+        delete sc;
+        return rc;
+    }
+    // host staging in planar (SoA) layout
+    std::vector<unsigned char> host(off, 0);
+    auto plane_d = [&](size_t o, const double *src, int k, int comps) {
+        double *d = reinterpret_cast<double *>(host.data() + o) + (size_t)k * st;
+        for (int64_t i = 0; i < n; i++) d[i] = src[i * comps + k];
+    };
+    auto plane_f = [&](size_t o, const double *src, int k, int comps) {
+        float *d = reinterpret_cast<float *>(host.data() + o) + (size_t)k * st;
+        for (int64_t i = 0; i < n; i++) d[i] = (float)src[i * comps + k];
+    };
+    for (int k = 0; k < 3; k++) {
+        plane_d(o_mean, means, k, 3);
+        plane_d(o_scale, scales, k, 3);
+        plane_f(o_dc, colors_dc, k, 3);
+    }
+    for (int k = 0; k < 4; k++) plane_d(o_rot, rotations, k, 4);
+    plane_f(o_opac, opacities, 0, 1);
+    plane_d(o_op64, opacities, 0, 1);
+    if (rsq) plane_d(o_rsq, rsq, 0, 1);
+    if (sc->has_sh) {
+        for (int k = 0; k < 48; k++) {
+            if (sc->sh_f32) plane_f(o_sh, sh_coeffs, k, 48);
+            else plane_d(o_sh, sh_coeffs, k, 48);
+        }
+    }
+    unsigned char *d = sc->block.as<unsigned char>();
+    cudaError_t e = cudaMemcpy(d, host.data(), off, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        delete sc;
+        return fail_cuda(e, "scene upload");
+    }
+    if (!rsq && n > 0) {
+        rsq_kernel<<<(unsigned)((n + 255) / 256), 256>>>(
+            reinterpret_cast<float *>(d + o_opac), reinterpret_cast<double *>(d + o_op64), n,
+            reinterpret_cast<double *>(d + o_rsq));
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            delete sc;
+            return fail_cuda(e, "rsq kernel");
+        }
+    }
+    SceneView &v = sc->view;
+    v.n = n;
+    v.stride = st;
+    v.mean = reinterpret_cast<const double *>(d + o_mean);
+    v.scale = reinterpret_cast<const double *>(d + o_scale);
+    v.rot = reinterpret_cast<const double *>(d + o_rot);
+    v.rsq = reinterpret_cast<const double *>(d + o_rsq);
+    v.opac = reinterpret_cast<const float *>(d + o_opac);
+    v.dc = reinterpret_cast<const float *>(d + o_dc);
+    v.sh = d + o_sh;
+    v.sh_f32 = sc->sh_f32;
+    *out = sc;
+    return GSR_OK;
+}
+
+int gsr_scene_destroy(gsr_scene *scene) {
+    if (!scene) return GSR_OK;
+    DeviceGuard g(scene->device);
+    delete scene;
+    return GSR_OK;
+}
+
+int64_t gsr_scene_count(const gsr_scene *scene) { return scene ? scene->n : -1; }
+
+int64_t gsr_scene_device_bytes(const gsr_scene *scene) {
+    return scene ? (int64_t)scene->block.bytes : 0;
+}
+
+int gsr_scene_sh_is_f32(const gsr_scene *scene) { return scene ? scene->sh_f32 : 0; }
+
+int gsr_ctx_create(gsr_ctx **out, int device) {
+    if (!out) return fail(GSR_E_INVALID, "out is null");
+    *out = nullptr;
+    int ndev = 0;
+    gsr_device_count(&ndev);
+    if (ndev == 0) return fail(GSR_E_NO_DEVICE, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(GSR_E_INVALID, "device index out of range");
+    DeviceGuard g(device);
+    gsr_ctx *c = new (std::nothrow) gsr_ctx();
+    if (!c) return fail(GSR_E_OOM, "host allocation failed");
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = radix_init_attributes();
+    for (int i = 0; i < 8 && e == cudaSuccess; i++) e = cudaEventCreate(&c->ev[i]);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters));
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hssim, sizeof(double) * 64);
+    if (e != cudaSuccess) {
+        int rc = fail_cuda(e, "context setup");
+        gsr_ctx_destroy(c);
+        return rc;
+    }
+    int rc = ensure(c->ctr, sizeof(FrameCounters));
+    if (!rc) rc = ensure(c->ssim_misc, 64);
+    if (!rc) rc = ensure(c->ssim_w, sizeof(double) * 11);
+    if (rc) {
+        gsr_ctx_destroy(c);
+        return rc;
+    }
+    // scipy _gaussian_kernel1d(sigma=1.5, order 0, radius 5), f64
+    double w[11], sum = 0.0;
+    for (int i = 0; i < 11; i++) {
+        const double x = (double)(i - 5);
+        w[i] = std::exp(-0.5 / (1.5 * 1.5) * (x * x));
+        sum += w[i];
+    }
+    for (int i = 0; i < 11; i++) w[i] = w[i] / sum;
+    e = cudaMemcpy(c->ssim_w.p, w, sizeof(w), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        int rc2 = fail_cuda(e, "ssim weights");
+        gsr_ctx_destroy(c);
+        return rc2;
+    }
+    *out = c;
+    return GSR_OK;
+}
+
+int gsr_ctx_destroy(gsr_ctx *ctx) {
+    if (!ctx) return GSR_OK;
+    DeviceGuard g(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->hctr) cudaFreeHost(ctx->hctr);
+    if (ctx->hssim) cudaFreeHost(ctx->hssim);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return GSR_OK;
+}
+
+int64_t gsr_ctx_device_bytes(const gsr_ctx *ctx) { return ctx ? ctx->bytes() : 0; }
+
+const uint8_t *gsr_ctx_frame_u8(const gsr_ctx *ctx) {
+    return ctx ? ctx->frame_u8.as<uint8_t>() : nullptr;
+}
+
+int gsr_render_async(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+                     const float background[3], int sh_degree, int frustum_cull) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    DeviceGuard g(ctx->device);
+    const float zero[3] = {0, 0, 0};
+    return enqueue_frame(ctx, scene, cam, background ? background : zero, sh_degree, frustum_cull,
+                         false, false);
+}
+
+int gsr_ctx_finish(gsr_ctx *ctx, uint8_t *out_u8, gsr_stats *stats) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    DeviceGuard g(ctx->device);
+    const gsr_scene *sc = ctx->saved.scene;
+    int rc = complete_frame(ctx);
+    if (rc) return rc;
+    if (out_u8) {
+        GSR_CUDA_OK(cudaMemcpyAsync(out_u8, ctx->frame_u8.p, (size_t)ctx->W * ctx->H * 3,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    }
+    fill_stats(ctx, sc, stats);
+    return GSR_OK;
+}
+
+int gsr_render(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+               const float background[3], int sh_degree, int frustum_cull, uint8_t *out_u8,
+               float *out_rgb, float *out_T, gsr_stats *stats) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    DeviceGuard g(ctx->device);
+    const float zero[3] = {0, 0, 0};
+    const bool want_rgb = out_rgb || out_T;
+    int rc = enqueue_frame(ctx, scene, cam, background ? background : zero, sh_degree,
+                           frustum_cull, want_rgb, false);
+    if (rc) return rc;
+    const size_t px = (size_t)cam->width * cam->height;
+    // copies ride the stream; if the frame overflows they are redone below
+    if (out_u8)
+        GSR_CUDA_OK(cudaMemcpyAsync(out_u8, ctx->frame_u8.p, px * 3, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    if ((rc = complete_frame(ctx))) return rc;
+    if (ctx->retries && out_u8)
+        GSR_CUDA_OK(cudaMemcpy(out_u8, ctx->frame_u8.p, px * 3, cudaMemcpyDeviceToHost));
+    if (out_rgb)
+        GSR_CUDA_OK(cudaMemcpy(out_rgb, ctx->frame_rgb.p, px * 3 * sizeof(float),
+                               cudaMemcpyDeviceToHost));
+    if (out_T)
+        GSR_CUDA_OK(cudaMemcpy(out_T, ctx->frame_t.p, px * sizeof(float), cudaMemcpyDeviceToHost));
+    fill_stats(ctx, scene, stats);
+    return GSR_OK;
+}
+
+int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+                         int sh_degree, int frustum_cull, uint8_t *out_keep, int64_t *out_order,
+                         float *out_packed, gsr_stats *stats) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    DeviceGuard g(ctx->device);
+    const float zero[3] = {0, 0, 0};
+    int rc = enqueue_frame(ctx, scene, cam, zero, sh_degree, frustum_cull, false, true);
+    if (rc) return rc;
+    if ((rc = complete_frame(ctx))) return rc;
+    const int64_t n = scene->n, k = ctx->hctr->K;
+    if (out_keep && n > 0)
+        GSR_CUDA_OK(cudaMemcpy(out_keep, ctx->keep.p, (size_t)n, cudaMemcpyDeviceToHost));
+    if (out_order && k > 0) {
+        std::vector<uint32_t> o((size_t)k);
+        const DevBuf &vb = ctx->vals[ctx->hctr->npass & 1];
+        GSR_CUDA_OK(cudaMemcpy(o.data(), vb.p, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < k; i++) out_order[i] = o[i];
+    }
+    if (out_packed && k > 0) {
+        std::vector<SplatRec> r((size_t)k);
+        GSR_CUDA_OK(cudaMemcpy(r.data(), ctx->srec.p, sizeof(SplatRec) * k, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < k; i++) {
+            float *p = out_packed + 11 * i;
+            const SplatRec &s = r[i];
+            p[0] = s.a.x; p[1] = s.a.y; p[2] = s.a.z; p[3] = s.a.w; p[4] = s.b.x; p[5] = s.b.y;
+            p[6] = s.c.x; p[7] = s.c.y; p[8] = s.c.z; p[9] = s.b.z; p[10] = s.b.w;
+        }
+    }
+    fill_stats(ctx, scene, stats);
+    return GSR_OK;
+}
+
+int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_ranks,
+                         int32_t *out_ranges, gsr_stats *stats) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    DeviceGuard g(ctx->device);
+    int rc = complete_frame(ctx);
+    if (rc) return rc;
+    const int64_t d = std::min<int64_t>(ctx->hctr->D, ctx->cap_d);
+    if (out_tiles && d > 0)
+        GSR_CUDA_OK(cudaMemcpy(out_tiles, ctx->final_tkeys, 4 * d, cudaMemcpyDeviceToHost));
+    if (out_ranks && d > 0)
+        GSR_CUDA_OK(cudaMemcpy(out_ranks, ctx->final_tvals, 4 * d, cudaMemcpyDeviceToHost));
+    if (out_ranges && ctx->ntiles > 0)
+        GSR_CUDA_OK(cudaMemcpy(out_ranges, ctx->ranges.p, sizeof(uint2) * ctx->ntiles,
+                               cudaMemcpyDeviceToHost));
+    if (stats) {
+        stats->tile_keys = ctx->hctr->D;
+        stats->splats_drawn = ctx->hctr->K;
+    }
+    return GSR_OK;
+}
+
+int gsr_resample_bilinear_u8(gsr_ctx *ctx, const uint8_t *src, int src_w, int src_h, uint8_t *dst,
+                             int dst_w, int dst_h) {
+    if (!ctx || !src || !dst) return fail(GSR_E_INVALID, "null argument");
+    if (src_w <= 0 || src_h <= 0 || dst_w <= 0 || dst_h <= 0)
+        return fail(GSR_E_INVALID, "dimensions must be positive");
+    DeviceGuard g(ctx->device);
+    int rc;
+    const size_t sb = (size_t)src_w * src_h * 3, db = (size_t)dst_w * dst_h * 3;
+    if ((rc = ensure(ctx->src_u8, sb))) return rc;
+    if ((rc = ensure(ctx->dst_u8, db))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->src_u8.p, src, sb, cudaMemcpyHostToDevice, ctx->stream));
+    if ((rc = resample_device(ctx, ctx->src_u8.as<uint8_t>(), src_w, src_h,
+                              ctx->dst_u8.as<uint8_t>(), dst_w, dst_h)))
+        return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(dst, ctx->dst_u8.p, db, cudaMemcpyDeviceToHost, ctx->stream));
+    GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    return GSR_OK;
+}
+
+int gsr_ssim_u8(gsr_ctx *ctx, const uint8_t *a, const uint8_t *b, int width, int height,
+                double *out_ssim) {
+    if (!ctx || !a || !b || !out_ssim) return fail(GSR_E_INVALID, "null argument");
+    if (width < 11 || height < 11) return fail(GSR_E_TOO_SMALL, "images must be at least 11x11");
+    DeviceGuard g(ctx->device);
+    int rc;
+    const size_t nb = (size_t)width * height * 3;
+    if ((rc = ensure(ctx->src_u8, nb))) return rc;
+    if ((rc = ensure(ctx->dst_u8, nb))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->src_u8.p, a, nb, cudaMemcpyHostToDevice, ctx->stream));
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->dst_u8.p, b, nb, cudaMemcpyHostToDevice, ctx->stream));
+    double *dout = reinterpret_cast<double *>(ctx->ssim_misc.as<unsigned char>() + 8);
+    SsimInput in{ctx->src_u8.as<uint8_t>(), ctx->dst_u8.as<uint8_t>(), nullptr, nullptr};
+    if ((rc = ssim_device(ctx, in, width, height, dout))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->hssim, dout, sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    *out_ssim = ctx->hssim[0];
+    return GSR_OK;
+}
+
+int gsr_ssim_luma_f64(gsr_ctx *ctx, const double *x, const double *y, int width, int height,
+                      double *out_ssim) {
+    if (!ctx || !x || !y || !out_ssim) return fail(GSR_E_INVALID, "null argument");
+    if (width < 11 || height < 11) return fail(GSR_E_TOO_SMALL, "images must be at least 11x11");
+    DeviceGuard g(ctx->device);
+    int rc;
+    const size_t nb = (size_t)width * height * sizeof(double);
+    if ((rc = ensure(ctx->src_u8, nb))) return rc;
+    if ((rc = ensure(ctx->dst_u8, nb))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->src_u8.p, x, nb, cudaMemcpyHostToDevice, ctx->stream));
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->dst_u8.p, y, nb, cudaMemcpyHostToDevice, ctx->stream));
+    double *dout = reinterpret_cast<double *>(ctx->ssim_misc.as<unsigned char>() + 8);
+    SsimInput in{nullptr, nullptr, ctx->src_u8.as<double>(), ctx->dst_u8.as<double>()};
+    if ((rc = ssim_device(ctx, in, width, height, dout))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->hssim, dout, sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    *out_ssim = ctx->hssim[0];
+    return GSR_OK;
+}
+
+int gsr_host_alloc(void **out, size_t bytes) {
+    if (!out) return fail(GSR_E_INVALID, "out is null");
+    *out = nullptr;
+    GSR_CUDA_OK(cudaMallocHost(out, bytes ? bytes : 1));
+    return GSR_OK;
+}
+
+int gsr_host_free(void *ptr) {
+    if (ptr) GSR_CUDA_OK(cudaFreeHost(ptr));
+    return GSR_OK;
+}
+
+int gsr_ladder_ssim(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *base_cam,
+                    const float background[3], int sh_degree, int n_rungs,
+                    const gsr_camera *rung_cams, double *out_ssim, gsr_stats *base_stats) {
+    if (!ctx || !base_cam || (n_rungs > 0 && (!rung_cams || !out_ssim)))
+        return fail(GSR_E_INVALID, "null argument");
+    if (n_rungs < 0 || n_rungs > 48) return fail(GSR_E_INVALID, "n_rungs must be in 0..48");
+    if (base_cam->width < 11 || base_cam->height < 11)
+        return fail(GSR_E_TOO_SMALL, "base frame must be at least 11x11");
+    DeviceGuard g(ctx->device);
+    const float zero[3] = {0, 0, 0};
+    const float *bg = background ? background : zero;
+    int rc = enqueue_frame(ctx, scene, base_cam, bg, sh_degree, 1, false, false);
+    if (rc) return rc;
+    if ((rc = complete_frame(ctx))) return rc;
+    fill_stats(ctx, scene, base_stats);
+    const int W = base_cam->width, H = base_cam->height;
+    const size_t nb = (size_t)W * H * 3;
+    if ((rc = ensure(ctx->base_u8, nb))) return rc;
+    if ((rc = ensure(ctx->up_u8, nb))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->base_u8.p, ctx->frame_u8.p, nb, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    double *dres = reinterpret_cast<double *>(ctx->ssim_misc.as<unsigned char>() + 8);
+    std::vector<double> res((size_t)n_rungs);
+    for (int i = 0; i < n_rungs; i++) {
+        const gsr_camera *rc_cam = &rung_cams[i];
+        if ((rc = enqueue_frame(ctx, scene, rc_cam, bg, sh_degree, 1, false, false))) return rc;
+        if ((rc = complete_frame(ctx))) return rc;
+        if ((rc = resample_device(ctx, ctx->frame_u8.as<uint8_t>(), rc_cam->width, rc_cam->height,
+                                  ctx->up_u8.as<uint8_t>(), W, H)))
+            return rc;
+        SsimInput in{ctx->up_u8.as<uint8_t>(), ctx->base_u8.as<uint8_t>(), nullptr, nullptr};
+        if ((rc = ssim_device(ctx, in, W, H, dres))) return rc;
+        GSR_CUDA_OK(cudaMemcpyAsync(ctx->hssim, dres, sizeof(double), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+        GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        res[(size_t)i] = ctx->hssim[0];
+    }
+    for (int i = 0; i < n_rungs; i++) out_ssim[i] = res[(size_t)i];
+    return GSR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,246 @@
+// preprocess.cu -- K1: per-Gaussian f64 projection, culling, SH colour and
+// packing, fused in one pass over the SoA scene.
+//
+// Restates, with the reference's exact f64 operation order (no FMA):
+//   _project_kernel      render.py:163-237
+//   eval_sh_colors       render.py:126-160 (degree 1..3; colors_dc for 0)
+//   packing              render.py:442-453 (c/det, -b/det, a/det, sqrt(c*rsq))
+// Culled Gaussians get the sentinel depth key ~0; the first depth-sort pass
+// drops them, which is the order-preserving compaction of render.py:279.
+#include "kernels.cuh"
+
+namespace gsr {
+
+namespace {
+
+constexpr double SH_C0 = 0.28209479177387814;
+constexpr double SH_C1 = 0.4886025119029199;
+constexpr double SH_C2_0 = 1.0925484305920792, SH_C2_1 = -1.0925484305920792,
+                 SH_C2_2 = 0.31539156525252005, SH_C2_3 = -1.0925484305920792,
+                 SH_C2_4 = 0.5462742152960396;
+constexpr double SH_C3_0 = -0.5900435899266435, SH_C3_1 = 2.890611442640554,
+                 SH_C3_2 = -0.4570457994644658, SH_C3_3 = 0.3731763325901154,
+                 SH_C3_4 = -0.4570457994644658, SH_C3_5 = 1.445305721320277,
+                 SH_C3_6 = -0.5900435899266435;
+
+template <typename T>
+__device__ __forceinline__ double ldsh(const T *sh, int64_t stride, int k, int c, int64_t i) {
+    return (double)__ldg(sh + (int64_t)(k * 3 + c) * stride + i);
+}
+
+// eval_sh_colors for one Gaussian and one channel, numpy expression order.
+template <typename T>
+__device__ __forceinline__ double sh_channel(const T *sh, int64_t stride, int64_t i, int c,
+                                             int degree, double x, double y, double z,
+                                             double xx, double yy, double zz, double xy,
+                                             double yz, double xz) {
+    double r = SH_C0 * ldsh(sh, stride, 0, c, i);
+    r = r - (SH_C1 * y) * ldsh(sh, stride, 1, c, i) + (SH_C1 * z) * ldsh(sh, stride, 2, c, i) -
+        (SH_C1 * x) * ldsh(sh, stride, 3, c, i);
+    if (degree >= 2) {
+        r = r + (SH_C2_0 * xy) * ldsh(sh, stride, 4, c, i) +
+            (SH_C2_1 * yz) * ldsh(sh, stride, 5, c, i) +
+            (SH_C2_2 * (2.0 * zz - xx - yy)) * ldsh(sh, stride, 6, c, i) +
+            (SH_C2_3 * xz) * ldsh(sh, stride, 7, c, i) +
+            (SH_C2_4 * (xx - yy)) * ldsh(sh, stride, 8, c, i);
+    }
+    if (degree >= 3) {
+        r = r + ((SH_C3_0 * y) * (3.0 * xx - yy)) * ldsh(sh, stride, 9, c, i) +
+            ((SH_C3_1 * xy) * z) * ldsh(sh, stride, 10, c, i) +
+            ((SH_C3_2 * y) * (4.0 * zz - xx - yy)) * ldsh(sh, stride, 11, c, i) +
+            ((SH_C3_3 * z) * (2.0 * zz - 3.0 * xx - 3.0 * yy)) * ldsh(sh, stride, 12, c, i) +
+            ((SH_C3_4 * x) * (4.0 * zz - xx - yy)) * ldsh(sh, stride, 13, c, i) +
+            ((SH_C3_5 * z) * (xx - yy)) * ldsh(sh, stride, 14, c, i) +
+            ((SH_C3_6 * x) * (xx - 3.0 * yy)) * ldsh(sh, stride, 15, c, i);
+    }
+    r = r + 0.5;
+    return r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);  // np.clip(result + 0.5, 0, 1)
+}
+
+__global__ void frame_init_kernel(FrameCounters *ctr) {
+    ctr->K = 0;
+    ctr->D = 0;
+    ctr->npass = 1;
+    ctr->pad0 = 0;
+    ctr->kmin = ~0ull;
+    ctr->kmax = 0ull;
+}
+
+template <typename ShT>
+__global__ void __launch_bounds__(256) preprocess_kernel(SceneView sc, CameraArgs cam,
+                                                         int sh_degree, int do_cull,
+                                                         unsigned long long *__restrict__ keys,
+                                                         SplatRec *__restrict__ rec,
+                                                         uint8_t *__restrict__ keep_out,
+                                                         FrameCounters *ctr) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t st = sc.stride;
+    bool kept = false;
+    unsigned long long key = ~0ull;
+    if (i < sc.n) {
+        const double r00 = cam.r[0], r01 = cam.r[1], r02 = cam.r[2];
+        const double r10 = cam.r[3], r11 = cam.r[4], r12 = cam.r[5];
+        const double r20 = cam.r[6], r21 = cam.r[7], r22 = cam.r[8];
+        const double mx = __ldg(sc.mean + i), my = __ldg(sc.mean + st + i),
+                     mz = __ldg(sc.mean + 2 * st + i);
+        // render.py:174-176
+        const double x = r00 * mx + r01 * my + r02 * mz + cam.t[0];
+        const double y = r10 * mx + r11 * my + r12 * mz + cam.t[1];
+        const double z = r20 * mx + r21 * my + r22 * mz + cam.t[2];
+        if (!(z <= kZNear)) {
+            const double qw = __ldg(sc.rot + i), qx = __ldg(sc.rot + st + i),
+                         qy = __ldg(sc.rot + 2 * st + i), qz = __ldg(sc.rot + 3 * st + i);
+            const double sx = __ldg(sc.scale + i), sy = __ldg(sc.scale + st + i),
+                         sz = __ldg(sc.scale + 2 * st + i);
+            // render.py:185-193
+            const double m00 = (1.0 - 2.0 * (qy * qy + qz * qz)) * sx;
+            const double m01 = (2.0 * (qx * qy - qw * qz)) * sy;
+            const double m02 = (2.0 * (qx * qz + qw * qy)) * sz;
+            const double m10 = (2.0 * (qx * qy + qw * qz)) * sx;
+            const double m11 = (1.0 - 2.0 * (qx * qx + qz * qz)) * sy;
+            const double m12 = (2.0 * (qy * qz - qw * qx)) * sz;
+            const double m20 = (2.0 * (qx * qz - qw * qy)) * sx;
+            const double m21 = (2.0 * (qy * qz + qw * qx)) * sy;
+            const double m22 = (1.0 - 2.0 * (qx * qx + qy * qy)) * sz;
+            // render.py:196-204
+            const double a00 = r00 * m00 + r01 * m10 + r02 * m20;
+            const double a01 = r00 * m01 + r01 * m11 + r02 * m21;
+            const double a02 = r00 * m02 + r01 * m12 + r02 * m22;
+            const double a10 = r10 * m00 + r11 * m10 + r12 * m20;
+            const double a11 = r10 * m01 + r11 * m11 + r12 * m21;
+            const double a12 = r10 * m02 + r11 * m12 + r12 * m22;
+            const double a20 = r20 * m00 + r21 * m10 + r22 * m20;
+            const double a21 = r20 * m01 + r21 * m11 + r22 * m21;
+            const double a22 = r20 * m02 + r21 * m12 + r22 * m22;
+            // render.py:206-220
+            const double inv_z = 1.0 / z;
+            const double jx = cam.fx * inv_z;
+            const double jy = cam.fy * inv_z;
+            const double gx = -cam.fx * x * inv_z * inv_z;
+            const double gy = -cam.fy * y * inv_z * inv_z;
+            const double p0 = jx * a00 + gx * a20;
+            const double p1 = jx * a01 + gx * a21;
+            const double p2 = jx * a02 + gx * a22;
+            const double q0 = jy * a10 + gy * a20;
+            const double q1 = jy * a11 + gy * a21;
+            const double q2 = jy * a12 + gy * a22;
+            const double ca = p0 * p0 + p1 * p1 + p2 * p2 + kCovFloor;
+            const double cb = p0 * q0 + p1 * q1 + p2 * q2;
+            const double cc = q0 * q0 + q1 * q1 + q2 * q2 + kCovFloor;
+            // render.py:222-223
+            const double u = cam.fx * x * inv_z + cam.cx;
+            const double v = cam.fy * y * inv_z + cam.cy;
+            bool k = true;
+            if (do_cull) {  // render.py:230-235
+                const double mid = 0.5 * (ca + cc);
+                const double d = ca - cc;
+                const double disc = 0.25 * (d * d) + cb * cb;
+                const double radius = kCutoffSigma * sqrt(mid + sqrt(disc));
+                k = (u + radius > 0.0 && u - radius < cam.width && v + radius > 0.0 &&
+                     v - radius < cam.height);
+            }
+            if (k) {
+                kept = true;
+                key = (unsigned long long)__double_as_longlong(z);
+                float cr, cg, cbl;
+                if (sh_degree == 0) {
+                    cr = __ldg(sc.dc + i);
+                    cg = __ldg(sc.dc + st + i);
+                    cbl = __ldg(sc.dc + 2 * st + i);
+                } else {  // render.py:134-160
+                    const double dx = mx - cam.campos[0];
+                    const double dy = my - cam.campos[1];
+                    const double dz = mz - cam.campos[2];
+                    const double norm = sqrt((dx * dx + dy * dy) + dz * dz);
+                    const double den = norm > 1e-12 ? norm : 1e-12;
+                    const double ux = dx / den, uy = dy / den, uz = dz / den;
+                    const double xx = ux * ux, yy = uy * uy, zz = uz * uz;
+                    const double xy = ux * uy, yz = uy * uz, xz = ux * uz;
+                    const ShT *sh = (const ShT *)sc.sh;
+                    cr = (float)sh_channel(sh, st, i, 0, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+                    cg = (float)sh_channel(sh, st, i, 1, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+                    cbl = (float)sh_channel(sh, st, i, 2, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+                }
+                // render.py:442-453
+                const double det = ca * cc - cb * cb;
+                const double rsq = __ldg(sc.rsq + i);
+                SplatRec o;
+                o.a = make_float4((float)u, (float)v, (float)(cc / det), (float)(-cb / det));
+                o.b = make_float4((float)(ca / det), (float)rsq, __ldg(sc.opac + i),
+                                  (float)sqrt(cc * rsq));
+                o.c = make_float4(cr, cg, cbl, 0.0f);
+                rec[i] = o;
+            }
+        }
+        keys[i] = key;
+        if (keep_out) keep_out[i] = kept ? 1 : 0;
+    }
+    // block reduction of K and of the kept key range (radix pass trimming)
+    __shared__ unsigned long long s_min[8], s_max[8];
+    __shared__ uint32_t s_cnt[8];
+    unsigned long long kmn = kept ? key : ~0ull, kmx = kept ? key : 0ull;
+    uint32_t cnt = __popc(__ballot_sync(0xffffffffu, kept));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long a = __shfl_xor_sync(0xffffffffu, kmn, o);
+        unsigned long long b = __shfl_xor_sync(0xffffffffu, kmx, o);
+        kmn = a < kmn ? a : kmn;
+        kmx = b > kmx ? b : kmx;
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_min[w] = kmn;
+        s_max[w] = kmx;
+        s_cnt[w] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = 0;
+        for (int j = 0; j < (int)(blockDim.x >> 5); j++) {
+            c += s_cnt[j];
+            kmn = s_min[j] < kmn ? s_min[j] : kmn;
+            kmx = s_max[j] > kmx ? s_max[j] : kmx;
+        }
+        if (c) {
+            atomicAdd(&ctr->K, c);
+            atomicMin(&ctr->kmin, kmn);
+            atomicMax(&ctr->kmax, kmx);
+        }
+    }
+}
+
+// number of 8-bit LSD passes over (key - kmin): ceil(bits(kmax - kmin) / 8), >= 1
+__global__ void depth_passes_kernel(FrameCounters *ctr) {
+    uint32_t np = 1;
+    if (ctr->K > 1 && ctr->kmax > ctr->kmin) {
+        int bits = 64 - __clzll((long long)(ctr->kmax - ctr->kmin));
+        np = (uint32_t)((bits + 7) / 8);
+    }
+    ctr->npass = np;
+}
+
+}  // namespace
+
+void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
+    frame_init_kernel<<<1, 1, 0, s>>>(ctr);
+}
+
+void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
+                       int frustum_cull, unsigned long long *keys, SplatRec *rec,
+                       uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s) {
+    if (scene.n == 0) return;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
+    if (scene.sh_f32)
+        preprocess_kernel<float><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, frustum_cull,
+                                                            keys, rec, keep_out, ctr);
+    else
+        preprocess_kernel<double><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, frustum_cull,
+                                                             keys, rec, keep_out, ctr);
+}
+
+void launch_depth_passes(FrameCounters *ctr, cudaStream_t s) {
+    depth_passes_kernel<<<1, 1, 0, s>>>(ctr);
+}
+
+}  // namespace gsr

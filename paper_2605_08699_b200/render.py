@@ -1,0 +1,374 @@
+"""Drop-in renderer API (mirror of splatstream/render.py) on the B200 path.
+
+``render_framebuffer`` / ``render_view`` keep the reference's signatures and
+return types (render.py:516-541); the work runs in libgsr.so (sm_100a CUDA):
+f64 projection + SH + packing, stable f64 radix depth sort, 16x16 tile
+binning and sort, per-tile front-to-back blend, u8 conversion.  Host work is
+only the reference's own pose math (camera.py) and, at scene upload, the
+view-independent cutoff radius (render.py:476-481) in numpy.
+
+Scenes are uploaded once per ActivatedPrimitives object and kept resident
+(the registry's lifecycle, model.py:311-421): the device copy is freed when
+the primitives are garbage collected or on ``evict``.  Primitives are
+immutable after ``activate`` (SPEC / model.py); call ``evict(prims)`` after
+mutating arrays in place.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import io
+import threading
+import time
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import RenderError
+from .camera import Intrinsics, camera_position, scale_intrinsics, world_to_camera
+
+# render.py:25-40, camera.py:17
+COV2D_FLOOR = 0.3
+ALPHA_MAX = 0.99
+TRANSMITTANCE_STOP = 1.0 / 255.0
+CUTOFF_SIGMA = 4.5
+TAIL_SAFETY = 32.0
+TILE = 16
+
+
+class EncodeFailure(RenderError):
+    """render.py:56-57."""
+
+
+class Framebuffer:
+    """render.py:95-100: width, height, rgb (H,W,3) f64 in [0,1],
+    accumulated_alpha (H,W) f64.  Built lazily from the device's f32 rgb/T
+    (the reference's own clip/convert, render.py:470-471); ``u8`` holds the
+    device-converted framebuffer_to_u8 result."""
+
+    def __init__(self, width, height, rgb=None, accumulated_alpha=None, *, rgb32=None,
+                 trans32=None, u8=None):
+        self.width = int(width)
+        self.height = int(height)
+        self._rgb = rgb
+        self._alpha = accumulated_alpha
+        self._rgb32 = rgb32
+        self._t32 = trans32
+        self.u8 = u8
+
+    @property
+    def rgb(self) -> np.ndarray:
+        if self._rgb is None and self._rgb32 is not None:
+            self._rgb = np.clip(self._rgb32.astype(np.float64), 0.0, 1.0)
+        return self._rgb
+
+    @rgb.setter
+    def rgb(self, value):
+        self._rgb = value
+        self.u8 = None
+
+    @property
+    def accumulated_alpha(self) -> np.ndarray:
+        if self._alpha is None and self._t32 is not None:
+            self._alpha = np.clip(1.0 - self._t32.astype(np.float64), 0.0, 1.0)
+        return self._alpha
+
+    @accumulated_alpha.setter
+    def accumulated_alpha(self, value):
+        self._alpha = value
+
+    def __repr__(self):
+        return f"Framebuffer(width={self.width}, height={self.height})"
+
+
+@dataclass
+class RenderStats:
+    """render.py:103-107 plus the device pipeline's counters and timings."""
+
+    render_ms: float = 0.0
+    splats_drawn: int = 0
+    splats_culled: int = 0
+    tile_keys: int = 0
+    device_ms: float = 0.0
+
+
+# ------------------------------------------------------------------ scenes --
+
+def cutoff_radius_sq(opacities: np.ndarray) -> np.ndarray:
+    """render.py:476-481 (view-independent; computed once at upload)."""
+    floor = 1.0 / (255.0 * TAIL_SAFETY)
+    with np.errstate(divide="ignore"):
+        rsq = 2.0 * np.log(np.maximum(opacities, floor) / floor)
+    return np.minimum(rsq, CUTOFF_SIGMA ** 2)
+
+
+class DeviceScene:
+    """An ActivatedPrimitives resident in HBM (gsr_scene)."""
+
+    def __init__(self, prims, device: int = 0):
+        lib = _lib.load()
+        means = np.ascontiguousarray(prims.means, dtype=np.float64).reshape(-1, 3)
+        n = means.shape[0]
+        scales = np.ascontiguousarray(prims.scales, dtype=np.float64).reshape(n, 3)
+        rots = np.ascontiguousarray(prims.rotations, dtype=np.float64).reshape(n, 4)
+        opac = np.ascontiguousarray(prims.opacities, dtype=np.float64).reshape(n)
+        dc = np.ascontiguousarray(prims.colors_dc, dtype=np.float64).reshape(n, 3)
+        sh = getattr(prims, "sh_coeffs", None)
+        sh = None if sh is None else np.ascontiguousarray(sh, dtype=np.float64).reshape(n, 16, 3)
+        rsq = np.ascontiguousarray(cutoff_radius_sq(opac), dtype=np.float64)
+        h = ctypes.c_void_p()
+        _lib.check(lib.gsr_scene_create(
+            ctypes.byref(h), int(device), n, _lib.ptr(means), _lib.ptr(scales), _lib.ptr(rots),
+            _lib.ptr(opac), _lib.ptr(dc), None if sh is None else _lib.ptr(sh), _lib.ptr(rsq)),
+            "gsr_scene_create")
+        self.handle = h
+        self.device = device
+        self.count = n
+        self.lib = lib
+        self._finalizer = weakref.finalize(self, lib.gsr_scene_destroy, h)
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self.lib.gsr_scene_device_bytes(self.handle))
+
+    def close(self):
+        self._finalizer()
+
+
+_scene_lock = threading.Lock()
+_scenes: dict = {}  # (id(prims), device) -> (weakref(prims), DeviceScene, signature)
+
+
+def _signature(prims):
+    arrs = [prims.means, prims.scales, prims.rotations, prims.opacities, prims.colors_dc,
+            getattr(prims, "sh_coeffs", None)]
+    return tuple((id(a), None if a is None else (a.__array_interface__["data"][0], a.shape))
+                 for a in arrs)
+
+
+def device_scene(prims, device: int = 0) -> DeviceScene:
+    """Upload-once cache keyed by the primitives object (registry record)."""
+    if isinstance(prims, DeviceScene):
+        return prims
+    key = (id(prims), device)
+    sig = _signature(prims)
+    with _scene_lock:
+        ent = _scenes.get(key)
+        if ent is not None and ent[0]() is prims and ent[2] == sig:
+            return ent[1]
+    sc = DeviceScene(prims, device)
+    with _scene_lock:
+        _scenes[key] = (weakref.ref(prims, lambda _r, k=key: _scenes.pop(k, None)), sc, sig)
+    return sc
+
+
+def evict(prims, device: int | None = None) -> None:
+    """Free the device copy of `prims` (model.py:394-408 eviction)."""
+    with _scene_lock:
+        for k in [k for k in _scenes if k[0] == id(prims) and (device is None or k[1] == device)]:
+            _scenes.pop(k)[1].close()
+
+
+_default_device = 0
+
+
+def set_device(device: int) -> None:
+    """Default CUDA device for this process (one process per GPU)."""
+    global _default_device
+    _default_device = int(device)
+
+
+# ------------------------------------------------------------------ render --
+
+def make_camera(pose, intr) -> _lib.GsrCamera:
+    """Host pose math exactly as the reference (camera.py:101-108, render.py:276)."""
+    view = world_to_camera(pose)
+    cam = _lib.GsrCamera()
+    w = np.ascontiguousarray(view.world_to_camera[:3, :], dtype=np.float64).ravel()
+    for i in range(12):
+        cam.w2c[i] = float(w[i])
+    cp = camera_position(view)
+    for i in range(3):
+        cam.campos[i] = float(cp[i])
+    cam.fx, cam.fy, cam.cx, cam.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
+    cam.width, cam.height = int(intr.width), int(intr.height)
+    return cam
+
+
+def _bg(background):
+    return (ctypes.c_float * 3)(*[float(np.float32(b)) for b in background])
+
+
+def _check_sh(sh_degree, n):
+    if sh_degree != 0 and not 0 <= sh_degree <= 3 and n > 0:
+        raise ValueError("SH degree must be in 0..3")  # render.py:131-132
+
+
+def _fill_stats(stats, st: _lib.GsrStats):
+    if stats is not None:
+        stats.splats_drawn = int(st.splats_drawn)
+        stats.splats_culled = int(st.splats_culled)
+        if hasattr(stats, "tile_keys"):
+            stats.tile_keys = int(st.tile_keys)
+        if hasattr(stats, "device_ms"):
+            stats.device_ms = float(st.ms_device)
+
+
+def render_framebuffer(prims, pose, intr, background=(0.0, 0.0, 0.0), sh_degree: int = 0,
+                       stats: RenderStats | None = None, *, device: int | None = None,
+                       frustum_culling: bool = True) -> Framebuffer:
+    """render.py:516-524 on the GPU.  Returns a Framebuffer whose f64 views are
+    the reference's clip of the device's f32 rgb/T; ``fb.u8`` is the frame."""
+    dev = _default_device if device is None else device
+    sc = device_scene(prims, dev)
+    _check_sh(sh_degree, sc.count)
+    ctx = _lib.context(dev)
+    cam = make_camera(pose, intr)
+    h, w = int(intr.height), int(intr.width)
+    u8 = np.empty((h, w, 3), dtype=np.uint8)
+    rgb32 = np.empty((h, w, 3), dtype=np.float32)
+    t32 = np.empty((h, w), dtype=np.float32)
+    st = _lib.GsrStats()
+    _lib.check(ctx.lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cam), _bg(background),
+                                  int(sh_degree), int(bool(frustum_culling)), _lib.ptr(u8),
+                                  _lib.ptr(rgb32), _lib.ptr(t32), ctypes.byref(st)),
+               "gsr_render")
+    _fill_stats(stats, st)
+    return Framebuffer(w, h, rgb32=rgb32, trans32=t32, u8=u8)
+
+
+def render_u8(prims, pose, intr, background=(0.0, 0.0, 0.0), sh_degree: int = 0,
+              stats: RenderStats | None = None, *, device: int | None = None,
+              out: np.ndarray | None = None) -> np.ndarray:
+    """Fast path: framebuffer_to_u8(render_framebuffer(...)) without the f32
+    planes; the (H,W,3) u8 frame is copied into `out` (or a pinned buffer)."""
+    dev = _default_device if device is None else device
+    sc = device_scene(prims, dev)
+    _check_sh(sh_degree, sc.count)
+    ctx = _lib.context(dev)
+    cam = make_camera(pose, intr)
+    h, w = int(intr.height), int(intr.width)
+    if out is None:
+        out = np.empty((h, w, 3), dtype=np.uint8)
+    elif out.shape != (h, w, 3) or out.dtype != np.uint8 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous (H, W, 3) uint8 array")
+    st = _lib.GsrStats()
+    _lib.check(ctx.lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cam), _bg(background),
+                                  int(sh_degree), 1, _lib.ptr(out), None, None, ctypes.byref(st)),
+               "gsr_render")
+    _fill_stats(stats, st)
+    return out
+
+
+def framebuffer_to_u8(fb) -> np.ndarray:
+    """render.py:484-485 (device-converted when available)."""
+    u8 = getattr(fb, "u8", None)
+    if u8 is not None:
+        return u8
+    return np.clip(fb.rgb * 255.0 + 0.5, 0.0, 255.0).astype(np.uint8)
+
+
+def encode_jpeg(fb, quality: int) -> bytes:
+    """render.py:488-498 (Pillow encode of the device u8 frame; JPEG on the
+    GPU is SURVEY.md 8f's next row)."""
+    from PIL import Image
+    if fb.width == 0 or fb.height == 0:
+        raise EncodeFailure("cannot encode a zero-dimension framebuffer")
+    if not 1 <= quality <= 100:
+        raise EncodeFailure(f"jpeg quality {quality} out of range 1..100")
+    img = Image.fromarray(framebuffer_to_u8(fb), mode="RGB")
+    buf = io.BytesIO()
+    img.save(buf, format="JPEG", quality=quality, subsampling=2 if quality < 90 else 0)
+    return buf.getvalue()
+
+
+def encode_png(fb) -> bytes:
+    """render.py:501-507."""
+    from PIL import Image
+    if fb.width == 0 or fb.height == 0:
+        raise EncodeFailure("cannot encode a zero-dimension framebuffer")
+    img = Image.fromarray(framebuffer_to_u8(fb), mode="RGB")
+    buf = io.BytesIO()
+    img.save(buf, format="PNG")
+    return buf.getvalue()
+
+
+def decode_image(data: bytes) -> np.ndarray:
+    """render.py:510-513."""
+    from PIL import Image
+    with Image.open(io.BytesIO(data)) as img:
+        return np.asarray(img.convert("RGB"))
+
+
+def render_view(prims, pose, base_intr, profile, background=(0.0, 0.0, 0.0),
+                sh_degree: int = 0) -> tuple[bytes, RenderStats]:
+    """render.py:527-541: rescale intrinsics to the rung, render, JPEG."""
+    stats = RenderStats()
+    start = time.perf_counter()
+    intr = scale_intrinsics(base_intr, profile.width, profile.height)
+    u8 = render_u8(prims, pose, intr, background, sh_degree, stats)
+    fb = Framebuffer(intr.width, intr.height, u8=u8)
+    payload = encode_jpeg(fb, profile.jpeg_quality)
+    stats.render_ms = (time.perf_counter() - start) * 1000.0
+    return payload, stats
+
+
+# ------------------------------------------------------------ parity hooks --
+
+def debug_preprocess(prims, pose, intr, sh_degree: int = 0, frustum_culling: bool = True,
+                     *, device: int | None = None):
+    """Stage outputs of the device pipeline for parity tests:
+    (keep (N,) bool, order (K,) int64 original indices in stable depth order,
+    packed (K, 11) f32 in depth order, GsrStats)."""
+    dev = _default_device if device is None else device
+    sc = device_scene(prims, dev)
+    ctx = _lib.context(dev)
+    cam = make_camera(pose, intr)
+    n = sc.count
+    keep = np.empty(n, dtype=np.uint8)
+    order = np.empty(max(n, 1), dtype=np.int64)
+    packed = np.empty((max(n, 1), 11), dtype=np.float32)
+    st = _lib.GsrStats()
+    _lib.check(ctx.lib.gsr_debug_preprocess(ctx.handle, sc.handle, ctypes.byref(cam),
+                                            int(sh_degree), int(bool(frustum_culling)),
+                                            _lib.ptr(keep), _lib.ptr(order), _lib.ptr(packed),
+                                            ctypes.byref(st)), "gsr_debug_preprocess")
+    k = int(st.splats_drawn)
+    return keep.astype(bool), order[:k].copy(), packed[:k].copy(), st
+
+
+def debug_tile_lists(*, device: int | None = None):
+    """Tile lists of the calling thread's last render: (tiles (D,), ranks (D,),
+    ranges (n_tiles, 2)) sorted by (tile, depth rank)."""
+    dev = _default_device if device is None else device
+    ctx = _lib.context(dev)
+    st = _lib.GsrStats()
+    _lib.check(ctx.lib.gsr_debug_tile_lists(ctx.handle, None, None, None, ctypes.byref(st)))
+    d = int(st.tile_keys)
+    tiles = np.empty(max(d, 1), dtype=np.int32)
+    ranks = np.empty(max(d, 1), dtype=np.int32)
+    # n_tiles from the last frame's size is not exposed; ranges are fetched
+    # separately by debug_tile_ranges when the caller knows W, H
+    _lib.check(ctx.lib.gsr_debug_tile_lists(ctx.handle, _lib.ptr(tiles), _lib.ptr(ranks), None,
+                                            ctypes.byref(st)))
+    return tiles[:d].copy(), ranks[:d].copy()
+
+
+def debug_tile_ranges(width: int, height: int, *, device: int | None = None) -> np.ndarray:
+    dev = _default_device if device is None else device
+    ctx = _lib.context(dev)
+    n_tiles = ((width + TILE - 1) // TILE) * ((height + TILE - 1) // TILE)
+    ranges = np.empty((n_tiles, 2), dtype=np.int32)
+    st = _lib.GsrStats()
+    _lib.check(ctx.lib.gsr_debug_tile_lists(ctx.handle, None, None, _lib.ptr(ranges),
+                                            ctypes.byref(st)))
+    return ranges
+
+
+__all__ = ["Framebuffer", "RenderStats", "RenderError", "EncodeFailure", "DeviceScene",
+           "device_scene", "evict", "set_device", "render_framebuffer", "render_u8",
+           "render_view", "framebuffer_to_u8", "encode_jpeg", "encode_png", "decode_image",
+           "cutoff_radius_sq", "make_camera", "debug_preprocess", "debug_tile_lists",
+           "debug_tile_ranges", "Intrinsics"]

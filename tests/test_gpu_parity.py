@@ -1,0 +1,328 @@
+"""GPU parity: the CUDA path through the C ABI against the reference's golden
+vectors and the CPU oracle.  Bars: culling, depth order, packed table and
+tile lists bit-exact; frames float-bit-exact (hence u8 max|delta| = 0 <= 1/255,
+PSNR capped); resample bit-exact; SSIM within 1e-4 (north_star)."""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, digest, golden_scene, load_json, sweep_scenes, textured
+
+pytestmark = pytest.mark.gpu
+
+SSIM_TOL = 1e-4  # north_star: SSIM must match within 1e-4
+
+
+@pytest.fixture(scope="module")
+def gsr():
+    import paper_2605_08699_b200 as g
+    from paper_2605_08699_b200 import _lib
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device visible to libgsr (GPU tests must run on the B200 box)")
+    return g
+
+
+def _intr(g, vals):
+    fx, fy, cx, cy, w, h = vals
+    return g.Intrinsics(fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h))
+
+
+def _pose(g, az, el, t):
+    return g.CameraPose(float(az), float(el), tuple(float(x) for x in t))
+
+
+def test_library_is_native(gsr):
+    from paper_2605_08699_b200 import _lib
+    assert _lib.load().gsr_abi_version() == 1
+    assert str(_lib.LIB_PATH).endswith("libgsr.so")
+
+
+def test_sweep_bit_exact(gsr):
+    intr = gsr.Intrinsics(fx=60.0, fy=60.0, cx=32.0, cy=32.0, width=64, height=64)
+    n = 0
+    for prims, pose, rgb32, t32, u8 in sweep_scenes():
+        fb = gsr.render_framebuffer(prims, _pose(gsr, pose[0], pose[1], pose[2]), intr)
+        assert np.array_equal(np.clip(fb._rgb32, 0, 1), rgb32)
+        assert np.array_equal(fb._t32, t32)
+        assert np.array_equal(fb.u8, u8)
+        assert np.array_equal(gsr.framebuffer_to_u8(fb), u8)
+        n += 1
+    assert n == 50
+
+
+@pytest.mark.parametrize("name", list(load_json("frames.json")))
+def test_frames_bit_exact(gsr, name):
+    from paper_2605_08699_b200.render import debug_preprocess, debug_tile_lists, debug_tile_ranges
+    case = load_json("frames.json")[name]
+    prims = golden_scene(case["scene"])
+    az, el, t = case["pose"]
+    pose = _pose(gsr, az, el, t)
+    intr = _intr(gsr, case["intr"])
+    keep, order, packed, st = debug_preprocess(prims, pose, intr, case["sh"])
+    assert int(st.splats_drawn) == case["drawn"]
+    assert int(st.splats_culled) == case["culled"]
+    assert digest(keep.astype(np.uint8)) == case["keep"]
+    # stable depth order over kept splats, as indices into the kept list
+    kept = np.flatnonzero(keep)
+    pos = np.searchsorted(kept, order)
+    assert digest(pos.astype(np.int64)) == case["order"]
+    if case["drawn"]:
+        assert digest(packed) == case["packed"]
+    stats = gsr.RenderStats()
+    fb = gsr.render_framebuffer(prims, pose, intr, tuple(case["bg"]), case["sh"], stats)
+    assert stats.splats_drawn == case["drawn"]
+    assert digest(np.clip(fb._rgb32, 0, 1)) == case["rgb32"]
+    assert digest(fb._t32) == case["t32"]
+    assert digest(fb.u8) == case["u8"]
+    tiles = load_json("tiles.json")[name]
+    tt, tr = debug_tile_lists()
+    assert tt.shape[0] == tiles["D"] == stats.tile_keys
+    assert digest(tt) == tiles["tiles"] and digest(tr) == tiles["ranks"]
+    ranges = debug_tile_ranges(intr.width, intr.height)
+    for t_id in np.unique(tt):
+        s, e = ranges[t_id]
+        assert np.all(tt[s:e] == t_id)
+
+
+def test_config1_frame_array(gsr):
+    case = load_json("frames.json")["c1_10k_sh0_256"]
+    g = np.load(GOLDEN / "frames.npz")
+    prims = golden_scene(case["scene"])
+    u8 = gsr.render_u8(prims, gsr.CameraPose(0.0, 0.0), _intr(gsr, case["intr"]))
+    assert np.array_equal(u8, g["c1_10k_sh0_256_u8"])
+
+
+def test_resample_bit_exact(gsr):
+    g = np.load(GOLDEN / "resample.npz")
+    rng = np.random.default_rng(77)
+    for i in range(int(g["n"])):
+        sh_, sw, dh, dw = (int(x) for x in g[f"seed{i}"])
+        src = rng.integers(0, 256, (sh_, sw, 3), dtype=np.uint8)
+        out = gsr.upscale_to(src, dw, dh)
+        assert out.shape == (dh, dw, 3)
+        assert bytes.fromhex(digest(out)) == g[f"digest{i}"].tobytes(), i
+    img = textured(30)
+    assert gsr.upscale_to(img, img.shape[1], img.shape[0]) is img
+
+
+def test_ssim_matches_reference(gsr):
+    ss = {k: float(v) for k, v in load_json("ssim.json").items()}
+    for i in range(6):
+        a = textured(3 + i)
+        b = np.clip(a.astype(int) + np.random.default_rng(4 + i).integers(-30, 31, a.shape),
+                    0, 255).astype(np.uint8)
+        assert abs(gsr.ssim(a, b) - ss[f"textured_{i}"]) < SSIM_TOL
+        assert abs(gsr.ssim(a, b) - ss[f"textured_{i}"]) < 1e-12
+        assert gsr.ssim(a, b) == pytest.approx(gsr.ssim(b, a), abs=1e-12)
+    assert gsr.ssim(textured(1), textured(1)) == 1.0
+    assert abs(gsr.ssim(textured(2), 255 - textured(2)) - ss["inverted"]) < 1e-12
+    r = np.random.default_rng(9)
+    a = r.integers(0, 256, (11, 22, 3), dtype=np.uint8)
+    b = r.integers(0, 256, (11, 22, 3), dtype=np.uint8)
+    assert abs(gsr.ssim(a, b) - ss["small_11x22"]) < 1e-12
+    a = r.integers(0, 256, (37, 53, 3), dtype=np.uint8)
+    c = np.clip(a.astype(int) + 7, 0, 255).astype(np.uint8)
+    assert abs(gsr.ssim(a, c) - ss["noise_37x53"]) < 1e-12
+    # float / grayscale inputs take the luma-plane entry point
+    assert abs(gsr.ssim(a.astype(np.float64), c.astype(np.float64)) - ss["noise_37x53"]) < 1e-12
+
+
+def test_ssim_errors(gsr):
+    with pytest.raises(gsr.TooSmall):
+        gsr.ssim(np.zeros((8, 8, 3)), np.zeros((8, 8, 3)))
+    with pytest.raises(gsr.DimensionMismatch):
+        gsr.ssim(np.zeros((16, 16, 3)), np.zeros((16, 17, 3)))
+
+
+def test_edge_cases(gsr, oracle):
+    from paper_2605_08699_b200.synth import ActivatedPrimitives
+    intr = gsr.Intrinsics(fx=60.0, fy=60.0, cx=32.0, cy=32.0, width=64, height=64)
+    empty = ActivatedPrimitives(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 4)),
+                                np.zeros(0), np.zeros((0, 3)), np.zeros((0, 16, 3)))
+    st = gsr.RenderStats()
+    fb = gsr.render_framebuffer(empty, gsr.CameraPose(0, 0), intr, (0.25, 0.5, 0.75), 0, st)
+    assert np.allclose(fb.rgb, [0.25, 0.5, 0.75]) and np.all(fb.accumulated_alpha == 0)
+    assert st.splats_drawn == 0 and st.splats_culled == 0
+    # behind-camera culling (test_render.py:114-120)
+    one = ActivatedPrimitives(np.array([[0, 0, -1.0]]), np.full((1, 3), 0.1),
+                              np.array([[1.0, 0, 0, 0]]), np.array([1.0]), np.ones((1, 3)),
+                              np.zeros((1, 16, 3)))
+    st = gsr.RenderStats()
+    gsr.render_framebuffer(one, gsr.CameraPose(0, 0), intr, stats=st)
+    assert st.splats_drawn == 0 and st.splats_culled == 1
+    # off-screen culled only with the flag (test_render.py:122-126)
+    off = ActivatedPrimitives(np.array([[100.0, 0, 2.0]]), np.full((1, 3), 0.01),
+                              np.array([[1.0, 0, 0, 0]]), np.array([1.0]), np.ones((1, 3)),
+                              np.zeros((1, 16, 3)))
+    st = gsr.RenderStats()
+    gsr.render_framebuffer(off, gsr.CameraPose(0, 0), intr, stats=st, frustum_culling=True)
+    assert st.splats_drawn == 0
+    gsr.render_framebuffer(off, gsr.CameraPose(0, 0), intr, stats=st, frustum_culling=False)
+    assert st.splats_drawn == 1
+    # single splat peak and falloff (test_render.py:207-215)
+    sp = ActivatedPrimitives(np.array([[0.0, 0.0, 4.0]]), np.full((1, 3), 0.2),
+                             np.array([[1.0, 0, 0, 0]]), np.array([0.95]),
+                             np.array([[0.0, 1.0, 0.0]]), np.zeros((1, 16, 3)))
+    i2 = gsr.Intrinsics(fx=60.0, fy=60.0, cx=32.5, cy=32.5, width=64, height=64)
+    green = gsr.render_framebuffer(sp, gsr.CameraPose(0, 0), i2).rgb[:, :, 1]
+    assert np.unravel_index(np.argmax(green), green.shape) == (32, 32)
+    assert np.all(np.diff(green[32, 32:]) <= 1e-12)
+    # invalid SH degree (render.py:131-132) and intrinsics
+    with pytest.raises(ValueError):
+        gsr.render_framebuffer(sp, gsr.CameraPose(0, 0), i2, sh_degree=4)
+    # odd sizes and 1x1 frames match the oracle exactly
+    prims = golden_scene((1000, 7, (0.02, 0.12), 1))
+    for (w, h) in [(1, 1), (17, 5), (97, 61), (300, 33)]:
+        it = gsr.Intrinsics(fx=0.8 * w + 1, fy=0.8 * w + 1, cx=w / 2, cy=h / 2, width=w, height=h)
+        for sh in (0, 3):
+            fb = gsr.render_framebuffer(prims, gsr.CameraPose(0.05, -0.02, (0, 0, 0.2)), it,
+                                        (0.1, 0.2, 0.3), sh)
+            rot, w2c = oracle.world_to_camera(0.05, -0.02, (0, 0, 0.2))
+            fr = oracle.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                               prims.colors_dc, prims.sh_coeffs, w2c, rot, it.fx, it.fy, it.cx,
+                               it.cy, w, h, (0.1, 0.2, 0.3), sh)
+            assert np.array_equal(fb._rgb32, fr.rgb32) and np.array_equal(fb._t32, fr.trans32)
+            assert np.array_equal(fb.u8, fr.u8)
+
+
+def test_reference_invariants(gsr):
+    from paper_2605_08699_b200.synth import ActivatedPrimitives
+    intr = gsr.Intrinsics(fx=60.0, fy=60.0, cx=32.0, cy=32.0, width=64, height=64)
+    rng = np.random.default_rng(4)
+
+    def scene(count):
+        means = np.column_stack([rng.uniform(-1.2, 1.2, count), rng.uniform(-1.2, 1.2, count),
+                                 rng.uniform(1.5, 6.0, count)])
+        q = rng.normal(size=(count, 4))
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+        return ActivatedPrimitives(means, rng.uniform(0.02, 0.5, (count, 3)), q,
+                                   rng.uniform(0.05, 1.0, count), rng.uniform(0, 1, (count, 3)),
+                                   np.zeros((count, 16, 3)))
+    # translation consistency, u8 bit-identical (test_render.py:233-246)
+    prims = scene(25)
+    offset = np.array([3.0, -2.0, 1.0])
+    moved = ActivatedPrimitives(prims.means + offset, prims.scales, prims.rotations,
+                                prims.opacities, prims.colors_dc, prims.sh_coeffs)
+    base = gsr.render_framebuffer(prims, gsr.CameraPose(0.2, 0.1, (0.0, 0.0, 0.0)), intr)
+    shifted = gsr.render_framebuffer(moved, gsr.CameraPose(0.2, 0.1, tuple(offset)), intr)
+    assert np.allclose(base.rgb, shifted.rgb, atol=1e-9)
+    assert np.array_equal(base.u8, shifted.u8)
+    # culling changes nothing visible (test_render.py:248-260)
+    prims = scene(40)
+    prims.means[::4, 0] += 50.0
+    a = gsr.render_framebuffer(prims, gsr.CameraPose(0, 0), intr, frustum_culling=True)
+    b = gsr.render_framebuffer(prims, gsr.CameraPose(0, 0), intr, frustum_culling=False)
+    assert np.max(np.abs(a.rgb - b.rgb)) <= 1.0 / 255.0
+    # bounds (test_render.py:226-231)
+    fb = gsr.render_framebuffer(scene(50), gsr.CameraPose(0, 0), intr)
+    assert np.all((fb.rgb >= 0) & (fb.rgb <= 1))
+    assert np.all((fb.accumulated_alpha >= 0) & (fb.accumulated_alpha <= 1))
+
+
+def _oracle_frame(oracle, prims, pose, intr, sh, bg=(0.0, 0.0, 0.0)):
+    rot, w2c = oracle.world_to_camera(pose.azimuth, pose.elevation, pose.translation)
+    return oracle.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                         prims.colors_dc, prims.sh_coeffs, w2c, rot, intr.fx, intr.fy, intr.cx,
+                         intr.cy, intr.width, intr.height, bg, sh)
+
+
+def test_config2_500k_720p_trace_vs_oracle(gsr, oracle):
+    """Config 2 (500k, SH3, 1280x720, pose trace): frames, order, tile lists exact."""
+    from paper_2605_08699_b200.render import debug_tile_lists
+    from paper_2605_08699_b200.synth import base_intrinsics_1080p, pose_trace, synthetic_scene
+    prims = synthetic_scene(500_000, seed=7, sh_degree=3)
+    intr = gsr.scale_intrinsics(base_intrinsics_1080p(), 1280, 720)
+    for tp in pose_trace(300, seed=2)[::100]:
+        pose = gsr.pose_from_degrees(tp.azimuth_deg, tp.elevation_deg, tp.translation)
+        st = gsr.RenderStats()
+        fb = gsr.render_framebuffer(prims, pose, intr, sh_degree=3, stats=st)
+        fr = _oracle_frame(oracle, prims, pose, intr, 3)
+        assert st.splats_drawn == fr.splats_drawn
+        assert np.array_equal(fb._rgb32, fr.rgb32)
+        assert np.array_equal(fb._t32, fr.trans32)
+        assert np.array_equal(fb.u8, fr.u8)
+        tt, tr = debug_tile_lists()
+        ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
+        assert np.array_equal(tt, ot) and np.array_equal(tr, orr)
+
+
+def test_config3_3m_1080p_vs_oracle(gsr, oracle):
+    """Config 3 at full size: 3M Gaussians, SH3, 1920x1080, exact vs the oracle."""
+    from paper_2605_08699_b200.render import debug_preprocess, debug_tile_lists
+    from paper_2605_08699_b200.synth import base_intrinsics_1080p, synthetic_scene
+    prims = synthetic_scene(3_000_000, seed=7, sh_degree=3)
+    intr = base_intrinsics_1080p()
+    pose = gsr.CameraPose(0.02, -0.01, (0.05, 0.0, 0.1))
+    keep, order, packed, st = debug_preprocess(prims, pose, intr, 3)
+    fr = _oracle_frame(oracle, prims, pose, intr, 3)
+    assert np.array_equal(keep, fr.keep)
+    assert np.array_equal(order, fr.kept[fr.order])
+    assert np.array_equal(packed, fr.packed)
+    fb = gsr.render_framebuffer(prims, pose, intr, sh_degree=3)
+    assert np.array_equal(fb.u8, fr.u8)
+    assert np.array_equal(fb._rgb32, fr.rgb32)
+    tt, tr = debug_tile_lists()
+    ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
+    assert tt.shape == ot.shape
+    assert np.array_equal(tt, ot) and np.array_equal(tr, orr)
+    # size-independent properties: depth order is sorted, tile keys sorted
+    z = fr.depths
+    assert np.all(np.diff(z) >= 0)
+    assert np.all(np.diff(tt) >= 0)
+
+
+def test_ladder_ssim_vs_oracle(gsr, oracle):
+    from paper_2605_08699_b200.synth import synthetic_scene
+    prims = synthetic_scene(20_000, seed=5, sh_degree=3)
+    base = gsr.Intrinsics(fx=554.2562584220407, fy=554.2562584220407, cx=320.0, cy=180.0,
+                          width=640, height=360)
+    pose = gsr.CameraPose(0.0, 0.0)
+    rungs = [(480, 270), (320, 180), (160, 90)]
+    scores, st = gsr.ladder_ssim(prims, pose, base, rungs, sh_degree=3)
+    gt = _oracle_frame(oracle, prims, pose, base, 3).u8
+    ref = []
+    for w, h in rungs:
+        lo = _oracle_frame(oracle, prims, pose, gsr.scale_intrinsics(base, w, h), 3).u8
+        ref.append(oracle.ssim(oracle.resample_bilinear(lo, base.width, base.height), gt))
+    assert np.allclose(scores, ref, atol=SSIM_TOL, rtol=0)
+    assert all(a > b for a, b in zip(scores, scores[1:]))
+
+
+def test_render_view_matches_reference_path(gsr):
+    from paper_2605_08699_b200.synth import synthetic_scene
+    from PIL import Image  # noqa: F401
+    prims = synthetic_scene(2000, seed=3, sh_degree=0)
+    base = gsr.Intrinsics(fx=1108.5, fy=1108.5, cx=640.0, cy=360.0, width=1280, height=720)
+
+    class Profile:
+        width, height, jpeg_quality = 320, 180, 10
+    payload, stats = gsr.render_view(prims, gsr.CameraPose(0, 0), base, Profile())
+    img = gsr.decode_image(payload)
+    assert img.shape == (180, 320, 3)
+    assert stats.splats_drawn + stats.splats_culled == prims.count
+    assert stats.render_ms > 0
+    again, _ = gsr.render_view(prims, gsr.CameraPose(0, 0), base, Profile())
+    assert again == payload
+
+
+def test_concurrent_threads_deterministic(gsr):
+    from paper_2605_08699_b200.synth import synthetic_scene
+    prims = synthetic_scene(50_000, seed=11, sh_degree=3)
+    intr = gsr.Intrinsics(fx=400.0, fy=400.0, cx=256.0, cy=144.0, width=512, height=288)
+    poses = [gsr.CameraPose(0.01 * i, -0.005 * i, (0.0, 0.0, 0.02 * i)) for i in range(8)]
+    ref = [gsr.render_u8(prims, p, intr, sh_degree=3) for p in poses]
+    out = [None] * 16
+
+    def work(k):
+        out[k] = gsr.render_u8(prims, poses[k % 8], intr, sh_degree=3)
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(16)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k in range(16):
+        assert np.array_equal(out[k], ref[k % 8])
