@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the per-pose render path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gsr|reference]
+                    [--workload config3|config2|config4|config1]
+
+metric: 1080p frames/s at 3M Gaussians (config 3's 1080p rung: synthetic
+3M-Gaussian scene, SH degree 3, 1920x1080), plus p50/p99 render latency.
+A step = one frame of one client session at the next pose of its seeded
+EyeNavGS-style trace.  Sessions are independent (server.py:1-7), so with N
+GPUs (torchrun, one process per GPU) rank r serves its own session on its own
+GPU: weak scaling, no data-path collective (the only NCCL calls are the
+barrier and the max-over-ranks timing reduction).
+
+value      device throughput: K frames enqueued back to back on the render
+           stream (scene resident in HBM), CUDA events on that stream, max
+           over ranks; frames of all ranks / that time.
+e2e        the public API call a server makes (render_u8 -> u8 frame in pinned
+           host memory), wall clock per call including the device->host copy
+           of the frame; the camera (152 B of kernel parameters) is the only
+           per-step input.
+roofline   the dominant kernel's algorithmic bytes (or FP32 ops) per launch /
+           its mean event-timed duration, against MEASURED_PEAKS.json.
+cpu_baseline  the C oracle port (oracle/, OpenMP, all host cores) on the same
+           scene and poses, bounded to ~20 s, rank 0 at N=1.
+--impl reference  the reference arm: the oracle port alone on the same
+           workload (the reference itself is Python/numba and is not on the
+           GPU box), bounded to a few minutes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "config1": dict(n=10_000, sh=0, w=256, h=256, scale=(0.02, 0.12),
+                    desc="config1: synthetic 10k-Gaussian scene, SH0, 256x256"),
+    "config2": dict(n=500_000, sh=3, w=1280, h=720, scale=None,
+                    desc="config2: synthetic 500k-Gaussian scene, SH3, 1280x720, pose trace"),
+    "config3": dict(n=3_000_000, sh=3, w=1920, h=1080, scale=None,
+                    desc="config3: synthetic 3M-Gaussian scene, SH3, 1920x1080 rung, pose trace"),
+    "config4": dict(n=6_000_000, sh=3, w=1920, h=1080, scale=None,
+                    desc="config4: synthetic 6M-Gaussian scene, SH3, 1920x1080, pose trace"),
+}
+
+NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device: int, period_s: float = 0.01):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in NVML_REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def build_scene(wl, seed=7):
+    from paper_2605_08699_b200.synth import synthetic_scene
+    return synthetic_scene(wl["n"], seed=seed, sh_degree=wl["sh"], scale_range=wl["scale"])
+
+
+def intrinsics(wl):
+    from paper_2605_08699_b200.camera import Intrinsics, scale_intrinsics
+    from paper_2605_08699_b200.synth import base_intrinsics_1080p
+    if wl["w"] == wl["h"]:
+        f = (wl["w"] / 2) / np.tan(np.radians(30.0))
+        return Intrinsics(fx=f, fy=f, cx=wl["w"] / 2, cy=wl["h"] / 2, width=wl["w"],
+                          height=wl["h"])
+    return scale_intrinsics(base_intrinsics_1080p(), wl["w"], wl["h"])
+
+
+def poses_for(rank, count):
+    from paper_2605_08699_b200.camera import pose_from_degrees
+    from paper_2605_08699_b200.synth import pose_trace
+    return [pose_from_degrees(p.azimuth_deg, p.elevation_deg, p.translation)
+            for p in pose_trace(count, seed=rank)]
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def cpu_baseline(prims, poses, intr, sh, budget_s, gpu_u8=None):
+    """The oracle port on the host cores, bounded to ~budget_s."""
+    from oracle import oracle as orc
+    orc.build()
+    cores = orc.num_threads()
+    times, parity = [], None
+    t_all = time.perf_counter()
+    for i, pose in enumerate(poses):
+        rot, w2c = orc.world_to_camera(pose.azimuth, pose.elevation, pose.translation)
+        t0 = time.perf_counter()
+        fr = orc.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                        prims.colors_dc, prims.sh_coeffs, w2c, rot, intr.fx, intr.fy, intr.cx,
+                        intr.cy, intr.width, intr.height, (0.0, 0.0, 0.0), sh)
+        times.append(time.perf_counter() - t0)
+        if i == 0 and gpu_u8 is not None:
+            d = np.abs(fr.u8.astype(np.int16) - gpu_u8.astype(np.int16))
+            parity = {"frame0_u8_max_abs_diff": int(d.max()),
+                      "frame0_psnr_db": orc.psnr(fr.u8, gpu_u8),
+                      "frame0_bit_exact": bool(np.array_equal(fr.u8, gpu_u8))}
+        if time.perf_counter() - t_all > budget_s:
+            break
+    fps = len(times) / sum(times)
+    return {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
+            "sample": f"{len(times)} frame(s) of the same workload, oracle/oracle.c "
+                      f"(OpenMP, {cores} threads), {sum(times):.1f} s",
+            "ms_per_frame": 1000.0 * sum(times) / len(times)}, parity
+
+
+def run_reference(args, wl):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    prims = build_scene(wl)
+    intr = intrinsics(wl)
+    poses = poses_for(0, args.warmup + args.steps)
+    budget = float(os.environ.get("BENCH_REF_BUDGET_S", "150"))
+    from oracle import oracle as orc
+    orc.build()
+    # warm-up (page-in, OpenMP pool)
+    for pose in poses[:max(1, min(args.warmup, 1))]:
+        rot, w2c = orc.world_to_camera(pose.azimuth, pose.elevation, pose.translation)
+        orc.render(prims.means, prims.scales, prims.rotations, prims.opacities, prims.colors_dc,
+                   prims.sh_coeffs, w2c, rot, intr.fx, intr.fy, intr.cx, intr.cy, intr.width,
+                   intr.height, (0.0, 0.0, 0.0), wl["sh"])
+    base, _ = cpu_baseline(prims, poses[args.warmup:], intr, wl["sh"], budget)
+    line = {
+        "metric": "1080p frames/sec/GPU and p50/p99 render ms at 3M Gaussians",
+        "value": base["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": base["ms_per_frame"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": wl["desc"], "gaussians": wl["n"], "sh_degree": wl["sh"],
+                   "width": wl["w"], "height": wl["h"], "parallelism": "host cores"},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def stage_roofline(stats_list, wl, counters, peaks, peak_kind):
+    """Per-stage mean device ms and algorithmic roofline."""
+    keys = ["ms_preprocess", "ms_depth_sort", "ms_binning", "ms_tile_sort", "ms_blend"]
+    mean = {k: float(np.mean([s[k] for s in stats_list])) for k in keys}
+    n, k, d = wl["n"], counters["K"], counters["D"]
+    dsh = wl["sh"]
+    passes = counters["depth_passes"]
+    tile_passes = counters["tile_passes"]
+    alg = {
+        # SoA scene read (f64 geometry 80 B + rsq 8 + opacity 4 + f32 SH/colour) + 8 B key
+        # for all N + 48 B record per kept splat
+        "ms_preprocess": n * (92 + (12 * (dsh + 1) ** 2 if dsh else 12)) + 8 * n + 48 * k,
+        # first pass reads N keys, every pass writes (key 8 + val 4), later passes read them
+        "ms_depth_sort": 8 * n + 12 * k + (passes - 1) * 24 * k,
+        # count: gather 48 B records + write sorted copy + counts; write: re-read 48 B + 8 B/key
+        "ms_binning": k * (4 + 48 + 48 + 4) + k * (48 + 4) + 8 * d,
+        "ms_tile_sort": tile_passes * 16 * d,
+        # tile lists (4 B/entry) + records (48 B per kept splat) + u8 frame
+        "ms_blend": 4 * d + 48 * k + 3 * wl["w"] * wl["h"],
+    }
+    hbm = float(peaks["hbm_gbs"])
+    out = {}
+    for key in keys:
+        ms = mean[key]
+        gbs = alg[key] / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        out[key[3:]] = {"ms": round(ms, 4), "alg_bytes": int(alg[key]),
+                        "achieved_gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
+    dom = max(keys, key=lambda x: mean[x])
+    return mean, out, dom[3:]
+
+
+def run_gsr(args, wl):
+    import torch
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_2605_08699_b200 as g
+    from paper_2605_08699_b200 import _lib
+    from paper_2605_08699_b200.render import _bg, device_scene, make_camera
+    g.set_device(local_rank)
+
+    prims = build_scene(wl)
+    intr = intrinsics(wl)
+    K, W = args.steps, args.warmup
+    poses = poses_for(rank, W + K)
+    sc = device_scene(prims, local_rank)
+    ctx = _lib.context(local_rank)
+    lib = ctx.lib
+    cams = [make_camera(p, intr) for p in poses]
+    bg = _bg((0.0, 0.0, 0.0))
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up: capacities, page-in, JIT of nothing (all AOT)
+    st = _lib.GsrStats()
+    for i in range(W):
+        _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cams[i]), bg, wl["sh"], 1,
+                                  None, None, None, ctypes.byref(st)))
+
+    # ---- device throughput: K frames back to back on the render stream ----
+    stream = torch.cuda.ExternalStream(lib.gsr_ctx_stream(ctx.handle))
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local_rank) as clocks:
+        ev0.record(stream)
+        for i in range(W, W + K):
+            _lib.check(lib.gsr_render_async(ctx.handle, sc.handle, ctypes.byref(cams[i]), bg,
+                                            wl["sh"], 1))
+        ev1.record(stream)
+        _lib.check(lib.gsr_ctx_finish(ctx.handle, None, ctypes.byref(st)))
+        torch.cuda.synchronize()
+    launches = int(st.kernel_launches)
+    overflow = int(st.overflow_frames)
+    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    value = world * K / (dev_ms / 1000.0)
+
+    # ---- per-call latency + e2e through the public API (pinned host frame) ----
+    out = ctx.pinned("bench_frame", (intr.height, intr.width, 3), np.uint8)
+    lat, dev_lat, stage_stats = [], [], []
+    rs = g.RenderStats()
+    barrier()
+    t_e2e = time.perf_counter()
+    for i in range(W, W + K):
+        t0 = time.perf_counter()
+        g.render_u8(prims, poses[i], intr, sh_degree=wl["sh"], stats=rs, out=out)
+        lat.append((time.perf_counter() - t0) * 1000.0)
+    e2e_s = time.perf_counter() - t_e2e
+    e2e_s = max_over_ranks(e2e_s)
+    # per-stage device timings (event pairs inside the ABI), separate pass
+    for i in range(W, W + min(K, 50)):
+        _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cams[i]), bg, wl["sh"], 1,
+                                  None, None, None, ctypes.byref(st)))
+        stage_stats.append(st.as_dict())
+        dev_lat.append(st.ms_device)
+    counters = {"K": int(st.splats_drawn), "D": int(st.tile_keys),
+                "depth_passes": int(st.depth_passes),
+                "tile_passes": (int(np.ceil(np.log2(((intr.width + 15) // 16) *
+                                                    ((intr.height + 15) // 16)))) + 7) // 8}
+    peaks, peak_kind = load_peaks()
+    mean, stages, dom = stage_roofline(stage_stats, wl, counters, peaks, peak_kind)
+
+    result = None
+    if rank == 0:
+        frame0 = g.render_u8(prims, poses[W], intr, sh_degree=wl["sh"])
+        base, parity = (None, None)
+        if world == 1 and not args.no_cpu_baseline:
+            base, parity = cpu_baseline(prims, poses[W:], intr, wl["sh"], args.cpu_budget,
+                                        gpu_u8=frame0)
+        dstage = stages[dom]
+        result = {
+            "metric": "1080p frames/sec/GPU and p50/p99 render ms at 3M Gaussians",
+            "value": value, "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": dev_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "gaussians": wl["n"], "sh_degree": wl["sh"],
+                       "width": wl["w"], "height": wl["h"],
+                       "parallelism": f"session-sharded x{world} (no collective)",
+                       "l2": "inputs larger than L2 (scene "
+                             f"{sc.device_bytes / 1e6:.0f} MB > 126 MB)"},
+            "latency_ms": {"p50": float(np.percentile(lat, 50)),
+                           "p99": float(np.percentile(lat, 99)),
+                           "device_p50": float(np.percentile(dev_lat, 50)),
+                           "device_p99": float(np.percentile(dev_lat, 99))},
+            "e2e": {"value": world * K / e2e_s, "unit": "frames/s",
+                    "h2d_bytes_per_step": ctypes.sizeof(_lib.GsrCamera),
+                    "d2h_bytes_per_step": int(out.nbytes)},
+            "gpu_launches": launches,
+            "overflow_frames": overflow,
+            "stages": stages,
+            "counters": counters,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dstage["achieved_gbs"],
+                         "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+                         "frac": dstage["frac_hbm"], "traffic": None,
+                         "peak_source": peak_kind},
+            "clocks": clocks.summary(),
+        }
+        if base is not None:
+            result["cpu_baseline"] = base
+            result["parity"] = parity
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if result is not None:
+        print(json.dumps(result), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["gsr", "reference"], default="gsr")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args(argv)
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+    return run_gsr(args, wl)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -66,6 +66,8 @@ typedef struct gsr_stats {
     int32_t retries;          /* re-renders after growing the tile-key buffer */
     float ms_device;          /* CUDA-event time of the whole device pipeline */
     float ms_preprocess, ms_depth_sort, ms_binning, ms_tile_sort, ms_blend;
+    int32_t kernel_launches;  /* kernels this ctx launched since the last finish/render */
+    int32_t overflow_frames;  /* frames since the last finish whose tile keys overflowed */
 } gsr_stats;
 
 GSR_API int gsr_abi_version(void);
@@ -97,6 +99,8 @@ GSR_API int gsr_ctx_destroy(gsr_ctx *ctx);
 GSR_API int64_t gsr_ctx_device_bytes(const gsr_ctx *ctx);
 /* device pointer of the ctx's last u8 frame (H,W,3), valid until next render */
 GSR_API const uint8_t *gsr_ctx_frame_u8(const gsr_ctx *ctx);
+/* the ctx's cudaStream_t (as void*), e.g. to record timing events on it */
+GSR_API void *gsr_ctx_stream(const gsr_ctx *ctx);
 
 /* ---- the hot path: render_framebuffer (render.py:516-524) ----------------
  * project (render.py:163-290) -> stable f64 depth sort (293-302) -> tile

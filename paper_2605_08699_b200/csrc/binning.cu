@@ -107,10 +107,11 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(
 __global__ void __launch_bounds__(kBinThreads) bin_write_kernel(
     const SplatRec *__restrict__ srec, const uint32_t *__restrict__ offsets, int64_t n_cap,
     const FrameCounters *ctr, int width, int height, uint32_t *__restrict__ tile_keys,
-    uint32_t *__restrict__ tile_vals, int64_t cap_d) {
+    uint32_t *__restrict__ tile_vals, int64_t cap_d, uint32_t *overflow_sticky) {
     const int lane = lane_id();
     const int64_t warps = (int64_t)gridDim.x * (kBinThreads / 32);
     const int64_t k = ctr->K;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (int64_t)ctr->D > cap_d) atomicAdd(overflow_sticky, 1u);
     const int tiles_x = (width + kTile - 1) / kTile;
     for (int64_t r = (int64_t)blockIdx.x * (kBinThreads / 32) + (threadIdx.x >> 5); r < k;
          r += warps) {
@@ -176,13 +177,14 @@ void launch_bin_count(const uint32_t *vals_even, const uint32_t *vals_odd, const
 
 void launch_bin_write(const SplatRec *srec, const uint32_t *offsets, int64_t n_cap,
                       const FrameCounters *ctr, int width, int height, uint32_t *tile_keys,
-                      uint32_t *tile_vals, int64_t cap_d, cudaStream_t s) {
+                      uint32_t *tile_vals, int64_t cap_d, uint32_t *overflow_sticky,
+                      cudaStream_t s) {
     if (n_cap <= 0) return;
     int64_t want = (n_cap + 7) / 8;
     int64_t blocks = sm_count() * 8;
     if (want < blocks) blocks = want;
-    bin_write_kernel<<<(unsigned)blocks, kBinThreads, 0, s>>>(srec, offsets, n_cap, ctr, width,
-                                                              height, tile_keys, tile_vals, cap_d);
+    bin_write_kernel<<<(unsigned)blocks, kBinThreads, 0, s>>>(
+        srec, offsets, n_cap, ctr, width, height, tile_keys, tile_vals, cap_d, overflow_sticky);
 }
 
 void launch_tile_ranges(const uint32_t *tile_keys, const FrameCounters *ctr, int64_t cap_d,

@@ -91,8 +91,9 @@ struct gsr_ctx {
     DevBuf tkeys[2], tvals[2];
     DevBuf ranges;
     DevBuf frame_u8, frame_rgb, frame_t;
-    DevBuf ctr;
+    DevBuf ctr, sticky;
     FrameCounters *hctr = nullptr;
+    int64_t launches = 0;  // kernels enqueued since the last finish/render
     cudaEvent_t ev[8] = {};
     // ladder / resample / ssim scratch
     DevBuf base_u8, up_u8, tmp_u8, src_u8, dst_u8, coefs, ssim_part, ssim_misc, ssim_w;
@@ -255,7 +256,8 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
                          c->srec.as<SplatRec>(), c->counts.as<uint32_t>(), n, ctr, W, H, s);
         launch_scan_exclusive(c->counts.as<uint32_t>(), c->offsets.as<uint32_t>(), n, &ctr->D, ws, s);
         launch_bin_write(c->srec.as<SplatRec>(), c->offsets.as<uint32_t>(), n, ctr, W, H,
-                         c->tkeys[0].as<uint32_t>(), c->tvals[0].as<uint32_t>(), c->cap_d, s);
+                         c->tkeys[0].as<uint32_t>(), c->tvals[0].as<uint32_t>(), c->cap_d,
+                         c->sticky.as<uint32_t>(), s);
     }
     cudaEventRecord(c->ev[3], s);
     const int tp = tile_sort_passes(c->ntiles);
@@ -283,6 +285,10 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     cudaEventRecord(c->ev[5], s);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s);
     GSR_CUDA_OK(cudaGetLastError());
+    // kernels of this frame: init + blend, and for a non-empty scene
+    // preprocess + pass count + 8 depth passes x (upsweep + 3 scan + downsweep)
+    // + bin count + 3 scan + bin write + tp tile passes x 5 + ranges
+    c->launches += 2 + (n > 0 ? 2 + 8 * 5 + 1 + 3 + 1 + 5 * tp + 1 : 0);
     c->saved.scene = sc;
     c->saved.cam = *cam;
     for (int i = 0; i < 3; i++) c->saved.bg[i] = bg[i];
@@ -334,6 +340,12 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     st->ms_binning = t[3];
     st->ms_tile_sort = t[4];
     st->ms_blend = t[5];
+    st->kernel_launches = (int32_t)c->launches;
+    c->launches = 0;
+    uint32_t ov = 0;
+    if (cudaMemcpy(&ov, c->sticky.p, sizeof(ov), cudaMemcpyDeviceToHost) == cudaSuccess && ov)
+        cudaMemset(c->sticky.p, 0, sizeof(ov));
+    st->overflow_frames = (int32_t)ov;
 }
 
 // ---- Pillow BILINEAR coefficients (Resample.c precompute_coeffs +
@@ -588,6 +600,9 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
         return rc;
     }
     int rc = ensure(c->ctr, sizeof(FrameCounters));
+    if (!rc) rc = ensure(c->sticky, sizeof(uint32_t));
+    if (!rc && cudaMemset(c->sticky.p, 0, sizeof(uint32_t)) != cudaSuccess)
+        rc = fail(GSR_E_CUDA, "memset");
     if (!rc) rc = ensure(c->ssim_misc, 64);
     if (!rc) rc = ensure(c->ssim_w, sizeof(double) * 11);
     if (rc) {
@@ -630,6 +645,8 @@ int64_t gsr_ctx_device_bytes(const gsr_ctx *ctx) { return ctx ? ctx->bytes() : 0
 const uint8_t *gsr_ctx_frame_u8(const gsr_ctx *ctx) {
     return ctx ? ctx->frame_u8.as<uint8_t>() : nullptr;
 }
+
+void *gsr_ctx_stream(const gsr_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
 
 int gsr_render_async(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
                      const float background[3], int sh_degree, int frustum_cull) {

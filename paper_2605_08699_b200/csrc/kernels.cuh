@@ -82,7 +82,8 @@ void launch_bin_count(const uint32_t *vals_even, const uint32_t *vals_odd,
                       cudaStream_t s);
 void launch_bin_write(const SplatRec *srec, const uint32_t *offsets, int64_t n_cap,
                       const FrameCounters *ctr, int width, int height, uint32_t *tile_keys,
-                      uint32_t *tile_vals, int64_t cap_d, cudaStream_t s);
+                      uint32_t *tile_vals, int64_t cap_d, uint32_t *overflow_sticky,
+                      cudaStream_t s);
 void launch_tile_ranges(const uint32_t *tile_keys, const FrameCounters *ctr, int64_t cap_d,
                         uint2 *ranges, int n_tiles, cudaStream_t s);
 
