@@ -86,7 +86,8 @@ struct gsr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int64_t cap_n = 0, cap_d = 0;
-    DevBuf keys[2], vals[2], rec, srec, counts, offsets, keep;
+    DevBuf keys[2], vals[2], rec, srec, bin_status, keep;
+    int sms = 148;
     DevBuf hist, partials;
     DevBuf tkeys[2], tvals[2];
     DevBuf ranges;
@@ -106,8 +107,8 @@ struct gsr_ctx {
     int retries = 0;
     int64_t bytes() const {
         int64_t s = 0;
-        const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &rec, &srec, &counts,
-                               &offsets, &keep, &hist, &partials, &tkeys[0], &tkeys[1],
+        const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &rec, &srec, &bin_status,
+                               &keep, &hist, &partials, &tkeys[0], &tkeys[1],
                                &tvals[0], &tvals[1], &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w};
@@ -185,8 +186,8 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
         }
         if ((rc = ensure(c->rec, sizeof(SplatRec) * cap))) return rc;
         if ((rc = ensure(c->srec, sizeof(SplatRec) * cap))) return rc;
-        if ((rc = ensure(c->counts, sizeof(uint32_t) * cap))) return rc;
-        if ((rc = ensure(c->offsets, sizeof(uint32_t) * cap))) return rc;
+        if ((rc = ensure(c->bin_status, sizeof(unsigned long long) * bin_status_words(cap))))
+            return rc;
         c->cap_n = cap;
     }
     if (want_keep && (rc = ensure(c->keep, (size_t)c->cap_n))) return rc;
@@ -252,12 +253,10 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     }
     cudaEventRecord(c->ev[2], s);
     if (n > 0) {
-        launch_bin_count(c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), c->rec.as<SplatRec>(),
-                         c->srec.as<SplatRec>(), c->counts.as<uint32_t>(), n, ctr, W, H, s);
-        launch_scan_exclusive(c->counts.as<uint32_t>(), c->offsets.as<uint32_t>(), n, &ctr->D, ws, s);
-        launch_bin_write(c->srec.as<SplatRec>(), c->offsets.as<uint32_t>(), n, ctr, W, H,
-                         c->tkeys[0].as<uint32_t>(), c->tvals[0].as<uint32_t>(), c->cap_d,
-                         c->sticky.as<uint32_t>(), s);
+        launch_bin(c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), c->rec.as<SplatRec>(),
+                   c->srec.as<SplatRec>(), n, ctr, W, H, c->tkeys[0].as<uint32_t>(),
+                   c->tvals[0].as<uint32_t>(), c->cap_d, c->bin_status.as<unsigned long long>(),
+                   c->sticky.as<uint32_t>(), s);
     }
     cudaEventRecord(c->ev[3], s);
     const int tp = tile_sort_passes(c->ntiles);
@@ -273,7 +272,8 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     c->final_tkeys = c->tkeys[tp & 1].as<uint32_t>();
     c->final_tvals = c->tvals[tp & 1].as<uint32_t>();
     if (n > 0) {
-        launch_tile_ranges(c->final_tkeys, ctr, c->cap_d, c->ranges.as<uint2>(), c->ntiles, s);
+        launch_tile_ranges(c->final_tkeys, ctr, c->cap_d, c->ranges.as<uint2>(), c->ntiles, c->sms,
+                           s);
     } else {
         cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
     }
@@ -288,7 +288,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     // kernels of this frame: init + blend, and for a non-empty scene
     // preprocess + pass count + 8 depth passes x (upsweep + 3 scan + downsweep)
     // + bin count + 3 scan + bin write + tp tile passes x 5 + ranges
-    c->launches += 2 + (n > 0 ? 2 + 8 * 5 + 1 + 3 + 1 + 5 * tp + 1 : 0);
+    c->launches += 2 + (n > 0 ? 2 + 8 * 5 + 1 + 5 * tp + 1 : 0);
     c->saved.scene = sc;
     c->saved.cam = *cam;
     for (int i = 0; i < 3; i++) c->saved.bg[i] = bg[i];
@@ -590,6 +590,7 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     if (!c) return fail(GSR_E_OOM, "host allocation failed");
     c->device = device;
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = radix_init_attributes();
     for (int i = 0; i < 8 && e == cudaSuccess; i++) e = cudaEventCreate(&c->ev[i]);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters));

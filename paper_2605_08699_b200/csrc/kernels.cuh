@@ -16,6 +16,7 @@ struct FrameCounters {
     uint32_t pad0;
     unsigned long long kmin;    // min / max kept depth key (f64 bits)
     unsigned long long kmax;
+    unsigned long long bin_ticket;  // block tickets of the binning kernel
 };
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.
@@ -75,17 +76,14 @@ void launch_radix_pass(const K *kin, const uint32_t *vin, K *kout, uint32_t *vou
                        int pass_index, bool drop_sentinel, uint32_t *hist,
                        const ScanWorkspace &ws, cudaStream_t s);
 
-// binning.cu
-void launch_bin_count(const uint32_t *vals_even, const uint32_t *vals_odd,
-                      const SplatRec *rec, SplatRec *srec, uint32_t *counts,
-                      int64_t n_cap, const FrameCounters *ctr, int width, int height,
-                      cudaStream_t s);
-void launch_bin_write(const SplatRec *srec, const uint32_t *offsets, int64_t n_cap,
-                      const FrameCounters *ctr, int width, int height, uint32_t *tile_keys,
-                      uint32_t *tile_vals, int64_t cap_d, uint32_t *overflow_sticky,
-                      cudaStream_t s);
+// binning.cu: fused gather + tile-list generation (one kernel, look-back scan)
+int64_t bin_status_words(int64_t n_cap);
+void launch_bin(const uint32_t *vals_even, const uint32_t *vals_odd, const SplatRec *rec,
+                SplatRec *srec, int64_t n_cap, FrameCounters *ctr, int width, int height,
+                uint32_t *tile_keys, uint32_t *tile_vals, int64_t cap_d,
+                unsigned long long *status, uint32_t *overflow_sticky, cudaStream_t s);
 void launch_tile_ranges(const uint32_t *tile_keys, const FrameCounters *ctr, int64_t cap_d,
-                        uint2 *ranges, int n_tiles, cudaStream_t s);
+                        uint2 *ranges, int n_tiles, int sms, cudaStream_t s);
 
 // blend.cu
 struct BlendOut {

@@ -64,6 +64,7 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->pad0 = 0;
     ctr->kmin = ~0ull;
     ctr->kmax = 0ull;
+    ctr->bin_ticket = 0ull;
 }
 
 template <typename ShT>
