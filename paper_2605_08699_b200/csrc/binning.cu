@@ -1,23 +1,33 @@
-// binning.cu -- K4/K5: tile duplication under the tile-list contract and
-// per-tile range identification.
+// binning.cu -- K4/K5: tile lists under the tile-list contract, sort-free.
 //
 // The reference composites per image row (render.py:357-421) and has no
 // tiles; the contract (restated in oracle/oracle.c
 // orc_tile_keys) lists depth-rank s in tile (tx, ty) iff tx lies in
 // [floor(min x0 / 16), floor((max x1 - 1) / 16)], min/max over the rows of
 // tile row ty whose exact reference interval (render.py:384-397, x0 clamped
-// at 0) is non-empty.  Rows are computed with the reference's f32 op order.
+// at 0) is non-empty.  Rows use the reference's f32 op order.  Each tile's
+// list holds its depth ranks in increasing order (global stable depth order).
 //
-// One fused kernel, one pass over the depth-sorted splats:
-//   * a block takes 256 consecutive depth ranks (in ticket order), gathers
-//     their records into the depth-sorted table srec (sort_splats' gathers,
-//     render.py:295-302) and computes each splat's row range;
-//   * the block expands its (splat, tile row) pairs in shared memory (block
-//     scan + binary search), one thread per pair computes the <= 16 exact row
-//     intervals of that tile row once and reduces them to (tx0, count);
-//   * a decoupled look-back over blocks turns the block's key count into its
-//     global offset; keys (tile id) and values (depth rank) are written in
-//     rank-major order, ready for the stable tile sort.
+// Every splat covers a run of tile rows and, in each, one contiguous run of
+// tile columns.  So the lists are built from (splat, tile row) pairs:
+//  1a gather   block of 256 depth ranks: gathers the depth-sorted records
+//              (sort_splats' column gathers, render.py:295-302) and counts
+//              its pairs per tile row (row range only, no interval math).
+//  1b row_scan exclusive scan of those counts, tile-row major: each (row,
+//              block) gets its output slot, each row its pair range.
+//  1c pairs    same blocks: one thread per pair computes the pair's exact
+//              tile-column span (tx0, count) -- the only interval arithmetic
+//              -- and stores (rank, tx0 | count << 16) at its slot: pairs end
+//              up grouped by tile row, in rank order within a row.
+//  2a segments each row's pairs are cut into segments of <= 1024 pairs.
+//  2b seg_count one warp per segment: keys per tile column (difference array).
+//  2c scans    per tile: prefix over the row's segments; tile starts, ranges, D.
+//  2d seg_place one warp per segment walks its pairs 32 at a time in rank
+//              order; a lane's position in tile t is the tile's cursor plus the
+//              number of earlier lanes of the chunk covering t (shuffle count),
+//              so each list comes out in increasing rank order.
+// Only 4-byte ranks are written per list entry; there is no key array and
+// no radix pass.  Counts stay on the device (no host synchronisation).
 #include "kernels.cuh"
 #include "scan.cuh"
 
@@ -25,196 +35,438 @@ namespace gsr {
 
 namespace {
 
-constexpr int BR = 256;            // depth ranks (= threads) per block
-constexpr int kPairCache = 4096;   // (splat, tile row) results kept in smem
+constexpr int BR = 256;          // depth ranks per block (stages 1a, 1c)
+constexpr int kPairCache = 4096; // per-block pair results kept in smem (1c)
+constexpr int kSeg = 1024;       // pairs per segment (stage 2)
+constexpr int kRowsMax = kMaxTileRows;
 
-struct BinSmem {
-    float u[BR], v[BR], ia[BR], ib[BR], ic[BR], rsq[BR];
-    int lo[BR], hi[BR];
-    uint32_t poff[BR + 1];
-    uint32_t pc[kPairCache];
-    uint32_t s_warp[33];
-    unsigned long long block_prefix;
-    unsigned long long ticket;
-    uint32_t npairs;
-};
+__device__ __forceinline__ bool overflowed(const BinArgs &a) {
+    return a.ctr->P > (unsigned long long)a.cap_p || (int64_t)a.ctr->D > a.cap_d;
+}
 
-// exact tile-column span of splat j in tile row ty (reference intervals)
-__device__ __forceinline__ void pair_tiles(const BinSmem &S, int j, int ty, int width, int &tx0,
-                                           int &cnt) {
-    const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
-    int mn = 0x7fffffff, mx = -0x7fffffff;
-    const float u = S.u[j], v = S.v[j], ia = S.ia[j], ib = S.ib[j], ic = S.ic[j], rsq = S.rsq[j];
-    for (int y = y0; y < y1; y++) {
-        int x0, x1;
-        if (row_interval(u, v, ia, ib, ic, rsq, (float)y + 0.5f, width, x0, x1)) {
-            x0 = x0 > 0 ? x0 : 0;
-            if (x0 < x1) {
-                mn = x0 < mn ? x0 : mn;
-                mx = x1 > mx ? x1 : mx;
-            }
-        }
+__device__ __forceinline__ int64_t seg_count_of(const BinArgs &a) {
+    const int64_t n = (int64_t)a.ctr->nseg;
+    return n < a.cap_seg ? n : a.cap_seg;
+}
+
+// ---------------------------------------------------------------- 1a -------
+__global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
+    __shared__ uint32_t cnt[kRowsMax];
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    const int64_t k = a.ctr->K;
+    const int64_t r = b * BR + tid;
+    for (int t = tid; t < a.n_rows; t += BR) cnt[t] = 0;
+    __syncthreads();
+    if (b * BR < k && r < k) {
+        const uint32_t *order = a.depth_sched[16] ? a.order1 : a.order0;
+        const uint32_t i = __ldg(order + r);
+        const float4 A = __ldg(&a.rec[i].a), B = __ldg(&a.rec[i].b), C = __ldg(&a.rec[i].c);
+        a.srec[r].a = A;
+        a.srec[r].b = B;
+        a.srec[r].c = C;
+        int lo, hi;
+        row_range(A.y, B.w, a.height, lo, hi);
+        if (lo < hi)
+            for (int ty = lo / kTile; ty <= (hi - 1) / kTile; ty++) atomicAdd(&cnt[ty], 1u);
     }
-    if (mn <= mx) {
-        tx0 = mn / kTile;
-        cnt = (mx - 1) / kTile - tx0 + 1;
-    } else {
-        tx0 = 0;
-        cnt = 0;
+    __syncthreads();
+    const int64_t nb = a.n_blocks;
+    for (int t = tid; t < a.n_rows; t += BR) a.row_blk[(int64_t)t * nb + b] = cnt[t];
+}
+
+// ---------------------------------------------------------------- 1b -------
+// exclusive scan of row_blk (n_rows x n_blocks, row major) in place:
+// 2048-element tiles in ticket order, decoupled look-back between tiles
+constexpr int kScanItems = 8;
+constexpr int kScanTile = 256 * kScanItems;
+
+__global__ void __launch_bounds__(256) row_scan_kernel(BinArgs a) {
+    __shared__ uint32_t s_warp[33];
+    __shared__ unsigned long long s_pre;
+    __shared__ uint32_t s_ticket;
+    if (threadIdx.x == 0) s_ticket = (uint32_t)atomicAdd(a.scan_work, 1ull);
+    __syncthreads();
+    const int64_t tile = s_ticket;
+    unsigned long long *status = a.scan_work + 1;
+    const int64_t n = (int64_t)a.n_rows * a.n_blocks;
+    const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems], s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        v[j] = base + j < n ? a.row_blk[base + j] : 0u;
+        s += v[j];
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan_u32(s, s_warp, &tot);
+    if (threadIdx.x < 32) {
+        const unsigned long long pre = lookback_exclusive(status, tile, tot);
+        if (threadIdx.x == 0) s_pre = pre;
+    }
+    __syncthreads();
+    const unsigned long long pre = s_pre;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        const int64_t idx = base + j;
+        if (idx < n) {
+            const unsigned long long o = pre + ex;
+            a.row_blk[idx] = (uint32_t)o;
+            if (idx % a.n_blocks == 0) a.row_start[idx / a.n_blocks] = (uint32_t)o;
+        }
+        ex += v[j];
+    }
+    if (threadIdx.x == 255 && (tile + 1) * kScanTile >= n) {  // last tile: totals
+        const unsigned long long p = pre + ex;
+        a.ctr->P = p;
+        a.row_start[a.n_rows] = (uint32_t)(p < 0xffffffffull ? p : 0xffffffffull);
+        if (p > (unsigned long long)a.cap_p) atomicAdd(a.overflow_sticky, 1u);
     }
 }
 
-__device__ __forceinline__ int rank_of_pair(const BinSmem &S, uint32_t q) {
-    // largest j in [0, BR) with poff[j] <= q  (poff[BR] = npairs > q)
-    int lo = 0, hi = BR;  // invariant: poff[lo] <= q < poff[hi]
+// ---------------------------------------------------------------- 1c -------
+struct PairSmem {
+    float u[BR], v[BR], ia[BR], ib[BR], ic[BR], rsq[BR];
+    int lo[BR], hi[BR];
+    uint32_t poff[BR + 1];
+    uint32_t s_warp[33];
+    uint32_t lr[kPairCache];         // in-warp rank of a pair within its row
+    uint32_t wpre[BR / 32][kRowsMax];  // per-warp counts, then exclusive prefix
+    int ty_lo, ty_hi;
+};
+
+__device__ __forceinline__ int rank_of_pair(const uint32_t *poff, uint32_t q) {
+    int lo = 0, hi = BR;  // poff[lo] <= q < poff[hi]
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (S.poff[mid] <= q) lo = mid;
+        if (poff[mid] <= q) lo = mid;
         else hi = mid;
     }
     return lo;
 }
 
-__global__ void __launch_bounds__(BR) bin_kernel(
-    const uint32_t *__restrict__ order_even, const uint32_t *__restrict__ order_odd,
-    const SplatRec *__restrict__ rec, SplatRec *__restrict__ srec, FrameCounters *ctr, int width,
-    int height, uint32_t *__restrict__ tile_keys, uint32_t *__restrict__ tile_vals, int64_t cap_d,
-    unsigned long long *__restrict__ status, uint32_t *overflow_sticky) {
-    __shared__ BinSmem S;
-    const int tid = threadIdx.x;
-    if (tid == 0) S.ticket = atomicAdd(&ctr->bin_ticket, 1ull);
-    __syncthreads();
-    const int64_t t = (int64_t)S.ticket;
-    const int64_t k = ctr->K;
-    const int64_t r0 = t * BR;
-    if (r0 >= k) return;
-    const uint32_t *order = (ctr->npass & 1) ? order_odd : order_even;
-    const int tiles_x = (width + kTile - 1) / kTile;
-
-    // ---- gather + row ranges -------------------------------------------
-    const int64_t r = r0 + tid;
+__global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
+    extern __shared__ __align__(16) unsigned char dyn_raw[];
+    PairSmem &S = *reinterpret_cast<PairSmem *>(dyn_raw);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t b = blockIdx.x;
+    const int64_t k = a.ctr->K;
+    if (b * BR >= k || overflowed(a)) return;
+    const int64_t r = b * BR + tid;
     uint32_t ntr = 0;
+    int lo = 0, hi = 0;
     if (r < k) {
-        const uint32_t i = __ldg(order + r);
-        const float4 A = __ldg(&rec[i].a), B = __ldg(&rec[i].b), C = __ldg(&rec[i].c);
-        srec[r].a = A;
-        srec[r].b = B;
-        srec[r].c = C;
-        int lo, hi;
-        row_range(A.y, B.w, height, lo, hi);
+        const float4 A = __ldg(&a.srec[r].a), B = __ldg(&a.srec[r].b);
+        row_range(A.y, B.w, a.height, lo, hi);
         S.u[tid] = A.x;
         S.v[tid] = A.y;
         S.ia[tid] = A.z;
         S.ib[tid] = A.w;
         S.ic[tid] = B.x;
         S.rsq[tid] = B.y;
-        S.lo[tid] = lo;
-        S.hi[tid] = hi;
         if (lo < hi) ntr = (uint32_t)((hi - 1) / kTile - lo / kTile + 1);
-    } else {
-        S.lo[tid] = 0;
-        S.hi[tid] = 0;
+    }
+    S.lo[tid] = lo;
+    S.hi[tid] = hi;
+    const int t0 = ntr ? lo / kTile : 0x7fffffff, t1 = ntr ? (hi - 1) / kTile : -1;
+    if (tid == 0) {
+        S.ty_lo = 0x7fffffff;
+        S.ty_hi = -1;
     }
     uint32_t npairs;
-    const uint32_t off = block_excl_scan_u32(ntr, S.s_warp, &npairs);
+    const uint32_t off = block_excl_scan_u32(ntr, S.s_warp, &npairs);  // (syncs)
     S.poff[tid] = off;
     if (tid == 0) S.poff[BR] = npairs;
+    atomicMin(&S.ty_lo, t0);
+    atomicMax(&S.ty_hi, t1);
     __syncthreads();
-
-    // ---- phase 1: (tx0, count) per (splat, tile row) --------------------
-    uint32_t my_keys = 0;
-    for (uint32_t q0 = 0; q0 < npairs; q0 += BR) {
-        const uint32_t q = q0 + tid;
-        if (q < npairs) {
-            const int j = rank_of_pair(S, q);
-            const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
-            int tx0, cnt;
-            pair_tiles(S, j, ty, width, tx0, cnt);
-            if (q < kPairCache) S.pc[q] = (uint32_t)tx0 | ((uint32_t)cnt << 16);
-            my_keys += (uint32_t)cnt;
+    // rank of each (splat, row) among the block's splats covering that row:
+    // warp ballots give the in-warp rank, a prefix over warps the rest
+    const int ylo = S.ty_lo, yhi = S.ty_hi;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int ty = ylo; ty <= yhi; ty++) {
+        const bool cov = ty >= t0 && ty <= t1;
+        const uint32_t m = __ballot_sync(0xffffffffu, cov);
+        if (cov) {
+            const uint32_t q = off + (uint32_t)(ty - t0);
+            if (q < kPairCache) S.lr[q] = __popc(m & lt_mask);
         }
+        if (lane == 0) S.wpre[w][ty] = __popc(m);
     }
-    uint32_t block_keys;
-    block_excl_scan_u32(my_keys, S.s_warp, &block_keys);
-
-    // ---- global offset of this block (decoupled look-back) --------------
-    if (tid < 32) {
-        const unsigned long long pre = lookback_exclusive(status, t, block_keys);
-        if (tid == 0) {
-            S.block_prefix = pre;
-            if (r0 + BR >= k) {  // last block: publish D
-                const unsigned long long d = pre + block_keys;
-                ctr->D = (uint32_t)(d < 0xffffffffull ? d : 0xffffffffull);
-                if ((int64_t)d > cap_d) atomicAdd(overflow_sticky, 1u);
-            }
+    __syncthreads();
+    for (int ty = ylo + tid; ty <= yhi; ty += BR) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int j = 0; j < BR / 32; j++) {
+            const uint32_t c = S.wpre[j][ty];
+            S.wpre[j][ty] = run;
+            run += c;
         }
     }
     __syncthreads();
-
-    // ---- phase 2: write keys in rank-major order ------------------------
-    unsigned long long run = S.block_prefix;
-    for (uint32_t q0 = 0; q0 < npairs; q0 += BR) {
-        const uint32_t q = q0 + tid;
-        int j = 0, ty = 0, tx0 = 0, cnt = 0;
-        if (q < npairs) {
-            j = rank_of_pair(S, q);
-            ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
-            if (q < kPairCache) {
-                const uint32_t pc = S.pc[q];
-                tx0 = (int)(pc & 0xffffu);
-                cnt = (int)(pc >> 16);
-            } else {
-                pair_tiles(S, j, ty, width, tx0, cnt);
+    // one thread per pair: exact tile span, stored at its grouped slot
+    const int64_t nb = a.n_blocks;
+    for (uint32_t q = tid; q < npairs; q += BR) {
+        const int j = rank_of_pair(S.poff, q);
+        const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
+        uint32_t in_warp;
+        if (q < kPairCache) {
+            in_warp = S.lr[q];
+        } else {  // rare: recount covering splats of this warp before j
+            in_warp = 0;
+            for (int jj = j & ~31; jj < j; jj++)
+                in_warp += (S.lo[jj] < S.hi[jj] && ty >= S.lo[jj] / kTile &&
+                            ty <= (S.hi[jj] - 1) / kTile);
+        }
+        const uint32_t slot = a.row_blk[(int64_t)ty * nb + b] + S.wpre[j >> 5][ty] + in_warp;
+        // exact tile-column span of splat j in tile row ty
+        const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
+        int mn = 0x7fffffff, mx = -0x7fffffff;
+        const float u = S.u[j], v = S.v[j], ia = S.ia[j], ib = S.ib[j], ic = S.ic[j],
+                    rsq = S.rsq[j];
+        for (int y = y0; y < y1; y++) {
+            int x0, x1;
+            if (row_interval(u, v, ia, ib, ic, rsq, (float)y + 0.5f, a.width, x0, x1)) {
+                x0 = x0 > 0 ? x0 : 0;
+                if (x0 < x1) {
+                    mn = x0 < mn ? x0 : mn;
+                    mx = x1 > mx ? x1 : mx;
+                }
             }
         }
-        uint32_t chunk;
-        const uint32_t o = block_excl_scan_u32((uint32_t)cnt, S.s_warp, &chunk);
-        const unsigned long long pos = run + o;
-        const uint32_t tid0 = (uint32_t)(ty * tiles_x + tx0);
-        const uint32_t rk = (uint32_t)(r0 + j);
-        for (int e = 0; e < cnt; e++) {
-            const unsigned long long p = pos + (unsigned long long)e;
-            if ((int64_t)p < cap_d) {
-                tile_keys[p] = tid0 + (uint32_t)e;
-                tile_vals[p] = rk;
-            }
+        uint32_t span = 0;
+        if (mn <= mx) {
+            const uint32_t tx0 = (uint32_t)(mn / kTile);
+            span = tx0 | (((uint32_t)((mx - 1) / kTile) - tx0 + 1u) << 16);
         }
-        run += chunk;
+        if ((int64_t)slot < a.cap_p) a.pairs[slot] = make_uint2((uint32_t)(b * BR + j), span);
     }
 }
 
-__global__ void tile_ranges_kernel(const uint32_t *__restrict__ keys, const FrameCounters *ctr,
-                                   int64_t cap_d, uint2 *__restrict__ ranges) {
-    int64_t d = ctr->D;
-    d = d < cap_d ? d : cap_d;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = keys[i];
-        if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
-        if (i == d - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+// ---------------------------------------------------------------- 2a -------
+// segments: row ty's pairs [row_start[ty], row_start[ty+1]) in pieces of kSeg
+__global__ void __launch_bounds__(1024) seg_table_kernel(BinArgs a) {
+    __shared__ uint32_t s_warp[33];
+    uint32_t carry = 0;
+    const bool ov = overflowed(a);
+    for (int base = 0; base < a.n_rows; base += 1024) {
+        const int ty = base + threadIdx.x;
+        uint32_t ns = 0;
+        if (ty < a.n_rows && !ov) {
+            const uint32_t len = a.row_start[ty + 1] - a.row_start[ty];
+            ns = (len + kSeg - 1) / kSeg;
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_u32(ns, s_warp, &tot);
+        for (uint32_t s = 0; s < ns; s++) {
+            const uint32_t g = carry + ex + s;
+            if ((int64_t)g < a.cap_seg) a.seg_row[g] = (uint32_t)ty;
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0) a.ctr->nseg = carry;
+}
+
+// first segment of tile row ty (seg_row is non-decreasing): binary search
+__device__ __forceinline__ int64_t first_seg_of_row(const BinArgs &a, uint32_t ty, int64_t nseg) {
+    int64_t lo = 0, hi = nseg;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a.seg_row[mid] < ty) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void seg_bounds(const BinArgs &a, int64_t g, int64_t nseg,
+                                           uint32_t &ty, uint32_t &p0, uint32_t &p1) {
+    ty = a.seg_row[g];
+    const int64_t first = first_seg_of_row(a, ty, nseg);
+    const uint32_t rs = a.row_start[ty], re = a.row_start[ty + 1];
+    p0 = rs + (uint32_t)(g - first) * kSeg;
+    p1 = min(re, p0 + kSeg);
+}
+
+// ---------------------------------------------------------------- 2b -------
+// one warp per segment: keys per tile column via a difference array
+__global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
+    extern __shared__ __align__(16) uint32_t diff_all[];  // [8][tiles_x + 1]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 8 + w;
+    if (overflowed(a)) return;
+    const int64_t nseg = seg_count_of(a);
+    if (g >= nseg) return;
+    const int tx_n = a.tiles_x;
+    uint32_t *diff = diff_all + w * (tx_n + 1);
+    for (int t = lane; t <= tx_n; t += 32) diff[t] = 0;
+    __syncwarp();
+    uint32_t ty, p0, p1;
+    seg_bounds(a, g, nseg, ty, p0, p1);
+    for (uint32_t p = p0 + lane; p < p1; p += 32) {
+        const uint32_t sp = a.pairs[p].y;
+        const uint32_t c = sp >> 16;
+        if (c) {
+            atomicAdd(&diff[sp & 0xffffu], 1u);
+            atomicSub(&diff[(sp & 0xffffu) + c], 1u);
+        }
+    }
+    __syncwarp();
+    // prefix over columns -> counts, written to seg_cnt[g][tx]
+    uint32_t carry = 0;
+    for (int t0 = 0; t0 < tx_n; t0 += 32) {
+        const int t = t0 + lane;
+        const uint32_t dv = t < tx_n ? diff[t] : 0u;
+        const uint32_t inc = warp_incl_scan_u32(dv) + carry;
+        if (t < tx_n) a.seg_cnt[g * tx_n + t] = inc;
+        carry = __shfl_sync(0xffffffffu, inc, 31);
+    }
+}
+
+// ---------------------------------------------------------------- 2c -------
+// thread per tile: exclusive prefix over its row's segments, tile total
+__global__ void seg_scan_kernel(BinArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.ntiles || overflowed(a)) return;
+    const int tx_n = a.tiles_x;
+    const int ty = t / tx_n, tx = t % tx_n;
+    const uint32_t rs = a.row_start[ty], re = a.row_start[ty + 1];
+    const uint32_t nrow = (re - rs + kSeg - 1) / kSeg;
+    const int64_t lo = first_seg_of_row(a, (uint32_t)ty, seg_count_of(a));
+    uint32_t run = 0;
+    uint32_t *base = a.seg_cnt + lo * tx_n + tx;
+    uint32_t s = 0;
+    for (; s + 8 <= nrow; s += 8) {  // 8 independent loads in flight
+        uint32_t c[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) c[j] = base[(int64_t)(s + j) * tx_n];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            base[(int64_t)(s + j) * tx_n] = run;
+            run += c[j];
+        }
+    }
+    for (; s < nrow; s++) {
+        const uint32_t c = base[(int64_t)s * tx_n];
+        base[(int64_t)s * tx_n] = run;
+        run += c;
+    }
+    a.tile_total[t] = run;
+}
+
+// one block of 1024: tile starts (exclusive scan of totals), ranges, D
+__global__ void __launch_bounds__(1024) tile_scan_kernel(BinArgs a) {
+    __shared__ uint32_t s_warp[33];
+    const bool ov_p = a.ctr->P > (unsigned long long)a.cap_p;
+    unsigned long long carry = 0;
+    for (int base = 0; base < a.ntiles; base += 1024) {
+        const int t = base + threadIdx.x;
+        const uint32_t v = (t < a.ntiles && !ov_p) ? a.tile_total[t] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_u32(v, s_warp, &tot);
+        if (t < a.ntiles) {
+            const unsigned long long s = carry + ex;
+            a.tile_start[t] = (uint32_t)s;
+            a.ranges[t] = make_uint2((uint32_t)s, (uint32_t)(s + v));
+        }
+        carry += tot;
+    }
+    const bool overflow = ov_p || (int64_t)carry > a.cap_d;
+    if (threadIdx.x == 0) {
+        a.ctr->D = (uint32_t)(carry < 0xffffffffull ? carry : 0xffffffffull);
+        if ((int64_t)carry > a.cap_d) atomicAdd(a.overflow_sticky, 1u);
+    }
+    if (overflow)  // lists are not placed: empty ranges keep the blend in bounds
+        for (int t = threadIdx.x; t < a.ntiles; t += 1024) a.ranges[t] = make_uint2(0u, 0u);
+}
+
+// ---------------------------------------------------------------- 2d -------
+__global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
+    // per warp: column cursors [tiles_x] and coverage masks [tiles_x]
+    extern __shared__ __align__(16) uint32_t place_smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 8 + w;
+    if (overflowed(a)) return;
+    const int64_t nseg = seg_count_of(a);
+    if (g >= nseg) return;
+    const int tx_n = a.tiles_x;
+    uint32_t *cur = place_smem + w * 2 * tx_n;
+    uint32_t *mask = cur + tx_n;
+    uint32_t ty, p0, p1;
+    seg_bounds(a, g, nseg, ty, p0, p1);
+    const uint32_t *tstart = a.tile_start + (int64_t)ty * tx_n;
+    for (int t = lane; t < tx_n; t += 32) {
+        cur[t] = tstart[t] + a.seg_cnt[g * tx_n + t];
+        mask[t] = 0;
+    }
+    __syncwarp();
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (uint32_t c0 = p0; c0 < p1; c0 += 32) {
+        const uint32_t p = c0 + lane;
+        uint32_t rank = 0, a0 = 0, n = 0;  // covers columns [a0, a0 + n)
+        if (p < p1) {
+            const uint2 pr = a.pairs[p];
+            rank = pr.x;
+            a0 = pr.y & 0xffffu;
+            n = pr.y >> 16;
+        }
+        // 1: coverage mask of every column touched by the chunk
+        for (uint32_t e = 0; e < n; e++) atomicOr(&mask[a0 + e], 1u << lane);
+        __syncwarp();
+        // 2: position = cursor + earlier (lower-rank) lanes covering the column
+        for (uint32_t e = 0; e < n; e++) {
+            const uint32_t t = a0 + e;
+            const uint32_t pos = cur[t] + __popc(mask[t] & lt_mask);
+            if ((int64_t)pos < a.cap_d) a.tile_vals[pos] = rank;
+        }
+        __syncwarp();
+        // 3: the highest covering lane advances the cursor and clears the mask
+        for (uint32_t e = 0; e < n; e++) {
+            const uint32_t t = a0 + e;
+            const uint32_t m = mask[t];
+            if ((m >> lane) == 1u) {
+                cur[t] += __popc(m);
+                mask[t] = 0;
+            }
+        }
+        __syncwarp();
     }
 }
 
 }  // namespace
 
-int64_t bin_status_words(int64_t n_cap) { return (n_cap + BR - 1) / BR + 1; }
+int64_t bin_blocks(int64_t n_cap) { return (n_cap + BR - 1) / BR; }
+int64_t bin_scan_tiles(int64_t n_blocks, int n_rows) {
+    return (n_blocks * n_rows + kScanTile - 1) / kScanTile;
+}
+int64_t bin_segments(int64_t cap_p, int n_rows) { return cap_p / kSeg + n_rows + 1; }
 
-void launch_bin(const uint32_t *vals_even, const uint32_t *vals_odd, const SplatRec *rec,
-                SplatRec *srec, int64_t n_cap, FrameCounters *ctr, int width, int height,
-                uint32_t *tile_keys, uint32_t *tile_vals, int64_t cap_d,
-                unsigned long long *status, uint32_t *overflow_sticky, cudaStream_t s) {
-    if (n_cap <= 0) return;
-    cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)bin_status_words(n_cap), s);
-    const unsigned blocks = (unsigned)((n_cap + BR - 1) / BR);
-    bin_kernel<<<blocks, BR, 0, s>>>(vals_even, vals_odd, rec, srec, ctr, width, height, tile_keys,
-                                     tile_vals, cap_d, status, overflow_sticky);
+cudaError_t binning_init_attributes() {
+    cudaError_t e = cudaFuncSetAttribute(bin_pairs_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(PairSmem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(seg_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(8 * (kMaxTilesX + 1) * sizeof(uint32_t)));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(seg_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(8 * 2 * kMaxTilesX * sizeof(uint32_t)));
+    return e;
 }
 
-void launch_tile_ranges(const uint32_t *tile_keys, const FrameCounters *ctr, int64_t cap_d,
-                        uint2 *ranges, int n_tiles, int sms, cudaStream_t s) {
-    cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
-    if (cap_d <= 0) return;
-    tile_ranges_kernel<<<(unsigned)(sms * 8), 256, 0, s>>>(tile_keys, ctr, cap_d, ranges);
+int launch_binning(const BinArgs &a, cudaStream_t s) {
+    if (a.n_blocks <= 0) return 0;
+    const unsigned nb = (unsigned)a.n_blocks;
+    bin_gather_kernel<<<nb, BR, 0, s>>>(a);
+    const int64_t scan_tiles = bin_scan_tiles(a.n_blocks, a.n_rows);
+    cudaMemsetAsync(a.scan_work, 0, sizeof(unsigned long long) * (size_t)(scan_tiles + 1), s);
+    row_scan_kernel<<<(unsigned)scan_tiles, 256, 0, s>>>(a);
+    bin_pairs_kernel<<<nb, BR, sizeof(PairSmem), s>>>(a);
+    seg_table_kernel<<<1, 1024, 0, s>>>(a);
+    const unsigned sb = (unsigned)((a.cap_seg + 7) / 8);
+    seg_count_kernel<<<sb, 256, 8 * (a.tiles_x + 1) * sizeof(uint32_t), s>>>(a);
+    seg_scan_kernel<<<(unsigned)((a.ntiles + 255) / 256), 256, 0, s>>>(a);
+    tile_scan_kernel<<<1, 1024, 0, s>>>(a);
+    seg_place_kernel<<<sb, 256, 8 * 2 * a.tiles_x * sizeof(uint32_t), s>>>(a);
+    return 8;
 }
 
 }  // namespace gsr

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
         const uint32_t j = c + lane;
         uint32_t mask = 0;
         if (j < rg.y) {
-            const uint32_t r = __ldg(tile_vals + j);
+            const uint32_t r = __ldg(tile_vals + j);  // depth rank
             const float4 A = __ldg(&srec[r].a);
             const float4 B = __ldg(&srec[r].b);
             const float4 C = __ldg(&srec[r].c);

@@ -85,11 +85,13 @@ struct SavedCall {
 struct gsr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    int64_t cap_n = 0, cap_d = 0;
-    DevBuf keys[2], vals[2], rec, srec, bin_status, keep;
+    int64_t cap_n = 0, cap_d = 0, cap_p = 0;
+    DevBuf keys[2], vals[2], rec, srec, keep;
     int sms = 148;
-    DevBuf hist, partials;
-    DevBuf tkeys[2], tvals[2];
+    DevBuf depth_work, sched;     // depth-sort scratch; sched[16] = result buffer
+    uint32_t *hsched = nullptr;   // pinned host copy of sched
+    // tile-list buffers (binning.cu)
+    DevBuf row_blk, row_start, scan_work, pairs, seg_row, seg_cnt, ttotal, tstart, tile_vals;
     DevBuf ranges;
     DevBuf frame_u8, frame_rgb, frame_t;
     DevBuf ctr, sticky;
@@ -101,15 +103,15 @@ struct gsr_ctx {
     double *hssim = nullptr;
     // last frame
     int W = 0, H = 0, ntiles = 0;
-    const uint32_t *final_tkeys = nullptr, *final_tvals = nullptr;
+    int tile_passes = 0;
     SavedCall saved;
     bool pending = false;
     int retries = 0;
     int64_t bytes() const {
         int64_t s = 0;
-        const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &rec, &srec, &bin_status,
-                               &keep, &hist, &partials, &tkeys[0], &tkeys[1],
-                               &tvals[0], &tvals[1], &ranges, &frame_u8, &frame_rgb, &frame_t,
+        const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &rec, &srec, &keep,
+                               &depth_work, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+                               &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w};
         for (auto *b : all) s += (int64_t)b->bytes;
@@ -146,8 +148,8 @@ int check_camera(const gsr_camera *cam) {
     if (!cam) return fail(GSR_E_INVALID, "camera is null");
     if (cam->width <= 0 || cam->height <= 0)
         return fail(GSR_E_INVALID, "image dimensions must be positive");
-    if (cam->width > 32768 || cam->height > 32768)
-        return fail(GSR_E_INVALID, "image dimensions above 32768 are not supported");
+    if (cam->width > 16 * kMaxTilesX || cam->height > 16 * kMaxTileRows)
+        return fail(GSR_E_INVALID, "image larger than 16384 x 8192 is not supported");
     if (!(cam->fx > 0) || !(cam->fy > 0)) return fail(GSR_E_INVALID, "focal lengths must be positive");
     return GSR_OK;
 }
@@ -170,12 +172,6 @@ CameraArgs camera_args(const gsr_camera *cam) {
     return a;
 }
 
-int tile_sort_passes(int ntiles) {
-    int bits = 0;
-    while ((1 << bits) < ntiles) bits++;
-    return (bits + 7) / 8;
-}
-
 int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool want_keep) {
     int rc;
     if (n > c->cap_n) {
@@ -186,23 +182,28 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
         }
         if ((rc = ensure(c->rec, sizeof(SplatRec) * cap))) return rc;
         if ((rc = ensure(c->srec, sizeof(SplatRec) * cap))) return rc;
-        if ((rc = ensure(c->bin_status, sizeof(unsigned long long) * bin_status_words(cap))))
-            return rc;
         c->cap_n = cap;
     }
     if (want_keep && (rc = ensure(c->keep, (size_t)c->cap_n))) return rc;
-    if (c->cap_d == 0) c->cap_d = round_up(std::max<int64_t>(int64_t(1) << 22, 12 * n), 4096);
-    for (int i = 0; i < 2; i++) {
-        if ((rc = ensure(c->tkeys[i], sizeof(uint32_t) * c->cap_d))) return rc;
-        if ((rc = ensure(c->tvals[i], sizeof(uint32_t) * c->cap_d))) return rc;
-    }
-    const int64_t big = std::max(c->cap_n, c->cap_d);
-    const int64_t hist_n = 256 * radix_tiles(big);
-    if ((rc = ensure(c->hist, sizeof(uint32_t) * hist_n))) return rc;
-    if ((rc = ensure(c->partials, sizeof(uint32_t) * scan_partials_needed(std::max(hist_n, big)))))
-        return rc;
-    const int ntiles = ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+    if (c->cap_d == 0) c->cap_d = round_up(std::max<int64_t>(int64_t(1) << 22, 16 * n), 4096);
+    if (c->cap_p == 0) c->cap_p = round_up(std::max<int64_t>(int64_t(1) << 20, 6 * n), 4096);
+    if ((rc = ensure(c->tile_vals, sizeof(uint32_t) * c->cap_d))) return rc;
+    if ((rc = ensure(c->pairs, sizeof(uint2) * c->cap_p))) return rc;
+    if ((rc = ensure(c->depth_work, sort_work_bytes(c->cap_n, 8, 8)))) return rc;
+    const int tiles_x = (W + kTile - 1) / kTile, n_rows = (H + kTile - 1) / kTile;
+    const int ntiles = tiles_x * n_rows;
     if ((rc = ensure(c->ranges, sizeof(uint2) * (size_t)ntiles))) return rc;
+    if ((rc = ensure(c->ttotal, sizeof(uint32_t) * (size_t)ntiles))) return rc;
+    if ((rc = ensure(c->tstart, sizeof(uint32_t) * (size_t)ntiles))) return rc;
+    if ((rc = ensure(c->row_blk, sizeof(uint32_t) * (size_t)n_rows * bin_blocks(c->cap_n))))
+        return rc;
+    if ((rc = ensure(c->row_start, sizeof(uint32_t) * (size_t)(n_rows + 1)))) return rc;
+    if ((rc = ensure(c->scan_work, sizeof(unsigned long long) *
+                                       (size_t)(bin_scan_tiles(bin_blocks(c->cap_n), n_rows) + 1))))
+        return rc;
+    const int64_t cap_seg = bin_segments(c->cap_p, n_rows);
+    if ((rc = ensure(c->seg_row, sizeof(uint32_t) * (size_t)cap_seg))) return rc;
+    if ((rc = ensure(c->seg_cnt, sizeof(uint32_t) * (size_t)cap_seg * tiles_x))) return rc;
     const int64_t px = (int64_t)W * H;
     if ((rc = ensure(c->frame_u8, (size_t)px * 3))) return rc;
     if (want_rgb) {
@@ -228,10 +229,11 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     cudaStream_t s = c->stream;
     FrameCounters *ctr = c->ctr.as<FrameCounters>();
     const CameraArgs ca = camera_args(cam);
-    ScanWorkspace ws{c->partials.as<uint32_t>(), (int64_t)(c->partials.bytes / 4)};
     c->W = W;
     c->H = H;
     c->ntiles = ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+    uint32_t *dsched = c->sched.as<uint32_t>();
+    int launches = 2;  // frame init + blend
 
     cudaEventRecord(c->ev[0], s);
     launch_frame_init(ctr, s);
@@ -239,56 +241,60 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         launch_preprocess(sc->view, ca, sh_degree, cull, c->keys[0].as<unsigned long long>(),
                           c->rec.as<SplatRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr, ctr,
                           s);
-        launch_depth_passes(ctr, s);
+        launches++;
     }
     cudaEventRecord(c->ev[1], s);
     if (n > 0) {
-        for (int p = 0; p < 8; p++) {
-            launch_radix_pass<unsigned long long>(
-                c->keys[p & 1].as<unsigned long long>(), p == 0 ? nullptr : c->vals[p & 1].as<uint32_t>(),
-                c->keys[(p + 1) & 1].as<unsigned long long>(), c->vals[(p + 1) & 1].as<uint32_t>(),
-                p == 0 ? nullptr : &ctr->K, n, 8 * p, &ctr->kmin, &ctr->npass, p, p == 0,
-                c->hist.as<uint32_t>(), ws, s);
-        }
+        // stable depth sort; first pass compacts (drops culled sentinels)
+        launches += launch_onesweep_sort<unsigned long long>(
+            c->keys[0].as<unsigned long long>(), c->keys[1].as<unsigned long long>(),
+            c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), true, true, &ctr->K, n, n, 8,
+            true, c->depth_work.p, dsched, &ctr->npass, c->sms, s);
     }
     cudaEventRecord(c->ev[2], s);
     if (n > 0) {
-        launch_bin(c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), c->rec.as<SplatRec>(),
-                   c->srec.as<SplatRec>(), n, ctr, W, H, c->tkeys[0].as<uint32_t>(),
-                   c->tvals[0].as<uint32_t>(), c->cap_d, c->bin_status.as<unsigned long long>(),
-                   c->sticky.as<uint32_t>(), s);
-    }
-    cudaEventRecord(c->ev[3], s);
-    const int tp = tile_sort_passes(c->ntiles);
-    if (n > 0) {
-        for (int p = 0; p < tp; p++) {
-            launch_radix_pass<uint32_t>(c->tkeys[p & 1].as<uint32_t>(), c->tvals[p & 1].as<uint32_t>(),
-                                        c->tkeys[(p + 1) & 1].as<uint32_t>(),
-                                        c->tvals[(p + 1) & 1].as<uint32_t>(), &ctr->D, c->cap_d,
-                                        8 * p, nullptr, nullptr, p, false, c->hist.as<uint32_t>(),
-                                        ws, s);
-        }
-    }
-    c->final_tkeys = c->tkeys[tp & 1].as<uint32_t>();
-    c->final_tvals = c->tvals[tp & 1].as<uint32_t>();
-    if (n > 0) {
-        launch_tile_ranges(c->final_tkeys, ctr, c->cap_d, c->ranges.as<uint2>(), c->ntiles, c->sms,
-                           s);
+        BinArgs ba;
+        ba.order0 = c->vals[0].as<uint32_t>();
+        ba.order1 = c->vals[1].as<uint32_t>();
+        ba.depth_sched = dsched;
+        ba.rec = c->rec.as<SplatRec>();
+        ba.srec = c->srec.as<SplatRec>();
+        ba.ctr = ctr;
+        ba.width = W;
+        ba.height = H;
+        ba.tiles_x = (W + kTile - 1) / kTile;
+        ba.n_rows = (H + kTile - 1) / kTile;
+        ba.ntiles = c->ntiles;
+        ba.n_blocks = bin_blocks(c->cap_n);
+        ba.row_blk = c->row_blk.as<uint32_t>();
+        ba.row_start = c->row_start.as<uint32_t>();
+        ba.scan_work = c->scan_work.as<unsigned long long>();
+        ba.pairs = c->pairs.as<uint2>();
+        ba.cap_p = c->cap_p;
+        ba.seg_row = c->seg_row.as<uint32_t>();
+        ba.cap_seg = bin_segments(c->cap_p, ba.n_rows);
+        ba.seg_cnt = c->seg_cnt.as<uint32_t>();
+        ba.tile_total = c->ttotal.as<uint32_t>();
+        ba.tile_start = c->tstart.as<uint32_t>();
+        ba.ranges = c->ranges.as<uint2>();
+        ba.tile_vals = c->tile_vals.as<uint32_t>();
+        ba.cap_d = c->cap_d;
+        ba.overflow_sticky = c->sticky.as<uint32_t>();
+        launches += launch_binning(ba, s);
     } else {
         cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
     }
+    cudaEventRecord(c->ev[3], s);
     cudaEventRecord(c->ev[4], s);
     BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
                  want_rgb ? c->frame_t.as<float>() : nullptr};
-    launch_blend(c->srec.as<SplatRec>(), c->final_tvals, c->ranges.as<uint2>(), W, H, bg[0], bg[1],
-                 bg[2], out, s);
+    launch_blend(c->srec.as<SplatRec>(), c->tile_vals.as<uint32_t>(), c->ranges.as<uint2>(), W, H,
+                 bg[0], bg[1], bg[2], out, s);
     cudaEventRecord(c->ev[5], s);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(c->hsched, dsched, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     GSR_CUDA_OK(cudaGetLastError());
-    // kernels of this frame: init + blend, and for a non-empty scene
-    // preprocess + pass count + 8 depth passes x (upsweep + 3 scan + downsweep)
-    // + bin count + 3 scan + bin write + tp tile passes x 5 + ranges
-    c->launches += 2 + (n > 0 ? 2 + 8 * 5 + 1 + 5 * tp + 1 : 0);
+    c->launches += launches;
     c->saved.scene = sc;
     c->saved.cam = *cam;
     for (int i = 0; i < 3; i++) c->saved.bg[i] = bg[i];
@@ -306,8 +312,13 @@ int complete_frame(gsr_ctx *c) {
     GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
     c->pending = false;
     c->retries = 0;
-    if ((int64_t)c->hctr->D > c->cap_d) {
-        c->cap_d = round_up((int64_t)c->hctr->D + (int64_t)c->hctr->D / 4 + (1 << 20), 4096);
+    const int64_t d = (int64_t)c->hctr->D, p = (int64_t)c->hctr->P;
+    if (d > c->cap_d || p > c->cap_p) {
+        // a pair overflow stops the pipeline before D is known: grow D too
+        if (d > c->cap_d || p > c->cap_p) c->cap_d = round_up(std::max(d, 3 * p) + d / 4 + (1 << 20), 4096);
+        if (p > c->cap_p) c->cap_p = round_up(p + p / 4 + (1 << 20), 4096);
+        if (c->cap_d >= (int64_t(1) << 32) || c->cap_p >= (int64_t(1) << 32))
+            return fail(GSR_E_OOM, "tile list exceeds 2^32 entries");
         SavedCall sv = c->saved;
         int rc = enqueue_frame(c, sv.scene, &sv.cam, sv.bg, sv.sh_degree, sv.cull, sv.want_rgb,
                                sv.want_keep);
@@ -315,7 +326,8 @@ int complete_frame(gsr_ctx *c) {
         GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
         c->pending = false;
         c->retries = 1;
-        if ((int64_t)c->hctr->D > c->cap_d) return fail(GSR_E_OOM, "tile-key buffer overflow");
+        if ((int64_t)c->hctr->D > c->cap_d || (int64_t)c->hctr->P > c->cap_p)
+            return fail(GSR_E_OOM, "tile list buffer overflow");
     }
     return GSR_OK;
 }
@@ -592,9 +604,11 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = radix_init_attributes();
+    if (e == cudaSuccess) e = binning_init_attributes();
     for (int i = 0; i < 8 && e == cudaSuccess; i++) e = cudaEventCreate(&c->ev[i]);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hssim, sizeof(double) * 64);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hsched, sizeof(uint32_t) * 64);
     if (e != cudaSuccess) {
         int rc = fail_cuda(e, "context setup");
         gsr_ctx_destroy(c);
@@ -602,6 +616,9 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     }
     int rc = ensure(c->ctr, sizeof(FrameCounters));
     if (!rc) rc = ensure(c->sticky, sizeof(uint32_t));
+    if (!rc) rc = ensure(c->sched, 64 * sizeof(uint32_t));
+    if (!rc && cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess)
+        rc = fail(GSR_E_CUDA, "memset");
     if (!rc && cudaMemset(c->sticky.p, 0, sizeof(uint32_t)) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
     if (!rc) rc = ensure(c->ssim_misc, 64);
@@ -636,6 +653,7 @@ int gsr_ctx_destroy(gsr_ctx *ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->hctr) cudaFreeHost(ctx->hctr);
     if (ctx->hssim) cudaFreeHost(ctx->hssim);
+    if (ctx->hsched) cudaFreeHost(ctx->hsched);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GSR_OK;
@@ -714,7 +732,7 @@ int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera 
         GSR_CUDA_OK(cudaMemcpy(out_keep, ctx->keep.p, (size_t)n, cudaMemcpyDeviceToHost));
     if (out_order && k > 0) {
         std::vector<uint32_t> o((size_t)k);
-        const DevBuf &vb = ctx->vals[ctx->hctr->npass & 1];
+        const DevBuf &vb = ctx->vals[ctx->hsched[16] & 1u];
         GSR_CUDA_OK(cudaMemcpy(o.data(), vb.p, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < k; i++) out_order[i] = o[i];
     }
@@ -739,13 +757,20 @@ int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_ranks,
     int rc = complete_frame(ctx);
     if (rc) return rc;
     const int64_t d = std::min<int64_t>(ctx->hctr->D, ctx->cap_d);
-    if (out_tiles && d > 0)
-        GSR_CUDA_OK(cudaMemcpy(out_tiles, ctx->final_tkeys, 4 * d, cudaMemcpyDeviceToHost));
-    if (out_ranks && d > 0)
-        GSR_CUDA_OK(cudaMemcpy(out_ranks, ctx->final_tvals, 4 * d, cudaMemcpyDeviceToHost));
-    if (out_ranges && ctx->ntiles > 0)
-        GSR_CUDA_OK(cudaMemcpy(out_ranges, ctx->ranges.p, sizeof(uint2) * ctx->ntiles,
+    std::vector<uint2> rg((size_t)ctx->ntiles);
+    if (ctx->ntiles > 0)
+        GSR_CUDA_OK(cudaMemcpy(rg.data(), ctx->ranges.p, sizeof(uint2) * ctx->ntiles,
                                cudaMemcpyDeviceToHost));
+    if (out_ranks && d > 0)
+        GSR_CUDA_OK(cudaMemcpy(out_ranks, ctx->tile_vals.p, 4 * d, cudaMemcpyDeviceToHost));
+    for (int t = 0; t < ctx->ntiles; t++) {
+        if (out_tiles)  // tile ids are implicit in the ranges (lists are tile-major)
+            for (uint32_t i = rg[t].x; i < rg[t].y && (int64_t)i < d; i++) out_tiles[i] = t;
+        if (out_ranges) {
+            out_ranges[2 * t] = (int32_t)rg[t].x;
+            out_ranges[2 * t + 1] = (int32_t)rg[t].y;
+        }
+    }
     if (stats) {
         stats->tile_keys = ctx->hctr->D;
         stats->splats_drawn = ctx->hctr->K;

@@ -16,7 +16,9 @@ struct FrameCounters {
     uint32_t pad0;
     unsigned long long kmin;    // min / max kept depth key (f64 bits)
     unsigned long long kmax;
-    unsigned long long bin_ticket;  // block tickets of the binning kernel
+    unsigned long long P;       // (splat, tile row) pairs
+    uint32_t nseg;              // binning segments
+    uint32_t pad1;
 };
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.
@@ -47,43 +49,60 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
                        int frustum_cull, unsigned long long *keys, SplatRec *rec,
                        uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s);
-void launch_depth_passes(FrameCounters *ctr, cudaStream_t s);
 
-// radix.cu
-struct ScanWorkspace {
-    uint32_t *partials;
-    int64_t partial_cap;
-};
-int64_t scan_partials_needed(int64_t n);
+// radix.cu: Onesweep stable LSD sort (see radix.cu header)
 cudaError_t radix_init_attributes();
-void launch_scan_exclusive(const uint32_t *in, uint32_t *out, int64_t n, uint32_t *total,
-                           const ScanWorkspace &ws, cudaStream_t s);
-
 constexpr int kRadixThreads = 256;
-constexpr int kRadixItems = 16;
-constexpr int kRadixTile = kRadixThreads * kRadixItems;
-inline int64_t radix_tiles(int64_t n_cap) { return (n_cap + kRadixTile - 1) / kRadixTile; }
-
-// One stable LSD pass over 8 bits at `shift` of (key - key_base).
-//  n = min(*n_dev, n_cap) (n_dev nullable -> n_cap).
-//  vin == nullptr -> value = input index.  drop_sentinel: keys == ~0 are
-//  removed (the order-preserving compaction of render.py:279).
-//  The pass is a no-op when pass_index >= *npass_dev (npass_dev nullable).
+// items per thread (8: keeps <= 64 registers, 4 blocks / 32 warps per SM)
+constexpr int radix_items(int key_bytes) { return key_bytes == 8 ? 8 : 8; }
+inline int64_t radix_tiles(int64_t n_cap, int key_bytes) {
+    const int64_t tile = (int64_t)kRadixThreads * radix_items(key_bytes);
+    return (n_cap + tile - 1) / tile;
+}
+// scratch for one sort (histograms, look-back status, tickets)
+size_t sort_work_bytes(int64_t n_items_cap, int passes, int key_bytes);
+// Sorts (keys0, vals0) over `passes` 8-bit digits; the result lands in buffer
+// sched[16] (0 or 1).  First pass: n_first items (>= 0) or *n_dev (n_first <
+// 0); later passes: min(*n_dev, n_cap).  implicit_first_vals: value = index;
+// drop_sentinel: first pass removes keys == ~0.  Returns kernels launched.
 template <typename K>
-void launch_radix_pass(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout,
-                       const uint32_t *n_dev, int64_t n_cap, int shift,
-                       const unsigned long long *key_base, const uint32_t *npass_dev,
-                       int pass_index, bool drop_sentinel, uint32_t *hist,
-                       const ScanWorkspace &ws, cudaStream_t s);
+int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
+                         bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
+                         int64_t n_first, int64_t n_cap, int passes, bool force_first,
+                         void *work, uint32_t *sched, uint32_t *npass_out, int sms,
+                         cudaStream_t s);
 
-// binning.cu: fused gather + tile-list generation (one kernel, look-back scan)
-int64_t bin_status_words(int64_t n_cap);
-void launch_bin(const uint32_t *vals_even, const uint32_t *vals_odd, const SplatRec *rec,
-                SplatRec *srec, int64_t n_cap, FrameCounters *ctr, int width, int height,
-                uint32_t *tile_keys, uint32_t *tile_vals, int64_t cap_d,
-                unsigned long long *status, uint32_t *overflow_sticky, cudaStream_t s);
-void launch_tile_ranges(const uint32_t *tile_keys, const FrameCounters *ctr, int64_t cap_d,
-                        uint2 *ranges, int n_tiles, int sms, cudaStream_t s);
+// binning.cu: sort-free tile lists (see binning.cu header)
+constexpr int kMaxTileRows = 512;   // height <= 8192
+constexpr int kMaxTilesX = 1024;    // width <= 16384
+struct BinArgs {
+    const uint32_t *order0, *order1;  // depth sort result buffers
+    const uint32_t *depth_sched;      // [16]: which of order0/order1 holds the result
+    const SplatRec *rec;              // records by Gaussian index (preprocess)
+    SplatRec *srec;                   // records by depth rank (written here)
+    FrameCounters *ctr;
+    int width, height, n_rows, tiles_x, ntiles;
+    int64_t n_blocks;       // blocks of 256 depth ranks (capacity)
+    uint32_t *row_blk;      // [n_rows][n_blocks] pair counts -> slots
+    uint32_t *row_start;    // [n_rows + 1]
+    unsigned long long *scan_work;  // [1 + scan tiles]: ticket, look-back status
+    uint2 *pairs;           // [cap_p] (rank, tx0 | count << 16), grouped by tile row
+    int64_t cap_p;
+    uint32_t *seg_row;      // [cap_seg] tile row of each segment
+    int64_t cap_seg;
+    uint32_t *seg_cnt;      // [cap_seg][tiles_x] keys per column -> offsets
+    uint32_t *tile_total;   // [ntiles]
+    uint32_t *tile_start;   // [ntiles]
+    uint2 *ranges;          // [ntiles] [start, end) into tile_vals
+    uint32_t *tile_vals;    // [cap_d] depth ranks, tile-major
+    int64_t cap_d;
+    uint32_t *overflow_sticky;
+};
+int64_t bin_blocks(int64_t n_cap);
+int64_t bin_scan_tiles(int64_t n_blocks, int n_rows);
+int64_t bin_segments(int64_t cap_p, int n_rows);
+cudaError_t binning_init_attributes();
+int launch_binning(const BinArgs &a, cudaStream_t s);  // returns kernels launched
 
 // blend.cu
 struct BlendOut {
@@ -91,9 +110,8 @@ struct BlendOut {
     float *rgb;     // (H,W,3) or null
     float *trans;   // (H,W) or null
 };
-void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *ranges,
-                  int width, int height, float bg0, float bg1, float bg2, BlendOut out,
-                  cudaStream_t s);
+void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *ranges, int width,
+                  int height, float bg0, float bg1, float bg2, BlendOut out, cudaStream_t s);
 
 // resample.cu
 struct ResampleAxis {

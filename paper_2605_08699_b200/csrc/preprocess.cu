@@ -64,7 +64,9 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->pad0 = 0;
     ctr->kmin = ~0ull;
     ctr->kmax = 0ull;
-    ctr->bin_ticket = 0ull;
+    ctr->P = 0ull;
+    ctr->nseg = 0;
+    ctr->pad1 = 0;
 }
 
 template <typename ShT>
@@ -210,16 +212,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(SceneView sc, CameraArg
     }
 }
 
-// number of 8-bit LSD passes over (key - kmin): ceil(bits(kmax - kmin) / 8), >= 1
-__global__ void depth_passes_kernel(FrameCounters *ctr) {
-    uint32_t np = 1;
-    if (ctr->K > 1 && ctr->kmax > ctr->kmin) {
-        int bits = 64 - __clzll((long long)(ctr->kmax - ctr->kmin));
-        np = (uint32_t)((bits + 7) / 8);
-    }
-    ctr->npass = np;
-}
-
 }  // namespace
 
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
@@ -238,10 +230,6 @@ void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_deg
     else
         preprocess_kernel<double><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, frustum_cull,
                                                              keys, rec, keep_out, ctr);
-}
-
-void launch_depth_passes(FrameCounters *ctr, cudaStream_t s) {
-    depth_passes_kernel<<<1, 1, 0, s>>>(ctr);
 }
 
 }  // namespace gsr

@@ -1,270 +1,287 @@
-// radix.cu -- device-wide exclusive scan and a stable LSD radix sort pass.
+// radix.cu -- stable LSD radix sort, Onesweep style (one kernel per 8-bit
+// digit with decoupled look-back), for
+//   (a) the stable f64 depth sort replacing np.argsort(depths, kind="stable")
+//       (render.py:293-302): keys are the IEEE bits of z (> 0, so unsigned
+//       order == numeric order); values are Gaussian indices; the first pass
+//       drops culled Gaussians (sentinel key ~0), which is the
+//       order-preserving compaction of render.py:279;
+//   (b) the stable tile sort of the rank-major (tile, depth rank) list.
+// Stability gives the reference's tie order (equal depths keep index order).
 //
-// Used for (a) the stable f64 depth sort that replaces
-// np.argsort(depths, kind="stable") (render.py:293-302) -- keys are the IEEE
-// bits of z (> 0, so unsigned order == numeric order), ties keep index order
-// because every pass is stable and the first pass reads in index order; and
-// (b) the stable tile sort of the (tile, depth-rank) list.
-//
-// Pass structure (per 8-bit digit): upsweep (per-tile digit histograms,
-// digit-major) -> exclusive scan -> downsweep (stable in-tile ranking with
-// warp match_any, shared-memory staging, coalesced scatter).  Item counts
-// are read from device memory so a whole frame is enqueued without host
-// synchronisation; grids are sized from capacities and idle tiles exit.
+// Per sort: one histogram kernel computes every pass's digit histogram in one
+// read of the keys; a 1-block plan kernel turns them into global digit
+// offsets and marks passes whose digit is constant as inactive (skipped: an
+// identity permutation), recording which ping-pong buffer each active pass
+// reads.  Each pass: a block takes a 4096-key tile in ticket order, ranks its
+// keys stably (warp match_any + per-warp digit counters), publishes its digit
+// counts, looks back over predecessor tiles per digit for its global
+// position, and scatters through shared memory so global writes are
+// coalesced runs.  Counts come from device memory: no host synchronisation.
 #include "kernels.cuh"
+#include "scan.cuh"
 
 namespace gsr {
 
 namespace {
 
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kScanChunk = kScanThreads * kScanItems;
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-    }
-    return v;
-}
-
-// exclusive block scan over blockDim.x (multiple of 32, <= 1024) values
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp,
-                                                    uint32_t *total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nw = blockDim.x >> 5;
-    uint32_t inc = warp_incl_scan(v);
-    if (lane == 31) s_warp[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        uint32_t x = lane < nw ? s_warp[lane] : 0u;
-        uint32_t xi = warp_incl_scan(x);
-        if (lane < nw) s_warp[lane] = xi - x;
-        if (lane == nw - 1) s_warp[32] = xi;
-    }
-    __syncthreads();
-    uint32_t r = s_warp[w] + inc - v;
-    if (total) *total = s_warp[32];
-    __syncthreads();
-    return r;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t *in, int64_t n,
-                                                                   uint32_t *partials) {
-    const int64_t base = (int64_t)blockIdx.x * kScanChunk;
-    uint32_t s = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        int64_t idx = base + j * kScanThreads + threadIdx.x;
-        if (idx < n) s += in[idx];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    __shared__ uint32_t sw[kScanThreads / 32];
-    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < kScanThreads / 32; w++) t += sw[w];
-        partials[blockIdx.x] = t;
-    }
-}
-
-// single block, 1024 threads: in-place exclusive scan of the partials
-__global__ void __launch_bounds__(1024) scan_partials_kernel(uint32_t *partials, int64_t m,
-                                                             uint32_t *total) {
-    __shared__ uint32_t s_warp[33];
-    uint32_t carry = 0;
-    for (int64_t base = 0; base < m; base += 1024) {
-        int64_t idx = base + threadIdx.x;
-        uint32_t v = idx < m ? partials[idx] : 0u;
-        uint32_t tot;
-        uint32_t ex = block_excl_scan(v, s_warp, &tot);
-        if (idx < m) partials[idx] = carry + ex;
-        carry += tot;
-    }
-    if (threadIdx.x == 0 && total) *total = carry;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t *in, uint32_t *out,
-                                                                 int64_t n,
-                                                                 const uint32_t *partials) {
-    __shared__ uint32_t s_warp[33];
-    const int64_t base = (int64_t)blockIdx.x * kScanChunk;
-    // blocked arrangement: thread t owns items [base + t*8, base + t*8 + 8)
-    uint32_t v[kScanItems];
-    uint32_t s = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        int64_t idx = base + (int64_t)threadIdx.x * kScanItems + j;
-        v[j] = idx < n ? in[idx] : 0u;
-        s += v[j];
-    }
-    uint32_t ex = block_excl_scan(s, s_warp, nullptr) + partials[blockIdx.x];
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        int64_t idx = base + (int64_t)threadIdx.x * kScanItems + j;
-        if (idx < n) out[idx] = ex;
-        ex += v[j];
-    }
-}
-
-// ---------------------------------------------------------------- radix ----
 constexpr int RB = kRadixThreads;
-constexpr int RI = kRadixItems;
-constexpr int RT = kRadixTile;
 constexpr int RW = RB / 32;
+template <typename K>
+struct Cfg {
+    static constexpr int RI = radix_items((int)sizeof(K));  // items per thread
+    static constexpr int RT = RB * RI;                      // items per tile
+};
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1u;
 
 template <typename K>
 __device__ __forceinline__ K sentinel() { return (K)~(K)0; }
 
+// Look-back status words carry flag and count in one 32-bit word, so relaxed
+// GPU-scope accesses suffice (acquire would emit an L1 invalidate, CCTL.IVALL,
+// on every poll).
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <typename K>
-struct PassArgs {
-    const K *kin;
-    const uint32_t *vin;
-    K *kout;
-    uint32_t *vout;
-    const uint32_t *n_dev;
-    int64_t n_cap;
-    int shift;
-    const unsigned long long *key_base;
-    const uint32_t *npass_dev;
-    int pass_index;
-    int drop_sentinel;
-    uint32_t *hist;
-    int64_t ntiles;
+struct SortArgs {
+    K *keys[2];
+    uint32_t *vals[2];
+    int implicit_first_vals;   // first pass: value = input index
+    int drop_sentinel;         // first pass: drop keys == ~0
+    const uint32_t *n_dev;     // items after the first pass (nullable -> n_first)
+    int64_t n_first;           // items read by the first pass
+    int64_t n_cap;             // capacity for n_dev
+    int64_t tiles;             // tiles per pass (grid)
+    int passes;
+    int force_first;           // pass 0 always active (compaction)
+    uint32_t *hist;            // [passes][256]: histogram, then exclusive offsets
+    uint32_t *status;          // [passes][tiles][256]
+    uint32_t *tickets;         // [passes]
+    uint32_t *sched;           // [0..7] active, [8..15] src buffer, [16] final buffer
+    uint32_t *npass_out;       // nullable: number of active passes
 };
 
 template <typename K>
-__device__ __forceinline__ bool pass_skipped(const PassArgs<K> &p) {
-    return p.npass_dev && (uint32_t)p.pass_index >= *p.npass_dev;
+__device__ __forceinline__ int64_t first_count(const SortArgs<K> &a) {
+    if (a.n_first >= 0) return a.n_first;
+    int64_t n = (int64_t)*a.n_dev;
+    return n < a.n_cap ? n : a.n_cap;
 }
 
 template <typename K>
-__device__ __forceinline__ int64_t pass_count(const PassArgs<K> &p) {
-    if (!p.n_dev) return p.n_cap;
-    int64_t n = (int64_t)*p.n_dev;
-    return n < p.n_cap ? n : p.n_cap;
+__device__ __forceinline__ int64_t items_after_first(const SortArgs<K> &a) {
+    if (!a.n_dev) return a.n_first;
+    int64_t n = (int64_t)*a.n_dev;
+    return n < a.n_cap ? n : a.n_cap;
 }
 
 template <typename K>
-__device__ __forceinline__ uint32_t digit_of(K k, K base, int shift) {
-    return (uint32_t)(((K)(k - base)) >> shift) & 255u;
-}
-
-template <typename K>
-__global__ void __launch_bounds__(RB) radix_upsweep_kernel(PassArgs<K> p) {
-    if (pass_skipped(p)) return;
-    __shared__ uint32_t h[RW][256];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int j = threadIdx.x; j < RW * 256; j += RB) (&h[0][0])[j] = 0;
+__global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
+    __shared__ uint32_t h[8][256];
+    for (int j = threadIdx.x; j < 8 * 256; j += RB) (&h[0][0])[j] = 0;
     __syncthreads();
-    const int64_t n = pass_count(p);
-    const int64_t base = (int64_t)blockIdx.x * RT + (int64_t)w * (RI * 32);
-    const K kb = p.key_base ? (K)*p.key_base : (K)0;
-    if ((int64_t)blockIdx.x * RT < n) {
-#pragma unroll 4
-        for (int r = 0; r < RI; r++) {
-            const int64_t idx = base + r * 32 + lane;
-            bool valid = idx < n;
-            K k = valid ? p.kin[idx] : (K)0;
-            if (p.drop_sentinel && k == sentinel<K>()) valid = false;
-            const uint32_t act = __ballot_sync(0xffffffffu, valid);
-            if (valid) {
-                const uint32_t d = digit_of(k, kb, p.shift);
-                const uint32_t peers = __match_any_sync(act, d);
-                if (lane == __ffs(peers) - 1) h[w][d] += __popc(peers);
-            }
-            __syncwarp();
+    const int64_t n = first_count(a);
+    const K *keys = a.keys[0];
+    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        const K k = keys[i];
+        if (a.drop_sentinel && k == sentinel<K>()) continue;
+#pragma unroll
+        for (int p = 0; p < (int)sizeof(K); p++)
+            if (p < a.passes) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < a.passes * 256; j += RB) {
+        const uint32_t c = (&h[0][0])[j];
+        if (c) atomicAdd(a.hist + j, c);
+    }
+}
+
+// 1 block x 256 threads: per-pass exclusive digit offsets + pass schedule
+template <typename K>
+__global__ void __launch_bounds__(256) radix_plan_kernel(SortArgs<K> a) {
+    __shared__ uint32_t s_warp[33];
+    __shared__ int s_active[8];
+    const int d = threadIdx.x;
+    for (int p = 0; p < a.passes; p++) {
+        const uint32_t c = a.hist[p * 256 + d];
+        const int nz = __syncthreads_count(c != 0u);
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_u32(c, s_warp, &tot);
+        a.hist[p * 256 + d] = ex;
+        if (d == 0) s_active[p] = (nz > 1) || (p == 0 && a.force_first);
+    }
+    __syncthreads();
+    if (d == 0) {
+        int cur = 0;
+        for (int p = 0; p < 8; p++) {
+            const int act = p < a.passes ? s_active[p] : 0;
+            a.sched[p] = (uint32_t)act;
+            a.sched[8 + p] = (uint32_t)cur;
+            cur ^= act;
+        }
+        a.sched[16] = (uint32_t)cur;
+        if (a.npass_out) {
+            uint32_t np = 0;
+            for (int p = 0; p < a.passes; p++) np += (uint32_t)s_active[p];
+            *a.npass_out = np;
         }
     }
-    __syncthreads();
-    for (int d = threadIdx.x; d < 256; d += RB) {
-        uint32_t s = 0;
-#pragma unroll
-        for (int j = 0; j < RW; j++) s += h[j][d];
-        p.hist[(int64_t)d * p.ntiles + blockIdx.x] = s;
-    }
 }
 
 template <typename K>
-struct DownSmem {
-    K keys[RT];
-    uint32_t vals[RT];
+struct PassSmem {
+    K keys[Cfg<K>::RT];
+    uint32_t vals[Cfg<K>::RT];
     uint32_t wcnt[RW][256];
+    uint32_t hcnt[256];
     uint32_t dstart[256];
     uint32_t gbase[256];
     uint32_t s_warp[33];
     uint32_t tile_n;
+    uint32_t ticket;
 };
 
 template <typename K>
-__global__ void __launch_bounds__(RB) radix_downsweep_kernel(PassArgs<K> p) {
-    if (pass_skipped(p)) return;
-    const int64_t n = pass_count(p);
-    if ((int64_t)blockIdx.x * RT >= n) return;
+__global__ void __launch_bounds__(RB, 4) onesweep_pass_kernel(SortArgs<K> a, int pass) {
+    constexpr int RI = Cfg<K>::RI, RT = Cfg<K>::RT;
+    if (!a.sched[pass]) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    DownSmem<K> &S = *reinterpret_cast<DownSmem<K> *>(smem_raw);
+    PassSmem<K> &S = *reinterpret_cast<PassSmem<K> *>(smem_raw);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint32_t src = a.sched[8 + pass];
+    // first active pass: reads the producer's buffer (0) with n_first items
+    bool first = true;
+    for (int p = 0; p < pass; p++) first = first && !a.sched[p];
+    const int64_t n = first ? first_count(a) : items_after_first(a);
+    if (threadIdx.x == 0) S.ticket = atomicAdd(a.tickets + pass, 1u);
     for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wcnt[0][0])[j] = 0;
-    for (int d = threadIdx.x; d < 256; d += RB) S.gbase[d] = p.hist[(int64_t)d * p.ntiles + blockIdx.x];
+    S.hcnt[threadIdx.x] = 0;
     __syncthreads();
+    const int64_t t = S.ticket;
+    if (t * RT >= n) return;
+    uint32_t *st = a.status + ((int64_t)pass * a.tiles) * 256;
+    // (ternaries, not a.keys[src]: runtime-indexed param arrays go to local memory)
+    const K *kin = src ? a.keys[1] : a.keys[0];
+    const uint32_t *vin = (first && a.implicit_first_vals) ? nullptr : (src ? a.vals[1] : a.vals[0]);
+    K *kout = src ? a.keys[0] : a.keys[1];
+    uint32_t *vout = src ? a.vals[0] : a.vals[1];
+    const bool drop = first && a.drop_sentinel;
+    const int shift = 8 * pass;
+    const uint32_t lt_mask = (1u << lane) - 1u;
 
-    const K kb = p.key_base ? (K)*p.key_base : (K)0;
-    const int64_t base = (int64_t)blockIdx.x * RT + (int64_t)w * (RI * 32);
+    // ---- stable in-tile ranking ----------------------------------------
+    const int64_t base = t * RT + (int64_t)w * (RI * 32);
     K keys[RI];
     uint32_t vals[RI];
     uint32_t loc[RI];
     uint32_t valid_bits = 0;
+    // all loads first (RI independent requests in flight per thread)
 #pragma unroll
     for (int r = 0; r < RI; r++) {
         const int64_t idx = base + r * 32 + lane;
-        bool valid = idx < n;
-        K k = valid ? p.kin[idx] : (K)0;
-        if (p.drop_sentinel && k == sentinel<K>()) valid = false;
-        keys[r] = k;
-        vals[r] = valid ? (p.vin ? p.vin[idx] : (uint32_t)idx) : 0u;
+        keys[r] = idx < n ? __ldg(kin + idx) : sentinel<K>();
+        vals[r] = idx < n ? (vin ? __ldg(vin + idx) : (uint32_t)idx) : 0u;
+        if (idx < n && !(drop && keys[r] == sentinel<K>())) valid_bits |= 1u << r;
+    }
+    // tile digit counts first, published as aggregates before the (slower)
+    // stable ranking so successors' look-back can proceed meanwhile
+#pragma unroll
+    for (int r = 0; r < RI; r++)
+        if ((valid_bits >> r) & 1u) atomicAdd(&S.hcnt[(uint32_t)(keys[r] >> shift) & 255u], 1u);
+    __syncthreads();
+    const uint32_t tot = S.hcnt[threadIdx.x];
+    if (t > 0) st_release_u32(st + t * 256 + threadIdx.x, kFlagAgg | tot);
+    // peers of every round first (independent MATCH ops pipeline), then one
+    // shared atomic per (round, digit group) by its leader -- a warp's
+    // shared-memory atomics to one address complete in program order, so the
+    // returned prior counts are stable -- broadcast with a shuffle
+    uint32_t peers[RI];
+#pragma unroll
+    for (int r = 0; r < RI; r++) {
+        const bool valid = (valid_bits >> r) & 1u;
         const uint32_t act = __ballot_sync(0xffffffffu, valid);
-        uint32_t prior = 0, peers = 0, d = 0;
-        if (valid) {
-            d = digit_of(k, kb, p.shift);
-            peers = __match_any_sync(act, d);
-            prior = S.wcnt[w][d];
-            loc[r] = prior + __popc(peers & lt_mask);
-            valid_bits |= 1u << r;
-        } else {
-            loc[r] = 0;
-        }
-        __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) S.wcnt[w][d] = prior + __popc(peers);
-        __syncwarp();
+        peers[r] = valid ? __match_any_sync(act, (uint32_t)(keys[r] >> shift) & 255u) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < RI; r++) {
+        const bool valid = (valid_bits >> r) & 1u;
+        const int leader = valid ? __ffs(peers[r]) - 1 : lane;
+        uint32_t old = 0;
+        if (valid && lane == leader)
+            old = atomicAdd(&S.wcnt[w][(uint32_t)(keys[r] >> shift) & 255u], __popc(peers[r]));
+        const uint32_t base = __shfl_sync(0xffffffffu, old, leader);
+        loc[r] = valid ? base + __popc(peers[r] & lt_mask) : 0u;
     }
     __syncthreads();
-    // per digit: exclusive prefix over warps, tile totals, then scan over digits
-    uint32_t tot = 0;
-    for (int d = threadIdx.x; d < 256; d += RB) {
+    {
+        const int d = threadIdx.x;
         uint32_t run = 0;
 #pragma unroll
         for (int j = 0; j < RW; j++) {
-            uint32_t c = S.wcnt[j][d];
+            const uint32_t c = S.wcnt[j][d];
             S.wcnt[j][d] = run;
             run += c;
         }
-        tot = run;
+    }
+    // ---- publish tile counts, look back per digit ----------------------
+    // One thread per digit walks back over predecessor tiles kLbWindow at a
+    // time (independent loads in flight), summing aggregates until it meets
+    // an inclusive prefix.
+    {
+        constexpr int kLbWindow = 8;
+        const int d = threadIdx.x;
+#ifdef GSR_RADIX_NO_LOOKBACK  // microbenchmark only (tools/radix_bench.cu): wrong output
+        if (true) {
+#else
+        if (t == 0) {
+#endif
+            st_release_u32(st + d, kFlagInc | tot);
+            S.gbase[d] = a.hist[pass * 256 + d];
+        } else {
+            uint32_t excl = 0;
+            int64_t tp = t - 1;
+            while (true) {
+                uint32_t s[kLbWindow];
+#pragma unroll
+                for (int i = 0; i < kLbWindow; i++)
+                    s[i] = tp - i >= 0 ? ld_acquire_u32(st + (tp - i) * 256 + d) : kFlagInc;
+                int used = 0;
+                bool done = false;
+#pragma unroll
+                for (int i = 0; i < kLbWindow; i++) {
+                    if (done || used < i) continue;  // stop at the first gap
+                    const uint32_t f = s[i] >> 30;
+                    if (f == 0u) continue;           // not published yet: retry from here
+                    excl += s[i] & kValMask;
+                    used = i + 1;
+                    if (f == 2u) done = true;
+                }
+                if (done) break;
+                tp -= used;
+            }
+            st_release_u32(st + t * 256 + d, kFlagInc | (excl + tot));
+            S.gbase[d] = a.hist[pass * 256 + d] + excl;
+        }
     }
     uint32_t tile_total;
-    const uint32_t ds = block_excl_scan(threadIdx.x < 256 ? tot : 0u, S.s_warp, &tile_total);
-    if (threadIdx.x < 256) S.dstart[threadIdx.x] = ds;
+    const uint32_t ds = block_excl_scan_u32(tot, S.s_warp, &tile_total);
+    S.dstart[threadIdx.x] = ds;
     if (threadIdx.x == 0) S.tile_n = tile_total;
     __syncthreads();
+    // ---- scatter through shared memory, then coalesced runs ------------
 #pragma unroll
     for (int r = 0; r < RI; r++) {
         if (valid_bits & (1u << r)) {
-            const uint32_t d = digit_of(keys[r], kb, p.shift);
+            const uint32_t d = (uint32_t)(keys[r] >> shift) & 255u;
             const uint32_t pos = S.dstart[d] + S.wcnt[w][d] + loc[r];
             S.keys[pos] = keys[r];
             S.vals[pos] = vals[r];
@@ -274,73 +291,92 @@ __global__ void __launch_bounds__(RB) radix_downsweep_kernel(PassArgs<K> p) {
     const uint32_t tn = S.tile_n;
     for (uint32_t i = threadIdx.x; i < tn; i += RB) {
         const K k = S.keys[i];
-        const uint32_t d = digit_of(k, kb, p.shift);
+        const uint32_t d = (uint32_t)(k >> shift) & 255u;
         const uint32_t o = S.gbase[d] + (i - S.dstart[d]);
-        p.kout[o] = k;
-        p.vout[o] = S.vals[i];
+        kout[o] = k;
+        vout[o] = S.vals[i];
     }
 }
 
 }  // namespace
 
-// per-device kernel attributes; called once per context after cudaSetDevice
 cudaError_t radix_init_attributes() {
-    cudaError_t e = cudaFuncSetAttribute(radix_downsweep_kernel<unsigned long long>,
+    cudaError_t e = cudaFuncSetAttribute(onesweep_pass_kernel<unsigned long long>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(DownSmem<unsigned long long>));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(radix_downsweep_kernel<uint32_t>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(DownSmem<uint32_t>));
+                                         (int)sizeof(PassSmem<unsigned long long>));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(onesweep_pass_kernel<uint32_t>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(PassSmem<uint32_t>));
+    // maximum shared-memory carveout so occupancy is register-limited, not smem-limited
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(onesweep_pass_kernel<unsigned long long>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(onesweep_pass_kernel<uint32_t>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return e;
 }
 
-int64_t scan_partials_needed(int64_t n) { return (n + kScanChunk - 1) / kScanChunk + 1; }
-
-void launch_scan_exclusive(const uint32_t *in, uint32_t *out, int64_t n, uint32_t *total,
-                           const ScanWorkspace &ws, cudaStream_t s) {
-    if (n <= 0) return;
-    const int64_t blocks = (n + kScanChunk - 1) / kScanChunk;
-    scan_reduce_kernel<<<(unsigned)blocks, kScanThreads, 0, s>>>(in, n, ws.partials);
-    scan_partials_kernel<<<1, 1024, 0, s>>>(ws.partials, blocks, total);
-    scan_down_kernel<<<(unsigned)blocks, kScanThreads, 0, s>>>(in, out, n, ws.partials);
+size_t sort_work_bytes(int64_t n_items_cap, int passes, int key_bytes) {
+    const int64_t tiles = radix_tiles(n_items_cap, key_bytes);
+    return sizeof(uint32_t) * ((size_t)passes * 256 + (size_t)passes * tiles * 256 + 8 + 32);
 }
 
 template <typename K>
-void launch_radix_pass(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout,
-                       const uint32_t *n_dev, int64_t n_cap, int shift,
-                       const unsigned long long *key_base, const uint32_t *npass_dev,
-                       int pass_index, bool drop_sentinel, uint32_t *hist,
-                       const ScanWorkspace &ws, cudaStream_t s) {
-    if (n_cap <= 0) return;
-    PassArgs<K> p;
-    p.kin = kin;
-    p.vin = vin;
-    p.kout = kout;
-    p.vout = vout;
-    p.n_dev = n_dev;
-    p.n_cap = n_cap;
-    p.shift = shift;
-    p.key_base = key_base;
-    p.npass_dev = npass_dev;
-    p.pass_index = pass_index;
-    p.drop_sentinel = drop_sentinel ? 1 : 0;
-    p.hist = hist;
-    p.ntiles = radix_tiles(n_cap);
-    radix_upsweep_kernel<K><<<(unsigned)p.ntiles, RB, 0, s>>>(p);
-    launch_scan_exclusive(hist, hist, 256 * p.ntiles, nullptr, ws, s);
-    const size_t smem = sizeof(DownSmem<K>);
-    radix_downsweep_kernel<K><<<(unsigned)p.ntiles, RB, smem, s>>>(p);
+int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
+                         bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
+                         int64_t n_first, int64_t n_cap, int passes, bool force_first,
+                         void *work, uint32_t *sched, uint32_t *npass_out, int sms,
+                         cudaStream_t s) {
+    SortArgs<K> a;
+    a.keys[0] = keys0;
+    a.keys[1] = keys1;
+    a.vals[0] = vals0;
+    a.vals[1] = vals1;
+    a.implicit_first_vals = implicit_first_vals ? 1 : 0;
+    a.drop_sentinel = drop_sentinel ? 1 : 0;
+    a.n_dev = n_dev;
+    a.n_first = n_first;
+    a.n_cap = n_cap;
+    const int64_t n_items_cap = n_first > n_cap ? n_first : n_cap;  // n_first < 0: from n_dev
+    a.tiles = radix_tiles(n_items_cap, (int)sizeof(K));
+    a.passes = passes;
+    a.force_first = force_first ? 1 : 0;
+    uint32_t *w = reinterpret_cast<uint32_t *>(work);
+    a.hist = w;
+    a.status = w + passes * 256;
+    a.tickets = a.status + (size_t)passes * a.tiles * 256;
+    a.sched = sched;
+    a.npass_out = npass_out;
+    cudaMemsetAsync(work, 0, sort_work_bytes(n_items_cap, passes, (int)sizeof(K)), s);
+    int launches = 0;
+    if (n_items_cap > 0) {
+        int64_t hb = (n_items_cap + RB * 16 - 1) / (RB * 16);
+        if (hb > sms * 4) hb = sms * 4;
+        if (hb < 1) hb = 1;
+        radix_hist_kernel<K><<<(unsigned)hb, RB, 0, s>>>(a);
+        launches++;
+    }
+    radix_plan_kernel<K><<<1, 256, 0, s>>>(a);
+    launches++;
+    if (n_items_cap > 0) {
+        for (int p = 0; p < passes; p++) {
+            onesweep_pass_kernel<K><<<(unsigned)a.tiles, RB, sizeof(PassSmem<K>), s>>>(a, p);
+            launches++;
+        }
+    }
+    return launches;
 }
 
-template void launch_radix_pass<unsigned long long>(const unsigned long long *, const uint32_t *,
-                                                    unsigned long long *, uint32_t *,
-                                                    const uint32_t *, int64_t, int,
-                                                    const unsigned long long *, const uint32_t *,
-                                                    int, bool, uint32_t *, const ScanWorkspace &,
-                                                    cudaStream_t);
-template void launch_radix_pass<uint32_t>(const uint32_t *, const uint32_t *, uint32_t *,
-                                          uint32_t *, const uint32_t *, int64_t, int,
-                                          const unsigned long long *, const uint32_t *, int,
-                                          bool, uint32_t *, const ScanWorkspace &, cudaStream_t);
+template int launch_onesweep_sort<unsigned long long>(unsigned long long *, unsigned long long *,
+                                                      uint32_t *, uint32_t *, bool, bool,
+                                                      const uint32_t *, int64_t, int64_t, int,
+                                                      bool, void *, uint32_t *, uint32_t *,
+                                                      int, cudaStream_t);
+template int launch_onesweep_sort<uint32_t>(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool,
+                                            bool, const uint32_t *, int64_t, int64_t, int, bool,
+                                            void *, uint32_t *, uint32_t *, int,
+                                            cudaStream_t);
 
 }  // namespace gsr

@@ -45,13 +45,15 @@ constexpr unsigned long long kLbAggregate = 1ull << 62;
 constexpr unsigned long long kLbInclusive = 2ull << 62;
 constexpr unsigned long long kLbValueMask = (1ull << 62) - 1;
 
+// flag and value share one 64-bit word: relaxed GPU-scope accesses suffice
+// (acquire loads would invalidate L1 on every poll)
 __device__ __forceinline__ void lb_store(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long lb_load(const unsigned long long *p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 

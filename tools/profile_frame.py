@@ -1,0 +1,16 @@
+"""Render a few config-3 frames (for ncu captures): python tools/profile_frame.py [n_frames]."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import bench  # noqa: E402
+import paper_2605_08699_b200 as g  # noqa: E402
+
+wl = bench.WORKLOADS[sys.argv[2] if len(sys.argv) > 2 else "config3"]
+prims = bench.build_scene(wl)
+intr = bench.intrinsics(wl)
+poses = bench.poses_for(0, int(sys.argv[1]) if len(sys.argv) > 1 else 3)
+st = g.RenderStats()
+for p in poses:
+    g.render_u8(prims, p, intr, sh_degree=wl["sh"], stats=st)
+print("frames", len(poses), "drawn", st.splats_drawn, "D", st.tile_keys)
