@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) row_scan_kernel(BinArgs a) {
 
 // ---------------------------------------------------------------- 1c -------
 struct PairSmem {
-    float u[BR], v[BR], ia[BR], ib[BR], ic[BR], rsq[BR];
+    float u[BR], v[BR], ia[BR], ib[BR], ic[BR], rsq[BR], rinv[BR];
     int lo[BR], hi[BR];
     uint32_t poff[BR + 1];
     uint32_t s_warp[33];
@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     int lo = 0, hi = 0;
     if (r < k) {
         const float4 A = __ldg(&a.srec[r].a), B = __ldg(&a.srec[r].b);
+        S.rinv[tid] = splat_fast_ok(A.y, A.z, A.w) ? __ldg(&a.srec[r].c.w) : 0.0f;
         row_range(A.y, B.w, a.height, lo, hi);
         S.u[tid] = A.x;
         S.v[tid] = A.y;
@@ -222,14 +223,43 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
         int mn = 0x7fffffff, mx = -0x7fffffff;
         const float u = S.u[j], v = S.v[j], ia = S.ia[j], ib = S.ib[j], ic = S.ic[j],
-                    rsq = S.rsq[j];
-        for (int y = y0; y < y1; y++) {
-            int x0, x1;
-            if (row_interval(u, v, ia, ib, ic, rsq, (float)y + 0.5f, a.width, x0, x1)) {
-                x0 = x0 > 0 ? x0 : 0;
-                if (x0 < x1) {
-                    mn = x0 < mn ? x0 : mn;
-                    mx = x1 > mx ? x1 : mx;
+                    rsq = S.rsq[j], rinv = S.rinv[j];
+        // fast exact path: min/max of the float interval ends over the rows
+        // whose interval meets [0, W) (floor/ceil are monotone, so one
+        // conversion per pair); rows with NaN/huge values take row_interval
+        bool slow = rinv == 0.0f;
+        if (!slow) {
+            float fmn = __int_as_float(0x7f800000), fmx = -__int_as_float(0x7f800000);
+            const float wf = (float)a.width;
+            for (int y = y0; y < y1; y++) {
+                float xl, xr;
+                const int k = row_xlr(u, v, ia, ib, ic, rsq, rinv, (float)y + 0.5f, xl, xr);
+                if (k < 0) slow = true;
+                if (k > 0 && xl < wf && xr > -1.0f) {
+                    fmn = fminf(fmn, xl);
+                    fmx = fmaxf(fmx, xr);
+                }
+            }
+            if (fmn <= fmx) {
+                if (fabsf(fmn) < 0x1p30f && fabsf(fmx) < 0x1p30f) {
+                    mn = max(0, __float2int_rd(fmn));
+                    mx = min(a.width, __float2int_ru(fmx) + 1);
+                } else {
+                    slow = true;
+                }
+            }
+        }
+        if (slow) {
+            mn = 0x7fffffff;
+            mx = -0x7fffffff;
+            for (int y = y0; y < y1; y++) {
+                int x0, x1;
+                if (row_interval(u, v, ia, ib, ic, rsq, (float)y + 0.5f, a.width, x0, x1)) {
+                    x0 = x0 > 0 ? x0 : 0;
+                    if (x0 < x1) {
+                        mn = x0 < mn ? x0 : mn;
+                        mx = x1 > mx ? x1 : mx;
+                    }
                 }
             }
         }

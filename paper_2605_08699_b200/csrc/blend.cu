@@ -16,10 +16,14 @@
 // Layout: one CTA per tile, 8 warps; warp w owns pixel rows 2w, 2w+1 of the
 // tile (lane & 15 = column, lane >> 4 = row).  A warp walks the tile list 32
 // splats at a time: lane j loads splat j's record (128-bit loads), computes
-// the two row intervals as a 32-bit coverage mask, then the warp iterates the
-// ballot of non-empty masks in depth order.  Warps leave as soon as all their
-// 32 pixels are saturated (warp-ballot early termination); no block barriers
-// in the loop.
+// its two row intervals (exact, row_xlr) as a 32-bit pixel-coverage mask and
+// stages the splat's per-row terms in shared memory (structure of arrays, so
+// any lane can read any splat without bank conflicts).  A 5-step shuffle
+// transpose turns the 32 splat masks into 32 per-pixel masks; each lane then
+// walks its OWN covering splats in depth order, so a warp iteration does
+// useful work on every lane that still has splats (not just on the lanes a
+// given splat covers).  Warps leave as soon as all their 32 pixels are
+// saturated (warp-vote early termination); no block barriers in the loop.
 #include "kernels.cuh"
 
 namespace gsr {
@@ -27,6 +31,7 @@ namespace gsr {
 namespace {
 
 constexpr int kBlendThreads = 256;
+constexpr int kWarps = kBlendThreads / 32;
 
 __device__ __forceinline__ uint32_t span_mask(int x0, int x1, int X) {
     // columns [x0, x1) intersected with [X, X+16), as a 16-bit mask
@@ -37,13 +42,93 @@ __device__ __forceinline__ uint32_t span_mask(int x0, int x1, int X) {
     return ((1u << b) - 1u) & ~((1u << a) - 1u);
 }
 
+// Coverage of one pixel row of the tile by one splat (render.py:329-333 row
+// range, 383-397 interval), as a 16-bit column mask.
+__device__ __forceinline__ uint32_t row_mask(const float4 &A, const float4 &B, float rinv, bool fast,
+                                             int iy, int lo, int hi, int X, int width) {
+    if (iy < lo || iy >= hi) return 0u;
+    const float py = (float)iy + 0.5f;
+    if (fast) {
+        float xl, xr;
+        const int k = row_xlr(A.x, A.y, A.z, A.w, B.x, B.y, rinv, py, xl, xr);
+        if (k == 0) return 0u;
+        if (k > 0 && fabsf(xl) < 0x1p30f && fabsf(xr) < 0x1p30f)
+            return span_mask(__float2int_rd(xl), min(__float2int_ru(xr) + 1, width), X);
+    }
+    int x0, x1;
+    if (!row_interval(A.x, A.y, A.z, A.w, B.x, B.y, py, width, x0, x1)) return 0u;
+    return span_mask(x0, x1, X);
+}
+
+// 32x32 bit-matrix transpose across a warp: on entry lane j holds row j
+// (bit p = element (j, p)); on exit lane p holds column p (bit j).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+#pragma unroll
+    for (int s = 16, k = 0; s >= 1; s >>= 1, k++) {
+        const uint32_t lo_mask = (s == 16) ? 0x0000ffffu : (s == 8) ? 0x00ff00ffu
+                               : (s == 4) ? 0x0f0f0f0fu : (s == 2) ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+        x = (lane & s) ? ((x & ~lo_mask) | ((y >> s) & lo_mask))
+                       : ((x & lo_mask) | ((y << s) & ~lo_mask));
+    }
+    return x;
+}
+
+// glibc expf constants (see common.cuh), in constant memory so the DFMAs take
+// them as operands instead of rematerialising 64-bit immediates per call
+__constant__ double kExpK[4] = {
+    0x1.71547652b82fep+0 * 32.0,                       // InvLn2N
+    0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0,         // C0
+    0x1.ebfce50fac4f3p-3 / 32.0 / 32.0,                // C1
+    0x1.62e42ff0c52d6p-1 / 32.0,                       // C2
+};
+
+__device__ __noinline__ float expf_special(float x, const unsigned long long *tab) {
+    return glibc_expf_tab(x, tab);
+}
+
+// glibc expf for |x| < 88 (its main path), table split into 32-bit halves in
+// shared memory (conflict-free per-lane lookups); other x go to the full
+// restatement.  Bit-identical to glibc_expf_tab.
+__device__ __forceinline__ float expf_blend(float x, const uint32_t *tlo, const uint32_t *thi,
+                                            const unsigned long long *tab) {
+    if (!(fabsf(x) < 88.0f)) return expf_special(x, tab);
+    const double kShift = 0x1.8p+52;
+    const double xd = (double)x;
+    double kd = __fma_rn(kExpK[0], xd, kShift);
+    const uint32_t ki = (uint32_t)__double2loint(kd);
+    kd = __dsub_rn(kd, kShift);
+    const double r = __fma_rn(kExpK[0], xd, -kd);
+    const uint32_t idx = ki & 31u;
+    unsigned long long t = ((unsigned long long)thi[idx] << 32) | tlo[idx];
+    t += (unsigned long long)(long long)(int)ki << 47;
+    const double sc = __longlong_as_double((long long)t);
+    const double z = __fma_rn(kExpK[1], r, kExpK[2]);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(kExpK[3], r, 1.0);
+    y = __fma_rn(z, r2, y);
+    y = __dmul_rn(y, sc);
+    return __double2float_rn(y);
+}
+
+struct WarpBatch {         // one warp's current 32 splats, structure of arrays
+    float u[32], ia[32], op[32], cr[32], cg[32], cb[32];
+    float cy[2][32], ibdy[2][32];  // per pixel row of the warp: (ic*dy)*dy, (2*ib)*dy
+};
+
 __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     const SplatRec *__restrict__ srec, const uint32_t *__restrict__ tile_vals,
     const uint2 *__restrict__ ranges, int width, int height, float bg0, float bg1, float bg2,
     BlendOut out) {
     __shared__ unsigned long long s_tab[32];
-    __shared__ float4 s_rec[kBlendThreads / 32][32][3];
-    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    __shared__ uint32_t s_tlo[32], s_thi[32];
+    __shared__ WarpBatch s_b[kWarps];
+    if (threadIdx.x < 32) {
+        const unsigned long long v = kExp2fTab[threadIdx.x];
+        s_tab[threadIdx.x] = v;
+        s_tlo[threadIdx.x] = (uint32_t)v;
+        s_thi[threadIdx.x] = (uint32_t)(v >> 32);
+    }
     __syncthreads();
 
     const int tiles_x = (width + kTile - 1) / kTile;
@@ -51,17 +136,17 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int X = tx * kTile;
     const int iy0 = ty * kTile + 2 * w;
-    const int iy = iy0 + (lane >> 4);
+    const int prow = lane >> 4;
+    const int iy = iy0 + prow;
     const int ix = X + (lane & 15);
     const bool inside = ix < width && iy < height;
     const float py0 = (float)iy0 + 0.5f, py1 = (float)(iy0 + 1) + 0.5f;
-    const float py = (float)iy + 0.5f;
     const float fx = (float)ix + 0.5f;
 
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
     const uint2 rg = ranges[blockIdx.x];
-    float4(*my)[3] = s_rec[w];
+    WarpBatch &B_ = s_b[w];
 
     for (uint32_t c = rg.x; c < rg.y; c += 32) {
         if (__all_sync(0xffffffffu, done)) break;
@@ -74,41 +159,46 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
             const float4 C = __ldg(&srec[r].c);
             int lo, hi;
             row_range(A.y, B.w, height, lo, hi);
-            int x0, x1;
-            if (iy0 >= lo && iy0 < hi &&
-                row_interval(A.x, A.y, A.z, A.w, B.x, B.y, py0, width, x0, x1))
-                mask = span_mask(x0, x1, X);
-            if (iy0 + 1 >= lo && iy0 + 1 < hi &&
-                row_interval(A.x, A.y, A.z, A.w, B.x, B.y, py1, width, x0, x1))
-                mask |= span_mask(x0, x1, X) << 16;
-            my[lane][0] = A;
-            my[lane][1] = B;
-            my[lane][2] = C;
+            const bool fast = splat_fast_ok(A.y, A.z, A.w);
+            mask = row_mask(A, B, C.w, fast, iy0, lo, hi, X, width) |
+                   (row_mask(A, B, C.w, fast, iy0 + 1, lo, hi, X, width) << 16);
+            if (mask) {
+                const float ib2 = 2.0f * A.w;
+                const float dy0 = py0 - A.y, dy1 = py1 - A.y;
+                B_.u[lane] = A.x;
+                B_.ia[lane] = A.z;
+                B_.op[lane] = B.z;
+                B_.cr[lane] = C.x;
+                B_.cg[lane] = C.y;
+                B_.cb[lane] = C.z;
+                B_.cy[0][lane] = B.x * dy0 * dy0;
+                B_.cy[1][lane] = B.x * dy1 * dy1;
+                B_.ibdy[0][lane] = ib2 * dy0;
+                B_.ibdy[1][lane] = ib2 * dy1;
+            }
         }
         __syncwarp();
-        uint32_t act = __ballot_sync(0xffffffffu, mask != 0u);
-        while (act) {
-            const int src = __ffs(act) - 1;
-            act &= act - 1u;
-            const uint32_t mk = __shfl_sync(0xffffffffu, mask, src);
-            if (((mk >> lane) & 1u) && !done) {
-                const float4 A = my[src][0];
-                const float4 B = my[src][1];
-                const float4 C = my[src][2];
-                const float u = A.x, v = A.y, ia = A.z, ib = A.w, ic = B.x, op = B.z;
-                const float dy = py - v;
-                const float cy_term = ic * dy * dy;
-                const float ib_dy = 2.0f * ib * dy;
-                const float dx = fx - u;
-                const float power = -0.5f * (ia * dx * dx + ib_dy * dx + cy_term);
-                float alpha = op * glibc_expf_tab(power, s_tab);
+        uint32_t mine = transpose32(mask, lane);
+        if (done) mine = 0u;
+        while (__any_sync(0xffffffffu, mine != 0u)) {
+            if (mine) {
+                const int s = __ffs(mine) - 1;
+                mine &= mine - 1u;
+                // render.py:405-421, reference operation order
+                const float dx = fx - B_.u[s];
+                const float ia = B_.ia[s];
+                const float power = -0.5f * (ia * dx * dx + B_.ibdy[prow][s] * dx + B_.cy[prow][s]);
+                float alpha = B_.op[s] * expf_blend(power, s_tlo, s_thi, s_tab);
                 if (alpha > kAlphaMax) alpha = kAlphaMax;
                 const float weight = T * alpha;
-                cr += weight * C.x;
-                cg += weight * C.y;
-                cb += weight * C.z;
+                cr += weight * B_.cr[s];
+                cg += weight * B_.cg[s];
+                cb += weight * B_.cb[s];
                 T = T * (1.0f - alpha);
-                if (T < kTStop) done = true;
+                if (T < kTStop) {
+                    done = true;
+                    mine = 0u;
+                }
             }
         }
         __syncwarp();

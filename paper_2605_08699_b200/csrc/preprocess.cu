@@ -168,10 +168,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(SceneView sc, CameraArg
                 const double det = ca * cc - cb * cb;
                 const double rsq = __ldg(sc.rsq + i);
                 SplatRec o;
-                o.a = make_float4((float)u, (float)v, (float)(cc / det), (float)(-cb / det));
+                const float ia32 = (float)(cc / det);
+                o.a = make_float4((float)u, (float)v, ia32, (float)(-cb / det));
                 o.b = make_float4((float)(ca / det), (float)rsq, __ldg(sc.opac + i),
                                   (float)sqrt(cc * rsq));
-                o.c = make_float4(cr, cg, cbl, 0.0f);
+                o.c = make_float4(cr, cg, cbl, __frcp_rn(ia32));
                 rec[i] = o;
             }
         }

@@ -22,17 +22,26 @@ def ncu(args):
     return subprocess.run(["ncu", "-i", *args], capture_output=True, text=True).stdout
 
 
-def main(rep, top=12):
+def main(rep, top=12, only=None):
     rows = list(csv.reader(io.StringIO(ncu([rep, "--page", "raw", "--csv"]))))
     hdr, units = rows[0], rows[1]
     for k, r in enumerate(rows[2:]):
         name = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+        if only is not None and k not in only:
+            continue
         print(f"=== [{k}] {name}")
         for m in METRICS:
             if m in hdr:
                 i = hdr.index(m)
                 print(f"  {m:66s} {r[i]:>16s} {units[i]}")
-        src = ncu([rep, "--page", "source", "--csv", "--launch-skip", str(k), "--launch-count", "1"])
+        if only is not None and k not in only:
+            continue
+        try:
+            src = ncu([rep, "--page", "source", "--csv", "--launch-skip", str(k),
+                       "--launch-count", "1"])
+        except Exception as e:  # noqa: BLE001
+            print(f"    (source page unavailable: {e})")
+            continue
         srows = list(csv.reader(io.StringIO(src)))
         if len(srows) < 3:
             continue
@@ -50,4 +59,5 @@ def main(rep, top=12):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 12)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 12,
+         {int(x) for x in sys.argv[3].split(",")} if len(sys.argv) > 3 else None)
