@@ -61,10 +61,10 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
     if (b * BR < k && r < k) {
         const uint32_t *order = a.depth_sched[16] ? a.order1 : a.order0;
         const uint32_t i = __ldg(order + r);
-        const float4 A = __ldg(&a.rec[i].a), B = __ldg(&a.rec[i].b), C = __ldg(&a.rec[i].c);
+        const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b), C = __ldg(a.col + i);
         a.srec[r].a = A;
         a.srec[r].b = B;
-        a.srec[r].c = C;
+        a.srec[r].c = make_float4(C.x, C.y, C.z, __ldg(a.rinv + i));
         int lo, hi;
         row_range(A.y, B.w, a.height, lo, hi);
         if (lo < hi)
@@ -429,15 +429,25 @@ __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
     }
     __syncwarp();
     const uint32_t lt_mask = (1u << lane) - 1u;
+    // software pipeline: the next chunks' pairs are in flight while this
+    // chunk is placed (the loop is otherwise bound by that load's latency)
+    constexpr int kAhead = 4;
+    uint2 nxt[kAhead];
+#pragma unroll
+    for (int q = 0; q < kAhead; q++) {
+        const uint32_t pq = p0 + 32u * q + lane;
+        nxt[q] = pq < p1 ? a.pairs[pq] : make_uint2(0u, 0u);
+    }
     for (uint32_t c0 = p0; c0 < p1; c0 += 32) {
-        const uint32_t p = c0 + lane;
-        uint32_t rank = 0, a0 = 0, n = 0;  // covers columns [a0, a0 + n)
-        if (p < p1) {
-            const uint2 pr = a.pairs[p];
-            rank = pr.x;
-            a0 = pr.y & 0xffffu;
-            n = pr.y >> 16;
+        const uint2 pr = nxt[0];
+#pragma unroll
+        for (int q = 0; q + 1 < kAhead; q++) nxt[q] = nxt[q + 1];
+        {
+            const uint32_t pq = c0 + 32u * kAhead + lane;
+            nxt[kAhead - 1] = pq < p1 ? a.pairs[pq] : make_uint2(0u, 0u);
         }
+        // covers columns [a0, a0 + n) (n = 0 past the segment end)
+        const uint32_t rank = pr.x, a0 = pr.y & 0xffffu, n = pr.y >> 16;
         // 1: coverage mask of every column touched by the chunk
         for (uint32_t e = 0; e < n; e++) atomicOr(&mask[a0 + e], 1u << lane);
         __syncwarp();

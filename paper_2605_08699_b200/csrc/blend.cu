@@ -87,48 +87,44 @@ __device__ __noinline__ float expf_special(float x, const unsigned long long *ta
     return glibc_expf_tab(x, tab);
 }
 
-// glibc expf for |x| < 88 (its main path), table split into 32-bit halves in
-// shared memory (conflict-free per-lane lookups); other x go to the full
-// restatement.  Bit-identical to glibc_expf_tab.
-__device__ __forceinline__ float expf_blend(float x, const uint32_t *tlo, const uint32_t *thi,
-                                            const unsigned long long *tab) {
+// glibc expf for |x| < 88 (its main path) with the 2^(i/32) table in shared
+// memory; other x go to the full restatement.  Bit-identical to
+// glibc_expf_tab.
+struct ExpK {
+    double inv_ln2n, c0, c1, c2;
+};
+
+__device__ __forceinline__ float expf_blend(float x, const unsigned long long *tab,
+                                            const ExpK &K) {
     if (!(fabsf(x) < 88.0f)) return expf_special(x, tab);
     const double kShift = 0x1.8p+52;
     const double xd = (double)x;
-    double kd = __fma_rn(kExpK[0], xd, kShift);
+    double kd = __fma_rn(K.inv_ln2n, xd, kShift);
     const uint32_t ki = (uint32_t)__double2loint(kd);
     kd = __dsub_rn(kd, kShift);
-    const double r = __fma_rn(kExpK[0], xd, -kd);
-    const uint32_t idx = ki & 31u;
-    unsigned long long t = ((unsigned long long)thi[idx] << 32) | tlo[idx];
-    t += (unsigned long long)(long long)(int)ki << 47;
+    const double r = __fma_rn(K.inv_ln2n, xd, -kd);
+    const unsigned long long t = tab[ki & 31u] + ((unsigned long long)ki << 47);
     const double sc = __longlong_as_double((long long)t);
-    const double z = __fma_rn(kExpK[1], r, kExpK[2]);
+    const double z = __fma_rn(K.c0, r, K.c1);
     const double r2 = __dmul_rn(r, r);
-    double y = __fma_rn(kExpK[3], r, 1.0);
+    double y = __fma_rn(K.c2, r, 1.0);
     y = __fma_rn(z, r2, y);
     y = __dmul_rn(y, sc);
     return __double2float_rn(y);
 }
 
-struct WarpBatch {         // one warp's current 32 splats, structure of arrays
-    float u[32], ia[32], op[32], cr[32], cg[32], cb[32];
-    float cy[2][32], ibdy[2][32];  // per pixel row of the warp: (ic*dy)*dy, (2*ib)*dy
+struct WarpBatch {         // one warp's current 32 splats
+    float4 geo[2][32];     // per pixel row of the warp: (u, ia, (2*ib)*dy, (ic*dy)*dy)
+    float4 col[32];        // (op, r, g, b)
 };
 
-__global__ void __launch_bounds__(kBlendThreads) blend_kernel(
+__global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
     const SplatRec *__restrict__ srec, const uint32_t *__restrict__ tile_vals,
     const uint2 *__restrict__ ranges, int width, int height, float bg0, float bg1, float bg2,
     BlendOut out) {
     __shared__ unsigned long long s_tab[32];
-    __shared__ uint32_t s_tlo[32], s_thi[32];
     __shared__ WarpBatch s_b[kWarps];
-    if (threadIdx.x < 32) {
-        const unsigned long long v = kExp2fTab[threadIdx.x];
-        s_tab[threadIdx.x] = v;
-        s_tlo[threadIdx.x] = (uint32_t)v;
-        s_thi[threadIdx.x] = (uint32_t)(v >> 32);
-    }
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
     __syncthreads();
 
     const int tiles_x = (width + kTile - 1) / kTile;
@@ -147,6 +143,13 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
     bool done = !inside;
     const uint2 rg = ranges[blockIdx.x];
     WarpBatch &B_ = s_b[w];
+    const float4 *geo = B_.geo[prow];
+    // pinned in registers (opaque to rematerialisation by constant reloads)
+    ExpK ek;
+    asm volatile("mov.b64 %0, %1;" : "=d"(ek.inv_ln2n) : "d"(kExpK[0]));
+    asm volatile("mov.b64 %0, %1;" : "=d"(ek.c0) : "d"(kExpK[1]));
+    asm volatile("mov.b64 %0, %1;" : "=d"(ek.c1) : "d"(kExpK[2]));
+    asm volatile("mov.b64 %0, %1;" : "=d"(ek.c2) : "d"(kExpK[3]));
 
     for (uint32_t c = rg.x; c < rg.y; c += 32) {
         if (__all_sync(0xffffffffu, done)) break;
@@ -162,19 +165,12 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
             const bool fast = splat_fast_ok(A.y, A.z, A.w);
             mask = row_mask(A, B, C.w, fast, iy0, lo, hi, X, width) |
                    (row_mask(A, B, C.w, fast, iy0 + 1, lo, hi, X, width) << 16);
-            if (mask) {
+            if (mask) {  // render.py:400-402 terms per pixel row
                 const float ib2 = 2.0f * A.w;
                 const float dy0 = py0 - A.y, dy1 = py1 - A.y;
-                B_.u[lane] = A.x;
-                B_.ia[lane] = A.z;
-                B_.op[lane] = B.z;
-                B_.cr[lane] = C.x;
-                B_.cg[lane] = C.y;
-                B_.cb[lane] = C.z;
-                B_.cy[0][lane] = B.x * dy0 * dy0;
-                B_.cy[1][lane] = B.x * dy1 * dy1;
-                B_.ibdy[0][lane] = ib2 * dy0;
-                B_.ibdy[1][lane] = ib2 * dy1;
+                B_.geo[0][lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
+                B_.geo[1][lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
+                B_.col[lane] = make_float4(B.z, C.x, C.y, C.z);
             }
         }
         __syncwarp();
@@ -185,15 +181,16 @@ __global__ void __launch_bounds__(kBlendThreads) blend_kernel(
                 const int s = __ffs(mine) - 1;
                 mine &= mine - 1u;
                 // render.py:405-421, reference operation order
-                const float dx = fx - B_.u[s];
-                const float ia = B_.ia[s];
-                const float power = -0.5f * (ia * dx * dx + B_.ibdy[prow][s] * dx + B_.cy[prow][s]);
-                float alpha = B_.op[s] * expf_blend(power, s_tlo, s_thi, s_tab);
+                const float4 g = geo[s];  // u, ia, ib_dy, cy_term
+                const float4 k = B_.col[s];
+                const float dx = fx - g.x;
+                const float power = -0.5f * (g.y * dx * dx + g.z * dx + g.w);
+                float alpha = k.x * expf_blend(power, s_tab, ek);
                 if (alpha > kAlphaMax) alpha = kAlphaMax;
                 const float weight = T * alpha;
-                cr += weight * B_.cr[s];
-                cg += weight * B_.cg[s];
-                cb += weight * B_.cb[s];
+                cr += weight * k.y;
+                cg += weight * k.z;
+                cb += weight * k.w;
                 T = T * (1.0f - alpha);
                 if (T < kTStop) {
                     done = true;

@@ -1,0 +1,106 @@
+// depth.cu -- K3: the stable f64 depth order of sort_splats (render.py:293-302,
+// np.argsort(depths, kind="stable") over the kept splats, render.py:279).
+//
+// Exact order needs the full f64 keys (f32 keys misorder 22% of positions at
+// 3M Gaussians), but 8 radix passes over 64-bit keys are mostly wasted: the
+// kept depths span [kmin, kmax] and are nearly all distinct at 32-bit
+// resolution of that span.  So:
+//  1 key32   k32 = min((bits(z) - kmin) >> shift, 2^32 - 2), shift chosen so
+//            the span fits 32 bits; culled Gaussians keep the sentinel ~0.
+//            Positive f64 bits order like the values, and the map is monotone,
+//            so sorting k32 orders every pair of splats whose k32 differ.
+//  2 sort32  stable Onesweep radix sort of (k32, index), <= 4 passes (the
+//            first drops the sentinels: the compaction of render.py:279).
+//  3 fixup   splats with equal k32 form runs, already in index order
+//            (stability); each run is re-sorted by the full f64 key, stably
+//            (insertion sort by (key, index)), which gives exactly the
+//            argsort tie order.  A run longer than kMaxRun sets a flag...
+//  4 sort64  ...and only then does the full 64-bit sort run (its kernels exit
+//            immediately otherwise): exact for any input.
+#include "kernels.cuh"
+
+namespace gsr {
+
+namespace {
+
+constexpr int kMaxRun = 16;
+
+__global__ void depth_key32_kernel(const unsigned long long *__restrict__ k64,
+                                   uint32_t *__restrict__ k32, int64_t n,
+                                   const FrameCounters *__restrict__ ctr) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long kmin = ctr->kmin, kmax = ctr->kmax;
+    const unsigned long long range = kmax > kmin ? kmax - kmin : 0ull;
+    const int bits = range ? 64 - __clzll((long long)range) : 0;
+    const int shift = bits > 32 ? bits - 32 : 0;
+    const unsigned long long k = k64[i];
+    uint32_t o = 0xffffffffu;
+    if (k != ~0ull) {
+        const unsigned long long q = (k - kmin) >> shift;
+        o = q < 0xfffffffeull ? (uint32_t)q : 0xfffffffeu;
+    }
+    k32[i] = o;
+}
+
+__global__ void depth_fixup_kernel(DepthArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t K = a.ctr->K;
+    if (i >= K) return;
+    const uint32_t b = a.sched32[16];
+    const uint32_t *ks = b ? a.keys32[1] : a.keys32[0];
+    uint32_t *vs = b ? a.vals[1] : a.vals[0];
+    const uint32_t c = ks[i];
+    if (i + 1 >= K || ks[i + 1] != c) return;  // not followed by an equal key
+    if (i > 0 && ks[i - 1] == c) return;       // not the first of its run
+    int64_t e = i + 2;
+    while (e < K && e - i <= kMaxRun && ks[e] == c) e++;
+    const int len = (int)(e - i);
+    if (len > kMaxRun) {
+        atomicOr(&a.ctr->long_runs, 1u);
+        return;
+    }
+    uint32_t idx[kMaxRun];
+    unsigned long long key[kMaxRun];
+    for (int j = 0; j < len; j++) {
+        idx[j] = vs[i + j];
+        key[j] = a.keys64[0][idx[j]];
+    }
+    // stable insertion sort by key (indices enter in increasing order)
+    for (int j = 1; j < len; j++) {
+        const uint32_t xi = idx[j];
+        const unsigned long long xk = key[j];
+        int m = j - 1;
+        while (m >= 0 && key[m] > xk) {
+            key[m + 1] = key[m];
+            idx[m + 1] = idx[m];
+            m--;
+        }
+        key[m + 1] = xk;
+        idx[m + 1] = xi;
+    }
+    for (int j = 0; j < len; j++) vs[i + j] = idx[j];
+}
+
+}  // namespace
+
+size_t depth_work32_bytes(int64_t n_cap) { return sort_work_bytes(n_cap, 4, 4); }
+size_t depth_work64_bytes(int64_t n_cap) { return sort_work_bytes(n_cap, 8, 8); }
+
+int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s) {
+    if (a.n <= 0) return 0;
+    const unsigned g = (unsigned)((a.n + 255) / 256);
+    depth_key32_kernel<<<g, 256, 0, s>>>(a.keys64[0], a.keys32[0], a.n, a.ctr);
+    int launches = 1;
+    launches += launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
+                                               true, true, &a.ctr->K, a.n, a.n, 4, true, a.work32,
+                                               a.sched32, &a.ctr->npass, sms, s);
+    depth_fixup_kernel<<<g, 256, 0, s>>>(a);
+    launches++;
+    launches += launch_onesweep_sort<unsigned long long>(
+        a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, &a.ctr->K, a.n, a.n, 8, true,
+        a.work64, a.sched, &a.ctr->npass_fb, sms, s, &a.ctr->long_runs, a.sched32);
+    return launches;
+}
+
+}  // namespace gsr

@@ -86,9 +86,9 @@ struct gsr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int64_t cap_n = 0, cap_d = 0, cap_p = 0;
-    DevBuf keys[2], vals[2], rec, srec, keep;
+    DevBuf keys[2], vals[2], keys32[2], geo, rinv, col, srec, keep;
     int sms = 148;
-    DevBuf depth_work, sched;     // depth-sort scratch; sched[16] = result buffer
+    DevBuf depth_work, depth_work32, sched, sched32;  // depth-sort scratch; sched[16] = result buffer
     uint32_t *hsched = nullptr;   // pinned host copy of sched
     // tile-list buffers (binning.cu)
     DevBuf row_blk, row_start, scan_work, pairs, seg_row, seg_cnt, ttotal, tstart, tile_vals;
@@ -109,8 +109,8 @@ struct gsr_ctx {
     int retries = 0;
     int64_t bytes() const {
         int64_t s = 0;
-        const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &rec, &srec, &keep,
-                               &depth_work, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+        const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
+                               &geo, &rinv, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &sched32, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w};
@@ -179,8 +179,11 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
         for (int i = 0; i < 2; i++) {
             if ((rc = ensure(c->keys[i], sizeof(unsigned long long) * cap))) return rc;
             if ((rc = ensure(c->vals[i], sizeof(uint32_t) * cap))) return rc;
+            if ((rc = ensure(c->keys32[i], sizeof(uint32_t) * cap))) return rc;
         }
-        if ((rc = ensure(c->rec, sizeof(SplatRec) * cap))) return rc;
+        if ((rc = ensure(c->geo, sizeof(GeoRec) * cap))) return rc;
+        if ((rc = ensure(c->rinv, sizeof(float) * cap))) return rc;
+        if ((rc = ensure(c->col, sizeof(float4) * cap))) return rc;
         if ((rc = ensure(c->srec, sizeof(SplatRec) * cap))) return rc;
         c->cap_n = cap;
     }
@@ -189,7 +192,8 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
     if (c->cap_p == 0) c->cap_p = round_up(std::max<int64_t>(int64_t(1) << 20, 6 * n), 4096);
     if ((rc = ensure(c->tile_vals, sizeof(uint32_t) * c->cap_d))) return rc;
     if ((rc = ensure(c->pairs, sizeof(uint2) * c->cap_p))) return rc;
-    if ((rc = ensure(c->depth_work, sort_work_bytes(c->cap_n, 8, 8)))) return rc;
+    if ((rc = ensure(c->depth_work, depth_work64_bytes(c->cap_n)))) return rc;
+    if ((rc = ensure(c->depth_work32, depth_work32_bytes(c->cap_n)))) return rc;
     const int tiles_x = (W + kTile - 1) / kTile, n_rows = (H + kTile - 1) / kTile;
     const int ntiles = tiles_x * n_rows;
     if ((rc = ensure(c->ranges, sizeof(uint2) * (size_t)ntiles))) return rc;
@@ -239,17 +243,26 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     launch_frame_init(ctr, s);
     if (n > 0) {
         launch_preprocess(sc->view, ca, sh_degree, cull, c->keys[0].as<unsigned long long>(),
-                          c->rec.as<SplatRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr, ctr,
-                          s);
-        launches++;
+                          c->geo.as<GeoRec>(), c->rinv.as<float>(), c->col.as<float4>(),
+                          want_keep ? c->keep.as<uint8_t>() : nullptr, ctr, s);
+        launches += 2;
     }
     cudaEventRecord(c->ev[1], s);
     if (n > 0) {
-        // stable depth sort; first pass compacts (drops culled sentinels)
-        launches += launch_onesweep_sort<unsigned long long>(
-            c->keys[0].as<unsigned long long>(), c->keys[1].as<unsigned long long>(),
-            c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), true, true, &ctr->K, n, n, 8,
-            true, c->depth_work.p, dsched, &ctr->npass, c->sms, s);
+        // stable f64 depth order; the first radix pass compacts (drops culled sentinels)
+        DepthArgs da;
+        for (int i = 0; i < 2; i++) {
+            da.keys64[i] = c->keys[i].as<unsigned long long>();
+            da.keys32[i] = c->keys32[i].as<uint32_t>();
+            da.vals[i] = c->vals[i].as<uint32_t>();
+        }
+        da.ctr = ctr;
+        da.n = n;
+        da.work32 = c->depth_work32.p;
+        da.work64 = c->depth_work.p;
+        da.sched32 = c->sched32.as<uint32_t>();
+        da.sched = dsched;
+        launches += launch_depth_sort(da, c->sms, s);
     }
     cudaEventRecord(c->ev[2], s);
     if (n > 0) {
@@ -257,7 +270,9 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.order0 = c->vals[0].as<uint32_t>();
         ba.order1 = c->vals[1].as<uint32_t>();
         ba.depth_sched = dsched;
-        ba.rec = c->rec.as<SplatRec>();
+        ba.geo = c->geo.as<GeoRec>();
+        ba.rinv = c->rinv.as<float>();
+        ba.col = c->col.as<float4>();
         ba.srec = c->srec.as<SplatRec>();
         ba.ctr = ctr;
         ba.width = W;
@@ -337,7 +352,7 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     st->splats_drawn = c->hctr->K;
     st->splats_culled = sc ? sc->n - (int64_t)c->hctr->K : 0;
     st->tile_keys = c->hctr->D;
-    st->depth_passes = (int32_t)c->hctr->npass;
+    st->depth_passes = (int32_t)(c->hctr->npass + c->hctr->npass_fb);
     st->retries = c->retries;
     float t[6] = {0, 0, 0, 0, 0, 0};
     cudaEventElapsedTime(&t[0], c->ev[0], c->ev[5]);
@@ -617,7 +632,9 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     int rc = ensure(c->ctr, sizeof(FrameCounters));
     if (!rc) rc = ensure(c->sticky, sizeof(uint32_t));
     if (!rc) rc = ensure(c->sched, 64 * sizeof(uint32_t));
-    if (!rc && cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess)
+    if (!rc) rc = ensure(c->sched32, 64 * sizeof(uint32_t));
+    if (!rc && (cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess ||
+                cudaMemset(c->sched32.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess))
         rc = fail(GSR_E_CUDA, "memset");
     if (!rc && cudaMemset(c->sticky.p, 0, sizeof(uint32_t)) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");

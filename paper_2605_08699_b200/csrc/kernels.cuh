@@ -12,13 +12,13 @@ namespace gsr {
 struct FrameCounters {
     uint32_t K;                 // kept splats
     uint32_t D;                 // tile keys under the contract (may exceed capacity)
-    uint32_t npass;             // depth-sort radix passes
-    uint32_t pad0;
+    uint32_t npass;             // depth-sort radix passes (32-bit key sort)
+    uint32_t npass_fb;          // passes of the 64-bit fallback sort (0: not needed)
     unsigned long long kmin;    // min / max kept depth key (f64 bits)
     unsigned long long kmax;
     unsigned long long P;       // (splat, tile row) pairs
     uint32_t nseg;              // binning segments
-    uint32_t pad1;
+    uint32_t long_runs;         // depth sort: a 32-bit key run too long for the fix-up
 };
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.
@@ -44,11 +44,14 @@ struct CameraArgs {
     int iwidth, iheight;
 };
 
-// preprocess.cu
+// preprocess.cu (2 kernels)
+struct GeoRec {  // SplatRec.a, SplatRec.b
+    float4 a, b;
+};
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                       int frustum_cull, unsigned long long *keys, SplatRec *rec,
-                       uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s);
+                       int frustum_cull, unsigned long long *keys, GeoRec *geo, float *rinv,
+                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s);
 
 // radix.cu: Onesweep stable LSD sort (see radix.cu header)
 cudaError_t radix_init_attributes();
@@ -70,7 +73,23 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
                          bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
                          int64_t n_first, int64_t n_cap, int passes, bool force_first,
                          void *work, uint32_t *sched, uint32_t *npass_out, int sms,
-                         cudaStream_t s);
+                         cudaStream_t s, const uint32_t *run_if = nullptr,
+                         const uint32_t *prev_sched = nullptr);
+
+// depth.cu: stable f64 depth order (see depth.cu header)
+struct DepthArgs {
+    unsigned long long *keys64[2];  // [0]: preprocess keys (sentinel ~0 = culled)
+    uint32_t *keys32[2];
+    uint32_t *vals[2];
+    FrameCounters *ctr;
+    int64_t n;
+    void *work32, *work64;
+    uint32_t *sched32;  // 32-bit sort schedule
+    uint32_t *sched;    // final schedule: sched[16] = buffer of vals holding the order
+};
+size_t depth_work32_bytes(int64_t n_cap);
+size_t depth_work64_bytes(int64_t n_cap);
+int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s);  // returns kernels launched
 
 // binning.cu: sort-free tile lists (see binning.cu header)
 constexpr int kMaxTileRows = 512;   // height <= 8192
@@ -78,7 +97,9 @@ constexpr int kMaxTilesX = 1024;    // width <= 16384
 struct BinArgs {
     const uint32_t *order0, *order1;  // depth sort result buffers
     const uint32_t *depth_sched;      // [16]: which of order0/order1 holds the result
-    const SplatRec *rec;              // records by Gaussian index (preprocess)
+    const GeoRec *geo;                // packed geometry by Gaussian index (preprocess)
+    const float *rinv;                // RN(1/ia) by Gaussian index
+    const float4 *col;                // (r, g, b, -) by Gaussian index
     SplatRec *srec;                   // records by depth rank (written here)
     FrameCounters *ctr;
     int width, height, n_rows, tiles_x, ntiles;

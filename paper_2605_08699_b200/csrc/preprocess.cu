@@ -1,5 +1,5 @@
 // preprocess.cu -- K1: per-Gaussian f64 projection, culling, SH colour and
-// packing, fused in one pass over the SoA scene.
+// packing.
 //
 // Restates, with the reference's exact f64 operation order (no FMA):
 //   _project_kernel      render.py:163-237
@@ -7,6 +7,15 @@
 //   packing              render.py:442-453 (c/det, -b/det, a/det, sqrt(c*rsq))
 // Culled Gaussians get the sentinel depth key ~0; the first depth-sort pass
 // drops them, which is the order-preserving compaction of render.py:279.
+//
+// Two streaming kernels rather than one fused pass: a fused kernel needs ~80
+// registers (the FP64 projection and the SH evaluation live at once), which
+// caps it at 24 warps per SM -- too few to hide HBM latency behind FP64
+// latency.  Split, each runs at high occupancy with all its loads coalesced:
+//   K1a geo    mean/scale/rotation/rsq/opacity (92 B) -> depth key, the
+//              packed geometry (u, v, ia, ib | ic, rsq, op, ry) and RN(1/ia)
+//   K1b colour kept Gaussians only: mean + SH planes (216 B) -> (r, g, b)
+// The binning gather (binning.cu) assembles the 48-byte splat record.
 #include "kernels.cuh"
 
 namespace gsr {
@@ -60,22 +69,19 @@ __device__ __forceinline__ double sh_channel(const T *sh, int64_t stride, int64_
 __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->K = 0;
     ctr->D = 0;
-    ctr->npass = 1;
-    ctr->pad0 = 0;
+    ctr->npass = 0;
+    ctr->npass_fb = 0;
     ctr->kmin = ~0ull;
     ctr->kmax = 0ull;
     ctr->P = 0ull;
     ctr->nseg = 0;
-    ctr->pad1 = 0;
+    ctr->long_runs = 0;
 }
 
-template <typename ShT>
-__global__ void __launch_bounds__(256) preprocess_kernel(SceneView sc, CameraArgs cam,
-                                                         int sh_degree, int do_cull,
-                                                         unsigned long long *__restrict__ keys,
-                                                         SplatRec *__restrict__ rec,
-                                                         uint8_t *__restrict__ keep_out,
-                                                         FrameCounters *ctr) {
+__global__ void __launch_bounds__(256) preprocess_geo_kernel(
+    SceneView sc, CameraArgs cam, int do_cull, unsigned long long *__restrict__ keys,
+    GeoRec *__restrict__ geo, float *__restrict__ rinv_out, uint8_t *__restrict__ keep_out,
+    FrameCounters *ctr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t st = sc.stride;
     bool kept = false;
@@ -95,6 +101,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(SceneView sc, CameraArg
                          qy = __ldg(sc.rot + 2 * st + i), qz = __ldg(sc.rot + 3 * st + i);
             const double sx = __ldg(sc.scale + i), sy = __ldg(sc.scale + st + i),
                          sz = __ldg(sc.scale + 2 * st + i);
+            const double rsq = __ldg(sc.rsq + i);
+            const float opac = __ldg(sc.opac + i);
             // render.py:185-193
             const double m00 = (1.0 - 2.0 * (qy * qy + qz * qz)) * sx;
             const double m01 = (2.0 * (qx * qy - qw * qz)) * sy;
@@ -145,35 +153,14 @@ __global__ void __launch_bounds__(256) preprocess_kernel(SceneView sc, CameraArg
             if (k) {
                 kept = true;
                 key = (unsigned long long)__double_as_longlong(z);
-                float cr, cg, cbl;
-                if (sh_degree == 0) {
-                    cr = __ldg(sc.dc + i);
-                    cg = __ldg(sc.dc + st + i);
-                    cbl = __ldg(sc.dc + 2 * st + i);
-                } else {  // render.py:134-160
-                    const double dx = mx - cam.campos[0];
-                    const double dy = my - cam.campos[1];
-                    const double dz = mz - cam.campos[2];
-                    const double norm = sqrt((dx * dx + dy * dy) + dz * dz);
-                    const double den = norm > 1e-12 ? norm : 1e-12;
-                    const double ux = dx / den, uy = dy / den, uz = dz / den;
-                    const double xx = ux * ux, yy = uy * uy, zz = uz * uz;
-                    const double xy = ux * uy, yz = uy * uz, xz = ux * uz;
-                    const ShT *sh = (const ShT *)sc.sh;
-                    cr = (float)sh_channel(sh, st, i, 0, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
-                    cg = (float)sh_channel(sh, st, i, 1, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
-                    cbl = (float)sh_channel(sh, st, i, 2, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
-                }
                 // render.py:442-453
                 const double det = ca * cc - cb * cb;
-                const double rsq = __ldg(sc.rsq + i);
-                SplatRec o;
                 const float ia32 = (float)(cc / det);
+                GeoRec o;
                 o.a = make_float4((float)u, (float)v, ia32, (float)(-cb / det));
-                o.b = make_float4((float)(ca / det), (float)rsq, __ldg(sc.opac + i),
-                                  (float)sqrt(cc * rsq));
-                o.c = make_float4(cr, cg, cbl, __frcp_rn(ia32));
-                rec[i] = o;
+                o.b = make_float4((float)(ca / det), (float)rsq, opac, (float)sqrt(cc * rsq));
+                geo[i] = o;
+                rinv_out[i] = __frcp_rn(ia32);
             }
         }
         keys[i] = key;
@@ -213,6 +200,37 @@ __global__ void __launch_bounds__(256) preprocess_kernel(SceneView sc, CameraArg
     }
 }
 
+template <typename ShT>
+__global__ void __launch_bounds__(256) preprocess_color_kernel(
+    SceneView sc, CameraArgs cam, int sh_degree, const unsigned long long *__restrict__ keys,
+    float4 *__restrict__ col) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= sc.n || __ldg(keys + i) == ~0ull) return;  // culled: no colour needed
+    const int64_t st = sc.stride;
+    float cr, cg, cbl;
+    if (sh_degree == 0) {  // render.py:129-130
+        cr = __ldg(sc.dc + i);
+        cg = __ldg(sc.dc + st + i);
+        cbl = __ldg(sc.dc + 2 * st + i);
+    } else {  // render.py:134-160
+        const double mx = __ldg(sc.mean + i), my = __ldg(sc.mean + st + i),
+                     mz = __ldg(sc.mean + 2 * st + i);
+        const double dx = mx - cam.campos[0];
+        const double dy = my - cam.campos[1];
+        const double dz = mz - cam.campos[2];
+        const double norm = sqrt((dx * dx + dy * dy) + dz * dz);
+        const double den = norm > 1e-12 ? norm : 1e-12;
+        const double ux = dx / den, uy = dy / den, uz = dz / den;
+        const double xx = ux * ux, yy = uy * uy, zz = uz * uz;
+        const double xy = ux * uy, yz = uy * uz, xz = ux * uz;
+        const ShT *sh = (const ShT *)sc.sh;
+        cr = (float)sh_channel(sh, st, i, 0, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+        cg = (float)sh_channel(sh, st, i, 1, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+        cbl = (float)sh_channel(sh, st, i, 2, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+    }
+    col[i] = make_float4(cr, cg, cbl, 0.0f);
+}
+
 }  // namespace
 
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
@@ -220,17 +238,18 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
 }
 
 void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                       int frustum_cull, unsigned long long *keys, SplatRec *rec,
-                       uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s) {
+                       int frustum_cull, unsigned long long *keys, GeoRec *geo, float *rinv,
+                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s) {
     if (scene.n == 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
-    if (scene.sh_f32)
-        preprocess_kernel<float><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, frustum_cull,
-                                                            keys, rec, keep_out, ctr);
+    preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, cam, frustum_cull, keys, geo, rinv,
+                                                     keep_out, ctr);
+    if (scene.sh_f32 || sh_degree == 0)
+        preprocess_color_kernel<float><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, keys, col);
     else
-        preprocess_kernel<double><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, frustum_cull,
-                                                             keys, rec, keep_out, ctr);
+        preprocess_color_kernel<double><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, keys,
+                                                                   col);
 }
 
 }  // namespace gsr
