@@ -204,35 +204,102 @@ def run_reference(args, wl):
     return 0
 
 
-def stage_roofline(stats_list, wl, counters, peaks, peak_kind):
-    """Per-stage mean device ms and algorithmic roofline."""
-    keys = ["ms_preprocess", "ms_depth_sort", "ms_binning", "ms_tile_sort", "ms_blend"]
-    mean = {k: float(np.mean([s[k] for s in stats_list])) for k in keys}
-    n, k, d = wl["n"], counters["K"], counters["D"]
-    dsh = wl["sh"]
-    passes = counters["depth_passes"]
-    tile_passes = counters["tile_passes"]
-    alg = {
-        # SoA scene read (f64 geometry 80 B + rsq 8 + opacity 4 + f32 SH/colour) + 8 B key
-        # for all N + 48 B record per kept splat
-        "ms_preprocess": n * (92 + (12 * (dsh + 1) ** 2 if dsh else 12)) + 8 * n + 48 * k,
-        # first pass reads N keys, every pass writes (key 8 + val 4), later passes read them
-        "ms_depth_sort": 8 * n + 12 * k + (passes - 1) * 24 * k,
-        # count: gather 48 B records + write sorted copy + counts; write: re-read 48 B + 8 B/key
-        "ms_binning": k * (4 + 48 + 48 + 4) + k * (48 + 4) + 8 * d,
-        "ms_tile_sort": tile_passes * 16 * d,
-        # tile lists (4 B/entry) + records (48 B per kept splat) + u8 frame
-        "ms_blend": 4 * d + 48 * k + 3 * wl["w"] * wl["h"],
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of each kernel, from
+# the committed `ncu --set full` capture (tools/ncu_traffic.py writes it)
+TRAFFIC = {}
+_tp = ROOT / "profiles" / "ncu_traffic_config3.json"
+if _tp.exists():
+    TRAFFIC = json.loads(_tp.read_text())
+
+
+def load_simt_peaks():
+    """FP32/FP64/smem/issue peaks measured by tools/peaks.cu on a B200 of this
+    pool (profiles/measured_simt_peaks.json), else the nominal figures."""
+    p = ROOT / "profiles" / "measured_simt_peaks.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["source"] = "measured (tools/peaks.cu)"
+        return d
+    # nominal: 148 SMs x 128 FP32 lanes x 1.965 GHz (no FMA), FP64 at half rate
+    return {"fp32_tops": 37.2, "fp64_tops": 18.6, "source": "nominal"}
+
+
+def kernel_work(name, wl, c):
+    """Algorithmic units of one frame's launches of a kernel (DESIGN.md
+    section 4): (bytes, fp32 ops)."""
+    n, k, d, p = wl["n"], c["K"], c["D"], c["P"]
+    sh_bytes = 12 * (wl["sh"] + 1) ** 2 if wl["sh"] else 12
+    px = wl["w"] * wl["h"]
+    table = {
+        # mean/scale/rotation/rsq f64 + opacity f32 in; key for all N; record + rinv of kept
+        "preprocess_geo": (n * 92 + n * 8 + k * 36, 0),
+        # key of all N; mean f64 + SH f32 (or DC) + rinv of kept in; colour out
+        "preprocess_color": (n * 8 + k * (28 + sh_bytes) + k * 16, 0),
+        "depth_key32": (n * 12, 0),
+        "radix32_hist": (k * 4, 0),
+        "radix32_pass": (k * 16, 0),  # per pass: key + index read and written
+        "depth_fixup": (k * 4, 0),
+        # order + geometry + colour gathered, 48 B record written
+        "bin_gather": (k * (4 + 32 + 16) + k * 48, 0),
+        # records in, pairs out; 20 FP32 ops per exact row interval (render.py:383-397)
+        "bin_pairs": (k * 36 + p * 8, 20 * c["Rp"]),
+        "seg_count": (p * 8, 0),
+        "seg_place": (p * 8 + d * 4, 0),
+        # lists + each record once + u8 frame; 20 FP32 ops per composited
+        # evaluation (render.py:405-421) and per row interval (383-397)
+        "blend": (d * 4 + k * 48 + 3 * px, 20 * (c["E"] + c["Rb"])),
     }
+    return table.get(name, (0, 0))
+
+
+BOUND = {"bin_pairs": "fp32", "blend": "fp32"}
+
+
+def kernel_profile(lib, ctx, sc, cams, sh, frames, wl, peaks, simt):
+    """Per-kernel device times: a CUDA event is recorded on the render stream
+    after every launch (gsr_ctx_set_kernel_timing); mean over `frames` frames."""
+    from paper_2605_08699_b200 import _lib
+    from paper_2605_08699_b200.render import _bg
+    _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 1))
+    names = ctypes.create_string_buffer(64 * 48)
+    ms = (ctypes.c_float * 64)()
+    cnt = ctypes.c_int(0)
+    agg, launches, counters = {}, {}, []
+    st = _lib.GsrStats()
+    try:
+        for cam in cams[:frames]:
+            _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cam), _bg((0, 0, 0)), sh,
+                                      1, None, None, None, ctypes.byref(st)))
+            _lib.check(lib.gsr_ctx_kernel_times(ctx.handle, 64, names, ms, ctypes.byref(cnt)))
+            for i in range(cnt.value):
+                nm = names.raw[48 * i:48 * i + 48].split(b"\0", 1)[0].decode()
+                agg[nm] = agg.get(nm, 0.0) + ms[i]
+                launches[nm] = launches.get(nm, 0) + 1
+            counters.append({"K": st.splats_drawn, "D": st.tile_keys, "P": st.pairs,
+                             "E": st.composited, "Rb": st.row_evals_blend,
+                             "Rp": st.row_evals_binning})
+    finally:
+        lib.gsr_ctx_set_kernel_timing(ctx.handle, 0)
+    nf = max(1, len(counters))
+    mean_c = {key: float(np.mean([c[key] for c in counters])) for key in counters[0]}
     hbm = float(peaks["hbm_gbs"])
+    fp32 = float(simt["fp32_tops"])
     out = {}
-    for key in keys:
-        ms = mean[key]
-        gbs = alg[key] / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-        out[key[3:]] = {"ms": round(ms, 4), "alg_bytes": int(alg[key]),
-                        "achieved_gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
-    dom = max(keys, key=lambda x: mean[x])
-    return mean, out, dom[3:]
+    for nm, tot in agg.items():
+        per_frame = tot / nf
+        nl = launches[nm] / nf
+        b, f = kernel_work(nm, wl, mean_c)
+        e = {"ms_per_frame": round(per_frame, 4), "launches_per_frame": nl,
+             "bound": BOUND.get(nm, "hbm")}
+        if b and per_frame > 0:
+            gbs = b / (per_frame * 1e-3) / 1e9
+            e.update(alg_bytes=int(b), achieved_gbs=round(gbs, 1), frac_hbm=round(gbs / hbm, 4))
+        if f and per_frame > 0:
+            tf = f / (per_frame * 1e-3) / 1e12
+            e.update(alg_fp32_ops=int(f), achieved_tflops=round(tf, 2),
+                     frac_fp32=round(tf / fp32, 4))
+        out[nm] = e
+    return out, mean_c
 
 
 def run_gsr(args, wl):
@@ -311,12 +378,41 @@ def run_gsr(args, wl):
                                   None, None, None, ctypes.byref(st)))
         stage_stats.append(st.as_dict())
         dev_lat.append(st.ms_device)
-    counters = {"K": int(st.splats_drawn), "D": int(st.tile_keys),
-                "depth_passes": int(st.depth_passes),
-                "tile_passes": (int(np.ceil(np.log2(((intr.width + 15) // 16) *
-                                                    ((intr.height + 15) // 16)))) + 7) // 8}
+    stages = {k[3:]: round(float(np.mean([x[k] for x in stage_stats])), 4)
+              for k in ["ms_preprocess", "ms_depth_sort", "ms_binning", "ms_blend"]}
     peaks, peak_kind = load_peaks()
-    mean, stages, dom = stage_roofline(stage_stats, wl, counters, peaks, peak_kind)
+    simt = load_simt_peaks()
+    kernels, counters = kernel_profile(lib, ctx, sc, cams[W:], wl["sh"], min(K, 30), wl, peaks,
+                                       simt)
+    dom = max(kernels, key=lambda x: kernels[x]["ms_per_frame"])
+    dk = kernels[dom]
+    if dk["bound"] == "fp32":
+        roof = {"bound": "fp32", "kernel": dom, "achieved": dk["achieved_tflops"],
+                "peak": float(simt["fp32_tops"]), "unit": "TFLOP/s", "frac": dk["frac_fp32"],
+                "peak_source": simt["source"]}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"],
+                "peak": float(peaks["hbm_gbs"]), "unit": "GB/s", "frac": dk["frac_hbm"],
+                "peak_source": peak_kind}
+    roof["traffic"] = TRAFFIC.get(dom)
+    roof["alg_per_frame"] = dk.get("alg_fp32_ops") or dk.get("alg_bytes")
+
+    # config 3's full ABR ladder: base + 3 rungs rendered, upsampled, SSIM-scored
+    ladder = None
+    if wl["w"] == 1920 and wl["h"] == 1080 and not args.no_ladder:
+        from paper_2605_08699_b200.metrics import ladder_ssim
+        from paper_2605_08699_b200.synth import ladder_1080p
+        rungs = [(r["width"], r["height"]) for r in ladder_1080p()[1:]]
+        ladder_ssim(prims, poses[W], intr, rungs, sh_degree=wl["sh"])  # warm
+        lt, ss = [], []
+        for i in range(W, W + min(K, 10)):
+            t0 = time.perf_counter()
+            ss, _ = ladder_ssim(prims, poses[i], intr, rungs, sh_degree=wl["sh"])
+            lt.append((time.perf_counter() - t0) * 1000.0)
+        ladder = {"rungs": ["1920x1080"] + [f"{w}x{h}" for w, h in rungs],
+                  "ssim_vs_1080p_last_pose": [round(x, 6) for x in ss],
+                  "ms_per_ladder_p50": float(np.percentile(lt, 50)),
+                  "what": "per pose: render 1080p + 3 rungs, upscale_to 1080p, ssim, on device"}
 
     result = None
     if rank == 0:
@@ -325,7 +421,6 @@ def run_gsr(args, wl):
         if world == 1 and not args.no_cpu_baseline:
             base, parity = cpu_baseline(prims, poses[W:], intr, wl["sh"], args.cpu_budget,
                                         gpu_u8=frame0)
-        dstage = stages[dom]
         result = {
             "metric": "1080p frames/sec/GPU and p50/p99 render ms at 3M Gaussians",
             "value": value, "unit": "frames/s", "n_gpus": world, "steps": K, "warmup": W,
@@ -345,12 +440,11 @@ def run_gsr(args, wl):
                     "d2h_bytes_per_step": int(out.nbytes)},
             "gpu_launches": launches,
             "overflow_frames": overflow,
-            "stages": stages,
-            "counters": counters,
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dstage["achieved_gbs"],
-                         "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
-                         "frac": dstage["frac_hbm"], "traffic": None,
-                         "peak_source": peak_kind},
+            "stages_ms": stages,
+            "kernels": kernels,
+            "counters": {k: int(v) for k, v in counters.items()},
+            "roofline": roof,
+            "ladder": ladder,
             "clocks": clocks.summary(),
         }
         if base is not None:
@@ -373,6 +467,7 @@ def main(argv=None):
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-ladder", action="store_true")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]

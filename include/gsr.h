@@ -68,6 +68,11 @@ typedef struct gsr_stats {
     float ms_preprocess, ms_depth_sort, ms_binning, ms_tile_sort, ms_blend;
     int32_t kernel_launches;  /* kernels this ctx launched since the last finish/render */
     int32_t overflow_frames;  /* frames since the last finish whose tile keys overflowed */
+    /* work counters of the last frame (roofline units) */
+    int64_t pairs;              /* P: (splat, 16-row tile row) pairs */
+    int64_t composited;         /* E: composited (pixel, splat) evaluations */
+    int64_t row_evals_blend;    /* (splat, pixel row) interval evaluations in the blend */
+    int64_t row_evals_binning;  /* (splat, pixel row) interval evaluations in the binning */
 } gsr_stats;
 
 GSR_API int gsr_abi_version(void);
@@ -101,6 +106,13 @@ GSR_API int64_t gsr_ctx_device_bytes(const gsr_ctx *ctx);
 GSR_API const uint8_t *gsr_ctx_frame_u8(const gsr_ctx *ctx);
 /* the ctx's cudaStream_t (as void*), e.g. to record timing events on it */
 GSR_API void *gsr_ctx_stream(const gsr_ctx *ctx);
+/* Per-kernel timing (profiling; off by default): when enabled, a CUDA event is
+ * recorded on the ctx stream after every kernel of a frame.
+ * gsr_ctx_kernel_times waits for the last frame and returns, for each kernel
+ * launch in order, its name (NUL-terminated, 48-byte slots in names) and its
+ * device time in ms (event after it minus event before it). */
+GSR_API int gsr_ctx_set_kernel_timing(gsr_ctx *ctx, int enable);
+GSR_API int gsr_ctx_kernel_times(gsr_ctx *ctx, int max, char *names, float *ms, int *n);
 
 /* ---- the hot path: render_framebuffer (render.py:516-524) ----------------
  * project (render.py:163-290) -> stable f64 depth sort (293-302) -> tile

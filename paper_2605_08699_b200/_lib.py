@@ -43,7 +43,9 @@ class GsrStats(ctypes.Structure):
                 ("ms_preprocess", ctypes.c_float), ("ms_depth_sort", ctypes.c_float),
                 ("ms_binning", ctypes.c_float), ("ms_tile_sort", ctypes.c_float),
                 ("ms_blend", ctypes.c_float), ("kernel_launches", ctypes.c_int32),
-                ("overflow_frames", ctypes.c_int32)]
+                ("overflow_frames", ctypes.c_int32), ("pairs", ctypes.c_int64),
+                ("composited", ctypes.c_int64), ("row_evals_blend", ctypes.c_int64),
+                ("row_evals_binning", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -66,6 +68,8 @@ SIGNATURES = [
     ("gsr_ctx_device_bytes", _i64, [_vp]),
     ("gsr_ctx_frame_u8", _vp, [_vp]),
     ("gsr_ctx_stream", _vp, [_vp]),
+    ("gsr_ctx_set_kernel_timing", _i32, [_vp, _i32]),
+    ("gsr_ctx_kernel_times", _i32, [_vp, _i32, _vp, _vp, _P(_i32)]),
     ("gsr_render", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32, _vp, _vp, _vp, _P(GsrStats)]),
     ("gsr_render_async", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32]),
     ("gsr_ctx_finish", _i32, [_vp, _vp, _P(GsrStats)]),

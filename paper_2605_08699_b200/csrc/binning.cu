@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
         const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b), C = __ldg(a.col + i);
         a.srec[r].a = A;
         a.srec[r].b = B;
-        a.srec[r].c = make_float4(C.x, C.y, C.z, __ldg(a.rinv + i));
+        a.srec[r].c = C;
         int lo, hi;
         row_range(A.y, B.w, a.height, lo, hi);
         if (lo < hi)
@@ -129,8 +129,9 @@ struct PairSmem {
     int lo[BR], hi[BR];
     uint32_t poff[BR + 1];
     uint32_t s_warp[33];
-    uint32_t lr[kPairCache];         // in-warp rank of a pair within its row
-    uint32_t wpre[BR / 32][kRowsMax];  // per-warp counts, then exclusive prefix
+    uint8_t lr[kPairCache];          // in-warp rank of a pair within its row
+    uint8_t owner[kPairCache];       // block-local splat of a pair
+    uint32_t wpre[BR / 32][kRowsMax];  // per-warp coverage masks -> counts -> exclusive prefix
     int ty_lo, ty_hi;
 };
 
@@ -181,18 +182,24 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     atomicMax(&S.ty_hi, t1);
     __syncthreads();
     // rank of each (splat, row) among the block's splats covering that row:
-    // warp ballots give the in-warp rank, a prefix over warps the rest
+    // per-warp coverage bitmasks per tile row (shared atomics, one per pair)
+    // give the in-warp rank, a prefix of the popcounts over warps the rest
     const int ylo = S.ty_lo, yhi = S.ty_hi;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int ty = ylo; ty <= yhi; ty++) {
-        const bool cov = ty >= t0 && ty <= t1;
-        const uint32_t m = __ballot_sync(0xffffffffu, cov);
-        if (cov) {
-            const uint32_t q = off + (uint32_t)(ty - t0);
-            if (q < kPairCache) S.lr[q] = __popc(m & lt_mask);
+    uint32_t *wm = S.wpre[w];
+    for (int ty = ylo + lane; ty <= yhi; ty += 32) wm[ty] = 0u;
+    __syncwarp();
+    for (int ty = t0; ty <= t1; ty++) atomicOr(&wm[ty], 1u << lane);
+    __syncwarp();
+    for (int ty = t0; ty <= t1; ty++) {
+        const uint32_t q = off + (uint32_t)(ty - t0);
+        if (q < kPairCache) {
+            S.lr[q] = (uint8_t)__popc(wm[ty] & lt_mask);
+            S.owner[q] = (uint8_t)tid;
         }
-        if (lane == 0) S.wpre[w][ty] = __popc(m);
     }
+    __syncwarp();
+    for (int ty = ylo + lane; ty <= yhi; ty += 32) wm[ty] = __popc(wm[ty]);
     __syncthreads();
     for (int ty = ylo + tid; ty <= yhi; ty += BR) {
         uint32_t run = 0;
@@ -206,8 +213,9 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     __syncthreads();
     // one thread per pair: exact tile span, stored at its grouped slot
     const int64_t nb = a.n_blocks;
+    uint32_t n_rows = 0;
     for (uint32_t q = tid; q < npairs; q += BR) {
-        const int j = rank_of_pair(S.poff, q);
+        const int j = q < kPairCache ? (int)S.owner[q] : rank_of_pair(S.poff, q);
         const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
         uint32_t in_warp;
         if (q < kPairCache) {
@@ -221,6 +229,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         const uint32_t slot = a.row_blk[(int64_t)ty * nb + b] + S.wpre[j >> 5][ty] + in_warp;
         // exact tile-column span of splat j in tile row ty
         const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
+        n_rows += (uint32_t)(y1 - y0);
         int mn = 0x7fffffff, mx = -0x7fffffff;
         const float u = S.u[j], v = S.v[j], ia = S.ia[j], ib = S.ib[j], ic = S.ic[j],
                     rsq = S.rsq[j], rinv = S.rinv[j];
@@ -270,6 +279,9 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         }
         if ((int64_t)slot < a.cap_p) a.pairs[slot] = make_uint2((uint32_t)(b * BR + j), span);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_rows += __shfl_xor_sync(0xffffffffu, n_rows, o);
+    if (lane == 0 && n_rows) atomicAdd(&a.ctr->Rp, (unsigned long long)n_rows);
 }
 
 // ---------------------------------------------------------------- 2a -------
@@ -492,20 +504,28 @@ cudaError_t binning_init_attributes() {
     return e;
 }
 
-int launch_binning(const BinArgs &a, cudaStream_t s) {
+int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark) {
     if (a.n_blocks <= 0) return 0;
     const unsigned nb = (unsigned)a.n_blocks;
     bin_gather_kernel<<<nb, BR, 0, s>>>(a);
+    mark("bin_gather");
     const int64_t scan_tiles = bin_scan_tiles(a.n_blocks, a.n_rows);
     cudaMemsetAsync(a.scan_work, 0, sizeof(unsigned long long) * (size_t)(scan_tiles + 1), s);
     row_scan_kernel<<<(unsigned)scan_tiles, 256, 0, s>>>(a);
+    mark("row_scan");
     bin_pairs_kernel<<<nb, BR, sizeof(PairSmem), s>>>(a);
+    mark("bin_pairs");
     seg_table_kernel<<<1, 1024, 0, s>>>(a);
+    mark("seg_table");
     const unsigned sb = (unsigned)((a.cap_seg + 7) / 8);
     seg_count_kernel<<<sb, 256, 8 * (a.tiles_x + 1) * sizeof(uint32_t), s>>>(a);
+    mark("seg_count");
     seg_scan_kernel<<<(unsigned)((a.ntiles + 255) / 256), 256, 0, s>>>(a);
+    mark("seg_scan");
     tile_scan_kernel<<<1, 1024, 0, s>>>(a);
+    mark("tile_scan");
     seg_place_kernel<<<sb, 256, 8 * 2 * a.tiles_x * sizeof(uint32_t), s>>>(a);
+    mark("seg_place");
     return 8;
 }
 

@@ -121,7 +121,7 @@ struct WarpBatch {         // one warp's current 32 splats
 __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
     const SplatRec *__restrict__ srec, const uint32_t *__restrict__ tile_vals,
     const uint2 *__restrict__ ranges, int width, int height, float bg0, float bg1, float bg2,
-    BlendOut out) {
+    BlendOut out, FrameCounters *__restrict__ ctr) {
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
 
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
     bool done = !inside;
+    uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
     const uint2 rg = ranges[blockIdx.x];
     WarpBatch &B_ = s_b[w];
     const float4 *geo = B_.geo[prow];
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
             int lo, hi;
             row_range(A.y, B.w, height, lo, hi);
             const bool fast = splat_fast_ok(A.y, A.z, A.w);
+            n_rows += (uint32_t)(iy0 >= lo && iy0 < hi) + (uint32_t)(iy0 + 1 >= lo && iy0 + 1 < hi);
             mask = row_mask(A, B, C.w, fast, iy0, lo, hi, X, width) |
                    (row_mask(A, B, C.w, fast, iy0 + 1, lo, hi, X, width) << 16);
             if (mask) {  // render.py:400-402 terms per pixel row
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
                 const int s = __ffs(mine) - 1;
                 mine &= mine - 1u;
                 // render.py:405-421, reference operation order
+                n_comp++;
                 const float4 g = geo[s];  // u, ia, ib_dy, cy_term
                 const float4 k = B_.col[s];
                 const float dx = fx - g.x;
@@ -199,6 +202,18 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
             }
         }
         __syncwarp();
+    }
+    {
+        unsigned long long e = n_comp, r = n_rows;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e += __shfl_xor_sync(0xffffffffu, e, o);
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&ctr->E, e);
+            atomicAdd(&ctr->Rb, r);
+        }
     }
     if (!inside) return;
     cr += T * bg0;
@@ -226,10 +241,12 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
 }  // namespace
 
 void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *ranges, int width,
-                  int height, float bg0, float bg1, float bg2, BlendOut out, cudaStream_t s) {
+                  int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
+                  cudaStream_t s, const KMark &mark) {
     const int tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
     blend_kernel<<<tiles, kBlendThreads, 0, s>>>(srec, tile_vals, ranges, width, height, bg0, bg1,
-                                                 bg2, out);
+                                                 bg2, out, ctr);
+    mark("blend");
 }
 
 }  // namespace gsr

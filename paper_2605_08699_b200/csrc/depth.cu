@@ -87,19 +87,22 @@ __global__ void depth_fixup_kernel(DepthArgs a) {
 size_t depth_work32_bytes(int64_t n_cap) { return sort_work_bytes(n_cap, 4, 4); }
 size_t depth_work64_bytes(int64_t n_cap) { return sort_work_bytes(n_cap, 8, 8); }
 
-int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s) {
+int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &mark) {
     if (a.n <= 0) return 0;
     const unsigned g = (unsigned)((a.n + 255) / 256);
     depth_key32_kernel<<<g, 256, 0, s>>>(a.keys64[0], a.keys32[0], a.n, a.ctr);
+    mark("depth_key32");
     int launches = 1;
     launches += launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
                                                true, true, &a.ctr->K, a.n, a.n, 4, true, a.work32,
-                                               a.sched32, &a.ctr->npass, sms, s);
+                                               a.sched32, &a.ctr->npass, sms, s, nullptr, nullptr,
+                                               mark);
     depth_fixup_kernel<<<g, 256, 0, s>>>(a);
+    mark("depth_fixup");
     launches++;
     launches += launch_onesweep_sort<unsigned long long>(
         a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, &a.ctr->K, a.n, a.n, 8, true,
-        a.work64, a.sched, &a.ctr->npass_fb, sms, s, &a.ctr->long_runs, a.sched32);
+        a.work64, a.sched, &a.ctr->npass_fb, sms, s, &a.ctr->long_runs, a.sched32, mark);
     return launches;
 }
 

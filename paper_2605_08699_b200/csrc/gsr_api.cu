@@ -98,6 +98,12 @@ struct gsr_ctx {
     FrameCounters *hctr = nullptr;
     int64_t launches = 0;  // kernels enqueued since the last finish/render
     cudaEvent_t ev[8] = {};
+    // per-kernel event timeline of the last frame (gsr_ctx_set_kernel_timing)
+    static constexpr int kMaxMarks = 64;
+    bool ktime = false;
+    int nmarks = 0;
+    cudaEvent_t kev[kMaxMarks + 1] = {};
+    const char *kname[kMaxMarks] = {};
     // ladder / resample / ssim scratch
     DevBuf base_u8, up_u8, tmp_u8, src_u8, dst_u8, coefs, ssim_part, ssim_misc, ssim_w;
     double *hssim = nullptr;
@@ -217,6 +223,13 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
     return GSR_OK;
 }
 
+void kmark_cb(void *self, const char *kernel) {
+    gsr_ctx *c = static_cast<gsr_ctx *>(self);
+    if (c->nmarks >= gsr_ctx::kMaxMarks) return;
+    c->kname[c->nmarks] = kernel;
+    cudaEventRecord(c->kev[++c->nmarks], c->stream);
+}
+
 // Enqueue one full frame on c->stream (no host synchronisation).
 int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const float bg[3],
                   int sh_degree, int cull, bool want_rgb, bool want_keep) {
@@ -239,12 +252,20 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     uint32_t *dsched = c->sched.as<uint32_t>();
     int launches = 2;  // frame init + blend
 
+    KMark mark;
+    if (c->ktime) {
+        mark.fn = kmark_cb;
+        mark.self = c;
+        c->nmarks = 0;
+    }
     cudaEventRecord(c->ev[0], s);
+    if (c->ktime) cudaEventRecord(c->kev[0], s);
     launch_frame_init(ctr, s);
+    mark("frame_init");
     if (n > 0) {
         launch_preprocess(sc->view, ca, sh_degree, cull, c->keys[0].as<unsigned long long>(),
                           c->geo.as<GeoRec>(), c->rinv.as<float>(), c->col.as<float4>(),
-                          want_keep ? c->keep.as<uint8_t>() : nullptr, ctr, s);
+                          want_keep ? c->keep.as<uint8_t>() : nullptr, ctr, s, mark);
         launches += 2;
     }
     cudaEventRecord(c->ev[1], s);
@@ -262,7 +283,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         da.work64 = c->depth_work.p;
         da.sched32 = c->sched32.as<uint32_t>();
         da.sched = dsched;
-        launches += launch_depth_sort(da, c->sms, s);
+        launches += launch_depth_sort(da, c->sms, s, mark);
     }
     cudaEventRecord(c->ev[2], s);
     if (n > 0) {
@@ -271,7 +292,6 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.order1 = c->vals[1].as<uint32_t>();
         ba.depth_sched = dsched;
         ba.geo = c->geo.as<GeoRec>();
-        ba.rinv = c->rinv.as<float>();
         ba.col = c->col.as<float4>();
         ba.srec = c->srec.as<SplatRec>();
         ba.ctr = ctr;
@@ -295,7 +315,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.tile_vals = c->tile_vals.as<uint32_t>();
         ba.cap_d = c->cap_d;
         ba.overflow_sticky = c->sticky.as<uint32_t>();
-        launches += launch_binning(ba, s);
+        launches += launch_binning(ba, s, mark);
     } else {
         cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
     }
@@ -304,7 +324,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
                  want_rgb ? c->frame_t.as<float>() : nullptr};
     launch_blend(c->srec.as<SplatRec>(), c->tile_vals.as<uint32_t>(), c->ranges.as<uint2>(), W, H,
-                 bg[0], bg[1], bg[2], out, s);
+                 bg[0], bg[1], bg[2], out, ctr, s, mark);
     cudaEventRecord(c->ev[5], s);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(c->hsched, dsched, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
@@ -373,6 +393,10 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     if (cudaMemcpy(&ov, c->sticky.p, sizeof(ov), cudaMemcpyDeviceToHost) == cudaSuccess && ov)
         cudaMemset(c->sticky.p, 0, sizeof(ov));
     st->overflow_frames = (int32_t)ov;
+    st->pairs = (int64_t)c->hctr->P;
+    st->composited = (int64_t)c->hctr->E;
+    st->row_evals_blend = (int64_t)c->hctr->Rb;
+    st->row_evals_binning = (int64_t)c->hctr->Rp;
 }
 
 // ---- Pillow BILINEAR coefficients (Resample.c precompute_coeffs +
@@ -621,6 +645,7 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     if (e == cudaSuccess) e = radix_init_attributes();
     if (e == cudaSuccess) e = binning_init_attributes();
     for (int i = 0; i < 8 && e == cudaSuccess; i++) e = cudaEventCreate(&c->ev[i]);
+    for (int i = 0; i <= gsr_ctx::kMaxMarks && e == cudaSuccess; i++) e = cudaEventCreate(&c->kev[i]);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hssim, sizeof(double) * 64);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hsched, sizeof(uint32_t) * 64);
@@ -668,6 +693,8 @@ int gsr_ctx_destroy(gsr_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto &e : ctx->kev)
+        if (e) cudaEventDestroy(e);
     if (ctx->hctr) cudaFreeHost(ctx->hctr);
     if (ctx->hssim) cudaFreeHost(ctx->hssim);
     if (ctx->hsched) cudaFreeHost(ctx->hsched);
@@ -683,6 +710,33 @@ const uint8_t *gsr_ctx_frame_u8(const gsr_ctx *ctx) {
 }
 
 void *gsr_ctx_stream(const gsr_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int gsr_ctx_set_kernel_timing(gsr_ctx *ctx, int enable) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    ctx->ktime = enable != 0;
+    ctx->nmarks = 0;
+    return GSR_OK;
+}
+
+int gsr_ctx_kernel_times(gsr_ctx *ctx, int max, char *names, float *ms, int *n) {
+    if (!ctx || !n) return fail(GSR_E_INVALID, "null argument");
+    DeviceGuard g(ctx->device);
+    int rc = complete_frame(ctx);
+    if (rc) return rc;
+    GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    const int cnt = ctx->nmarks < max ? ctx->nmarks : max;
+    for (int i = 0; i < cnt; i++) {
+        float t = 0.0f;
+        GSR_CUDA_OK(cudaEventElapsedTime(&t, ctx->kev[i], ctx->kev[i + 1]));
+        if (ms) ms[i] = t;
+        if (names) {
+            std::strncpy(names + 48 * i, ctx->kname[i], 47);
+            names[48 * i + 47] = '\0';
+        }
+    }
+    *n = cnt;
+    return GSR_OK;
+}
 
 int gsr_render_async(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
                      const float background[3], int sh_degree, int frustum_cull) {

@@ -8,6 +8,16 @@
 
 namespace gsr {
 
+// Per-kernel timing hook: launchers call mark("kernel") after every launch;
+// a profiling context records a CUDA event there (gsr_ctx_set_kernel_timing).
+struct KMark {
+    void (*fn)(void *self, const char *kernel) = nullptr;
+    void *self = nullptr;
+    void operator()(const char *k) const {
+        if (fn) fn(self, k);
+    }
+};
+
 // Per-frame device counters (one struct, reset by frame_init_kernel).
 struct FrameCounters {
     uint32_t K;                 // kept splats
@@ -19,6 +29,10 @@ struct FrameCounters {
     unsigned long long P;       // (splat, tile row) pairs
     uint32_t nseg;              // binning segments
     uint32_t long_runs;         // depth sort: a 32-bit key run too long for the fix-up
+    // work counters for the roofline (algorithmic units)
+    unsigned long long E;       // blend: composited (pixel, splat) evaluations
+    unsigned long long Rb;      // blend: (splat, pixel row) interval evaluations
+    unsigned long long Rp;      // binning: (splat, pixel row) interval evaluations
 };
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.
@@ -51,7 +65,8 @@ struct GeoRec {  // SplatRec.a, SplatRec.b
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
                        int frustum_cull, unsigned long long *keys, GeoRec *geo, float *rinv,
-                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s);
+                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s,
+                       const KMark &mark = KMark());
 
 // radix.cu: Onesweep stable LSD sort (see radix.cu header)
 cudaError_t radix_init_attributes();
@@ -74,7 +89,7 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
                          int64_t n_first, int64_t n_cap, int passes, bool force_first,
                          void *work, uint32_t *sched, uint32_t *npass_out, int sms,
                          cudaStream_t s, const uint32_t *run_if = nullptr,
-                         const uint32_t *prev_sched = nullptr);
+                         const uint32_t *prev_sched = nullptr, const KMark &mark = KMark());
 
 // depth.cu: stable f64 depth order (see depth.cu header)
 struct DepthArgs {
@@ -89,7 +104,8 @@ struct DepthArgs {
 };
 size_t depth_work32_bytes(int64_t n_cap);
 size_t depth_work64_bytes(int64_t n_cap);
-int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s);  // returns kernels launched
+int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s,
+                      const KMark &mark = KMark());  // returns kernels launched
 
 // binning.cu: sort-free tile lists (see binning.cu header)
 constexpr int kMaxTileRows = 512;   // height <= 8192
@@ -98,8 +114,7 @@ struct BinArgs {
     const uint32_t *order0, *order1;  // depth sort result buffers
     const uint32_t *depth_sched;      // [16]: which of order0/order1 holds the result
     const GeoRec *geo;                // packed geometry by Gaussian index (preprocess)
-    const float *rinv;                // RN(1/ia) by Gaussian index
-    const float4 *col;                // (r, g, b, -) by Gaussian index
+    const float4 *col;                // (r, g, b, RN(1/ia)) by Gaussian index
     SplatRec *srec;                   // records by depth rank (written here)
     FrameCounters *ctr;
     int width, height, n_rows, tiles_x, ntiles;
@@ -123,7 +138,8 @@ int64_t bin_blocks(int64_t n_cap);
 int64_t bin_scan_tiles(int64_t n_blocks, int n_rows);
 int64_t bin_segments(int64_t cap_p, int n_rows);
 cudaError_t binning_init_attributes();
-int launch_binning(const BinArgs &a, cudaStream_t s);  // returns kernels launched
+int launch_binning(const BinArgs &a, cudaStream_t s,
+                   const KMark &mark = KMark());  // returns kernels launched
 
 // blend.cu
 struct BlendOut {
@@ -132,7 +148,8 @@ struct BlendOut {
     float *trans;   // (H,W) or null
 };
 void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *ranges, int width,
-                  int height, float bg0, float bg1, float bg2, BlendOut out, cudaStream_t s);
+                  int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
+                  cudaStream_t s, const KMark &mark = KMark());
 
 // resample.cu
 struct ResampleAxis {

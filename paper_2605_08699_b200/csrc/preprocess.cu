@@ -14,7 +14,7 @@
 // latency.  Split, each runs at high occupancy with all its loads coalesced:
 //   K1a geo    mean/scale/rotation/rsq/opacity (92 B) -> depth key, the
 //              packed geometry (u, v, ia, ib | ic, rsq, op, ry) and RN(1/ia)
-//   K1b colour kept Gaussians only: mean + SH planes (216 B) -> (r, g, b)
+//   K1b colour kept Gaussians only: mean + SH planes (216 B) -> (r, g, b, rinv)
 // The binning gather (binning.cu) assembles the 48-byte splat record.
 #include "kernels.cuh"
 
@@ -76,6 +76,9 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->P = 0ull;
     ctr->nseg = 0;
     ctr->long_runs = 0;
+    ctr->E = 0ull;
+    ctr->Rb = 0ull;
+    ctr->Rp = 0ull;
 }
 
 __global__ void __launch_bounds__(256) preprocess_geo_kernel(
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(256) preprocess_geo_kernel(
 template <typename ShT>
 __global__ void __launch_bounds__(256) preprocess_color_kernel(
     SceneView sc, CameraArgs cam, int sh_degree, const unsigned long long *__restrict__ keys,
-    float4 *__restrict__ col) {
+    const float *__restrict__ rinv, float4 *__restrict__ col) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sc.n || __ldg(keys + i) == ~0ull) return;  // culled: no colour needed
     const int64_t st = sc.stride;
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(256) preprocess_color_kernel(
         cg = (float)sh_channel(sh, st, i, 1, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
         cbl = (float)sh_channel(sh, st, i, 2, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
     }
-    col[i] = make_float4(cr, cg, cbl, 0.0f);
+    col[i] = make_float4(cr, cg, cbl, __ldg(rinv + i));  // SplatRec.c
 }
 
 }  // namespace
@@ -239,17 +242,21 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
 
 void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
                        int frustum_cull, unsigned long long *keys, GeoRec *geo, float *rinv,
-                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s) {
+                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s,
+                       const KMark &mark) {
     if (scene.n == 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
     preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, cam, frustum_cull, keys, geo, rinv,
                                                      keep_out, ctr);
+    mark("preprocess_geo");
     if (scene.sh_f32 || sh_degree == 0)
-        preprocess_color_kernel<float><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, keys, col);
+        preprocess_color_kernel<float><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, keys, rinv,
+                                                                  col);
     else
         preprocess_color_kernel<double><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, keys,
-                                                                   col);
+                                                                   rinv, col);
+    mark("preprocess_color");
 }
 
 }  // namespace gsr

@@ -348,7 +348,8 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
                          bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
                          int64_t n_first, int64_t n_cap, int passes, bool force_first,
                          void *work, uint32_t *sched, uint32_t *npass_out, int sms,
-                         cudaStream_t s, const uint32_t *run_if, const uint32_t *prev_sched) {
+                         cudaStream_t s, const uint32_t *run_if, const uint32_t *prev_sched,
+                         const KMark &mark) {
     SortArgs<K> a;
     a.run_if = run_if;
     a.prev_sched = prev_sched;
@@ -378,13 +379,16 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
         if (hb > sms * 4) hb = sms * 4;
         if (hb < 1) hb = 1;
         radix_hist_kernel<K><<<(unsigned)hb, RB, 0, s>>>(a);
+        mark(sizeof(K) == 8 ? "radix64_hist" : "radix32_hist");
         launches++;
     }
     radix_plan_kernel<K><<<1, 256, 0, s>>>(a);
+    mark(sizeof(K) == 8 ? "radix64_plan" : "radix32_plan");
     launches++;
     if (n_items_cap > 0) {
         for (int p = 0; p < passes; p++) {
             onesweep_pass_kernel<K><<<(unsigned)a.tiles, RB, sizeof(PassSmem<K>), s>>>(a, p);
+            mark(sizeof(K) == 8 ? "radix64_pass" : "radix32_pass");
             launches++;
         }
     }
@@ -396,10 +400,11 @@ template int launch_onesweep_sort<unsigned long long>(unsigned long long *, unsi
                                                       const uint32_t *, int64_t, int64_t, int,
                                                       bool, void *, uint32_t *, uint32_t *,
                                                       int, cudaStream_t, const uint32_t *,
-                                                      const uint32_t *);
+                                                      const uint32_t *, const KMark &);
 template int launch_onesweep_sort<uint32_t>(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool,
                                             bool, const uint32_t *, int64_t, int64_t, int, bool,
                                             void *, uint32_t *, uint32_t *, int,
-                                            cudaStream_t, const uint32_t *, const uint32_t *);
+                                            cudaStream_t, const uint32_t *, const uint32_t *,
+                                            const KMark &);
 
 }  // namespace gsr
