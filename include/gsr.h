@@ -133,6 +133,16 @@ GSR_API int gsr_render_async(gsr_ctx *ctx, const gsr_scene *scene, const gsr_cam
                      const float background[3], int sh_degree, int frustum_cull);
 GSR_API int gsr_ctx_finish(gsr_ctx *ctx, uint8_t *out_u8, gsr_stats *stats);
 
+/* Pipelined serving: waits for the ctx's previous frame (if any), enqueues
+ * this frame and the device->host copy of its u8 frame into out_u8 (host,
+ * pinned for an asynchronous copy; valid after gsr_ctx_finish or the next
+ * enqueue on this ctx) and returns.  With two or more contexts a caller keeps
+ * several frames in flight, so copies and launch gaps of one frame overlap
+ * the kernels of the next. */
+GSR_API int gsr_render_enqueue(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+                               const float background[3], int sh_degree, int frustum_cull,
+                               uint8_t *out_u8);
+
 /* ---- stage entry points for parity tests (same kernels as gsr_render) ---
  * out_keep (N,) u8; out_order (K,) i64 original indices in depth order
  * (kept[argsort(z[kept], stable)], render.py:279-302); out_packed (K,11) f32

@@ -9,14 +9,15 @@ __version__ = "0.1.0"
 
 from .camera import CameraPose, Intrinsics, pose_from_degrees, scale_intrinsics, world_to_camera
 from .metrics import DimensionMismatch, TooSmall, ladder_ssim, psnr, ssim, upscale_to
-from .render import (DeviceScene, EncodeFailure, Framebuffer, RenderError, RenderStats,
+from .render import (DeviceScene, EncodeFailure, Framebuffer, RenderError, RenderPipeline,
+                     RenderStats,
                      decode_image, device_scene, encode_jpeg, encode_png, evict,
                      framebuffer_to_u8, render_framebuffer, render_u8, render_view, set_device)
 from .synth import ActivatedPrimitives
 
 __all__ = [
     "ActivatedPrimitives", "CameraPose", "DeviceScene", "DimensionMismatch", "EncodeFailure",
-    "Framebuffer", "Intrinsics", "RenderError", "RenderStats", "TooSmall", "decode_image",
+    "Framebuffer", "Intrinsics", "RenderError", "RenderPipeline", "RenderStats", "TooSmall", "decode_image",
     "device_scene", "encode_jpeg", "encode_png", "evict", "framebuffer_to_u8", "ladder_ssim",
     "pose_from_degrees", "psnr", "render_framebuffer", "render_u8", "render_view",
     "scale_intrinsics", "set_device", "ssim", "upscale_to", "world_to_camera",

@@ -73,6 +73,7 @@ SIGNATURES = [
     ("gsr_render", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32, _vp, _vp, _vp, _P(GsrStats)]),
     ("gsr_render_async", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32]),
     ("gsr_ctx_finish", _i32, [_vp, _vp, _P(GsrStats)]),
+    ("gsr_render_enqueue", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32, _vp]),
     ("gsr_debug_preprocess", _i32, [_vp, _vp, _P(GsrCamera), _i32, _i32, _vp, _vp, _vp,
                                     _P(GsrStats)]),
     ("gsr_debug_tile_lists", _i32, [_vp, _vp, _vp, _vp, _P(GsrStats)]),

@@ -14,9 +14,10 @@
 //  3 fixup   splats with equal k32 form runs, already in index order
 //            (stability); each run is re-sorted by the full f64 key, stably
 //            (insertion sort by (key, index)), which gives exactly the
-//            argsort tie order.  A run longer than kMaxRun sets a flag...
-//  4 sort64  ...and only then does the full 64-bit sort run (its kernels exit
-//            immediately otherwise): exact for any input.
+//            argsort tie order.  A run longer than kMaxRun sets a flag; the
+//            host sees it when the frame completes and re-renders the frame
+//            with the full 64-bit sort (8 passes over the raw key bits), so
+//            the order is exact for any input at no cost in the common case.
 #include "kernels.cuh"
 
 namespace gsr {
@@ -47,7 +48,7 @@ __global__ void depth_fixup_kernel(DepthArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t K = a.ctr->K;
     if (i >= K) return;
-    const uint32_t b = a.sched32[16];
+    const uint32_t b = a.sched[16];
     const uint32_t *ks = b ? a.keys32[1] : a.keys32[0];
     uint32_t *vs = b ? a.vals[1] : a.vals[0];
     const uint32_t c = ks[i];
@@ -89,21 +90,20 @@ size_t depth_work64_bytes(int64_t n_cap) { return sort_work_bytes(n_cap, 8, 8); 
 
 int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &mark) {
     if (a.n <= 0) return 0;
+    if (a.full64)  // exact for any input: 8 passes over the raw f64 key bits
+        return launch_onesweep_sort<unsigned long long>(
+            a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, &a.ctr->K, a.n, a.n, 8,
+            true, a.work64, a.sched, &a.ctr->npass_fb, sms, s, mark);
     const unsigned g = (unsigned)((a.n + 255) / 256);
     depth_key32_kernel<<<g, 256, 0, s>>>(a.keys64[0], a.keys32[0], a.n, a.ctr);
     mark("depth_key32");
     int launches = 1;
     launches += launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
                                                true, true, &a.ctr->K, a.n, a.n, 4, true, a.work32,
-                                               a.sched32, &a.ctr->npass, sms, s, nullptr, nullptr,
-                                               mark);
+                                               a.sched, &a.ctr->npass, sms, s, mark);
     depth_fixup_kernel<<<g, 256, 0, s>>>(a);
     mark("depth_fixup");
-    launches++;
-    launches += launch_onesweep_sort<unsigned long long>(
-        a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, &a.ctr->K, a.n, a.n, 8, true,
-        a.work64, a.sched, &a.ctr->npass_fb, sms, s, &a.ctr->long_runs, a.sched32, mark);
-    return launches;
+    return launches + 1;
 }
 
 }  // namespace gsr

@@ -88,7 +88,7 @@ struct gsr_ctx {
     int64_t cap_n = 0, cap_d = 0, cap_p = 0;
     DevBuf keys[2], vals[2], keys32[2], geo, rinv, col, srec, keep;
     int sms = 148;
-    DevBuf depth_work, depth_work32, sched, sched32;  // depth-sort scratch; sched[16] = result buffer
+    DevBuf depth_work, depth_work32, sched;  // depth-sort scratch; sched[16] = result buffer
     uint32_t *hsched = nullptr;   // pinned host copy of sched
     // tile-list buffers (binning.cu)
     DevBuf row_blk, row_start, scan_work, pairs, seg_row, seg_cnt, ttotal, tstart, tile_vals;
@@ -111,12 +111,14 @@ struct gsr_ctx {
     int W = 0, H = 0, ntiles = 0;
     int tile_passes = 0;
     SavedCall saved;
+    uint8_t *saved_out = nullptr;  // host destination of an enqueued frame (gsr_render_enqueue)
+    bool saved_full64 = false;  // depth order via the full 64-bit sort (long key runs)
     bool pending = false;
     int retries = 0;
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &rinv, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &sched32, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+                               &geo, &rinv, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w};
@@ -281,8 +283,8 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         da.n = n;
         da.work32 = c->depth_work32.p;
         da.work64 = c->depth_work.p;
-        da.sched32 = c->sched32.as<uint32_t>();
         da.sched = dsched;
+        da.full64 = c->saved_full64;
         launches += launch_depth_sort(da, c->sms, s, mark);
     }
     cudaEventRecord(c->ev[2], s);
@@ -337,32 +339,45 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     c->saved.cull = cull;
     c->saved.want_rgb = want_rgb;
     c->saved.want_keep = want_keep;
+    c->saved_out = nullptr;
     c->pending = true;
     return GSR_OK;
 }
 
-// Wait for the pending frame; on tile-key overflow grow and re-render once.
+// Wait for the pending frame.  Re-render it once if the tile-key buffer
+// overflowed (after growing it) or if the 32-bit depth sort reported a run of
+// equal span keys too long for its fix-up (then with the full 64-bit sort).
 int complete_frame(gsr_ctx *c) {
     if (!c->pending) return GSR_OK;
     GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
     c->pending = false;
     c->retries = 0;
     const int64_t d = (int64_t)c->hctr->D, p = (int64_t)c->hctr->P;
-    if (d > c->cap_d || p > c->cap_p) {
-        // a pair overflow stops the pipeline before D is known: grow D too
-        if (d > c->cap_d || p > c->cap_p) c->cap_d = round_up(std::max(d, 3 * p) + d / 4 + (1 << 20), 4096);
-        if (p > c->cap_p) c->cap_p = round_up(p + p / 4 + (1 << 20), 4096);
-        if (c->cap_d >= (int64_t(1) << 32) || c->cap_p >= (int64_t(1) << 32))
-            return fail(GSR_E_OOM, "tile list exceeds 2^32 entries");
+    const bool overflow = d > c->cap_d || p > c->cap_p;
+    const bool long_runs = c->hctr->long_runs != 0 && !c->saved_full64;
+    if (overflow || long_runs) {
+        if (overflow) {
+            // a pair overflow stops the pipeline before D is known: grow D too
+            c->cap_d = round_up(std::max(d, 3 * p) + d / 4 + (1 << 20), 4096);
+            if (p > c->cap_p) c->cap_p = round_up(p + p / 4 + (1 << 20), 4096);
+            if (c->cap_d >= (int64_t(1) << 32) || c->cap_p >= (int64_t(1) << 32))
+                return fail(GSR_E_OOM, "tile list exceeds 2^32 entries");
+        }
+        if (long_runs) c->saved_full64 = true;
         SavedCall sv = c->saved;
+        uint8_t *out = c->saved_out;
         int rc = enqueue_frame(c, sv.scene, &sv.cam, sv.bg, sv.sh_degree, sv.cull, sv.want_rgb,
                                sv.want_keep);
+        c->saved_full64 = false;
         if (rc) return rc;
         GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
         c->pending = false;
         c->retries = 1;
         if ((int64_t)c->hctr->D > c->cap_d || (int64_t)c->hctr->P > c->cap_p)
             return fail(GSR_E_OOM, "tile list buffer overflow");
+        if (out)
+            GSR_CUDA_OK(cudaMemcpy(out, c->frame_u8.p, (size_t)c->W * c->H * 3,
+                                   cudaMemcpyDeviceToHost));
     }
     return GSR_OK;
 }
@@ -657,9 +672,7 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     int rc = ensure(c->ctr, sizeof(FrameCounters));
     if (!rc) rc = ensure(c->sticky, sizeof(uint32_t));
     if (!rc) rc = ensure(c->sched, 64 * sizeof(uint32_t));
-    if (!rc) rc = ensure(c->sched32, 64 * sizeof(uint32_t));
-    if (!rc && (cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess ||
-                cudaMemset(c->sched32.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess))
+    if (!rc && cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
     if (!rc && cudaMemset(c->sticky.p, 0, sizeof(uint32_t)) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
@@ -745,6 +758,23 @@ int gsr_render_async(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam
     const float zero[3] = {0, 0, 0};
     return enqueue_frame(ctx, scene, cam, background ? background : zero, sh_degree, frustum_cull,
                          false, false);
+}
+
+int gsr_render_enqueue(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
+                       const float background[3], int sh_degree, int frustum_cull,
+                       uint8_t *out_u8) {
+    if (!ctx || !out_u8) return fail(GSR_E_INVALID, "null argument");
+    DeviceGuard g(ctx->device);
+    int rc = complete_frame(ctx);  // a ctx holds one frame in flight
+    if (rc) return rc;
+    const float zero[3] = {0, 0, 0};
+    rc = enqueue_frame(ctx, scene, cam, background ? background : zero, sh_degree, frustum_cull,
+                       false, false);
+    if (rc) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(out_u8, ctx->frame_u8.p, (size_t)cam->width * cam->height * 3,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->saved_out = out_u8;
+    return GSR_OK;
 }
 
 int gsr_ctx_finish(gsr_ctx *ctx, uint8_t *out_u8, gsr_stats *stats) {

@@ -23,7 +23,7 @@ struct FrameCounters {
     uint32_t K;                 // kept splats
     uint32_t D;                 // tile keys under the contract (may exceed capacity)
     uint32_t npass;             // depth-sort radix passes (32-bit key sort)
-    uint32_t npass_fb;          // passes of the 64-bit fallback sort (0: not needed)
+    uint32_t npass_fb;          // passes of the full 64-bit sort (frames re-rendered after long_runs)
     unsigned long long kmin;    // min / max kept depth key (f64 bits)
     unsigned long long kmax;
     unsigned long long P;       // (splat, tile row) pairs
@@ -88,8 +88,7 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
                          bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
                          int64_t n_first, int64_t n_cap, int passes, bool force_first,
                          void *work, uint32_t *sched, uint32_t *npass_out, int sms,
-                         cudaStream_t s, const uint32_t *run_if = nullptr,
-                         const uint32_t *prev_sched = nullptr, const KMark &mark = KMark());
+                         cudaStream_t s, const KMark &mark = KMark());
 
 // depth.cu: stable f64 depth order (see depth.cu header)
 struct DepthArgs {
@@ -99,8 +98,8 @@ struct DepthArgs {
     FrameCounters *ctr;
     int64_t n;
     void *work32, *work64;
-    uint32_t *sched32;  // 32-bit sort schedule
-    uint32_t *sched;    // final schedule: sched[16] = buffer of vals holding the order
+    uint32_t *sched;    // sort schedule: sched[16] = buffer of vals holding the order
+    bool full64;        // full 64-bit key sort (after a frame reported long runs)
 };
 size_t depth_work32_bytes(int64_t n_cap);
 size_t depth_work64_bytes(int64_t n_cap);

@@ -32,36 +32,28 @@ constexpr double SH_C3_0 = -0.5900435899266435, SH_C3_1 = 2.890611442640554,
                  SH_C3_4 = -0.4570457994644658, SH_C3_5 = 1.445305721320277,
                  SH_C3_6 = -0.5900435899266435;
 
-template <typename T>
-__device__ __forceinline__ double ldsh(const T *sh, int64_t stride, int k, int c, int64_t i) {
-    return (double)__ldg(sh + (int64_t)(k * 3 + c) * stride + i);
-}
-
-// eval_sh_colors for one Gaussian and one channel, numpy expression order.
-template <typename T>
-__device__ __forceinline__ double sh_channel(const T *sh, int64_t stride, int64_t i, int c,
-                                             int degree, double x, double y, double z,
+// eval_sh_colors for one Gaussian and one channel, numpy expression order;
+// v holds the Gaussian's coefficients already in registers (plane k*3 + c).
+template <int DEG, typename T>
+__device__ __forceinline__ double sh_channel(const T *v, int c, double x, double y, double z,
                                              double xx, double yy, double zz, double xy,
                                              double yz, double xz) {
-    double r = SH_C0 * ldsh(sh, stride, 0, c, i);
-    r = r - (SH_C1 * y) * ldsh(sh, stride, 1, c, i) + (SH_C1 * z) * ldsh(sh, stride, 2, c, i) -
-        (SH_C1 * x) * ldsh(sh, stride, 3, c, i);
-    if (degree >= 2) {
-        r = r + (SH_C2_0 * xy) * ldsh(sh, stride, 4, c, i) +
-            (SH_C2_1 * yz) * ldsh(sh, stride, 5, c, i) +
-            (SH_C2_2 * (2.0 * zz - xx - yy)) * ldsh(sh, stride, 6, c, i) +
-            (SH_C2_3 * xz) * ldsh(sh, stride, 7, c, i) +
-            (SH_C2_4 * (xx - yy)) * ldsh(sh, stride, 8, c, i);
+#define SHV(k) ((double)v[(k) * 3 + c])
+    double r = SH_C0 * SHV(0);
+    r = r - (SH_C1 * y) * SHV(1) + (SH_C1 * z) * SHV(2) - (SH_C1 * x) * SHV(3);
+    if (DEG >= 2) {
+        r = r + (SH_C2_0 * xy) * SHV(4) + (SH_C2_1 * yz) * SHV(5) +
+            (SH_C2_2 * (2.0 * zz - xx - yy)) * SHV(6) + (SH_C2_3 * xz) * SHV(7) +
+            (SH_C2_4 * (xx - yy)) * SHV(8);
     }
-    if (degree >= 3) {
-        r = r + ((SH_C3_0 * y) * (3.0 * xx - yy)) * ldsh(sh, stride, 9, c, i) +
-            ((SH_C3_1 * xy) * z) * ldsh(sh, stride, 10, c, i) +
-            ((SH_C3_2 * y) * (4.0 * zz - xx - yy)) * ldsh(sh, stride, 11, c, i) +
-            ((SH_C3_3 * z) * (2.0 * zz - 3.0 * xx - 3.0 * yy)) * ldsh(sh, stride, 12, c, i) +
-            ((SH_C3_4 * x) * (4.0 * zz - xx - yy)) * ldsh(sh, stride, 13, c, i) +
-            ((SH_C3_5 * z) * (xx - yy)) * ldsh(sh, stride, 14, c, i) +
-            ((SH_C3_6 * x) * (xx - 3.0 * yy)) * ldsh(sh, stride, 15, c, i);
+    if (DEG >= 3) {
+        r = r + ((SH_C3_0 * y) * (3.0 * xx - yy)) * SHV(9) + ((SH_C3_1 * xy) * z) * SHV(10) +
+            ((SH_C3_2 * y) * (4.0 * zz - xx - yy)) * SHV(11) +
+            ((SH_C3_3 * z) * (2.0 * zz - 3.0 * xx - 3.0 * yy)) * SHV(12) +
+            ((SH_C3_4 * x) * (4.0 * zz - xx - yy)) * SHV(13) + ((SH_C3_5 * z) * (xx - yy)) * SHV(14) +
+            ((SH_C3_6 * x) * (xx - 3.0 * yy)) * SHV(15);
     }
+#undef SHV
     r = r + 0.5;
     return r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);  // np.clip(result + 0.5, 0, 1)
 }
@@ -203,19 +195,27 @@ __global__ void __launch_bounds__(256) preprocess_geo_kernel(
     }
 }
 
-template <typename ShT>
+// All of a Gaussian's loads are issued before any arithmetic (one memory
+// round trip per thread instead of one per SH degree block).
+template <typename ShT, int DEG>
 __global__ void __launch_bounds__(256) preprocess_color_kernel(
-    SceneView sc, CameraArgs cam, int sh_degree, const unsigned long long *__restrict__ keys,
+    SceneView sc, CameraArgs cam, const unsigned long long *__restrict__ keys,
     const float *__restrict__ rinv, float4 *__restrict__ col) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sc.n || __ldg(keys + i) == ~0ull) return;  // culled: no colour needed
     const int64_t st = sc.stride;
+    const float ri = __ldg(rinv + i);
     float cr, cg, cbl;
-    if (sh_degree == 0) {  // render.py:129-130
+    if (DEG == 0) {  // render.py:129-130
         cr = __ldg(sc.dc + i);
         cg = __ldg(sc.dc + st + i);
         cbl = __ldg(sc.dc + 2 * st + i);
     } else {  // render.py:134-160
+        constexpr int NC = (DEG + 1) * (DEG + 1) * 3;
+        const ShT *sh = (const ShT *)sc.sh;
+        ShT v[NC];
+#pragma unroll
+        for (int k = 0; k < NC; k++) v[k] = __ldg(sh + (int64_t)k * st + i);
         const double mx = __ldg(sc.mean + i), my = __ldg(sc.mean + st + i),
                      mz = __ldg(sc.mean + 2 * st + i);
         const double dx = mx - cam.campos[0];
@@ -226,12 +226,11 @@ __global__ void __launch_bounds__(256) preprocess_color_kernel(
         const double ux = dx / den, uy = dy / den, uz = dz / den;
         const double xx = ux * ux, yy = uy * uy, zz = uz * uz;
         const double xy = ux * uy, yz = uy * uz, xz = ux * uz;
-        const ShT *sh = (const ShT *)sc.sh;
-        cr = (float)sh_channel(sh, st, i, 0, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
-        cg = (float)sh_channel(sh, st, i, 1, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
-        cbl = (float)sh_channel(sh, st, i, 2, sh_degree, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+        cr = (float)sh_channel<DEG>(v, 0, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+        cg = (float)sh_channel<DEG>(v, 1, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+        cbl = (float)sh_channel<DEG>(v, 2, ux, uy, uz, xx, yy, zz, xy, yz, xz);
     }
-    col[i] = make_float4(cr, cg, cbl, __ldg(rinv + i));  // SplatRec.c
+    col[i] = make_float4(cr, cg, cbl, ri);  // SplatRec.c
 }
 
 }  // namespace
@@ -250,12 +249,16 @@ void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_deg
     preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, cam, frustum_cull, keys, geo, rinv,
                                                      keep_out, ctr);
     mark("preprocess_geo");
-    if (scene.sh_f32 || sh_degree == 0)
-        preprocess_color_kernel<float><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, keys, rinv,
-                                                                  col);
-    else
-        preprocess_color_kernel<double><<<blocks, threads, 0, s>>>(scene, cam, sh_degree, keys,
-                                                                   rinv, col);
+#define GSR_COLOR(T, D)                                                                   \
+    preprocess_color_kernel<T, D><<<blocks, threads, 0, s>>>(scene, cam, keys, rinv, col)
+    if (sh_degree == 0) GSR_COLOR(float, 0);
+    else if (scene.sh_f32 && sh_degree == 1) GSR_COLOR(float, 1);
+    else if (scene.sh_f32 && sh_degree == 2) GSR_COLOR(float, 2);
+    else if (scene.sh_f32) GSR_COLOR(float, 3);
+    else if (sh_degree == 1) GSR_COLOR(double, 1);
+    else if (sh_degree == 2) GSR_COLOR(double, 2);
+    else GSR_COLOR(double, 3);
+#undef GSR_COLOR
     mark("preprocess_color");
 }
 

@@ -68,8 +68,6 @@ struct SortArgs {
     uint32_t *tickets;         // [passes]
     uint32_t *sched;           // [0..7] active, [8..15] src buffer, [16] final buffer
     uint32_t *npass_out;       // nullable: number of active passes
-    const uint32_t *run_if;    // nullable: the whole sort is skipped when *run_if == 0
-    const uint32_t *prev_sched;  // skipped sort: result buffer copied from prev_sched[16]
 };
 
 template <typename K>
@@ -87,14 +85,8 @@ __device__ __forceinline__ int64_t items_after_first(const SortArgs<K> &a) {
 }
 
 template <typename K>
-__device__ __forceinline__ bool sort_skipped(const SortArgs<K> &a) {
-    return a.run_if && *a.run_if == 0u;
-}
-
-template <typename K>
 __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
     __shared__ uint32_t h[8][256];
-    if (sort_skipped(a)) return;
     {   // zero the look-back status words and tickets of every pass (the
         // passes run after this kernel; only hist is cleared by memset)
         uint32_t *z = a.status;
@@ -126,11 +118,6 @@ __global__ void __launch_bounds__(256) radix_plan_kernel(SortArgs<K> a) {
     __shared__ uint32_t s_warp[33];
     __shared__ int s_active[8];
     const int d = threadIdx.x;
-    if (sort_skipped(a)) {  // result stays where the previous sort left it
-        if (d < 16) a.sched[d] = 0u;
-        if (d == 0) a.sched[16] = a.prev_sched[16];
-        return;
-    }
     for (int p = 0; p < a.passes; p++) {
         const uint32_t c = a.hist[p * 256 + d];
         const int nz = __syncthreads_count(c != 0u);
@@ -348,11 +335,8 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
                          bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
                          int64_t n_first, int64_t n_cap, int passes, bool force_first,
                          void *work, uint32_t *sched, uint32_t *npass_out, int sms,
-                         cudaStream_t s, const uint32_t *run_if, const uint32_t *prev_sched,
-                         const KMark &mark) {
+                         cudaStream_t s, const KMark &mark) {
     SortArgs<K> a;
-    a.run_if = run_if;
-    a.prev_sched = prev_sched;
     a.keys[0] = keys0;
     a.keys[1] = keys1;
     a.vals[0] = vals0;
@@ -399,12 +383,10 @@ template int launch_onesweep_sort<unsigned long long>(unsigned long long *, unsi
                                                       uint32_t *, uint32_t *, bool, bool,
                                                       const uint32_t *, int64_t, int64_t, int,
                                                       bool, void *, uint32_t *, uint32_t *,
-                                                      int, cudaStream_t, const uint32_t *,
-                                                      const uint32_t *, const KMark &);
+                                                      int, cudaStream_t, const KMark &);
 template int launch_onesweep_sort<uint32_t>(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool,
                                             bool, const uint32_t *, int64_t, int64_t, int, bool,
                                             void *, uint32_t *, uint32_t *, int,
-                                            cudaStream_t, const uint32_t *, const uint32_t *,
-                                            const KMark &);
+                                            cudaStream_t, const KMark &);
 
 }  // namespace gsr

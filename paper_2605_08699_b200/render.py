@@ -262,6 +262,64 @@ def render_u8(prims, pose, intr, background=(0.0, 0.0, 0.0), sh_degree: int = 0,
     return out
 
 
+class RenderPipeline:
+    """Frames in flight for serving: `depth` device contexts (streams) used
+    round-robin; each `submit` enqueues a render plus the device->host copy of
+    its u8 frame into a pinned slot (gsr_render_enqueue) and returns, so the
+    copy and launch gaps of one frame overlap the kernels of the next.  Once
+    `depth` frames are in flight, `submit` first completes the oldest and
+    returns it as (tag, frame); `drain` completes the rest.  A returned frame
+    is a view of a pinned slot, valid until that slot is reused (`depth`
+    submits later): copy it to keep it.  Results are the same frames
+    render_u8 returns, in submission order."""
+
+    def __init__(self, intr, sh_degree: int = 0, background=(0.0, 0.0, 0.0), depth: int = 2,
+                 device: int | None = None):
+        self.device = _default_device if device is None else device
+        self.intr = intr
+        self.sh_degree = int(sh_degree)
+        self.bg = _bg(background)
+        self.ctxs = [_lib.Context(self.device) for _ in range(max(1, int(depth)))]
+        shape = (int(intr.height), int(intr.width), 3)
+        self.slots = [c.pinned("pipeline", shape, np.uint8) for c in self.ctxs]
+        self.inflight = []  # (ctx index, tag), oldest first
+        self.next = 0
+
+    def _finish(self, i):
+        ctx = self.ctxs[i]
+        _lib.check(ctx.lib.gsr_ctx_finish(ctx.handle, None, None), "gsr_ctx_finish")
+        return self.slots[i]
+
+    def submit(self, prims, pose, tag=None):
+        done = None
+        if len(self.inflight) == len(self.ctxs):
+            i, t = self.inflight.pop(0)
+            done = (t, self._finish(i))
+        i = self.next
+        self.next = (self.next + 1) % len(self.ctxs)
+        sc = device_scene(prims, self.device)
+        _check_sh(self.sh_degree, sc.count)
+        cam = make_camera(pose, self.intr)
+        ctx = self.ctxs[i]
+        _lib.check(ctx.lib.gsr_render_enqueue(ctx.handle, sc.handle, ctypes.byref(cam), self.bg,
+                                              self.sh_degree, 1, _lib.ptr(self.slots[i])),
+                   "gsr_render_enqueue")
+        self.inflight.append((i, tag))
+        return done
+
+    def drain(self):
+        out = []
+        while self.inflight:
+            i, t = self.inflight.pop(0)
+            out.append((t, self._finish(i)))
+        return out
+
+    def close(self):
+        self.drain()
+        for c in self.ctxs:
+            c.close()
+
+
 def framebuffer_to_u8(fb) -> np.ndarray:
     """render.py:484-485 (device-converted when available)."""
     u8 = getattr(fb, "u8", None)
@@ -368,6 +426,7 @@ def debug_tile_ranges(width: int, height: int, *, device: int | None = None) -> 
 
 
 __all__ = ["Framebuffer", "RenderStats", "RenderError", "EncodeFailure", "DeviceScene",
+           "RenderPipeline",
            "device_scene", "evict", "set_device", "render_framebuffer", "render_u8",
            "render_view", "framebuffer_to_u8", "encode_jpeg", "encode_png", "decode_image",
            "cutoff_radius_sq", "make_camera", "debug_preprocess", "debug_tile_lists",

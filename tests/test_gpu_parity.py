@@ -326,3 +326,58 @@ def test_concurrent_threads_deterministic(gsr):
         t.join()
     for k in range(16):
         assert np.array_equal(out[k], ref[k % 8])
+
+
+def test_depth_ties_and_long_key_runs(gsr, oracle):
+    """Stable depth order under exact f64 ties and under runs of nearly-equal
+    depths: short runs are resolved by the 32-bit sort's fix-up, a run longer
+    than its limit makes the frame re-render with the full 64-bit sort
+    (np.argsort(kind="stable") tie order, render.py:295)."""
+    from paper_2605_08699_b200.render import debug_preprocess
+    from paper_2605_08699_b200.synth import ActivatedPrimitives
+    rng = np.random.default_rng(11)
+    intr = gsr.Intrinsics(fx=120.0, fy=120.0, cx=64.0, cy=64.0, width=128, height=128)
+    for n_plane, spread in [(12, 0.0), (200, 0.0), (300, 1e-12)]:
+        n = 2000
+        z = rng.uniform(2.0, 6.0, n)
+        z[:n_plane] = 3.0 + spread * np.arange(n_plane)  # a plane of (nearly) equal depths
+        perm = rng.permutation(n)
+        means = np.column_stack([rng.uniform(-1.5, 1.5, n), rng.uniform(-1.5, 1.5, n), z])[perm]
+        q = rng.normal(size=(n, 4))
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+        prims = ActivatedPrimitives(means, rng.uniform(0.01, 0.05, (n, 3)), q,
+                                    rng.uniform(0.2, 0.99, n), rng.uniform(0, 1, (n, 3)),
+                                    rng.normal(0, 0.2, (n, 16, 3)))
+        pose = gsr.CameraPose(0.0, 0.0)
+        keep, order, packed, st = debug_preprocess(prims, pose, intr, 0)
+        rot, w2c = oracle.world_to_camera(0.0, 0.0, (0.0, 0.0, 0.0))
+        fr = oracle.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                           prims.colors_dc, prims.sh_coeffs, w2c, rot, intr.fx, intr.fy, intr.cx,
+                           intr.cy, intr.width, intr.height, (0.0, 0.0, 0.0), 0)
+        assert np.array_equal(keep, fr.keep)
+        assert np.array_equal(order, fr.kept[fr.order])
+        fb = gsr.render_framebuffer(prims, pose, intr)
+        assert np.array_equal(fb.u8, fr.u8)
+        if n_plane > 16:  # long run: full 64-bit sort on the re-render
+            assert st.retries == 1 and st.depth_passes >= 5
+
+
+def test_render_pipeline_matches_render_u8(gsr):
+    """RenderPipeline (frames in flight on several streams, gsr_render_enqueue)
+    returns, in order, exactly the frames render_u8 returns."""
+    prims = golden_scene((20000, 3, (0.01, 0.05), 1))
+    intr = gsr.Intrinsics(fx=300.0, fy=300.0, cx=160.0, cy=120.0, width=320, height=240)
+    poses = [gsr.CameraPose(0.02 * i, -0.01 * i, (0.01 * i, 0.0, 0.1)) for i in range(7)]
+    ref = [gsr.render_u8(prims, p, intr, sh_degree=3).copy() for p in poses]
+    for depth in (1, 2, 3):
+        pipe = gsr.RenderPipeline(intr, sh_degree=3, depth=depth)
+        got = []
+        for i, p in enumerate(poses):
+            r = pipe.submit(prims, p, tag=i)
+            if r is not None:
+                got.append((r[0], r[1].copy()))
+        got += [(t, f.copy()) for t, f in pipe.drain()]
+        pipe.close()
+        assert [t for t, _ in got] == list(range(len(poses)))
+        for (_, f), r in zip(got, ref):
+            assert np.array_equal(f, r)
