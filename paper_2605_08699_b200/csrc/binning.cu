@@ -132,6 +132,7 @@ struct PairSmem {
     uint8_t lr[kPairCache];          // in-warp rank of a pair within its row
     uint8_t owner[kPairCache];       // block-local splat of a pair
     uint32_t wpre[BR / 32][kRowsMax];  // per-warp coverage masks -> counts -> exclusive prefix
+    uint32_t rowbase[kRowsMax];      // this block's first slot in each tile row (row_blk)
     int ty_lo, ty_hi;
 };
 
@@ -209,10 +210,10 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
             S.wpre[j][ty] = run;
             run += c;
         }
+        S.rowbase[ty] = run ? a.row_blk[(int64_t)ty * a.n_blocks + b] : 0u;
     }
     __syncthreads();
     // one thread per pair: exact tile span, stored at its grouped slot
-    const int64_t nb = a.n_blocks;
     uint32_t n_rows = 0;
     for (uint32_t q = tid; q < npairs; q += BR) {
         const int j = q < kPairCache ? (int)S.owner[q] : rank_of_pair(S.poff, q);
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
                 in_warp += (S.lo[jj] < S.hi[jj] && ty >= S.lo[jj] / kTile &&
                             ty <= (S.hi[jj] - 1) / kTile);
         }
-        const uint32_t slot = a.row_blk[(int64_t)ty * nb + b] + S.wpre[j >> 5][ty] + in_warp;
+        const uint32_t slot = S.rowbase[ty] + S.wpre[j >> 5][ty] + in_warp;
         // exact tile-column span of splat j in tile row ty
         const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
         n_rows += (uint32_t)(y1 - y0);

@@ -13,8 +13,9 @@
 // contributions per pixel are the reference's.  After the list: rgb += T*bg
 // (render.py:423-427), then the u8 conversion of render.py:470+484-485.
 //
-// Layout: one CTA per tile, 8 warps; warp w owns pixel rows 2w, 2w+1 of the
-// tile (lane & 15 = column, lane >> 4 = row).  A warp walks the tile list 32
+// Layout: a work item is one warp's 2x16 pixels, pixel rows 2w, 2w+1 of a
+// 16x16 tile (lane & 15 = column, lane >> 4 = row), taken from a work queue by
+// a persistent grid (see blend_kernel).  A warp walks the tile list 32
 // splats at a time: lane j loads splat j's record (128-bit loads), computes
 // its two row intervals (exact, row_xlr) as a 32-bit pixel-coverage mask and
 // stages the splat's per-row terms in shared memory (structure of arrays, so
@@ -24,6 +25,8 @@
 // useful work on every lane that still has splats (not just on the lanes a
 // given splat covers).  Warps leave as soon as all their 32 pixels are
 // saturated (warp-vote early termination); no block barriers in the loop.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace gsr {
@@ -94,16 +97,19 @@ struct ExpK {
     double inv_ln2n, c0, c1, c2;
 };
 
+template <bool kChecked>
 __device__ __forceinline__ float expf_blend(float x, const unsigned long long *tab,
-                                            const ExpK &K) {
-    if (!(fabsf(x) < 88.0f)) return expf_special(x, tab);
+                                            uint32_t tab_s, const ExpK &K) {
+    if (kChecked && !(fabsf(x) < 88.0f)) return expf_special(x, tab);
     const double kShift = 0x1.8p+52;
     const double xd = (double)x;
     double kd = __fma_rn(K.inv_ln2n, xd, kShift);
     const uint32_t ki = (uint32_t)__double2loint(kd);
     kd = __dsub_rn(kd, kShift);
     const double r = __fma_rn(K.inv_ln2n, xd, -kd);
-    const unsigned long long t = tab[ki & 31u] + ((unsigned long long)ki << 47);
+    unsigned long long t;  // tab[ki & 31] through a precomputed shared-window address
+    asm("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(tab_s + ((ki & 31u) << 3)));
+    t += (unsigned long long)ki << 47;
     const double sc = __longlong_as_double((long long)t);
     const double z = __fma_rn(K.c0, r, K.c1);
     const double r2 = __dmul_rn(r, r);
@@ -113,11 +119,62 @@ __device__ __forceinline__ float expf_blend(float x, const unsigned long long *t
     return __double2float_rn(y);
 }
 
+// A splat whose record is finite with ia <= 4, rsq <= 21 and ib^2 <= ia*ic
+// cannot give |power| >= 88 on any pixel of its mask: on a pixel row, the
+// quadratic form is rsq at the interval ends (mid -+ span), the mask reaches at
+// most 1.5 px beyond them, and ia*span = sqrt(disc) <= sqrt(ia*rsq), so
+// Q <= rsq + 3*sqrt(ia*rsq) + 2.25*ia < 53, |power| < 27.  Batches of such
+// splats skip glibc's |x| >= 88 special cases.
+__device__ __forceinline__ bool exp_safe(const float4 &A, const float4 &B) {
+    const float u = A.x, v = A.y, ia = A.z, ib = A.w, ic = B.x, rsq = B.y;
+    return fabsf(u) < 1e30f && fabsf(v) < 1e30f && ia > 0.0f && ia <= 4.0f && ic > 0.0f &&
+           ic < 1e30f && fabsf(ib) < 1e30f && rsq >= 0.0f && rsq <= 21.0f && ib * ib <= ia * ic;
+}
+
 struct WarpBatch {         // one warp's current 32 splats
     float4 geo[2][32];     // per pixel row of the warp: (u, ia, (2*ib)*dy, (ic*dy)*dy)
     float4 col[32];        // (op, r, g, b)
 };
 
+// Each lane walks its own covering splats of the batch in depth order
+// (render.py:405-421, reference operation order).  (Software-pipelining the
+// next splat's alpha against the transmittance chain was measured slower:
+// the kernel is issue-bound, not latency-bound.)
+template <bool kChecked>
+__device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, const float4 *col,
+                                          float fx, const unsigned long long *tab, uint32_t tab_s,
+                                          const ExpK &ek, float &T, float &cr, float &cg,
+                                          float &cb, bool &done, uint32_t &n_comp) {
+    while (__any_sync(0xffffffffu, mine != 0u)) {
+        if (mine) {
+            const int s = __ffs(mine) - 1;
+            mine &= mine - 1u;
+            n_comp++;
+            const float4 g = geo[s];  // u, ia, ib_dy, cy_term
+            const float4 k = col[s];  // op, r, g, b
+            const float dx = fx - g.x;
+            const float power = -0.5f * (g.y * dx * dx + g.z * dx + g.w);
+            float alpha = k.x * expf_blend<kChecked>(power, tab, tab_s, ek);
+            if (alpha > kAlphaMax) alpha = kAlphaMax;
+            const float weight = T * alpha;
+            cr += weight * k.y;
+            cg += weight * k.z;
+            cb += weight * k.w;
+            T = T * (1.0f - alpha);
+            if (T < kTStop) {
+                done = true;
+                mine = 0u;
+            }
+        }
+    }
+}
+
+// Persistent kernel: the work items are (tile, pixel-row pair) = one warp's
+// 2x16 pixels; warps take items from a frame-global queue (ctr->blend_next)
+// until it is empty.  Item lengths vary by orders of magnitude (a warp leaves
+// as soon as its 32 pixels saturate, or walks the whole tile list if they
+// never do), so binding 8 warps to a CTA per tile would leave most of a CTA's
+// warps idle behind its slowest one; the queue keeps every warp busy.
 __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
     const SplatRec *__restrict__ srec, const uint32_t *__restrict__ tile_vals,
     const uint2 *__restrict__ ranges, int width, int height, float bg0, float bg1, float bg2,
@@ -128,124 +185,129 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
     __syncthreads();
 
     const int tiles_x = (width + kTile - 1) / kTile;
-    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int n_items = tiles_x * ((height + kTile - 1) / kTile) * kWarps;
     const int lane = lane_id(), w = threadIdx.x >> 5;
-    const int X = tx * kTile;
-    const int iy0 = ty * kTile + 2 * w;
     const int prow = lane >> 4;
-    const int iy = iy0 + prow;
-    const int ix = X + (lane & 15);
-    const bool inside = ix < width && iy < height;
-    const float py0 = (float)iy0 + 0.5f, py1 = (float)(iy0 + 1) + 0.5f;
-    const float fx = (float)ix + 0.5f;
-
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-    bool done = !inside;
-    uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
-    const uint2 rg = ranges[blockIdx.x];
     WarpBatch &B_ = s_b[w];
     const float4 *geo = B_.geo[prow];
+    const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(s_tab);
     // pinned in registers (opaque to rematerialisation by constant reloads)
     ExpK ek;
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.inv_ln2n) : "d"(kExpK[0]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c0) : "d"(kExpK[1]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c1) : "d"(kExpK[2]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c2) : "d"(kExpK[3]));
+    uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
 
-    for (uint32_t c = rg.x; c < rg.y; c += 32) {
-        if (__all_sync(0xffffffffu, done)) break;
-        const uint32_t j = c + lane;
-        uint32_t mask = 0;
-        if (j < rg.y) {
-            const uint32_t r = __ldg(tile_vals + j);  // depth rank
-            const float4 A = __ldg(&srec[r].a);
-            const float4 B = __ldg(&srec[r].b);
-            const float4 C = __ldg(&srec[r].c);
-            int lo, hi;
-            row_range(A.y, B.w, height, lo, hi);
-            const bool fast = splat_fast_ok(A.y, A.z, A.w);
-            n_rows += (uint32_t)(iy0 >= lo && iy0 < hi) + (uint32_t)(iy0 + 1 >= lo && iy0 + 1 < hi);
-            mask = row_mask(A, B, C.w, fast, iy0, lo, hi, X, width) |
-                   (row_mask(A, B, C.w, fast, iy0 + 1, lo, hi, X, width) << 16);
-            if (mask) {  // render.py:400-402 terms per pixel row
-                const float ib2 = 2.0f * A.w;
-                const float dy0 = py0 - A.y, dy1 = py1 - A.y;
-                B_.geo[0][lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
-                B_.geo[1][lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
-                B_.col[lane] = make_float4(B.z, C.x, C.y, C.z);
-            }
-        }
-        __syncwarp();
-        uint32_t mine = transpose32(mask, lane);
-        if (done) mine = 0u;
-        while (__any_sync(0xffffffffu, mine != 0u)) {
-            if (mine) {
-                const int s = __ffs(mine) - 1;
-                mine &= mine - 1u;
-                // render.py:405-421, reference operation order
-                n_comp++;
-                const float4 g = geo[s];  // u, ia, ib_dy, cy_term
-                const float4 k = B_.col[s];
-                const float dx = fx - g.x;
-                const float power = -0.5f * (g.y * dx * dx + g.z * dx + g.w);
-                float alpha = k.x * expf_blend(power, s_tab, ek);
-                if (alpha > kAlphaMax) alpha = kAlphaMax;
-                const float weight = T * alpha;
-                cr += weight * k.y;
-                cg += weight * k.z;
-                cb += weight * k.w;
-                T = T * (1.0f - alpha);
-                if (T < kTStop) {
-                    done = true;
-                    mine = 0u;
+    while (true) {
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(&ctr->blend_next, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= n_items) break;
+        const int tile = item / kWarps, wr = item % kWarps;
+        const int tx = tile % tiles_x, ty = tile / tiles_x;
+        const int X = tx * kTile;
+        const int iy0 = ty * kTile + 2 * wr;
+        const int iy = iy0 + prow;
+        const int ix = X + (lane & 15);
+        const bool inside = ix < width && iy < height;
+        const float py0 = (float)iy0 + 0.5f, py1 = (float)(iy0 + 1) + 0.5f;
+        const float fx = (float)ix + 0.5f;
+
+        float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+        bool done = !inside;
+        const uint2 rg = ranges[tile];
+
+        for (uint32_t c = rg.x; c < rg.y; c += 32) {
+            if (__all_sync(0xffffffffu, done)) break;
+            const uint32_t j = c + lane;
+            uint32_t mask = 0;
+            bool safe = true;
+            if (j < rg.y) {
+                const uint32_t r = __ldg(tile_vals + j);  // depth rank
+                const float4 A = __ldg(&srec[r].a);
+                const float4 B = __ldg(&srec[r].b);
+                const float4 C = __ldg(&srec[r].c);
+                int lo, hi;
+                row_range(A.y, B.w, height, lo, hi);
+                const bool fast = splat_fast_ok(A.y, A.z, A.w);
+                n_rows += (uint32_t)(iy0 >= lo && iy0 < hi) +
+                          (uint32_t)(iy0 + 1 >= lo && iy0 + 1 < hi);
+                mask = row_mask(A, B, C.w, fast, iy0, lo, hi, X, width) |
+                       (row_mask(A, B, C.w, fast, iy0 + 1, lo, hi, X, width) << 16);
+                if (mask) {  // render.py:400-402 terms per pixel row
+                    safe = exp_safe(A, B);
+                    const float ib2 = 2.0f * A.w;
+                    const float dy0 = py0 - A.y, dy1 = py1 - A.y;
+                    B_.geo[0][lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
+                    B_.geo[1][lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
+                    B_.col[lane] = make_float4(B.z, C.x, C.y, C.z);
                 }
             }
+            __syncwarp();
+            uint32_t mine = transpose32(mask, lane);
+            if (done) mine = 0u;
+            if (__all_sync(0xffffffffu, safe))
+                composite<false>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, done,
+                                 n_comp);
+            else
+                composite<true>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, done,
+                                n_comp);
+            __syncwarp();
         }
-        __syncwarp();
-    }
-    {
-        unsigned long long e = n_comp, r = n_rows;
+        if (inside) {
+            cr += T * bg0;
+            cg += T * bg1;
+            cb += T * bg2;
+            const int64_t p = (int64_t)iy * width + ix;
+            if (out.rgb) {
+                out.rgb[3 * p + 0] = cr;
+                out.rgb[3 * p + 1] = cg;
+                out.rgb[3 * p + 2] = cb;
+            }
+            if (out.trans) out.trans[p] = T;
+            // render.py:470 + 484-485: trunc(clip(clip(f64(c), 0, 1) * 255 + 0.5, 0, 255))
+            const float ch[3] = {cr, cg, cb};
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            e += __shfl_xor_sync(0xffffffffu, e, o);
-            r += __shfl_xor_sync(0xffffffffu, r, o);
-        }
-        if (lane == 0) {
-            atomicAdd(&ctr->E, e);
-            atomicAdd(&ctr->Rb, r);
+            for (int k = 0; k < 3; k++) {
+                double d = (double)ch[k];
+                d = d < 0.0 ? 0.0 : (d > 1.0 ? 1.0 : d);
+                double q = d * 255.0 + 0.5;
+                q = q < 0.0 ? 0.0 : (q > 255.0 ? 255.0 : q);
+                out.u8[3 * p + k] = (uint8_t)(int)q;
+            }
         }
     }
-    if (!inside) return;
-    cr += T * bg0;
-    cg += T * bg1;
-    cb += T * bg2;
-    const int64_t p = (int64_t)iy * width + ix;
-    if (out.rgb) {
-        out.rgb[3 * p + 0] = cr;
-        out.rgb[3 * p + 1] = cg;
-        out.rgb[3 * p + 2] = cb;
-    }
-    if (out.trans) out.trans[p] = T;
-    // render.py:470 + 484-485: trunc(clip(clip(f64(c), 0, 1) * 255 + 0.5, 0, 255))
-    const float ch[3] = {cr, cg, cb};
+    unsigned long long e = n_comp, r = n_rows;
 #pragma unroll
-    for (int k = 0; k < 3; k++) {
-        double d = (double)ch[k];
-        d = d < 0.0 ? 0.0 : (d > 1.0 ? 1.0 : d);
-        double s = d * 255.0 + 0.5;
-        s = s < 0.0 ? 0.0 : (s > 255.0 ? 255.0 : s);
-        out.u8[3 * p + k] = (uint8_t)(int)s;
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&ctr->E, e);
+        atomicAdd(&ctr->Rb, r);
     }
 }
+
+int g_blend_grid = 0;
 
 }  // namespace
 
 void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *ranges, int width,
                   int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
                   cudaStream_t s, const KMark &mark) {
+    if (!g_blend_grid) {  // persistent grid: every SM full
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel, kBlendThreads, 0);
+        g_blend_grid = sms * (per_sm > 0 ? per_sm : 1);
+    }
     const int tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
-    blend_kernel<<<tiles, kBlendThreads, 0, s>>>(srec, tile_vals, ranges, width, height, bg0, bg1,
-                                                 bg2, out, ctr);
+    const int grid = std::min(g_blend_grid, tiles);
+    blend_kernel<<<grid, kBlendThreads, 0, s>>>(srec, tile_vals, ranges, width, height, bg0, bg1,
+                                                bg2, out, ctr);
     mark("blend");
 }
 

@@ -33,6 +33,8 @@ struct FrameCounters {
     unsigned long long E;       // blend: composited (pixel, splat) evaluations
     unsigned long long Rb;      // blend: (splat, pixel row) interval evaluations
     unsigned long long Rp;      // binning: (splat, pixel row) interval evaluations
+    uint32_t blend_next;        // blend work queue: next (tile, pixel-row pair) item
+    uint32_t pad2;
 };
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.

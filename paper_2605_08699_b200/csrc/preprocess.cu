@@ -71,6 +71,8 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->E = 0ull;
     ctr->Rb = 0ull;
     ctr->Rp = 0ull;
+    ctr->blend_next = 0;
+    ctr->pad2 = 0;
 }
 
 __global__ void __launch_bounds__(256) preprocess_geo_kernel(
@@ -85,19 +87,20 @@ __global__ void __launch_bounds__(256) preprocess_geo_kernel(
         const double r00 = cam.r[0], r01 = cam.r[1], r02 = cam.r[2];
         const double r10 = cam.r[3], r11 = cam.r[4], r12 = cam.r[5];
         const double r20 = cam.r[6], r21 = cam.r[7], r22 = cam.r[8];
+        // every load first (one memory round trip), then the f64 math
         const double mx = __ldg(sc.mean + i), my = __ldg(sc.mean + st + i),
                      mz = __ldg(sc.mean + 2 * st + i);
+        const double qw = __ldg(sc.rot + i), qx = __ldg(sc.rot + st + i),
+                     qy = __ldg(sc.rot + 2 * st + i), qz = __ldg(sc.rot + 3 * st + i);
+        const double sx = __ldg(sc.scale + i), sy = __ldg(sc.scale + st + i),
+                     sz = __ldg(sc.scale + 2 * st + i);
+        const double rsq = __ldg(sc.rsq + i);
+        const float opac = __ldg(sc.opac + i);
         // render.py:174-176
         const double x = r00 * mx + r01 * my + r02 * mz + cam.t[0];
         const double y = r10 * mx + r11 * my + r12 * mz + cam.t[1];
         const double z = r20 * mx + r21 * my + r22 * mz + cam.t[2];
         if (!(z <= kZNear)) {
-            const double qw = __ldg(sc.rot + i), qx = __ldg(sc.rot + st + i),
-                         qy = __ldg(sc.rot + 2 * st + i), qz = __ldg(sc.rot + 3 * st + i);
-            const double sx = __ldg(sc.scale + i), sy = __ldg(sc.scale + st + i),
-                         sz = __ldg(sc.scale + 2 * st + i);
-            const double rsq = __ldg(sc.rsq + i);
-            const float opac = __ldg(sc.opac + i);
             // render.py:185-193
             const double m00 = (1.0 - 2.0 * (qy * qy + qz * qz)) * sx;
             const double m01 = (2.0 * (qx * qy - qw * qz)) * sy;

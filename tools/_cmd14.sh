@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-ladder 2>&1 | tail -1 > gpurun_out/bench.json
+python -c "import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['value_single_stream'], d['e2e']['value']); [print(k, v['ms_per_frame']) for k, v in d['kernels'].items()]"
+NCU_K="blend_kernel|seg_place|onesweep" NCU_S=5 NCU_C=5 NCU_NAME=bb bash tools/ncu_full.sh
