@@ -228,8 +228,8 @@ def load_simt_peaks():
 
 
 def kernel_work(name, wl, c):
-    """Algorithmic units of one frame's launches of a kernel (DESIGN.md
-    section 4): (bytes, fp32 ops)."""
+    """Algorithmic units of ONE launch of a kernel:
+    (bytes, fp32 ops)."""
     n, k, d, p = wl["n"], c["K"], c["D"], c["P"]
     sh_bytes = 12 * (wl["sh"] + 1) ** 2 if wl["sh"] else 12
     px = wl["w"] * wl["h"]
@@ -292,6 +292,7 @@ def kernel_profile(lib, ctx, sc, cams, sh, frames, wl, peaks, simt):
         per_frame = tot / nf
         nl = launches[nm] / nf
         b, f = kernel_work(nm, wl, mean_c)
+        b, f = b * nl, f * nl  # per frame
         e = {"ms_per_frame": round(per_frame, 4), "launches_per_frame": nl,
              "bound": BOUND.get(nm, "hbm")}
         if b and per_frame > 0:

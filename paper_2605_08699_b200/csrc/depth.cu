@@ -5,11 +5,11 @@
 // 3M Gaussians), but 8 radix passes over 64-bit keys are mostly wasted: the
 // kept depths span [kmin, kmax] and are nearly all distinct at 32-bit
 // resolution of that span.  So:
-//  1 key32   k32 = min((bits(z) - kmin) >> shift, 2^32 - 2), shift chosen so
-//            the span fits 32 bits; culled Gaussians keep the sentinel ~0.
+//  1 key32   k32 = min((bits(z) - kmin) >> shift, 2^24 - 1), shift chosen so
+//            the span fits 24 bits; culled Gaussians keep the sentinel ~0.
 //            Positive f64 bits order like the values, and the map is monotone,
 //            so sorting k32 orders every pair of splats whose k32 differ.
-//  2 sort32  stable Onesweep radix sort of (k32, index), <= 4 passes (the
+//  2 sort32  stable Onesweep radix sort of (k32, index), <= 3 passes (the
 //            first drops the sentinels: the compaction of render.py:279).
 //  3 fixup   splats with equal k32 form runs, already in index order
 //            (stability); each run is re-sorted by the full f64 key, stably
@@ -25,6 +25,10 @@ namespace gsr {
 namespace {
 
 constexpr int kMaxRun = 16;
+// Span key width: 24 bits = 3 radix passes.  At 3M kept splats a bucket holds
+// 0.2 splats on average; the fix-up resolves the resulting short runs.
+constexpr int kSpanBits = 24;
+constexpr unsigned long long kSpanMax = (1ull << kSpanBits) - 1;
 
 __global__ void depth_key32_kernel(const unsigned long long *__restrict__ k64,
                                    uint32_t *__restrict__ k32, int64_t n,
@@ -34,12 +38,12 @@ __global__ void depth_key32_kernel(const unsigned long long *__restrict__ k64,
     const unsigned long long kmin = ctr->kmin, kmax = ctr->kmax;
     const unsigned long long range = kmax > kmin ? kmax - kmin : 0ull;
     const int bits = range ? 64 - __clzll((long long)range) : 0;
-    const int shift = bits > 32 ? bits - 32 : 0;
+    const int shift = bits > kSpanBits ? bits - kSpanBits : 0;
     const unsigned long long k = k64[i];
     uint32_t o = 0xffffffffu;
     if (k != ~0ull) {
         const unsigned long long q = (k - kmin) >> shift;
-        o = q < 0xfffffffeull ? (uint32_t)q : 0xfffffffeu;
+        o = q < kSpanMax ? (uint32_t)q : (uint32_t)kSpanMax;
     }
     k32[i] = o;
 }
@@ -99,7 +103,7 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &
     mark("depth_key32");
     int launches = 1;
     launches += launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
-                                               true, true, &a.ctr->K, a.n, a.n, 4, true, a.work32,
+                                               true, true, &a.ctr->K, a.n, a.n, kSpanBits / 8, true, a.work32,
                                                a.sched, &a.ctr->npass, sms, s, mark);
     depth_fixup_kernel<<<g, 256, 0, s>>>(a);
     mark("depth_fixup");
