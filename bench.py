@@ -12,7 +12,7 @@ GPUs (torchrun, one process per GPU) rank r serves its own session on its own
 GPU: weak scaling, no data-path collective (the only NCCL calls are the
 barrier and the max-over-ranks timing reduction).
 
-value      device throughput with --streams S (default 2) frames in flight:
+value      device throughput with --streams S (default 4) frames in flight:
            K frames enqueued round-robin on S contexts (CUDA streams), the
            scene resident in HBM; CUDA events (start on stream 0, which the
            others wait on; end on every stream), max over ranks; frames of
@@ -523,7 +523,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-ladder", action="store_true")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=4,
                     help="frames in flight (contexts/streams) for value and e2e")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)

@@ -130,11 +130,15 @@ struct PairSmem {
     uint32_t poff[BR + 1];
     uint32_t s_warp[33];
     uint8_t lr[kPairCache];          // in-warp rank of a pair within its row
-    uint8_t owner[kPairCache];       // block-local splat of a pair
-    uint32_t wpre[BR / 32][kRowsMax];  // per-warp coverage masks -> counts -> exclusive prefix
-    uint32_t rowbase[kRowsMax];      // this block's first slot in each tile row (row_blk)
+    uint16_t owner[kPairCache];      // block-local splat of a pair
     int ty_lo, ty_hi;
+    // followed in dynamic shared memory by (n_rows = tile rows of the frame):
+    //   uint32_t wpre[BR / 32][n_rows]  per-warp coverage masks -> counts -> prefix
+    //   uint32_t rowbase[n_rows]        this block's first slot per tile row (row_blk)
 };
+__host__ __device__ inline size_t pair_smem_bytes(int n_rows) {
+    return sizeof(PairSmem) + sizeof(uint32_t) * (size_t)(BR / 32 + 1) * (size_t)n_rows;
+}
 
 __device__ __forceinline__ int rank_of_pair(const uint32_t *poff, uint32_t q) {
     int lo = 0, hi = BR;  // poff[lo] <= q < poff[hi]
@@ -149,6 +153,9 @@ __device__ __forceinline__ int rank_of_pair(const uint32_t *poff, uint32_t q) {
 __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     extern __shared__ __align__(16) unsigned char dyn_raw[];
     PairSmem &S = *reinterpret_cast<PairSmem *>(dyn_raw);
+    const int nr = a.n_rows;
+    uint32_t *wpre_all = reinterpret_cast<uint32_t *>(dyn_raw + sizeof(PairSmem));
+    uint32_t *rowbase = wpre_all + (BR / 32) * nr;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t b = blockIdx.x;
     const int64_t k = a.ctr->K;
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     // give the in-warp rank, a prefix of the popcounts over warps the rest
     const int ylo = S.ty_lo, yhi = S.ty_hi;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    uint32_t *wm = S.wpre[w];
+    uint32_t *wm = wpre_all + w * nr;
     for (int ty = ylo + lane; ty <= yhi; ty += 32) wm[ty] = 0u;
     __syncwarp();
     for (int ty = t0; ty <= t1; ty++) atomicOr(&wm[ty], 1u << lane);
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         const uint32_t q = off + (uint32_t)(ty - t0);
         if (q < kPairCache) {
             S.lr[q] = (uint8_t)__popc(wm[ty] & lt_mask);
-            S.owner[q] = (uint8_t)tid;
+            S.owner[q] = (uint16_t)tid;
         }
     }
     __syncwarp();
@@ -206,11 +213,11 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         uint32_t run = 0;
 #pragma unroll
         for (int j = 0; j < BR / 32; j++) {
-            const uint32_t c = S.wpre[j][ty];
-            S.wpre[j][ty] = run;
+            const uint32_t c = wpre_all[j * nr + ty];
+            wpre_all[j * nr + ty] = run;
             run += c;
         }
-        S.rowbase[ty] = run ? a.row_blk[(int64_t)ty * a.n_blocks + b] : 0u;
+        rowbase[ty] = run ? a.row_blk[(int64_t)ty * a.n_blocks + b] : 0u;
     }
     __syncthreads();
     // one thread per pair: exact tile span, stored at its grouped slot
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
                 in_warp += (S.lo[jj] < S.hi[jj] && ty >= S.lo[jj] / kTile &&
                             ty <= (S.hi[jj] - 1) / kTile);
         }
-        const uint32_t slot = S.rowbase[ty] + S.wpre[j >> 5][ty] + in_warp;
+        const uint32_t slot = rowbase[ty] + wpre_all[(j >> 5) * nr + ty] + in_warp;
         // exact tile-column span of splat j in tile row ty
         const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
         n_rows += (uint32_t)(y1 - y0);
@@ -495,7 +502,7 @@ int64_t bin_segments(int64_t cap_p, int n_rows) { return cap_p / kSeg + n_rows +
 cudaError_t binning_init_attributes() {
     cudaError_t e = cudaFuncSetAttribute(bin_pairs_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(PairSmem));
+                                         (int)pair_smem_bytes(kRowsMax));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(seg_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(8 * (kMaxTilesX + 1) * sizeof(uint32_t)));
@@ -514,7 +521,7 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark) {
     cudaMemsetAsync(a.scan_work, 0, sizeof(unsigned long long) * (size_t)(scan_tiles + 1), s);
     row_scan_kernel<<<(unsigned)scan_tiles, 256, 0, s>>>(a);
     mark("row_scan");
-    bin_pairs_kernel<<<nb, BR, sizeof(PairSmem), s>>>(a);
+    bin_pairs_kernel<<<nb, BR, pair_smem_bytes(a.n_rows), s>>>(a);
     mark("bin_pairs");
     seg_table_kernel<<<1, 1024, 0, s>>>(a);
     mark("seg_table");
