@@ -464,6 +464,33 @@ def run_gsr(args, wl):
                   "ms_per_ladder_p50": float(np.percentile(lt, 50)),
                   "what": "per pose: render 1080p + 3 rungs, upscale_to 1080p, ssim, on device"}
 
+    # JPEG of the rendered frame on the device (render_view's
+    # encode), byte-identical to Pillow; Pillow on the host timed beside it
+    jpeg = None
+    if not args.no_ladder:
+        import io
+        from PIL import Image
+        from paper_2605_08699_b200.render import _jpeg
+        frame = g.render_u8(prims, poses[W], intr, sh_degree=wl["sh"]).copy()
+        jpeg = {}
+        for q in (90, 65, 35):
+            for _ in range(3):
+                _jpeg(ctx, None, intr.width, intr.height, q)  # warm (device frame)
+            jt = []
+            for _ in range(20):
+                g.render_u8(prims, poses[W], intr, sh_degree=wl["sh"], out=out)
+                t0 = time.perf_counter()
+                payload = _jpeg(ctx, None, intr.width, intr.height, q)
+                jt.append((time.perf_counter() - t0) * 1000.0)
+            buf = io.BytesIO()
+            t0 = time.perf_counter()
+            Image.fromarray(frame, "RGB").save(buf, format="JPEG", quality=q,
+                                               subsampling=2 if q < 90 else 0)
+            pil_ms = (time.perf_counter() - t0) * 1000.0
+            jpeg[f"q{q}"] = {"gpu_ms_p50": float(np.percentile(jt, 50)), "bytes": len(payload),
+                             "pillow_ms": pil_ms,
+                             "identical_to_pillow": payload == buf.getvalue()}
+
     result = None
     if rank == 0:
         frame0 = g.render_u8(prims, poses[W], intr, sh_degree=wl["sh"])
@@ -500,6 +527,7 @@ def run_gsr(args, wl):
             "counters": {k: int(v) for k, v in counters.items()},
             "roofline": roof,
             "ladder": ladder,
+            "jpeg": jpeg,
             "clocks": clocks.summary(),
         }
         if base is not None:

@@ -169,6 +169,18 @@ GSR_API int gsr_ssim_u8(gsr_ctx *ctx, const uint8_t *a, const uint8_t *b, int wi
 GSR_API int gsr_ssim_luma_f64(gsr_ctx *ctx, const double *x, const double *y, int width,
                               int height, double *out_ssim);
 
+/* ---- JPEG: render.encode_jpeg (render.py:488-498), SURVEY.md 8f row 1 ----
+ * Baseline JPEG of an (H,W,3) u8 frame, byte-identical to Pillow 12.2 /
+ * libjpeg-turbo (islow DCT, standard Huffman tables, no restart markers):
+ * quality 1..100, subsampling 2 (4:2:0) or 0 (4:4:4) as Pillow's
+ * subsampling= (render_view uses 4:2:0 below quality 90).  rgb: host frame,
+ * or NULL to encode the ctx's last rendered frame in place on the device.
+ * *out_len receives the JPEG size; out may be NULL to query it (the encode
+ * runs either way), else out_cap must hold *out_len bytes. */
+GSR_API int gsr_encode_jpeg(gsr_ctx *ctx, const uint8_t *rgb, int width, int height,
+                            int quality, int subsampling, uint8_t *out, size_t out_cap,
+                            size_t *out_len);
+
 /* ---- pinned host memory for end-to-end frame readback ------------------- */
 GSR_API int gsr_host_alloc(void **out, size_t bytes);
 GSR_API int gsr_host_free(void *ptr);

@@ -16,6 +16,7 @@ the reference's own stage order:
 * tile-list contract             SURVEY.md A.4     -> orc_tile_keys
 * ``upscale_to`` (Pillow)        metrics.py:125-130 -> orc_resample_bilinear
 * ``ssim`` (scipy)               metrics.py:76-114 -> orc_ssim
+* ``encode_jpeg`` (Pillow/libjpeg-turbo) render.py:488-498 -> orc_jpeg
 
 Pinned by tests/test_oracle_golden.py against vectors produced by the
 reference itself (tests/golden/make_golden.py).
@@ -91,6 +92,8 @@ def _declare(L):
     L.orc_resample_bilinear.argtypes = [vp, i32, i32, vp, i32, i32]
     L.orc_ssim.argtypes = [vp, vp, i32, i32]
     L.orc_ssim.restype = dbl
+    L.orc_jpeg.argtypes = [vp, i32, i32, i32, i32, vp, i64]
+    L.orc_jpeg.restype = i64
     L.orc_num_threads.restype = i32
     L.orc_set_num_threads.argtypes = [i32]
 
@@ -284,6 +287,17 @@ def ssim(a, b):
     if min(a.shape[0], a.shape[1]) < 11:
         raise ValueError("too small")
     return float(lib().orc_ssim(_p(a), _p(b), a.shape[0], a.shape[1]))
+
+
+def jpeg(img, quality):
+    """render.encode_jpeg restated (Pillow/libjpeg-turbo baseline JPEG,
+    4:2:0 below quality 90, 4:4:4 at 90+)."""
+    img = _c(img, np.uint8)
+    h, w = img.shape[:2]
+    cap = 4096 + h * w * 8
+    out = np.empty(cap, dtype=np.uint8)
+    n = lib().orc_jpeg(_p(img), w, h, int(quality), 1 if quality < 90 else 0, _p(out), cap)
+    return out[:n].tobytes()
 
 
 def psnr(a, b):

@@ -106,6 +106,8 @@ struct gsr_ctx {
     const char *kname[kMaxMarks] = {};
     // ladder / resample / ssim scratch
     DevBuf base_u8, up_u8, tmp_u8, src_u8, dst_u8, coefs, ssim_part, ssim_misc, ssim_w;
+    DevBuf jpeg_ws;                  // jpeg.cu workspace
+    uint32_t *hjpeg = nullptr;       // pinned [bits, stuffed bytes]
     double *hssim = nullptr;
     // last frame
     int W = 0, H = 0, ntiles = 0;
@@ -121,7 +123,7 @@ struct gsr_ctx {
                                &geo, &rinv, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
-                               &ssim_part, &ssim_misc, &ssim_w};
+                               &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws};
         for (auto *b : all) s += (int64_t)b->bytes;
         return s;
     }
@@ -344,41 +346,41 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     return GSR_OK;
 }
 
-// Wait for the pending frame.  Re-render it once if the tile-key buffer
-// overflowed (after growing it) or if the 32-bit depth sort reported a run of
-// equal span keys too long for its fix-up (then with the full 64-bit sort).
+// Wait for the pending frame.  Re-render it if the tile-key or pair buffer
+// overflowed (after growing it; a pair overflow stops the pipeline before D
+// is known, so up to three rounds) or if the 32-bit depth sort reported a run
+// of equal span keys too long for its fix-up (then with the full 64-bit sort).
 int complete_frame(gsr_ctx *c) {
     if (!c->pending) return GSR_OK;
     GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
     c->pending = false;
     c->retries = 0;
-    const int64_t d = (int64_t)c->hctr->D, p = (int64_t)c->hctr->P;
-    const bool overflow = d > c->cap_d || p > c->cap_p;
-    const bool long_runs = c->hctr->long_runs != 0 && !c->saved_full64;
-    if (overflow || long_runs) {
-        if (overflow) {
-            // a pair overflow stops the pipeline before D is known: grow D too
-            c->cap_d = round_up(std::max(d, 3 * p) + d / 4 + (1 << 20), 4096);
-            if (p > c->cap_p) c->cap_p = round_up(p + p / 4 + (1 << 20), 4096);
-            if (c->cap_d >= (int64_t(1) << 32) || c->cap_p >= (int64_t(1) << 32))
-                return fail(GSR_E_OOM, "tile list exceeds 2^32 entries");
-        }
+    uint8_t *out = c->saved_out;
+    for (int round = 0;; round++) {
+        const int64_t d = (int64_t)c->hctr->D, p = (int64_t)c->hctr->P;
+        const bool ov_p = p > c->cap_p, ov_d = !ov_p && d > c->cap_d;
+        const bool long_runs = c->hctr->long_runs != 0 && !c->saved_full64;
+        if (!ov_p && !ov_d && !long_runs) break;
+        if (round == 3) return fail(GSR_E_OOM, "tile list buffer overflow");
+        if (ov_p) c->cap_p = round_up(p + p / 4 + (1 << 20), 4096);
+        if (ov_p || ov_d) c->cap_d = round_up(std::max(d, 3 * p) + std::max(d, 3 * p) / 4 + (1 << 20), 4096);
+        if (c->cap_d >= (int64_t(1) << 32) || c->cap_p >= (int64_t(1) << 32))
+            return fail(GSR_E_OOM, "tile list exceeds 2^32 entries");
         if (long_runs) c->saved_full64 = true;
         SavedCall sv = c->saved;
-        uint8_t *out = c->saved_out;
+        const bool full64 = c->saved_full64;
         int rc = enqueue_frame(c, sv.scene, &sv.cam, sv.bg, sv.sh_degree, sv.cull, sv.want_rgb,
                                sv.want_keep);
-        c->saved_full64 = false;
+        c->saved_full64 = full64;
         if (rc) return rc;
         GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
         c->pending = false;
-        c->retries = 1;
-        if ((int64_t)c->hctr->D > c->cap_d || (int64_t)c->hctr->P > c->cap_p)
-            return fail(GSR_E_OOM, "tile list buffer overflow");
-        if (out)
-            GSR_CUDA_OK(cudaMemcpy(out, c->frame_u8.p, (size_t)c->W * c->H * 3,
-                                   cudaMemcpyDeviceToHost));
+        c->retries = round + 1;
     }
+    c->saved_full64 = false;
+    if (c->retries && out)
+        GSR_CUDA_OK(cudaMemcpy(out, c->frame_u8.p, (size_t)c->W * c->H * 3,
+                               cudaMemcpyDeviceToHost));
     return GSR_OK;
 }
 
@@ -509,6 +511,60 @@ int ssim_device(gsr_ctx *c, const SsimInput &in, int W, int H, double *dev_out) 
                 c->ssim_misc.as<uint32_t>(), dev_out, c->stream);
     GSR_CUDA_OK(cudaGetLastError());
     return GSR_OK;
+}
+
+// JFIF headers exactly as Pillow / libjpeg-turbo write them (jcmarker.c):
+// SOI, APP0 (JFIF 1.01, aspect 1:1), DQT x2 (zigzag order), SOF0, DHT x4
+// (standard tables), SOS.
+void jpeg_headers(int W, int H, int quality, int sub, std::vector<uint8_t> &h) {
+    static const int kZigzag[64] = {
+        0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,  12, 19, 26, 33, 40, 48,
+        41, 34, 27, 20, 13, 6,  7,  14, 21, 28, 35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23,
+        30, 37, 44, 51, 58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+    auto put16 = [&](int v) {
+        h.push_back((uint8_t)(v >> 8));
+        h.push_back((uint8_t)v);
+    };
+    h = {0xFF, 0xD8, 0xFF, 0xE0};
+    put16(16);
+    const uint8_t jfif[14] = {'J', 'F', 'I', 'F', 0, 1, 1, 0, 0, 1, 0, 1, 0, 0};
+    h.insert(h.end(), jfif, jfif + 14);
+    uint16_t qt[2][64];
+    jpeg_quant_tables(quality, qt);
+    for (int t = 0; t < 2; t++) {
+        h.push_back(0xFF);
+        h.push_back(0xDB);
+        put16(67);
+        h.push_back((uint8_t)t);
+        for (int i = 0; i < 64; i++) h.push_back((uint8_t)qt[t][kZigzag[i]]);
+    }
+    h.push_back(0xFF);
+    h.push_back(0xC0);
+    put16(17);
+    h.push_back(8);
+    put16(H);
+    put16(W);
+    h.push_back(3);
+    const uint8_t ysamp = sub ? 0x22 : 0x11;
+    const uint8_t comps[9] = {1, ysamp, 0, 2, 0x11, 1, 3, 0x11, 1};
+    h.insert(h.end(), comps, comps + 9);
+    for (int t = 0; t < 2; t++)
+        for (int ac = 0; ac < 2; ac++) {
+            const uint8_t *bits, *vals;
+            int nv;
+            jpeg_huffman_spec(t, ac, &bits, &vals, &nv);
+            h.push_back(0xFF);
+            h.push_back(0xC4);
+            put16(2 + 1 + 16 + nv);
+            h.push_back((uint8_t)((ac << 4) | t));
+            h.insert(h.end(), bits, bits + 16);
+            h.insert(h.end(), vals, vals + nv);
+        }
+    h.push_back(0xFF);
+    h.push_back(0xDA);
+    put16(12);
+    const uint8_t sos[10] = {3, 1, 0x00, 2, 0x11, 3, 0x11, 0, 63, 0};
+    h.insert(h.end(), sos, sos + 10);
 }
 
 }  // namespace
@@ -664,6 +720,7 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hssim, sizeof(double) * 64);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hsched, sizeof(uint32_t) * 64);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hjpeg, sizeof(uint32_t) * 4);
     if (e != cudaSuccess) {
         int rc = fail_cuda(e, "context setup");
         gsr_ctx_destroy(c);
@@ -711,6 +768,7 @@ int gsr_ctx_destroy(gsr_ctx *ctx) {
     if (ctx->hctr) cudaFreeHost(ctx->hctr);
     if (ctx->hssim) cudaFreeHost(ctx->hssim);
     if (ctx->hsched) cudaFreeHost(ctx->hsched);
+    if (ctx->hjpeg) cudaFreeHost(ctx->hjpeg);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GSR_OK;
@@ -949,6 +1007,49 @@ int gsr_host_alloc(void **out, size_t bytes) {
 
 int gsr_host_free(void *ptr) {
     if (ptr) GSR_CUDA_OK(cudaFreeHost(ptr));
+    return GSR_OK;
+}
+
+int gsr_encode_jpeg(gsr_ctx *ctx, const uint8_t *rgb, int width, int height, int quality,
+                    int subsampling, uint8_t *out, size_t out_cap, size_t *out_len) {
+    if (!ctx || !out_len) return fail(GSR_E_INVALID, "null argument");
+    if (width <= 0 || height <= 0 || width > 65535 || height > 65535)
+        return fail(GSR_E_INVALID, "cannot encode a zero-dimension or oversized frame");
+    if (quality < 1 || quality > 100) return fail(GSR_E_INVALID, "jpeg quality out of range 1..100");
+    if (subsampling != 0 && subsampling != 2)
+        return fail(GSR_E_INVALID, "subsampling must be 0 (4:4:4) or 2 (4:2:0)");
+    DeviceGuard g(ctx->device);
+    int rc;
+    const uint8_t *src = nullptr;
+    const size_t nb = (size_t)width * height * 3;
+    if (rgb) {
+        if ((rc = ensure(ctx->src_u8, nb))) return rc;
+        GSR_CUDA_OK(cudaMemcpyAsync(ctx->src_u8.p, rgb, nb, cudaMemcpyHostToDevice, ctx->stream));
+        src = ctx->src_u8.as<uint8_t>();
+    } else {
+        if ((rc = complete_frame(ctx))) return rc;
+        if (ctx->W != width || ctx->H != height)
+            return fail(GSR_E_INVALID, "frame size differs from the ctx's last render");
+        src = ctx->frame_u8.as<uint8_t>();
+    }
+    JpegLayout L;
+    const size_t ws = jpeg_workspace_bytes(width, height, subsampling == 2, &L);
+    if ((rc = ensure(ctx->jpeg_ws, ws))) return rc;
+    GSR_CUDA_OK(launch_jpeg(src, width, height, quality, L, ctx->jpeg_ws.as<unsigned char>(),
+                            ctx->hjpeg, ctx->stream));
+    std::vector<uint8_t> hdr;
+    jpeg_headers(width, height, quality, subsampling == 2, hdr);
+    const size_t scan = ctx->hjpeg[1];
+    const size_t total = hdr.size() + scan + 2;
+    *out_len = total;
+    if (!out) return GSR_OK;
+    if (out_cap < total) return fail(GSR_E_INVALID, "output buffer too small");
+    std::memcpy(out, hdr.data(), hdr.size());
+    GSR_CUDA_OK(cudaMemcpyAsync(out + hdr.size(), ctx->jpeg_ws.as<unsigned char>() + L.off_out,
+                                scan, cudaMemcpyDeviceToHost, ctx->stream));
+    GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    out[total - 2] = 0xFF;
+    out[total - 1] = 0xD9;
     return GSR_OK;
 }
 

@@ -152,6 +152,23 @@ void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *
                   int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
                   cudaStream_t s, const KMark &mark = KMark());
 
+// jpeg.cu: baseline JPEG of a device u8 frame (Pillow / libjpeg-turbo exact)
+struct JpegLayout {
+    int sub, mcux, mcuy, blocks_per_mcu;
+    int cw[3], ch[3], wb[3], hb[3], mw[3];
+    int64_t coef_off[3], n_real, n_scan;
+    uint64_t max_bits;
+    size_t words, stuff_threads;
+    size_t off_coef, off_bits, off_words, off_aux, off_len, off_out;
+};
+size_t jpeg_workspace_bytes(int W, int H, int sub, JpegLayout *L);
+void jpeg_quant_tables(int quality, uint16_t qt[2][64]);
+void jpeg_huffman_spec(int t, int ac, const uint8_t **bits, const uint8_t **vals, int *nvals);
+// encodes; host_len2 (pinned, 2 words) receives [bits, stuffed bytes]; stuffed
+// scan bytes are at ws + L.off_out.  Synchronises the stream.
+cudaError_t launch_jpeg(const uint8_t *rgb, int W, int H, int quality, const JpegLayout &L,
+                        unsigned char *ws, uint32_t *host_len2, cudaStream_t s);
+
 // resample.cu
 struct ResampleAxis {
     const int32_t *bounds;   // (out, 2): xmin, xlen

@@ -381,3 +381,87 @@ def test_render_pipeline_matches_render_u8(gsr):
         assert [t for t, _ in got] == list(range(len(poses)))
         for (_, f), r in zip(got, ref):
             assert np.array_equal(f, r)
+
+
+def _pil_jpeg(img, quality):
+    import io
+    from PIL import Image
+    buf = io.BytesIO()  # render.py:494-497
+    Image.fromarray(img, mode="RGB").save(buf, format="JPEG", quality=quality,
+                                          subsampling=2 if quality < 90 else 0)
+    return buf.getvalue()
+
+
+@pytest.mark.parametrize("quality", [1, 5, 10, 25, 35, 50, 65, 75, 89, 90, 95, 100])
+def test_jpeg_byte_identical_to_pillow(gsr, quality):
+    """encode_jpeg on the GPU (jpeg.cu) returns the
+    reference's Pillow/libjpeg-turbo bytes exactly, edge sizes included."""
+    rng = np.random.default_rng(quality)
+    for (h, w) in [(1, 1), (5, 7), (8, 8), (16, 16), (17, 15), (33, 17), (31, 64), (240, 320)]:
+        for kind in ("noise", "smooth"):
+            if kind == "noise":
+                img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+            else:
+                yy, xx = np.mgrid[0:h, 0:w]
+                img = np.stack([(xx * 255 // max(w - 1, 1)), (yy * 255 // max(h - 1, 1)),
+                                ((xx + yy) * 7) % 256], axis=-1).astype(np.uint8)
+            fb = gsr.Framebuffer(w, h, u8=img)
+            got = gsr.encode_jpeg(fb, quality)
+            assert got == _pil_jpeg(img, quality), (h, w, kind, quality)
+
+
+def test_jpeg_rendered_frames_and_render_view(gsr):
+    """Rendered 1080p/ladder frames: GPU JPEG bytes == Pillow's; render_view
+    (render + encode on the device) == encode_jpeg(render_u8(...))."""
+    from paper_2605_08699_b200.synth import base_intrinsics_1080p, ladder_1080p, synthetic_scene
+    prims = synthetic_scene(200_000, seed=5, sh_degree=3)
+    base = base_intrinsics_1080p()
+    pose = gsr.CameraPose(0.05, -0.02, (0.02, 0.0, 0.1))
+    for rung in ladder_1080p():
+        class Profile:
+            width, height, jpeg_quality = rung["width"], rung["height"], rung["jpeg_quality"]
+        intr = gsr.scale_intrinsics(base, rung["width"], rung["height"])
+        frame = gsr.render_u8(prims, pose, intr, sh_degree=3).copy()
+        ref = _pil_jpeg(frame, rung["jpeg_quality"])
+        assert gsr.encode_jpeg(gsr.Framebuffer(intr.width, intr.height, u8=frame),
+                               rung["jpeg_quality"]) == ref
+        payload, _ = gsr.render_view(prims, pose, base, Profile(), sh_degree=3)
+        assert payload == ref
+    with pytest.raises(gsr.EncodeFailure):
+        gsr.encode_jpeg(gsr.Framebuffer(4, 4, u8=np.zeros((4, 4, 3), np.uint8)), 0)
+
+
+def test_buffer_overflow_rerender(gsr, oracle):
+    """A fresh context sizes its pair / tile-key buffers from N; a scene of a
+    few huge splats overflows both, and the frame is re-rendered (possibly
+    twice) with grown buffers: the result still equals the oracle."""
+    from paper_2605_08699_b200.render import debug_preprocess
+    from paper_2605_08699_b200.synth import ActivatedPrimitives
+    rng = np.random.default_rng(21)
+    n = 3000
+    means = np.column_stack([rng.uniform(-1, 1, n), rng.uniform(-0.6, 0.6, n),
+                             rng.uniform(2.0, 4.0, n)])
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    prims = ActivatedPrimitives(means, rng.uniform(0.1, 0.4, (n, 3)), q,
+                                rng.uniform(0.01, 0.2, n), rng.uniform(0, 1, (n, 3)),
+                                np.zeros((n, 16, 3)))
+    intr = gsr.scale_intrinsics(gsr.Intrinsics(fx=1662.7688, fy=1662.7688, cx=960.0, cy=540.0,
+                                               width=1920, height=1080), 1920, 1080)
+    result = {}
+
+    def run():  # a new thread gets a fresh context (server.py:99-100 worker)
+        st = gsr.RenderStats()
+        fb = gsr.render_framebuffer(prims, gsr.CameraPose(0.0, 0.0), intr, stats=st)
+        _, _, _, gst = debug_preprocess(prims, gsr.CameraPose(0.0, 0.0), intr, 0)
+        result["u8"], result["keys"], result["retries"] = fb.u8, st.tile_keys, gst.retries
+
+    t = threading.Thread(target=run)
+    t.start()
+    t.join()
+    rot, w2c = oracle.world_to_camera(0.0, 0.0, (0.0, 0.0, 0.0))
+    fr = oracle.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                       prims.colors_dc, prims.sh_coeffs, w2c, rot, intr.fx, intr.fy, intr.cx,
+                       intr.cy, intr.width, intr.height, (0.0, 0.0, 0.0), 0)
+    assert result["keys"] > 16 * n  # beyond the initial capacity
+    assert np.array_equal(result["u8"], fr.u8)

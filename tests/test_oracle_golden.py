@@ -131,3 +131,24 @@ def test_ssim_matches_reference(oracle):
     a = r.integers(0, 256, (37, 53, 3), dtype=np.uint8)
     c = np.clip(a.astype(int) + 7, 0, 255).astype(np.uint8)
     assert abs(oracle.ssim(a, c) - ss["noise_37x53"]) < 1e-10
+
+
+@pytest.mark.parametrize("quality", [1, 5, 10, 25, 35, 50, 65, 75, 89, 90, 95, 100])
+def test_jpeg_matches_pillow(oracle, quality):
+    """orc_jpeg (libjpeg-turbo restated) == Pillow's bytes (render.py:488-498);
+    this pins the algorithm jpeg.cu runs on the GPU."""
+    import io
+    from PIL import Image
+    rng = np.random.default_rng(quality)
+    for (h, w) in [(1, 1), (5, 7), (8, 8), (16, 16), (17, 15), (33, 17), (31, 64), (120, 160)]:
+        for kind in ("noise", "smooth"):
+            if kind == "noise":
+                img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+            else:
+                yy, xx = np.mgrid[0:h, 0:w]
+                img = np.stack([(xx * 255 // max(w - 1, 1)), (yy * 255 // max(h - 1, 1)),
+                                ((xx + yy) * 7) % 256], axis=-1).astype(np.uint8)
+            buf = io.BytesIO()
+            Image.fromarray(img, mode="RGB").save(buf, format="JPEG", quality=quality,
+                                                  subsampling=2 if quality < 90 else 0)
+            assert oracle.jpeg(img, quality) == buf.getvalue(), (h, w, kind, quality)
