@@ -275,6 +275,28 @@ def test_config3_3m_1080p_vs_oracle(gsr, oracle):
     assert np.all(np.diff(tt) >= 0)
 
 
+def test_config4_6m_1080p_vs_oracle(gsr, oracle):
+    """Config 4 at full size (6M Gaussians, SH3, 1920x1080: the sort/binning
+    and tile-list memory stress): culling, depth order, tile lists and frame
+    exact vs the oracle; lists sorted by (tile, rank)."""
+    from paper_2605_08699_b200.render import debug_preprocess, debug_tile_lists
+    from paper_2605_08699_b200.synth import base_intrinsics_1080p, synthetic_scene
+    prims = synthetic_scene(6_000_000, seed=7, sh_degree=3)
+    intr = base_intrinsics_1080p()
+    pose = gsr.CameraPose(-0.03, 0.02, (-0.05, 0.02, 0.2))
+    keep, order, packed, st = debug_preprocess(prims, pose, intr, 3)
+    fr = _oracle_frame(oracle, prims, pose, intr, 3)
+    assert np.array_equal(keep, fr.keep)
+    assert np.array_equal(order, fr.kept[fr.order])
+    fb = gsr.render_framebuffer(prims, pose, intr, sh_degree=3)
+    assert np.array_equal(fb.u8, fr.u8)
+    tt, tr = debug_tile_lists()
+    ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
+    assert np.array_equal(tt, ot) and np.array_equal(tr, orr)
+    key = tt.astype(np.int64) * (1 << 32) + tr
+    assert np.all(np.diff(key) > 0)
+
+
 def test_ladder_ssim_vs_oracle(gsr, oracle):
     from paper_2605_08699_b200.synth import synthetic_scene
     prims = synthetic_scene(20_000, seed=5, sh_degree=3)

@@ -1,0 +1,12 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "frame/" \
+  -o gpurun_out/frame_full -f python tools/profile_frame.py 3 > gpurun_out/ncu_full.log 2>&1
+tail -2 gpurun_out/ncu_full.log
+python tools/ncu_traffic.py gpurun_out/frame_full.ncu-rep gpurun_out/ncu_traffic_config3.json gpurun_out/ncu_frame_summary.txt
+cat gpurun_out/ncu_frame_summary.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "frame/" \
+  --csv --log-file gpurun_out/launches.csv python tools/profile_frame.py 4 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches.csv 1 | tee gpurun_out/launches.txt
+timeout 900 python -m pytest tests -m gpu -q -k "config4" 2>&1 | tail -3
+bash tools/sanitize.sh

@@ -8,13 +8,13 @@ nvcc -O3 -fmad=false -gencode arch=compute_100a,code=sm_100a tools/peaks.cu -o t
   tools/_build/peaks > gpurun_out/measured_simt_peaks.json
 cat gpurun_out/measured_simt_peaks.json
 cp gpurun_out/measured_simt_peaks.json profiles/measured_simt_peaks.json
-timeout 1200 ncu --set full --clock-control none --import-source on -s 60 -c 30 \
+timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "frame/" \
   -o gpurun_out/frame_full -f python tools/profile_frame.py 3 > gpurun_out/ncu_full.log 2>&1
 python tools/ncu_traffic.py gpurun_out/frame_full.ncu-rep profiles/ncu_traffic_config3.json gpurun_out/ncu_frame_summary.txt
 cat gpurun_out/ncu_frame_summary.txt
 cp profiles/ncu_traffic_config3.json gpurun_out/
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 60 --csv \
-  --log-file gpurun_out/launches.csv python tools/profile_frame.py 6 > /dev/null 2>&1
-python tools/launch_summary.py gpurun_out/launches.csv 2 | tee gpurun_out/launches.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "frame/" \
+  --csv --log-file gpurun_out/launches.csv python tools/profile_frame.py 4 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches.csv 1 | tee gpurun_out/launches.txt
 timeout 900 python bench.py --steps 200 --warmup 10 2>&1 | tail -1 > gpurun_out/bench.json
 cat gpurun_out/bench.json

@@ -1,8 +1,14 @@
-"""Render a few config-3 frames (for ncu captures): python tools/profile_frame.py [n_frames]."""
+"""Render config-3 frames for ncu captures; the LAST frame runs inside an NVTX
+range "frame" so captures can select exactly one whole frame:
+
+    ncu --nvtx --nvtx-include "frame/" ... python tools/profile_frame.py [n_frames] [workload]
+"""
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402  (NVTX markers only)
+
 import bench  # noqa: E402
 import paper_2605_08699_b200 as g  # noqa: E402
 
@@ -11,6 +17,11 @@ prims = bench.build_scene(wl)
 intr = bench.intrinsics(wl)
 poses = bench.poses_for(0, int(sys.argv[1]) if len(sys.argv) > 1 else 3)
 st = g.RenderStats()
-for p in poses:
+for i, p in enumerate(poses):
+    last = i == len(poses) - 1
+    if last:
+        torch.cuda.nvtx.range_push("frame")
     g.render_u8(prims, p, intr, sh_degree=wl["sh"], stats=st)
+    if last:
+        torch.cuda.nvtx.range_pop()
 print("frames", len(poses), "drawn", st.splats_drawn, "D", st.tile_keys)

@@ -1,0 +1,32 @@
+# compute-sanitizer over a small render (config-1-like), the ladder, JPEG and
+# the depth-tie / overflow paths: memcheck (device memory errors) and
+# racecheck / synccheck (shared-memory hazards, barrier misuse).
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+cat > /tmp/san_case.py <<'PY'
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2605_08699_b200 as g
+from paper_2605_08699_b200.synth import synthetic_scene
+prims = synthetic_scene(20000, seed=3, sh_degree=3)
+intr = g.Intrinsics(fx=300.0, fy=300.0, cx=160.0, cy=120.0, width=320, height=240)
+for i in range(2):
+    fb = g.render_framebuffer(prims, g.CameraPose(0.02 * i, -0.01, (0.0, 0.0, 0.1)), intr,
+                              sh_degree=3)
+jp = g.encode_jpeg(fb, 75)
+up = g.upscale_to(fb.u8[::2, ::2].copy(), 320, 240)
+s = g.ssim(up, fb.u8)
+pipe = g.RenderPipeline(intr, sh_degree=3, depth=2)
+for i in range(3):
+    pipe.submit(prims, g.CameraPose(0.01 * i, 0.0))
+pipe.drain()
+pipe.close()
+print("case ok", len(jp), round(s, 6))
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_case.py \
+    > gpurun_out/sanitizer_$tool.txt 2>&1
+  echo "$tool exit=$?" | tee -a gpurun_out/sanitizer_summary.txt
+  tail -3 gpurun_out/sanitizer_$tool.txt
+done
