@@ -541,13 +541,84 @@ def run_gsr(args, wl):
     return 0
 
 
+def run_config5(args):
+    """BASELINE config 5: 64 concurrent pose-trace sessions over the 14
+    synthetic scene sizes N_k = round(250k * 24^(k/13)) (250k ... 6M), sharded
+    session i -> GPU i mod N with no collective (sessions.py).  Each rank holds
+    replicas of the scenes its sessions use and serves its sessions
+    round-robin through RenderPipeline (--streams frames in flight), 1080p, SH3.
+    value: whole-box frames/s (frames of all ranks / max-over-ranks wall time)."""
+    import torch
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_2605_08699_b200 as g
+    from paper_2605_08699_b200.sessions import config5_sessions, scenes_for, shard
+    from paper_2605_08699_b200.synth import base_intrinsics_1080p, synthetic_scene
+    g.set_device(local_rank)
+    mine = shard(config5_sessions(64), rank, world)
+    scenes = {k: synthetic_scene(next(s.gaussians for s in mine if s.scene == k), seed=k,
+                                 sh_degree=3) for k in scenes_for(mine)}
+    intr = base_intrinsics_1080p()
+    traces = {s.index: poses_for(s.index, args.warmup + args.steps) for s in mine}
+    pipe = g.RenderPipeline(intr, sh_degree=3, depth=args.streams, device=local_rank)
+    for s in mine:  # upload every scene + warm
+        pipe.submit(scenes[s.scene], traces[s.index][0])
+    pipe.drain()
+    K = args.steps
+    order = [(mine[i % len(mine)], args.warmup + i // len(mine)) for i in range(K)]
+    order = [(s, min(t, args.warmup + args.steps - 1)) for s, t in order]
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    with ClockSampler(local_rank) as clocks:
+        t0 = time.perf_counter()
+        for s, t in order:
+            pipe.submit(scenes[s.scene], traces[s.index][t])
+        pipe.drain()
+        wall = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        wall = float(tt.item())
+    pipe.close()
+    if rank == 0:
+        line = {
+            "metric": "box frames/s, 64 sessions x 14 scene sizes, 1080p",
+            "value": world * K / wall, "unit": "frames/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * wall / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": "config5: 64 pose-trace sessions over 14 scene sizes "
+                                   "(250k..6M Gaussians, SH3, 1920x1080), session i -> GPU i mod N",
+                       "sessions_per_gpu": len(mine), "scenes_per_gpu": len(scenes),
+                       "gaussians_resident": int(sum(p.count for p in scenes.values())),
+                       "parallelism": f"session-sharded x{world} (no collective)",
+                       "frames_in_flight": args.streams},
+            "e2e": {"value": world * K / wall, "unit": "frames/s", "h2d_bytes_per_step": 160,
+                    "d2h_bytes_per_step": 3 * intr.width * intr.height,
+                    "api": "RenderPipeline.submit"},
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["gsr", "reference"], default="gsr")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config3")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["config5"], default="config3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-ladder", action="store_true")
@@ -555,6 +626,8 @@ def main(argv=None):
                     help="frames in flight (contexts/streams) for value and e2e")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+    if args.workload == "config5":
+        return run_config5(args)
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args, wl)

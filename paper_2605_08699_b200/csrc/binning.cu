@@ -248,9 +248,10 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         if (!slow) {
             float fmn = __int_as_float(0x7f800000), fmx = -__int_as_float(0x7f800000);
             const float wf = (float)a.width;
-            for (int y = y0; y < y1; y++) {
+            float py = (float)y0 + 0.5f;  // f32(y) + 0.5, stepped exactly (y < 2^23)
+            for (int y = y0; y < y1; y++, py += 1.0f) {
                 float xl, xr;
-                const int k = row_xlr(u, v, ia, ib, ic, rsq, rinv, (float)y + 0.5f, xl, xr);
+                const int k = row_xlr(u, v, ia, ib, ic, rsq, rinv, py, xl, xr);
                 if (k < 0) slow = true;
                 if (k > 0 && xl < wf && xr > -1.0f) {
                     fmn = fminf(fmn, xl);
@@ -472,14 +473,24 @@ __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
         for (uint32_t e = 0; e < n; e++) atomicOr(&mask[a0 + e], 1u << lane);
         __syncwarp();
         // 2: position = cursor + earlier (lower-rank) lanes covering the column
+        //    (and remember the columns this lane is the highest covering lane of)
+        uint32_t top = 0;
         for (uint32_t e = 0; e < n; e++) {
             const uint32_t t = a0 + e;
-            const uint32_t pos = cur[t] + __popc(mask[t] & lt_mask);
+            const uint32_t m = mask[t];
+            const uint32_t pos = cur[t] + __popc(m & lt_mask);
             if ((int64_t)pos < a.cap_d) a.tile_vals[pos] = rank;
+            if ((m >> lane) == 1u) top |= e < 32 ? 1u << e : 0u;
         }
         __syncwarp();
-        // 3: the highest covering lane advances the cursor and clears the mask
-        for (uint32_t e = 0; e < n; e++) {
+        // 3: the highest covering lane of each column advances its cursor and
+        //    clears its mask (only that lane touches the column in this phase)
+        for (uint32_t bits = top; bits; bits &= bits - 1u) {
+            const uint32_t t = a0 + (uint32_t)(__ffs(bits) - 1);
+            cur[t] += __popc(mask[t]);
+            mask[t] = 0;
+        }
+        for (uint32_t e = 32; e < n; e++) {  // spans beyond 32 tiles (512 px)
             const uint32_t t = a0 + e;
             const uint32_t m = mask[t];
             if ((m >> lane) == 1u) {

@@ -22,6 +22,8 @@
 // (4) each block writes its bits at its offset (shared boundary words by
 // atomicOr); (5) byte stuffing via a second scan.  Headers are built on the
 // host (gsr_api.cu).
+#include <mutex>
+
 #include "kernels.cuh"
 #include "scan.cuh"
 
@@ -35,8 +37,6 @@ constexpr int kNaturalOrder[64] = {
     30, 37, 44, 51, 58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
 
 __constant__ int c_natural[64];
-__constant__ uint16_t c_recip[2][64], c_corr[2][64];
-__constant__ int8_t c_shift[2][64];
 // Huffman codes (code, length) for DC lum/chrom [12] and AC lum/chrom [256]
 __constant__ uint16_t c_dc_code[2][12];
 __constant__ uint8_t c_dc_len[2][12];
@@ -50,7 +50,15 @@ struct Comp {
     int64_t coef_off;    // first block's coefficients in the coefficient buffer
 };
 
+// jcdctmgr.c divisors for one quality (kernel parameter: encodes of different
+// qualities from concurrent contexts must not share mutable state)
+struct QuantRecip {
+    uint16_t recip[2][64], corr[2][64];
+    int8_t shift[2][64];
+};
+
 struct JpegArgs {
+    QuantRecip q;
     const uint8_t *rgb;  // (H, W, 3) device frame
     int W, H;
     int sub;             // 1: 4:2:0, 0: 4:4:4
@@ -170,8 +178,8 @@ __global__ void __launch_bounds__(128) jpeg_blocks_kernel(JpegArgs a, int64_t n_
         int v = d[k];
         const bool neg = v < 0;
         const unsigned x = (unsigned)(neg ? -v : v);
-        const unsigned p = (x + c_corr[t][k]) * (unsigned)c_recip[t][k];
-        const int q = (int)(uint16_t)(p >> (16 + c_shift[t][k]));
+        const unsigned p = (x + a.q.corr[t][k]) * (unsigned)a.q.recip[t][k];
+        const int q = (int)(uint16_t)(p >> (16 + a.q.shift[t][k]));
         out[k] = (int16_t)(neg ? -q : q);
     }
 }
@@ -337,7 +345,10 @@ __global__ void jpeg_stuff_kernel(JpegArgs a, uint32_t nbytes) {
     }
 }
 
-bool g_tables_ready = false;
+// the quality-independent tables live in constant memory, uploaded once per
+// device (one process may drive several devices)
+std::mutex g_tables_mu;
+uint64_t g_tables_ready = 0;  // bit d: device d
 
 }  // namespace
 
@@ -416,30 +427,34 @@ void jpeg_huffman_spec(int t, int ac, const uint8_t **bits, const uint8_t **vals
     *nvals = ac ? 162 : 12;
 }
 
-static cudaError_t upload_tables(int quality) {
-    cudaError_t e = cudaSuccess;
-    if (!g_tables_ready) {
-        uint16_t dcc[2][12] = {}, acc[2][256] = {};
-        uint8_t dcl[2][12] = {}, acl[2][256] = {};
-        for (int t = 0; t < 2; t++) {
-            const uint8_t *b, *v;
-            int nv;
-            jpeg_huffman_spec(t, 0, &b, &v, &nv);
-            derive_codes(b, v, nv, dcc[t], dcl[t]);
-            jpeg_huffman_spec(t, 1, &b, &v, &nv);
-            derive_codes(b, v, nv, acc[t], acl[t]);
-        }
-        e = cudaMemcpyToSymbol(c_natural, kNaturalOrder, sizeof(kNaturalOrder));
-        if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_dc_code, dcc, sizeof(dcc));
-        if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_dc_len, dcl, sizeof(dcl));
-        if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_ac_code, acc, sizeof(acc));
-        if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_ac_len, acl, sizeof(acl));
-        if (e != cudaSuccess) return e;
-        g_tables_ready = true;
+static cudaError_t upload_tables() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(g_tables_mu);
+    if (dev < 64 && (g_tables_ready >> dev) & 1ull) return cudaSuccess;
+    uint16_t dcc[2][12] = {}, acc[2][256] = {};
+    uint8_t dcl[2][12] = {}, acl[2][256] = {};
+    for (int t = 0; t < 2; t++) {
+        const uint8_t *b, *v;
+        int nv;
+        jpeg_huffman_spec(t, 0, &b, &v, &nv);
+        derive_codes(b, v, nv, dcc[t], dcl[t]);
+        jpeg_huffman_spec(t, 1, &b, &v, &nv);
+        derive_codes(b, v, nv, acc[t], acl[t]);
     }
-    // jcdctmgr.c compute_reciprocal for divisor = qval << 3, 16-bit DCTELEM
-    uint16_t qt[2][64], recip[2][64], corr[2][64];
-    int8_t shift[2][64];
+    e = cudaMemcpyToSymbol(c_natural, kNaturalOrder, sizeof(kNaturalOrder));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_dc_code, dcc, sizeof(dcc));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_dc_len, dcl, sizeof(dcl));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_ac_code, acc, sizeof(acc));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_ac_len, acl, sizeof(acl));
+    if (e == cudaSuccess && dev < 64) g_tables_ready |= 1ull << dev;
+    return e;
+}
+
+// jcdctmgr.c compute_reciprocal for divisor = qval << 3, 16-bit DCTELEM
+static void quant_recip(int quality, QuantRecip &q) {
+    uint16_t qt[2][64];
     jpeg_quant_tables(quality, qt);
     for (int t = 0; t < 2; t++)
         for (int i = 0; i < 64; i++) {
@@ -457,14 +472,10 @@ static cudaError_t upload_tables(int quality) {
             } else {
                 fq++;
             }
-            recip[t][i] = (uint16_t)fq;
-            corr[t][i] = (uint16_t)c;
-            shift[t][i] = (int8_t)(r - 16);
+            q.recip[t][i] = (uint16_t)fq;
+            q.corr[t][i] = (uint16_t)c;
+            q.shift[t][i] = (int8_t)(r - 16);
         }
-    e = cudaMemcpyToSymbol(c_recip, recip, sizeof(recip));
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_corr, corr, sizeof(corr));
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_shift, shift, sizeof(shift));
-    return e;
 }
 
 size_t jpeg_workspace_bytes(int W, int H, int sub, JpegLayout *L) {
@@ -505,9 +516,10 @@ size_t jpeg_workspace_bytes(int W, int H, int sub, JpegLayout *L) {
 
 cudaError_t launch_jpeg(const uint8_t *rgb, int W, int H, int quality, const JpegLayout &L,
                         unsigned char *ws, uint32_t *host_len2, cudaStream_t s) {
-    cudaError_t e = upload_tables(quality);
+    cudaError_t e = upload_tables();
     if (e != cudaSuccess) return e;
     JpegArgs a;
+    quant_recip(quality, a.q);
     a.rgb = rgb;
     a.W = W;
     a.H = H;

@@ -487,3 +487,26 @@ def test_buffer_overflow_rerender(gsr, oracle):
                        intr.cy, intr.width, intr.height, (0.0, 0.0, 0.0), 0)
     assert result["keys"] > 16 * n  # beyond the initial capacity
     assert np.array_equal(result["u8"], fr.u8)
+
+
+def test_jpeg_concurrent_threads(gsr):
+    """Encodes of different qualities from concurrent serving threads (one
+    context each, server.py:99-100) do not interfere."""
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, (96, 160, 3), dtype=np.uint8)
+    qualities = [10, 35, 65, 90, 95, 50, 75, 20]
+    ref = {q: _pil_jpeg(img, q) for q in qualities}
+    bad = []
+
+    def work(q):
+        fb = gsr.Framebuffer(160, 96, u8=img)
+        for _ in range(20):
+            if gsr.encode_jpeg(fb, q) != ref[q]:
+                bad.append(q)
+
+    ts = [threading.Thread(target=work, args=(q,)) for q in qualities]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not bad
