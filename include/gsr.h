@@ -181,6 +181,21 @@ GSR_API int gsr_encode_jpeg(gsr_ctx *ctx, const uint8_t *rgb, int width, int hei
                             int quality, int subsampling, uint8_t *out, size_t out_cap,
                             size_t *out_len);
 
+/* ---- session evaluation: metrics.py:133-214 --------
+ * gsr_sse_u8: sum of squared differences of two host u8 buffers of n bytes
+ * (metrics.psnr's numerator, metrics.py:57-66; integer, exact).
+ * gsr_eval_frame: one evaluation triplet on the device -- renders the ground
+ * truth at the base camera (metrics.py:205, the PNG round trip is lossless),
+ * uploads the transmitted (th,tw,3) u8 frame, upscale_to's it to the base
+ * size (metrics.py:208), and returns ssim(transmitted, gt) and the SSE of the
+ * pair (psnr, metrics.py:161-162); out_gt_u8 (nullable) receives the GT. */
+GSR_API int gsr_sse_u8(gsr_ctx *ctx, const uint8_t *a, const uint8_t *b, int64_t n,
+                       uint64_t *out_sse);
+GSR_API int gsr_eval_frame(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *base_cam,
+                           const float background[3], int sh_degree, const uint8_t *transmitted,
+                           int tw, int th, uint8_t *out_gt_u8, double *out_ssim,
+                           uint64_t *out_sse);
+
 /* ---- pinned host memory for end-to-end frame readback ------------------- */
 GSR_API int gsr_host_alloc(void **out, size_t bytes);
 GSR_API int gsr_host_free(void *ptr);

@@ -8,7 +8,9 @@ CUDA for sm_100a behind the C ABI in include/gsr.h.  See DESIGN.md.
 __version__ = "0.1.0"
 
 from .camera import CameraPose, Intrinsics, pose_from_degrees, scale_intrinsics, world_to_camera
-from .metrics import DimensionMismatch, TooSmall, ladder_ssim, psnr, ssim, upscale_to
+from .metrics import (DimensionMismatch, EmptyInput, EvalTriplet, IndexOutOfRange, TooSmall,
+                      aggregate_session, evaluate_session_dir, ladder_ssim,
+                      materialize_ground_truth, psnr, ssim, upscale_to)
 from .render import (DeviceScene, EncodeFailure, Framebuffer, RenderError, RenderPipeline,
                      RenderStats,
                      decode_image, device_scene, encode_jpeg, encode_png, evict,
@@ -16,7 +18,9 @@ from .render import (DeviceScene, EncodeFailure, Framebuffer, RenderError, Rende
 from .synth import ActivatedPrimitives
 
 __all__ = [
-    "ActivatedPrimitives", "CameraPose", "DeviceScene", "DimensionMismatch", "EncodeFailure",
+    "ActivatedPrimitives", "CameraPose", "DeviceScene", "DimensionMismatch", "EmptyInput",
+    "EncodeFailure", "EvalTriplet", "IndexOutOfRange", "aggregate_session", "evaluate_session_dir",
+    "materialize_ground_truth",
     "Framebuffer", "Intrinsics", "RenderError", "RenderPipeline", "RenderStats", "TooSmall", "decode_image",
     "device_scene", "encode_jpeg", "encode_png", "evict", "framebuffer_to_u8", "ladder_ssim",
     "pose_from_degrees", "psnr", "render_framebuffer", "render_u8", "render_view",

@@ -81,6 +81,9 @@ SIGNATURES = [
     ("gsr_ssim_u8", _i32, [_vp, _vp, _vp, _i32, _i32, _P(_dbl)]),
     ("gsr_ssim_luma_f64", _i32, [_vp, _vp, _vp, _i32, _i32, _P(_dbl)]),
     ("gsr_encode_jpeg", _i32, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _sz, _P(_sz)]),
+    ("gsr_sse_u8", _i32, [_vp, _vp, _vp, _i64, _P(ctypes.c_uint64)]),
+    ("gsr_eval_frame", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _vp, _i32, _i32, _vp,
+                              _P(_dbl), _P(ctypes.c_uint64)]),
     ("gsr_host_alloc", _i32, [_P(_vp), _sz]),
     ("gsr_host_free", _i32, [_vp]),
     ("gsr_ladder_ssim", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32, _P(GsrCamera),

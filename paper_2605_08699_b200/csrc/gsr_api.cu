@@ -1053,6 +1053,62 @@ int gsr_encode_jpeg(gsr_ctx *ctx, const uint8_t *rgb, int width, int height, int
     return GSR_OK;
 }
 
+int gsr_sse_u8(gsr_ctx *ctx, const uint8_t *a, const uint8_t *b, int64_t n,
+               uint64_t *out_sse) {
+    if (!ctx || !a || !b || !out_sse || n < 0) return fail(GSR_E_INVALID, "null argument");
+    DeviceGuard g(ctx->device);
+    int rc;
+    if ((rc = ensure(ctx->src_u8, (size_t)n))) return rc;
+    if ((rc = ensure(ctx->dst_u8, (size_t)n))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->src_u8.p, a, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->dst_u8.p, b, (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    unsigned long long *dsse = reinterpret_cast<unsigned long long *>(ctx->ssim_misc.as<unsigned char>() + 16);
+    launch_sse(ctx->src_u8.as<uint8_t>(), ctx->dst_u8.as<uint8_t>(), n, dsse, ctx->stream);
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->hssim, dsse, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(out_sse, ctx->hssim, 8);
+    return GSR_OK;
+}
+
+int gsr_eval_frame(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *base_cam,
+                   const float background[3], int sh_degree, const uint8_t *transmitted,
+                   int tw, int th, uint8_t *out_gt_u8, double *out_ssim, uint64_t *out_sse) {
+    if (!ctx || !base_cam || !transmitted || !out_ssim || !out_sse)
+        return fail(GSR_E_INVALID, "null argument");
+    if (tw <= 0 || th <= 0) return fail(GSR_E_INVALID, "dimensions must be positive");
+    const int W = base_cam->width, H = base_cam->height;
+    if (W < 11 || H < 11) return fail(GSR_E_TOO_SMALL, "images must be at least 11x11");
+    DeviceGuard g(ctx->device);
+    const float zero[3] = {0, 0, 0};
+    int rc = enqueue_frame(ctx, scene, base_cam, background ? background : zero, sh_degree, 1,
+                           false, false);
+    if (rc) return rc;
+    if ((rc = complete_frame(ctx))) return rc;
+    const size_t nb = (size_t)W * H * 3, tb = (size_t)tw * th * 3;
+    if ((rc = ensure(ctx->src_u8, tb))) return rc;
+    if ((rc = ensure(ctx->up_u8, nb))) return rc;
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->src_u8.p, transmitted, tb, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    // metrics.py:208 upscale_to(transmitted, W, H) (identity when equal)
+    if ((rc = resample_device(ctx, ctx->src_u8.as<uint8_t>(), tw, th, ctx->up_u8.as<uint8_t>(),
+                              W, H)))
+        return rc;
+    double *dres = reinterpret_cast<double *>(ctx->ssim_misc.as<unsigned char>() + 8);
+    unsigned long long *dsse = reinterpret_cast<unsigned long long *>(ctx->ssim_misc.as<unsigned char>() + 16);
+    SsimInput in{ctx->up_u8.as<uint8_t>(), ctx->frame_u8.as<uint8_t>(), nullptr, nullptr};
+    if ((rc = ssim_device(ctx, in, W, H, dres))) return rc;
+    launch_sse(ctx->up_u8.as<uint8_t>(), ctx->frame_u8.as<uint8_t>(), (int64_t)nb, dsse,
+               ctx->stream);
+    GSR_CUDA_OK(cudaMemcpyAsync(ctx->hssim, dres, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out_gt_u8)
+        GSR_CUDA_OK(cudaMemcpyAsync(out_gt_u8, ctx->frame_u8.p, nb, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    GSR_CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    *out_ssim = ctx->hssim[0];
+    std::memcpy(out_sse, &ctx->hssim[1], 8);
+    return GSR_OK;
+}
+
 int gsr_ladder_ssim(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *base_cam,
                     const float background[3], int sh_degree, int n_rungs,
                     const gsr_camera *rung_cams, double *out_ssim, gsr_stats *base_stats) {

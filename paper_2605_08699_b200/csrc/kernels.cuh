@@ -187,6 +187,8 @@ struct SsimInput {
     const double *la, *lb;
 };
 int ssim_partials_needed(int width, int height);
+void launch_sse(const uint8_t *a, const uint8_t *b, int64_t n, unsigned long long *out,
+                cudaStream_t s);
 void launch_ssim(const SsimInput &in, int width, int height, const double *weights11,
                  double *partials, uint32_t *neq, double *out, cudaStream_t s);
 

@@ -132,7 +132,30 @@ __global__ void ssim_final_kernel(const double *__restrict__ partials, int n, co
     }
 }
 
+// Sum of squared differences of two u8 buffers (metrics.psnr's numerator,
+// metrics.py:57-66): integer, so the result is exact whatever the order.
+__global__ void __launch_bounds__(256) sse_kernel(const uint8_t *__restrict__ a,
+                                                  const uint8_t *__restrict__ b, int64_t n,
+                                                  unsigned long long *out) {
+    unsigned long long s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int d = (int)a[i] - (int)b[i];
+        s += (unsigned long long)(d * d);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
 }  // namespace
+
+void launch_sse(const uint8_t *a, const uint8_t *b, int64_t n, unsigned long long *out,
+                cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+    const int64_t blocks = (n + 255) / 256;
+    sse_kernel<<<(unsigned)(blocks < 1184 ? (blocks > 0 ? blocks : 1) : 1184), 256, 0, s>>>(a, b, n, out);
+}
 
 int ssim_partials_needed(int width, int height) {
     const int gx = (width - 2 * R + TW - 1) / TW, gy = (height - 2 * R + TH - 1) / TH;

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -42,12 +43,29 @@ class IndexOutOfRange(MetricError):
     pass
 
 
-def psnr(a, b) -> float:
-    """metrics.py:57-66."""
+def _psnr_from_mse(mse: float) -> float:
+    if mse == 0:
+        return PSNR_CAP_DB
+    return min(PSNR_CAP_DB, 10.0 * math.log10(255.0 ** 2 / mse))
+
+
+def psnr(a, b, *, device: int | None = None) -> float:
+    """metrics.py:57-66.  u8 images: the sum of squared differences on the GPU
+    (an integer, so the mean -- one f64 division, as numpy's -- and the dB
+    value are the reference's exactly); other dtypes: the reference's numpy."""
     a = np.asarray(a)
     b = np.asarray(b)
     if a.shape != b.shape:
         raise DimensionMismatch(f"shapes differ: {a.shape} vs {b.shape}")
+    if a.dtype == np.uint8 and b.dtype == np.uint8 and a.size > 0:
+        from .render import _default_device
+        ctx = _lib.context(_default_device if device is None else device)
+        sse = ctypes.c_uint64(0)
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        _lib.check(ctx.lib.gsr_sse_u8(ctx.handle, _lib.ptr(a), _lib.ptr(b), a.size,
+                                      ctypes.byref(sse)), "gsr_sse_u8")
+        return _psnr_from_mse(float(sse.value) / a.size)
     mse = np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2)
     if mse == 0:
         return PSNR_CAP_DB
@@ -126,5 +144,110 @@ def ladder_ssim(prims, pose, base_intr, rungs, background=(0.0, 0.0, 0.0), sh_de
     return [float(out[i]) for i in range(len(rungs))], st
 
 
+# ---------------------------------------------- session evaluation (8f row 3) --
+
+@dataclass
+class EvalTriplet:
+    """metrics.py EvalTriplet: transmitted and ground-truth u8 frames."""
+
+    transmitted: np.ndarray
+    ground_truth: np.ndarray
+    pose: object
+    level: int
+
+
+def materialize_ground_truth(prims, log, sample_indices, background=(0.0, 0.0, 0.0)):
+    """metrics.py:133-150: re-render logged poses at base resolution (GPU) as
+    lossless PNGs (Pillow, host)."""
+    from .camera import pose_from_degrees
+    from .render import encode_png, render_framebuffer
+    pngs = []
+    for idx in sample_indices:
+        if not 0 <= idx < len(log.frames):
+            raise IndexOutOfRange(f"sample index {idx} outside log of {len(log.frames)}")
+        f = log.frames[idx]
+        pose = pose_from_degrees(f.azimuth_deg, f.elevation_deg, (f.tx, f.ty, f.tz))
+        pngs.append(encode_png(render_framebuffer(prims, pose, log.base_intrinsics, background)))
+    return pngs
+
+
+def _report(rows):
+    """metrics.py:153-182's report from (psnr, ssim, level) rows."""
+    psnrs = [r[0] for r in rows]
+    ssims = [r[1] for r in rows]
+    by_level: dict = {}
+    for p, s_, lvl in rows:
+        by_level.setdefault(lvl, []).append((p, s_))
+    return {
+        "frames": len(rows),
+        "mean_psnr_db": float(np.mean(psnrs)),
+        "min_psnr_db": float(np.min(psnrs)),
+        "mean_ssim": float(np.mean(ssims)),
+        "min_ssim": float(np.min(ssims)),
+        "per_level": {
+            str(level): {
+                "frames": len(vals),
+                "mean_psnr_db": float(np.mean([v[0] for v in vals])),
+                "mean_ssim": float(np.mean([v[1] for v in vals])),
+            }
+            for level, vals in sorted(by_level.items())
+        },
+    }
+
+
+def aggregate_session(triplets) -> dict:
+    """metrics.py:153-182: mean/min PSNR and SSIM plus a per-level breakdown."""
+    if not triplets:
+        raise EmptyInput("no triplets to aggregate")
+    return _report([(psnr(t.transmitted, t.ground_truth), ssim(t.transmitted, t.ground_truth),
+                     t.level) for t in triplets])
+
+
+def evaluate_session_dir(prims, session_dir, background=(0.0, 0.0, 0.0), sh_degree: int = 0,
+                         *, device: int | None = None) -> dict:
+    """metrics.py:185-214 with each triplet evaluated on the device in one call
+    (gsr_eval_frame: GT render at base intrinsics, upscale_to of the decoded
+    transmitted frame, SSIM and SSE); only the JPEG decode stays on the host."""
+    import json
+    from pathlib import Path
+
+    from .camera import Intrinsics, pose_from_degrees
+    from .render import _bg, _default_device, decode_image, device_scene, make_camera
+    session_dir = Path(session_dir)
+    sidecar_path = session_dir / "samples.json"
+    if not sidecar_path.is_file():
+        raise EmptyInput(f"no samples.json under {session_dir}")
+    sidecar = json.loads(sidecar_path.read_text())
+    samples = sidecar.get("samples", [])
+    if not samples:
+        raise EmptyInput("session has no sampled frames")
+    base = sidecar["base_intrinsics"]
+    base_intr = Intrinsics(fx=base["fx"], fy=base["fy"], cx=base["cx"], cy=base["cy"],
+                           width=int(base["width"]), height=int(base["height"]))
+    dev = _default_device if device is None else device
+    sc = device_scene(prims, dev)
+    ctx = _lib.context(dev)
+    rows = []
+    for sample in samples:
+        pose = pose_from_degrees(sample["azimuth_deg"], sample["elevation_deg"],
+                                 tuple(sample["translation"]))
+        transmitted = np.ascontiguousarray(
+            decode_image((session_dir / sample["file"]).read_bytes()), dtype=np.uint8)
+        cam = make_camera(pose, base_intr)
+        out_ssim = ctypes.c_double(0.0)
+        sse = ctypes.c_uint64(0)
+        _lib.check(ctx.lib.gsr_eval_frame(ctx.handle, sc.handle, ctypes.byref(cam),
+                                          _bg(background), int(sh_degree),
+                                          _lib.ptr(transmitted), transmitted.shape[1],
+                                          transmitted.shape[0], None, ctypes.byref(out_ssim),
+                                          ctypes.byref(sse)), "gsr_eval_frame")
+        mse = float(sse.value) / (base_intr.width * base_intr.height * 3)
+        rows.append((_psnr_from_mse(mse), float(out_ssim.value), int(sample["level"])))
+    report = _report(rows)
+    report["model_id"] = sidecar.get("model_id", "")
+    return report
+
+
 __all__ = ["psnr", "ssim", "upscale_to", "ladder_ssim", "MetricError", "DimensionMismatch",
-           "TooSmall", "EmptyInput", "IndexOutOfRange"]
+           "TooSmall", "EmptyInput", "IndexOutOfRange", "EvalTriplet", "aggregate_session",
+           "evaluate_session_dir", "materialize_ground_truth"]

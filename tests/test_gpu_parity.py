@@ -510,3 +510,71 @@ def test_jpeg_concurrent_threads(gsr):
     for t in ts:
         t.join()
     assert not bad
+
+
+def test_evaluate_session_dir_vs_oracle(gsr, oracle, tmp_path):
+    """evaluate_session_dir (metrics.py:185-214) with GT
+    render + upscale + SSIM + PSNR on the device, vs the same computation from
+    the oracle; materialize_ground_truth PNGs identical; aggregate_session."""
+    import io
+    import json
+    from PIL import Image
+    from paper_2605_08699_b200.synth import synthetic_scene
+    prims = synthetic_scene(30_000, seed=4, sh_degree=0)
+    base = gsr.Intrinsics(fx=554.2562584220407, fy=554.2562584220407, cx=320.0, cy=180.0,
+                          width=640, height=360)
+    levels = [(640, 360, 90), (480, 270, 65), (320, 180, 35)]
+    samples, expect = [], []
+    for i in range(5):
+        az, el, t = 2.0 * i, -1.0 * i, (0.02 * i, 0.0, 0.05)
+        lvl = i % 3
+        w, h, q = levels[lvl]
+
+        class Profile:
+            width, height, jpeg_quality = w, h, q
+        pose = gsr.pose_from_degrees(az, el, t)
+        payload, _ = gsr.render_view(prims, pose, base, Profile())
+        (tmp_path / f"f{i}.jpg").write_bytes(payload)
+        samples.append({"azimuth_deg": az, "elevation_deg": el, "translation": list(t),
+                        "file": f"f{i}.jpg", "level": lvl})
+        rot, w2c = oracle.world_to_camera(pose.azimuth, pose.elevation, pose.translation)
+        gt = oracle.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                           prims.colors_dc, prims.sh_coeffs, w2c, rot, base.fx, base.fy,
+                           base.cx, base.cy, base.width, base.height, (0.0, 0.0, 0.0), 0).u8
+        tr = np.asarray(Image.open(io.BytesIO(payload)).convert("RGB"))
+        tr = oracle.resample_bilinear(tr, base.width, base.height)
+        expect.append((oracle.psnr(tr, gt), oracle.ssim(tr, gt), lvl))
+    (tmp_path / "samples.json").write_text(json.dumps({
+        "model_id": "synth", "samples": samples,
+        "base_intrinsics": {"fx": base.fx, "fy": base.fy, "cx": base.cx, "cy": base.cy,
+                            "width": base.width, "height": base.height}}))
+    rep = gsr.evaluate_session_dir(prims, tmp_path)
+    assert rep["frames"] == 5 and rep["model_id"] == "synth"
+    assert rep["mean_psnr_db"] == pytest.approx(float(np.mean([e[0] for e in expect])), abs=1e-9)
+    assert rep["mean_ssim"] == pytest.approx(float(np.mean([e[1] for e in expect])), abs=1e-9)
+    assert rep["min_ssim"] == pytest.approx(min(e[1] for e in expect), abs=1e-9)
+    assert set(rep["per_level"]) == {"0", "1", "2"}
+    # aggregate_session on host triplets gives the same report numbers
+    trips = []
+    for s, e in zip(samples, expect):
+        pose = gsr.pose_from_degrees(s["azimuth_deg"], s["elevation_deg"], tuple(s["translation"]))
+        gt = gsr.render_u8(prims, pose, base).copy()
+        tr = gsr.upscale_to(gsr.decode_image((tmp_path / s["file"]).read_bytes()), 640, 360)
+        trips.append(gsr.EvalTriplet(tr, gt, pose, s["level"]))
+        assert gsr.psnr(tr, gt) == e[0]
+    rep2 = gsr.aggregate_session(trips)
+    assert rep2["mean_psnr_db"] == rep["mean_psnr_db"]
+    assert rep2["mean_ssim"] == pytest.approx(rep["mean_ssim"], abs=1e-15)
+    with pytest.raises(gsr.EmptyInput):
+        gsr.aggregate_session([])
+
+    class Log:
+        base_intrinsics = base
+        frames = [type("F", (), {"azimuth_deg": s["azimuth_deg"], "elevation_deg": s["elevation_deg"],
+                                 "tx": s["translation"][0], "ty": s["translation"][1],
+                                 "tz": s["translation"][2]})() for s in samples]
+    pngs = gsr.materialize_ground_truth(prims, Log(), [0, 3])
+    for png, idx in zip(pngs, [0, 3]):
+        assert np.array_equal(gsr.decode_image(png), trips[idx].ground_truth)
+    with pytest.raises(gsr.IndexOutOfRange):
+        gsr.materialize_ground_truth(prims, Log(), [99])
