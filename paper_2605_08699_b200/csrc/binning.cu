@@ -431,20 +431,23 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(BinArgs a) {
 
 // ---------------------------------------------------------------- 2d -------
 __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
-    // per warp and tile column: (cursor, coverage mask) side by side, so one
-    // 64-bit shared access reads or writes both
-    extern __shared__ __align__(16) uint2 place_smem[];
+    // per warp: column cursors [tiles_x] and coverage masks [tiles_x]
+    extern __shared__ __align__(16) uint32_t place_smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t g = (int64_t)blockIdx.x * 8 + w;
     if (overflowed(a)) return;
     const int64_t nseg = seg_count_of(a);
     if (g >= nseg) return;
     const int tx_n = a.tiles_x;
-    uint2 *cm = place_smem + w * tx_n;
+    uint32_t *cur = place_smem + w * 2 * tx_n;
+    uint32_t *mask = cur + tx_n;
     uint32_t ty, p0, p1;
     seg_bounds(a, g, nseg, ty, p0, p1);
     const uint32_t *tstart = a.tile_start + (int64_t)ty * tx_n;
-    for (int t = lane; t < tx_n; t += 32) cm[t] = make_uint2(tstart[t] + a.seg_cnt[g * tx_n + t], 0u);
+    for (int t = lane; t < tx_n; t += 32) {
+        cur[t] = tstart[t] + a.seg_cnt[g * tx_n + t];
+        mask[t] = 0;
+    }
     __syncwarp();
     const uint32_t lt_mask = (1u << lane) - 1u;
     // software pipeline: the next chunks' pairs are in flight while this
@@ -467,28 +470,33 @@ __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
         // covers columns [a0, a0 + n) (n = 0 past the segment end)
         const uint32_t rank = pr.x, a0 = pr.y & 0xffffu, n = pr.y >> 16;
         // 1: coverage mask of every column touched by the chunk
-        for (uint32_t e = 0; e < n; e++) atomicOr(&cm[a0 + e].y, 1u << lane);
+        for (uint32_t e = 0; e < n; e++) atomicOr(&mask[a0 + e], 1u << lane);
         __syncwarp();
         // 2: position = cursor + earlier (lower-rank) lanes covering the column
         //    (and remember the columns this lane is the highest covering lane of)
         uint32_t top = 0;
         for (uint32_t e = 0; e < n; e++) {
-            const uint2 v = cm[a0 + e];
-            const uint32_t pos = v.x + __popc(v.y & lt_mask);
+            const uint32_t t = a0 + e;
+            const uint32_t m = mask[t];
+            const uint32_t pos = cur[t] + __popc(m & lt_mask);
             if ((int64_t)pos < a.cap_d) a.tile_vals[pos] = rank;
-            if ((v.y >> lane) == 1u) top |= e < 32 ? 1u << e : 0u;
+            if ((m >> lane) == 1u) top |= e < 32 ? 1u << e : 0u;
         }
         __syncwarp();
         // 3: the highest covering lane of each column advances its cursor and
         //    clears its mask (only that lane touches the column in this phase)
         for (uint32_t bits = top; bits; bits &= bits - 1u) {
             const uint32_t t = a0 + (uint32_t)(__ffs(bits) - 1);
-            const uint2 v = cm[t];
-            cm[t] = make_uint2(v.x + __popc(v.y), 0u);
+            cur[t] += __popc(mask[t]);
+            mask[t] = 0;
         }
         for (uint32_t e = 32; e < n; e++) {  // spans beyond 32 tiles (512 px)
-            const uint2 v = cm[a0 + e];
-            if ((v.y >> lane) == 1u) cm[a0 + e] = make_uint2(v.x + __popc(v.y), 0u);
+            const uint32_t t = a0 + e;
+            const uint32_t m = mask[t];
+            if ((m >> lane) == 1u) {
+                cur[t] += __popc(m);
+                mask[t] = 0;
+            }
         }
         __syncwarp();
     }
@@ -511,7 +519,7 @@ cudaError_t binning_init_attributes() {
                                  (int)(8 * (kMaxTilesX + 1) * sizeof(uint32_t)));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(seg_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(8 * kMaxTilesX * sizeof(uint2)));
+                                 (int)(8 * 2 * kMaxTilesX * sizeof(uint32_t)));
     return e;
 }
 
@@ -535,7 +543,7 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark) {
     mark("seg_scan");
     tile_scan_kernel<<<1, 1024, 0, s>>>(a);
     mark("tile_scan");
-    seg_place_kernel<<<sb, 256, 8 * a.tiles_x * sizeof(uint2), s>>>(a);
+    seg_place_kernel<<<sb, 256, 8 * 2 * a.tiles_x * sizeof(uint32_t), s>>>(a);
     mark("seg_place");
     return 8;
 }
