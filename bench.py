@@ -234,23 +234,23 @@ def kernel_work(name, wl, c):
     sh_bytes = 12 * (wl["sh"] + 1) ** 2 if wl["sh"] else 12
     px = wl["w"] * wl["h"]
     table = {
-        # mean/scale/rotation/rsq f64 + opacity f32 in; key for all N; record + rinv of kept
-        "preprocess_geo": (n * 92 + n * 8 + k * 36, 0),
-        # key of all N; mean f64 + SH f32 (or DC) + rinv of kept in; colour out
-        "preprocess_color": (n * 8 + k * (28 + sh_bytes) + k * 16, 0),
+        # mean/scale/rotation/rsq f64 + opacity f32 in; key for all N; record of kept
+        "preprocess_geo": (n * 92 + n * 8 + k * 32, 0),
+        # key of all N; mean f64 + SH f32 (or DC) of kept in; colour out
+        "preprocess_color": (n * 8 + k * (24 + sh_bytes) + k * 16, 0),
         "depth_key32": (n * 12, 0),
         "radix32_hist": (k * 4, 0),
         "radix32_pass": (k * 16, 0),  # per pass: key + index read and written
         "depth_fixup": (k * 4, 0),
-        # order + geometry + colour gathered, 48 B record written
-        "bin_gather": (k * (4 + 32 + 16) + k * 48, 0),
+        # order + geometry gathered, 32 B record written
+        "bin_gather": (k * (4 + 32) + k * 32, 0),
         # records in, pairs out; 20 FP32 ops per exact row interval (render.py:383-397)
-        "bin_pairs": (k * 36 + p * 8, 20 * c["Rp"]),
+        "bin_pairs": (k * 32 + p * 8, 20 * c["Rp"]),
         "seg_count": (p * 8, 0),
         "seg_place": (p * 8 + d * 4, 0),
-        # lists + each record once + u8 frame; 20 FP32 ops per composited
-        # evaluation (render.py:405-421) and per row interval (383-397)
-        "blend": (d * 4 + k * 48 + 3 * px, 20 * (c["E"] + c["Rb"])),
+        # lists + each record (and colour) once + u8 frame; 20 FP32 ops per
+        # composited evaluation (render.py:405-421) and per row interval (383-397)
+        "blend": (d * 4 + k * 52 + 3 * px, 20 * (c["E"] + c["Rb"])),
     }
     return table.get(name, (0, 0))
 

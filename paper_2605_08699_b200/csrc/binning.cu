@@ -10,8 +10,8 @@
 //
 // Every splat covers a run of tile rows and, in each, one contiguous run of
 // tile columns.  So the lists are built from (splat, tile row) pairs:
-//  1a gather   block of 256 depth ranks: gathers the depth-sorted records
-//              (sort_splats' column gathers, render.py:295-302) and counts
+//  1a gather   block of 256 depth ranks: gathers the depth-sorted geometry
+//              records (sort_splats' column gathers, render.py:295-302) and counts
 //              its pairs per tile row (row range only, no interval math).
 //  1b row_scan exclusive scan of those counts, tile-row major: each (row,
 //              block) gets its output slot, each row its pair range.
@@ -61,10 +61,9 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
     if (b * BR < k && r < k) {
         const uint32_t *order = a.depth_sched[16] ? a.order1 : a.order0;
         const uint32_t i = __ldg(order + r);
-        const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b), C = __ldg(a.col + i);
+        const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b);
         a.srec[r].a = A;
         a.srec[r].b = B;
-        a.srec[r].c = C;
         int lo, hi;
         row_range(A.y, B.w, a.height, lo, hi);
         if (lo < hi)
@@ -165,7 +164,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     int lo = 0, hi = 0;
     if (r < k) {
         const float4 A = __ldg(&a.srec[r].a), B = __ldg(&a.srec[r].b);
-        S.rinv[tid] = splat_fast_ok(A.y, A.z, A.w) ? __ldg(&a.srec[r].c.w) : 0.0f;
+        S.rinv[tid] = splat_fast_ok(A.y, A.z, A.w) ? __frcp_rn(A.z) : 0.0f;
         row_range(A.y, B.w, a.height, lo, hi);
         S.u[tid] = A.x;
         S.v[tid] = A.y;

@@ -176,9 +176,9 @@ __device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, cons
 // never do), so binding 8 warps to a CTA per tile would leave most of a CTA's
 // warps idle behind its slowest one; the queue keeps every warp busy.
 __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
-    const SplatRec *__restrict__ srec, const uint32_t *__restrict__ tile_vals,
-    const uint2 *__restrict__ ranges, int width, int height, float bg0, float bg1, float bg2,
-    BlendOut out, FrameCounters *__restrict__ ctr) {
+    const SplatRec *__restrict__ srec, const float4 *__restrict__ col, DepthOrder ord,
+    const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
+    int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *__restrict__ ctr) {
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c1) : "d"(kExpK[2]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c2) : "d"(kExpK[3]));
     uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
+    const uint32_t *__restrict__ order = ord.sched[16] ? ord.order1 : ord.order0;
 
     while (true) {
         int item = 0;
@@ -227,15 +228,17 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
                 const uint32_t r = __ldg(tile_vals + j);  // depth rank
                 const float4 A = __ldg(&srec[r].a);
                 const float4 B = __ldg(&srec[r].b);
-                const float4 C = __ldg(&srec[r].c);
+                const uint32_t gi = __ldg(order + r);  // issued with the record loads
                 int lo, hi;
                 row_range(A.y, B.w, height, lo, hi);
                 const bool fast = splat_fast_ok(A.y, A.z, A.w);
+                const float rinv = fast ? __frcp_rn(A.z) : 0.0f;
                 n_rows += (uint32_t)(iy0 >= lo && iy0 < hi) +
                           (uint32_t)(iy0 + 1 >= lo && iy0 + 1 < hi);
-                mask = row_mask(A, B, C.w, fast, iy0, lo, hi, X, width) |
-                       (row_mask(A, B, C.w, fast, iy0 + 1, lo, hi, X, width) << 16);
+                mask = row_mask(A, B, rinv, fast, iy0, lo, hi, X, width) |
+                       (row_mask(A, B, rinv, fast, iy0 + 1, lo, hi, X, width) << 16);
                 if (mask) {  // render.py:400-402 terms per pixel row
+                    const float4 C = __ldg(col + gi);  // (r, g, b)
                     safe = exp_safe(A, B);
                     const float ib2 = 2.0f * A.w;
                     const float dy0 = py0 - A.y, dy1 = py1 - A.y;
@@ -294,7 +297,8 @@ int g_blend_grid = 0;
 
 }  // namespace
 
-void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *ranges, int width,
+void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
+                  const uint32_t *tile_vals, const uint2 *ranges, int width,
                   int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
                   cudaStream_t s, const KMark &mark) {
     if (!g_blend_grid) {  // persistent grid: every SM full
@@ -306,8 +310,8 @@ void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *
     }
     const int tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
     const int grid = std::min(g_blend_grid, tiles);
-    blend_kernel<<<grid, kBlendThreads, 0, s>>>(srec, tile_vals, ranges, width, height, bg0, bg1,
-                                                bg2, out, ctr);
+    blend_kernel<<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges, width, height,
+                                                bg0, bg1, bg2, out, ctr);
     mark("blend");
 }
 

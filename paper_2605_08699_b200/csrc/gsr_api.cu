@@ -86,7 +86,7 @@ struct gsr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int64_t cap_n = 0, cap_d = 0, cap_p = 0;
-    DevBuf keys[2], vals[2], keys32[2], geo, rinv, col, srec, keep;
+    DevBuf keys[2], vals[2], keys32[2], geo, col, srec, keep;
     int sms = 148;
     DevBuf depth_work, depth_work32, sched;  // depth-sort scratch; sched[16] = result buffer
     uint32_t *hsched = nullptr;   // pinned host copy of sched
@@ -120,7 +120,7 @@ struct gsr_ctx {
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &rinv, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+                               &geo, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws};
@@ -192,7 +192,6 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
             if ((rc = ensure(c->keys32[i], sizeof(uint32_t) * cap))) return rc;
         }
         if ((rc = ensure(c->geo, sizeof(GeoRec) * cap))) return rc;
-        if ((rc = ensure(c->rinv, sizeof(float) * cap))) return rc;
         if ((rc = ensure(c->col, sizeof(float4) * cap))) return rc;
         if ((rc = ensure(c->srec, sizeof(SplatRec) * cap))) return rc;
         c->cap_n = cap;
@@ -268,7 +267,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     mark("frame_init");
     if (n > 0) {
         launch_preprocess(sc->view, ca, sh_degree, cull, c->keys[0].as<unsigned long long>(),
-                          c->geo.as<GeoRec>(), c->rinv.as<float>(), c->col.as<float4>(),
+                          c->geo.as<GeoRec>(), c->col.as<float4>(),
                           want_keep ? c->keep.as<uint8_t>() : nullptr, ctr, s, mark);
         launches += 2;
     }
@@ -296,7 +295,6 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.order1 = c->vals[1].as<uint32_t>();
         ba.depth_sched = dsched;
         ba.geo = c->geo.as<GeoRec>();
-        ba.col = c->col.as<float4>();
         ba.srec = c->srec.as<SplatRec>();
         ba.ctr = ctr;
         ba.width = W;
@@ -327,7 +325,9 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     cudaEventRecord(c->ev[4], s);
     BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
                  want_rgb ? c->frame_t.as<float>() : nullptr};
-    launch_blend(c->srec.as<SplatRec>(), c->tile_vals.as<uint32_t>(), c->ranges.as<uint2>(), W, H,
+    DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
+    launch_blend(c->srec.as<SplatRec>(), c->col.as<float4>(), ord, c->tile_vals.as<uint32_t>(),
+                 c->ranges.as<uint2>(), W, H,
                  bg[0], bg[1], bg[2], out, ctr, s, mark);
     cudaEventRecord(c->ev[5], s);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s);
@@ -897,12 +897,19 @@ int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera 
     }
     if (out_packed && k > 0) {
         std::vector<SplatRec> r((size_t)k);
+        std::vector<uint32_t> o((size_t)k);
+        std::vector<float4> col((size_t)scene->n);
+        const DevBuf &vb = ctx->vals[ctx->hsched[16] & 1u];
         GSR_CUDA_OK(cudaMemcpy(r.data(), ctx->srec.p, sizeof(SplatRec) * k, cudaMemcpyDeviceToHost));
+        GSR_CUDA_OK(cudaMemcpy(o.data(), vb.p, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost));
+        GSR_CUDA_OK(cudaMemcpy(col.data(), ctx->col.p, sizeof(float4) * scene->n,
+                               cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < k; i++) {
             float *p = out_packed + 11 * i;
             const SplatRec &s = r[i];
+            const float4 &cc = col[o[i]];
             p[0] = s.a.x; p[1] = s.a.y; p[2] = s.a.z; p[3] = s.a.w; p[4] = s.b.x; p[5] = s.b.y;
-            p[6] = s.c.x; p[7] = s.c.y; p[8] = s.c.z; p[9] = s.b.z; p[10] = s.b.w;
+            p[6] = cc.x; p[7] = cc.y; p[8] = cc.z; p[9] = s.b.z; p[10] = s.b.w;
         }
     }
     fill_stats(ctx, scene, stats);

@@ -61,12 +61,10 @@ struct CameraArgs {
 };
 
 // preprocess.cu (2 kernels)
-struct GeoRec {  // SplatRec.a, SplatRec.b
-    float4 a, b;
-};
+using GeoRec = SplatRec;  // by Gaussian index (preprocess), by depth rank (gather)
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                       int frustum_cull, unsigned long long *keys, GeoRec *geo, float *rinv,
+                       int frustum_cull, unsigned long long *keys, GeoRec *geo,
                        float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s,
                        const KMark &mark = KMark());
 
@@ -115,7 +113,6 @@ struct BinArgs {
     const uint32_t *order0, *order1;  // depth sort result buffers
     const uint32_t *depth_sched;      // [16]: which of order0/order1 holds the result
     const GeoRec *geo;                // packed geometry by Gaussian index (preprocess)
-    const float4 *col;                // (r, g, b, RN(1/ia)) by Gaussian index
     SplatRec *srec;                   // records by depth rank (written here)
     FrameCounters *ctr;
     int width, height, n_rows, tiles_x, ntiles;
@@ -148,7 +145,12 @@ struct BlendOut {
     float *rgb;     // (H,W,3) or null
     float *trans;   // (H,W) or null
 };
-void launch_blend(const SplatRec *srec, const uint32_t *tile_vals, const uint2 *ranges, int width,
+struct DepthOrder {  // depth rank -> Gaussian index (the depth sort's result buffer)
+    const uint32_t *order0, *order1;
+    const uint32_t *sched;  // sched[16]: which buffer holds the result
+};
+void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
+                  const uint32_t *tile_vals, const uint2 *ranges, int width,
                   int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
                   cudaStream_t s, const KMark &mark = KMark());
 

@@ -12,10 +12,10 @@
 // registers (the FP64 projection and the SH evaluation live at once), which
 // caps it at 24 warps per SM -- too few to hide HBM latency behind FP64
 // latency.  Split, each runs at high occupancy with all its loads coalesced:
-//   K1a geo    mean/scale/rotation/rsq/opacity (92 B) -> depth key, the
-//              packed geometry (u, v, ia, ib | ic, rsq, op, ry) and RN(1/ia)
-//   K1b colour kept Gaussians only: mean + SH planes (216 B) -> (r, g, b, rinv)
-// The binning gather (binning.cu) assembles the 48-byte splat record.
+//   K1a geo    mean/scale/rotation/rsq/opacity (92 B) -> depth key and the
+//              packed geometry (u, v, ia, ib | ic, rsq, op, ry)
+//   K1b colour kept Gaussians only: mean + SH planes (216 B) -> (r, g, b)
+// The binning gather (binning.cu) puts the geometry records in depth order.
 #include "kernels.cuh"
 
 namespace gsr {
@@ -77,7 +77,7 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
 
 __global__ void __launch_bounds__(256) preprocess_geo_kernel(
     SceneView sc, CameraArgs cam, int do_cull, unsigned long long *__restrict__ keys,
-    GeoRec *__restrict__ geo, float *__restrict__ rinv_out, uint8_t *__restrict__ keep_out,
+    GeoRec *__restrict__ geo, uint8_t *__restrict__ keep_out,
     FrameCounters *ctr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t st = sc.stride;
@@ -158,7 +158,6 @@ __global__ void __launch_bounds__(256) preprocess_geo_kernel(
                 o.a = make_float4((float)u, (float)v, ia32, (float)(-cb / det));
                 o.b = make_float4((float)(ca / det), (float)rsq, opac, (float)sqrt(cc * rsq));
                 geo[i] = o;
-                rinv_out[i] = __frcp_rn(ia32);
             }
         }
         keys[i] = key;
@@ -203,11 +202,10 @@ __global__ void __launch_bounds__(256) preprocess_geo_kernel(
 template <typename ShT, int DEG>
 __global__ void __launch_bounds__(256) preprocess_color_kernel(
     SceneView sc, CameraArgs cam, const unsigned long long *__restrict__ keys,
-    const float *__restrict__ rinv, float4 *__restrict__ col) {
+    float4 *__restrict__ col) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= sc.n || __ldg(keys + i) == ~0ull) return;  // culled: no colour needed
     const int64_t st = sc.stride;
-    const float ri = __ldg(rinv + i);
     float cr, cg, cbl;
     if (DEG == 0) {  // render.py:129-130
         cr = __ldg(sc.dc + i);
@@ -233,7 +231,7 @@ __global__ void __launch_bounds__(256) preprocess_color_kernel(
         cg = (float)sh_channel<DEG>(v, 1, ux, uy, uz, xx, yy, zz, xy, yz, xz);
         cbl = (float)sh_channel<DEG>(v, 2, ux, uy, uz, xx, yy, zz, xy, yz, xz);
     }
-    col[i] = make_float4(cr, cg, cbl, ri);  // SplatRec.c
+    col[i] = make_float4(cr, cg, cbl, 0.0f);
 }
 
 }  // namespace
@@ -243,17 +241,17 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
 }
 
 void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                       int frustum_cull, unsigned long long *keys, GeoRec *geo, float *rinv,
+                       int frustum_cull, unsigned long long *keys, GeoRec *geo,
                        float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s,
                        const KMark &mark) {
     if (scene.n == 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
-    preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, cam, frustum_cull, keys, geo, rinv,
+    preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, cam, frustum_cull, keys, geo,
                                                      keep_out, ctr);
     mark("preprocess_geo");
 #define GSR_COLOR(T, D)                                                                   \
-    preprocess_color_kernel<T, D><<<blocks, threads, 0, s>>>(scene, cam, keys, rinv, col)
+    preprocess_color_kernel<T, D><<<blocks, threads, 0, s>>>(scene, cam, keys, col)
     if (sh_degree == 0) GSR_COLOR(float, 0);
     else if (scene.sh_f32 && sh_degree == 1) GSR_COLOR(float, 1);
     else if (scene.sh_f32 && sh_degree == 2) GSR_COLOR(float, 2);
