@@ -15,10 +15,11 @@ from .render import (DeviceScene, EncodeFailure, Framebuffer, RenderError, Rende
                      RenderStats,
                      decode_image, device_scene, encode_jpeg, encode_png, evict,
                      framebuffer_to_u8, render_framebuffer, render_u8, render_view, set_device)
+from .registry import DeviceRegistry
 from .synth import ActivatedPrimitives
 
 __all__ = [
-    "ActivatedPrimitives", "CameraPose", "DeviceScene", "DimensionMismatch", "EmptyInput",
+    "ActivatedPrimitives", "CameraPose", "DeviceRegistry", "DeviceScene", "DimensionMismatch", "EmptyInput",
     "EncodeFailure", "EvalTriplet", "IndexOutOfRange", "aggregate_session", "evaluate_session_dir",
     "materialize_ground_truth",
     "Framebuffer", "Intrinsics", "RenderError", "RenderPipeline", "RenderStats", "TooSmall", "decode_image",

@@ -578,3 +578,47 @@ def test_evaluate_session_dir_vs_oracle(gsr, oracle, tmp_path):
         assert np.array_equal(gsr.decode_image(png), trips[idx].ground_truth)
     with pytest.raises(gsr.IndexOutOfRange):
         gsr.materialize_ground_truth(prims, Log(), [99])
+
+
+def test_device_registry_residency(gsr):
+    """a DeviceRegistry over a registry with the
+    reference's interface keeps the GPU copy in step: one upload per host
+    load, renders reuse it, eviction frees it."""
+    from paper_2605_08699_b200 import render as R
+    from paper_2605_08699_b200.registry import DeviceRegistry
+    from paper_2605_08699_b200.synth import synthetic_scene
+
+    class HostRegistry:
+        def __init__(self):
+            self.loaded, self.refs = {}, {}
+
+        def acquire(self, mid):
+            if mid not in self.loaded:
+                self.loaded[mid] = synthetic_scene(5000, seed=len(mid), sh_degree=0)
+            self.refs[mid] = self.refs.get(mid, 0) + 1
+            return self.loaded[mid]
+
+        def release(self, mid):
+            self.refs[mid] -= 1
+
+        def evict_inactive(self, now=None):
+            gone = [m for m in self.loaded if self.refs.get(m, 0) == 0]
+            for m in gone:
+                del self.loaded[m]
+            return gone
+
+        def snapshot(self):
+            return [{"id": m} for m in sorted(self.loaded)]
+
+    reg = DeviceRegistry(HostRegistry(), device=0)
+    intr = gsr.Intrinsics(fx=120.0, fy=120.0, cx=64.0, cy=64.0, width=128, height=128)
+    frames = []
+    for _ in range(3):
+        with reg.lease("garden") as prims:
+            frames.append(gsr.render_u8(prims, gsr.CameraPose(0.0, 0.0), intr).copy())
+    assert reg.uploads == 1 and reg.device_bytes() > 0
+    assert all(np.array_equal(f, frames[0]) for f in frames)
+    key = [k for k in R._scenes if k[1] == 0]
+    assert len(key) >= 1
+    assert reg.evict_inactive() == ["garden"]
+    assert reg.device_bytes() == 0
