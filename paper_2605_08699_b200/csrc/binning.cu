@@ -130,6 +130,8 @@ struct PairSmem {
     uint32_t s_warp[33];
     uint8_t lr[kPairCache];          // in-warp rank of a pair within its row
     uint16_t owner[kPairCache];      // block-local splat of a pair
+    uint16_t perm[kPairCache];       // pairs ordered by row count (see below)
+    uint32_t bucket[17];             // row-count histogram -> cursors
     int ty_lo, ty_hi;
     // followed in dynamic shared memory by (n_rows = tile rows of the frame):
     //   uint32_t wpre[BR / 32][n_rows]  per-warp coverage masks -> counts -> prefix
@@ -219,9 +221,42 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         rowbase[ty] = run ? a.row_blk[(int64_t)ty * a.n_blocks + b] : 0u;
     }
     __syncthreads();
-    // one thread per pair: exact tile span, stored at its grouped slot
+    // One thread per pair: exact tile span, stored at its grouped slot.  A
+    // pair has 1..16 rows; threads take the pairs in decreasing row count
+    // (a counting sort of the block's pairs) so the 32 row loops of a warp
+    // run similar trip counts.  The order only affects scheduling: each
+    // pair's slot is fixed above.
+    const bool sorted = npairs <= (uint32_t)kPairCache;
+    if (sorted) {
+        if (tid < 17) S.bucket[tid] = 0;
+        __syncthreads();
+        for (uint32_t q = tid; q < npairs; q += BR) {
+            const int j = S.owner[q];
+            const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
+            const int nrow = min(S.hi[j], ty * kTile + kTile) - max(S.lo[j], ty * kTile);
+            atomicAdd(&S.bucket[16 - nrow], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t run = 0;
+            for (int i = 0; i < 17; i++) {
+                const uint32_t c = S.bucket[i];
+                S.bucket[i] = run;
+                run += c;
+            }
+        }
+        __syncthreads();
+        for (uint32_t q = tid; q < npairs; q += BR) {
+            const int j = S.owner[q];
+            const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
+            const int nrow = min(S.hi[j], ty * kTile + kTile) - max(S.lo[j], ty * kTile);
+            S.perm[atomicAdd(&S.bucket[16 - nrow], 1u)] = (uint16_t)q;
+        }
+        __syncthreads();
+    }
     uint32_t n_rows = 0;
-    for (uint32_t q = tid; q < npairs; q += BR) {
+    for (uint32_t qi = tid; qi < npairs; qi += BR) {
+        const uint32_t q = sorted ? (uint32_t)S.perm[qi] : qi;
         const int j = q < kPairCache ? (int)S.owner[q] : rank_of_pair(S.poff, q);
         const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
         uint32_t in_warp;
