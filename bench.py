@@ -238,8 +238,8 @@ def kernel_work(name, wl, c):
         "preprocess_geo": (n * 92 + n * 8 + k * 32, 0),
         # key of all N; mean f64 + SH f32 (or DC) of kept in; colour out
         "preprocess_color": (n * 8 + k * (24 + sh_bytes) + k * 16, 0),
-        "depth_key32": (n * 12, 0),
-        "radix32_hist": (k * 4, 0),
+        # reads the f64 depth key of all N, writes the 32-bit span key
+        "radix32_hist": (n * 12, 0),
         "radix32_pass": (k * 16, 0),  # per pass: key + index read and written
         "depth_fixup": (k * 4, 0),
         # order + geometry gathered, 32 B record written

@@ -33,8 +33,9 @@ namespace gsr {
 
 namespace {
 
-constexpr int kBlendThreads = 256;
+constexpr int kBlendThreads = 128;              // 4 warps: finer occupancy granularity
 constexpr int kWarps = kBlendThreads / 32;
+constexpr int kRowPairs = kTile / 2;           // work items per tile (2 pixel rows each)
 
 __device__ __forceinline__ uint32_t span_mask(int x0, int x1, int X) {
     // columns [x0, x1) intersected with [X, X+16), as a 16-bit mask
@@ -175,7 +176,7 @@ __device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, cons
 // as soon as its 32 pixels saturate, or walks the whole tile list if they
 // never do), so binding 8 warps to a CTA per tile would leave most of a CTA's
 // warps idle behind its slowest one; the queue keeps every warp busy.
-__global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
+__global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
     const SplatRec *__restrict__ srec, const float4 *__restrict__ col, DepthOrder ord,
     const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
     int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *__restrict__ ctr) {
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
     __syncthreads();
 
     const int tiles_x = (width + kTile - 1) / kTile;
-    const int n_items = tiles_x * ((height + kTile - 1) / kTile) * kWarps;
+    const int n_items = tiles_x * ((height + kTile - 1) / kTile) * kRowPairs;
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int prow = lane >> 4;
     WarpBatch &B_ = s_b[w];
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) blend_kernel(
         if (lane == 0) item = (int)atomicAdd(&ctr->blend_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= n_items) break;
-        const int tile = item / kWarps, wr = item % kWarps;
+        const int tile = item / kRowPairs, wr = item % kRowPairs;
         const int tx = tile % tiles_x, ty = tile / tiles_x;
         const int X = tx * kTile;
         const int iy0 = ty * kTile + 2 * wr;

@@ -6,7 +6,8 @@
 // kept depths span [kmin, kmax] and are nearly all distinct at 32-bit
 // resolution of that span.  So:
 //  1 key32   k32 = min((bits(z) - kmin) >> shift, 2^24 - 1), shift chosen so
-//            the span fits 24 bits; culled Gaussians keep the sentinel ~0.
+//            the span fits 24 bits; culled Gaussians keep the sentinel ~0
+//            (computed and written by the sort's histogram kernel).
 //            Positive f64 bits order like the values, and the map is monotone,
 //            so sorting k32 orders every pair of splats whose k32 differ.
 //  2 sort32  stable Onesweep radix sort of (k32, index), <= 3 passes (the
@@ -28,25 +29,6 @@ constexpr int kMaxRun = 16;
 // Span key width: 24 bits = 3 radix passes.  At 3M kept splats a bucket holds
 // 0.2 splats on average; the fix-up resolves the resulting short runs.
 constexpr int kSpanBits = 24;
-constexpr unsigned long long kSpanMax = (1ull << kSpanBits) - 1;
-
-__global__ void depth_key32_kernel(const unsigned long long *__restrict__ k64,
-                                   uint32_t *__restrict__ k32, int64_t n,
-                                   const FrameCounters *__restrict__ ctr) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const unsigned long long kmin = ctr->kmin, kmax = ctr->kmax;
-    const unsigned long long range = kmax > kmin ? kmax - kmin : 0ull;
-    const int bits = range ? 64 - __clzll((long long)range) : 0;
-    const int shift = bits > kSpanBits ? bits - kSpanBits : 0;
-    const unsigned long long k = k64[i];
-    uint32_t o = 0xffffffffu;
-    if (k != ~0ull) {
-        const unsigned long long q = (k - kmin) >> shift;
-        o = q < kSpanMax ? (uint32_t)q : (uint32_t)kSpanMax;
-    }
-    k32[i] = o;
-}
 
 __global__ void depth_fixup_kernel(DepthArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -99,12 +81,15 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &
             a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, &a.ctr->K, a.n, a.n, 8,
             true, a.work64, a.sched, &a.ctr->npass_fb, sms, s, mark);
     const unsigned g = (unsigned)((a.n + 255) / 256);
-    depth_key32_kernel<<<g, 256, 0, s>>>(a.keys64[0], a.keys32[0], a.n, a.ctr);
-    mark("depth_key32");
-    int launches = 1;
-    launches += launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
-                                               true, true, &a.ctr->K, a.n, a.n, kSpanBits / 8, true, a.work32,
-                                               a.sched, &a.ctr->npass, sms, s, mark);
+    SpanKeys span;  // the histogram kernel writes the span keys (step 1)
+    span.src = a.keys64[0];
+    span.kmin = &a.ctr->kmin;
+    span.kmax = &a.ctr->kmax;
+    span.bits = kSpanBits;
+    int launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
+                                                  true, true, &a.ctr->K, a.n, a.n, kSpanBits / 8,
+                                                  true, a.work32, a.sched, &a.ctr->npass, sms, s,
+                                                  mark, span);
     depth_fixup_kernel<<<g, 256, 0, s>>>(a);
     mark("depth_fixup");
     return launches + 1;

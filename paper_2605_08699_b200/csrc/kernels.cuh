@@ -79,6 +79,15 @@ inline int64_t radix_tiles(int64_t n_cap, int key_bytes) {
 }
 // scratch for one sort (histograms, look-back status, tickets)
 size_t sort_work_bytes(int64_t n_items_cap, int passes, int key_bytes);
+// Optional key source of a 32-bit sort: the histogram kernel derives each key
+// from a 64-bit one, k32 = min((k64 - kmin) >> shift, max_key) with shift
+// chosen from [kmin, kmax] so the span fits `bits` bits (sentinel ~0 kept),
+// and writes it to keys0 -- the depth sort's span keys (depth.cu).
+struct SpanKeys {
+    const unsigned long long *src = nullptr;
+    const unsigned long long *kmin = nullptr, *kmax = nullptr;
+    int bits = 24;
+};
 // Sorts (keys0, vals0) over `passes` 8-bit digits; the result lands in buffer
 // sched[16] (0 or 1).  First pass: n_first items (>= 0) or *n_dev (n_first <
 // 0); later passes: min(*n_dev, n_cap).  implicit_first_vals: value = index;
@@ -88,7 +97,8 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
                          bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
                          int64_t n_first, int64_t n_cap, int passes, bool force_first,
                          void *work, uint32_t *sched, uint32_t *npass_out, int sms,
-                         cudaStream_t s, const KMark &mark = KMark());
+                         cudaStream_t s, const KMark &mark = KMark(),
+                         const SpanKeys &span = SpanKeys());
 
 // depth.cu: stable f64 depth order (see depth.cu header)
 struct DepthArgs {

@@ -68,6 +68,7 @@ struct SortArgs {
     uint32_t *tickets;         // [passes]
     uint32_t *sched;           // [0..7] active, [8..15] src buffer, [16] final buffer
     uint32_t *npass_out;       // nullable: number of active passes
+    SpanKeys span;             // 32-bit sorts: keys derived from 64-bit ones (hist kernel)
 };
 
 template <typename K>
@@ -98,8 +99,27 @@ __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
     __syncthreads();
     const int64_t n = first_count(a);
     const K *keys = a.keys[0];
+    unsigned long long kmin = 0;
+    int shift = 0;
+    unsigned long long kcap = 0;
+    if (sizeof(K) == 4 && a.span.src) {
+        kmin = *a.span.kmin;
+        const unsigned long long kmax = *a.span.kmax;
+        const unsigned long long range = kmax > kmin ? kmax - kmin : 0ull;
+        const int bits = range ? 64 - __clzll((long long)range) : 0;
+        shift = bits > a.span.bits ? bits - a.span.bits : 0;
+        kcap = (1ull << a.span.bits) - 1ull;
+    }
     for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        const K k = keys[i];
+        K k;
+        if (sizeof(K) == 4 && a.span.src) {  // span key of the depth bits
+            const unsigned long long k64 = a.span.src[i];
+            const unsigned long long q = (k64 - kmin) >> shift;
+            k = k64 == ~0ull ? sentinel<K>() : (K)(q < kcap ? q : kcap);
+            a.keys[0][i] = k;
+        } else {
+            k = keys[i];
+        }
         if (a.drop_sentinel && k == sentinel<K>()) continue;
 #pragma unroll
         for (int p = 0; p < (int)sizeof(K); p++)
@@ -335,8 +355,9 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
                          bool implicit_first_vals, bool drop_sentinel, const uint32_t *n_dev,
                          int64_t n_first, int64_t n_cap, int passes, bool force_first,
                          void *work, uint32_t *sched, uint32_t *npass_out, int sms,
-                         cudaStream_t s, const KMark &mark) {
+                         cudaStream_t s, const KMark &mark, const SpanKeys &span) {
     SortArgs<K> a;
+    a.span = span;
     a.keys[0] = keys0;
     a.keys[1] = keys1;
     a.vals[0] = vals0;
@@ -383,10 +404,11 @@ template int launch_onesweep_sort<unsigned long long>(unsigned long long *, unsi
                                                       uint32_t *, uint32_t *, bool, bool,
                                                       const uint32_t *, int64_t, int64_t, int,
                                                       bool, void *, uint32_t *, uint32_t *,
-                                                      int, cudaStream_t, const KMark &);
+                                                      int, cudaStream_t, const KMark &,
+                                                      const SpanKeys &);
 template int launch_onesweep_sort<uint32_t>(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool,
                                             bool, const uint32_t *, int64_t, int64_t, int, bool,
                                             void *, uint32_t *, uint32_t *, int,
-                                            cudaStream_t, const KMark &);
+                                            cudaStream_t, const KMark &, const SpanKeys &);
 
 }  // namespace gsr
