@@ -145,12 +145,14 @@ template <bool kChecked>
 __device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, const float4 *col,
                                           float fx, const unsigned long long *tab, uint32_t tab_s,
                                           const ExpK &ek, float &T, float &cr, float &cg,
-                                          float &cb, bool &done, uint32_t &n_comp) {
+                                          float &cb, uint32_t &n_comp) {
+    // (a lane that saturates drops its remaining bits; the caller derives
+    //  `done` from T, and the composite count from the dropped bits)
+    n_comp += __popc(mine);
     while (__any_sync(0xffffffffu, mine != 0u)) {
         if (mine) {
             const int s = __ffs(mine) - 1;
             mine &= mine - 1u;
-            n_comp++;
             const float4 g = geo[s];  // u, ia, ib_dy, cy_term
             const float4 k = col[s];  // op, r, g, b
             const float dx = fx - g.x;
@@ -163,7 +165,7 @@ __device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, cons
             cb += weight * k.w;
             T = T * (1.0f - alpha);
             if (T < kTStop) {
-                done = true;
+                n_comp -= __popc(mine);
                 mine = 0u;
             }
         }
@@ -191,7 +193,10 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
     const int prow = lane >> 4;
     WarpBatch &B_ = s_b[w];
     const float4 *geo = B_.geo[prow];
-    const uint32_t tab_s = (uint32_t)__cvta_generic_to_shared(s_tab);
+    // (opaque to the compiler, so the table base stays in a register instead
+    //  of being rebuilt from the CTA id in the inner loop)
+    uint32_t tab_s;
+    asm volatile("mov.u32 %0, %1;" : "=r"(tab_s) : "r"((uint32_t)__cvta_generic_to_shared(s_tab)));
     // pinned in registers (opaque to rematerialisation by constant reloads)
     ExpK ek;
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.inv_ln2n) : "d"(kExpK[0]));
@@ -220,13 +225,16 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
         bool done = !inside;
         const uint2 rg = ranges[tile];
 
+        // the next batch's list entry is loaded one batch ahead
+        uint32_t r_next = rg.x + lane < rg.y ? __ldg(tile_vals + rg.x + lane) : 0u;
         for (uint32_t c = rg.x; c < rg.y; c += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const uint32_t j = c + lane;
+            const uint32_t r = r_next;  // depth rank
+            r_next = j + 32 < rg.y ? __ldg(tile_vals + j + 32) : 0u;
             uint32_t mask = 0;
             bool safe = true;
             if (j < rg.y) {
-                const uint32_t r = __ldg(tile_vals + j);  // depth rank
                 const float4 A = __ldg(&srec[r].a);
                 const float4 B = __ldg(&srec[r].b);
                 const uint32_t gi = __ldg(order + r);  // issued with the record loads
@@ -252,11 +260,10 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
             uint32_t mine = transpose32(mask, lane);
             if (done) mine = 0u;
             if (__all_sync(0xffffffffu, safe))
-                composite<false>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, done,
-                                 n_comp);
+                composite<false>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
             else
-                composite<true>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, done,
-                                n_comp);
+                composite<true>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
+            done = done || T < kTStop;
             __syncwarp();
         }
         if (inside) {
