@@ -225,16 +225,13 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
         bool done = !inside;
         const uint2 rg = ranges[tile];
 
-        // the next batch's list entry is loaded one batch ahead
-        uint32_t r_next = rg.x + lane < rg.y ? __ldg(tile_vals + rg.x + lane) : 0u;
         for (uint32_t c = rg.x; c < rg.y; c += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const uint32_t j = c + lane;
-            const uint32_t r = r_next;  // depth rank
-            r_next = j + 32 < rg.y ? __ldg(tile_vals + j + 32) : 0u;
             uint32_t mask = 0;
             bool safe = true;
             if (j < rg.y) {
+                const uint32_t r = __ldg(tile_vals + j);  // depth rank
                 const float4 A = __ldg(&srec[r].a);
                 const float4 B = __ldg(&srec[r].b);
                 const uint32_t gi = __ldg(order + r);  // issued with the record loads
