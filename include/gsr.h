@@ -42,6 +42,10 @@ extern "C" {
 #define GSR_E_DIM_MISMATCH (-4)   /* metrics.DimensionMismatch (metrics.py:85-86) */
 #define GSR_E_TOO_SMALL (-5)      /* metrics.TooSmall (metrics.py:87-88) */
 #define GSR_E_NO_DEVICE (-6)      /* RenderError: no CUDA device */
+#define GSR_E_PLY_HEADER (-7)     /* model.MalformedHeader (model.py:44-45) */
+#define GSR_E_PLY_PROPERTY (-8)   /* model.MissingProperty (model.py:48-49) */
+#define GSR_E_PLY_TRUNCATED (-9)  /* model.TruncatedBody (model.py:52-53) */
+#define GSR_E_NONFINITE (-10)     /* model.NonFiniteAttribute (model.py:56-57) */
 
 typedef struct gsr_scene gsr_scene;
 typedef struct gsr_ctx gsr_ctx;
@@ -96,6 +100,57 @@ GSR_API int gsr_scene_destroy(gsr_scene *scene);
 GSR_API int64_t gsr_scene_count(const gsr_scene *scene);
 GSR_API int64_t gsr_scene_device_bytes(const gsr_scene *scene);
 GSR_API int gsr_scene_sh_is_f32(const gsr_scene *scene);
+
+/* ---- PLY scenes on the device: replaces
+ * activate(parse_ply(path.read_bytes())) of the registry's load
+ * (model.py:354, parse_ply 169-208, activate 211-252) -------------------- */
+
+/* Columns of the loader's properties in the vertex table, in this order
+ * (model.py:31-36 REQUIRED_PROPERTIES, then f_rest_0..44, model.py:195). */
+#define GSR_PLY_NCOLS 59
+typedef struct gsr_ply_info {
+    int64_t count;        /* vertex count (element vertex N) */
+    int64_t body_offset;  /* first byte of the vertex table */
+    int64_t body_bytes;   /* count * n_props * 4 */
+    int32_t n_props;      /* float32 properties per vertex */
+    int32_t has_rest;     /* all 45 f_rest_* present (model.py:196) */
+    int32_t col[GSR_PLY_NCOLS];  /* last column of each name (model.py:189), -1 absent */
+    int32_t reserved;
+} gsr_ply_info;
+
+/* _parse_header (model.py:105-166) + the property / length checks of
+ * parse_ply (model.py:176-186): MalformedHeader / MissingProperty /
+ * TruncatedBody with the reference's messages.  Host only (no device). */
+GSR_API int gsr_ply_parse_header(const uint8_t *data, int64_t len, gsr_ply_info *info);
+
+typedef struct gsr_ply_stats {
+    double h2d_ms;       /* host -> device copy of the vertex table */
+    double kernel_ms;    /* decode + checks + activation kernels */
+    double total_ms;     /* whole call (host clock) */
+    int64_t body_bytes;  /* bytes of the vertex table read */
+    int64_t scene_bytes; /* device bytes of the resident scene */
+} gsr_ply_stats;
+
+/* Parse + validate + activate a binary PLY on `device` straight into a
+ * resident scene: f64 means / scales (np.exp) / rotations (q / |q|) /
+ * opacities (scipy expit) / f32 colours and SH / cutoff radius, all equal
+ * bit-for-bit to the reference's arrays.  Non-finite raw or activated
+ * attributes fail with GSR_E_NONFINITE and the reference's message (checked
+ * in the reference's order, model.py:199-203, 239-243).  `stats` nullable. */
+GSR_API int gsr_scene_create_ply(gsr_scene **out, int device, const uint8_t *data, int64_t len,
+                                 gsr_ply_stats *stats);
+
+/* Read an ActivatedPrimitives attribute back as the reference's f64 array
+ * (row-major): GSR_ATTR_MEANS (N,3), SCALES (N,3), ROTATIONS (N,4),
+ * OPACITIES (N,), COLORS_DC (N,3; PLY scenes only), SH (N,16,3), RSQ (N,). */
+#define GSR_ATTR_MEANS 0
+#define GSR_ATTR_SCALES 1
+#define GSR_ATTR_ROTATIONS 2
+#define GSR_ATTR_OPACITIES 3
+#define GSR_ATTR_COLORS_DC 4
+#define GSR_ATTR_SH 5
+#define GSR_ATTR_RSQ 6   /* (N,) cutoff radius^2 of render.py:476-481 */
+GSR_API int gsr_scene_read(const gsr_scene *scene, int attribute, double *host_out);
 
 /* ---- contexts: one CUDA stream + workspace (one per serving thread,
  * server.py:99-100) ------------------------------------------------------- */

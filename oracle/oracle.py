@@ -59,7 +59,8 @@ def build(force: bool = False) -> Path:
             and LIB_PATH.stat().st_mtime >= src.stat().st_mtime):
         return LIB_PATH
     LIB_PATH.parent.mkdir(parents=True, exist_ok=True)
-    cmd = [_cc(), "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+    cmd = [_cc(), "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-frounding-math",
+           "-fopenmp",
            "-fPIC", "-shared", "-o", str(LIB_PATH), str(src), "-lm"]
     subprocess.run(cmd, check=True)
     return LIB_PATH
@@ -94,6 +95,9 @@ def _declare(L):
     L.orc_ssim.restype = dbl
     L.orc_jpeg.argtypes = [vp, i32, i32, i32, i32, vp, i64]
     L.orc_jpeg.restype = i64
+    L.orc_np_exp.argtypes = [i64, vp, vp]
+    L.orc_glibc_exp.argtypes = [i64, vp, vp]
+    L.orc_np_log.argtypes = [i64, vp, vp]
     L.orc_num_threads.restype = i32
     L.orc_set_num_threads.argtypes = [i32]
 
@@ -310,3 +314,146 @@ def psnr(a, b):
 
 if __name__ == "__main__":  # pragma: no cover
     print(build(force=True))
+
+
+# --------------------------------------------------------------------------
+# PLY load, model.py:105-252 (numpy restatement; transcendental calls through
+# the C restatements of numpy's SVML exp/log and glibc's exp)
+# --------------------------------------------------------------------------
+
+class PlyError(Exception):
+    """Carries the reference's exception class name (model.py:40-57)."""
+
+    def __init__(self, kind: str, message: str):
+        super().__init__(message)
+        self.kind = kind
+
+
+PLY_REQUIRED = ("x", "y", "z", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2",
+                "rot_3", "opacity", "f_dc_0", "f_dc_1", "f_dc_2")
+PLY_REST = tuple(f"f_rest_{i}" for i in range(45))
+SH_DC_COEFF = 0.28209479177
+
+
+def np_exp(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    lib().orc_np_exp(x.size, _p(x), _p(y))
+    return y
+
+
+def glibc_exp(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    lib().orc_glibc_exp(x.size, _p(x), _p(y))
+    return y
+
+
+def np_log(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    lib().orc_np_log(x.size, _p(x), _p(y))
+    return y
+
+
+def ply_header(data: bytes):
+    """_parse_header (model.py:105-166): (properties, count, body_offset)."""
+    end = data.find(b"end_header")
+    if end < 0:
+        raise PlyError("MalformedHeader", "no end_header line found")
+    newline = data.find(b"\n", end)
+    if newline < 0:
+        raise PlyError("MalformedHeader", "end_header line is not terminated")
+    try:
+        text = data[:end].decode("ascii")
+    except UnicodeDecodeError as exc:
+        raise PlyError("MalformedHeader", f"header is not ASCII: {exc}") from None
+    lines = [ln.strip() for ln in text.splitlines() if ln.strip()]
+    if not lines or lines[0] != "ply":
+        raise PlyError("MalformedHeader", "missing 'ply' magic line")
+    fmt, count, props, in_vertex = False, None, [], False
+    for line in lines[1:]:
+        parts = line.split()
+        bad = lambda m: PlyError("MalformedHeader", m)  # noqa: E731
+        if parts[0] == "comment":
+            continue
+        if parts[0] == "format":
+            if parts[1:] != ["binary_little_endian", "1.0"]:
+                raise bad(f"unsupported format: {line!r}")
+            fmt = True
+        elif parts[0] == "element":
+            if len(parts) != 3:
+                raise bad(f"bad element line: {line!r}")
+            if parts[1] != "vertex":
+                raise bad(f"unsupported element {parts[1]!r}")
+            if count is not None:
+                raise bad("multiple vertex elements")
+            try:
+                count = int(parts[2])
+            except ValueError:
+                raise bad(f"bad vertex count: {parts[2]!r}") from None
+            if count < 0:
+                raise bad("negative vertex count")
+            in_vertex = True
+        elif parts[0] == "property":
+            if not in_vertex:
+                raise bad("property outside the vertex element")
+            if len(parts) != 3:
+                raise bad(f"bad property line: {line!r}")
+            if parts[1] != "float":
+                raise bad(f"only float32 properties supported, got {parts[1]!r}")
+            props.append(parts[2])
+        else:
+            raise bad(f"unexpected header line: {line!r}")
+    if not fmt:
+        raise PlyError("MalformedHeader", "missing format line")
+    if count is None:
+        raise PlyError("MalformedHeader", "missing vertex element")
+    return props, count, newline + 1
+
+
+def ply_load(data: bytes) -> dict:
+    """activate(parse_ply(data)) (model.py:169-252) + rsq (render.py:476-481).
+
+    Returns the ActivatedPrimitives arrays as a dict, or raises PlyError.
+    """
+    props, count, off = ply_header(data)
+    for name in PLY_REQUIRED:
+        if name not in props:
+            raise PlyError("MissingProperty", f"required property {name!r} absent")
+    n_props = len(props)
+    expected = count * n_props * 4
+    body = data[off:off + expected]
+    if len(body) < expected:
+        raise PlyError("TruncatedBody",
+                       f"body holds {len(body)} bytes, need {expected} for {count} vertices")
+    table = np.frombuffer(body, dtype="<f4").reshape(count, n_props).astype(np.float64)
+    col = {name: i for i, name in enumerate(props)}
+    grab = lambda names: table[:, [col[n] for n in names]]  # noqa: E731
+    means = grab(PLY_REQUIRED[0:3])
+    log_scales = grab(PLY_REQUIRED[3:6])
+    quats = grab(PLY_REQUIRED[6:10])
+    logits = table[:, col["opacity"]]
+    sh = np.zeros((count, 16, 3))
+    sh[:, 0, :] = grab(PLY_REQUIRED[11:14])
+    if all(n in col for n in PLY_REST):
+        sh[:, 1:, :] = grab(PLY_REST).reshape(count, 3, 15).transpose(0, 2, 1)
+    for name, arr in (("means", means), ("scales", log_scales), ("rotations", quats),
+                      ("opacities", logits), ("sh", sh)):
+        if not np.all(np.isfinite(arr)):
+            raise PlyError("NonFiniteAttribute", f"non-finite values in {name}")
+    scales = np_exp(log_scales)
+    opac = 1.0 / (1.0 + glibc_exp(-logits))
+    s = quats * quats
+    norms = np.sqrt(((s[:, 0] + s[:, 1]) + s[:, 2]) + s[:, 3])[:, None]
+    with np.errstate(invalid="ignore", divide="ignore"):
+        rots = quats / norms
+    colors = np.clip(SH_DC_COEFF * sh[:, 0, :] + 0.5, 0.0, 1.0)
+    for name, arr in (("scales", scales), ("opacities", opac), ("rotations", rots),
+                      ("colors", colors)):
+        if not np.all(np.isfinite(arr)):
+            raise PlyError("NonFiniteAttribute", f"activation produced non-finite {name}")
+    floor = 1.0 / (255.0 * TAIL_SAFETY)
+    rsq = np.minimum(2.0 * np_log(np.maximum(opac, floor) / floor), CUTOFF_SIGMA ** 2)
+    return {"means": means, "scales": scales, "rotations": rots, "opacities": opac,
+            "colors_dc": colors, "sh_coeffs": sh, "rsq": rsq}

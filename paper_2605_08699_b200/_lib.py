@@ -24,6 +24,11 @@ GSR_E_OOM = -3
 GSR_E_DIM_MISMATCH = -4
 GSR_E_TOO_SMALL = -5
 GSR_E_NO_DEVICE = -6
+GSR_E_PLY_HEADER = -7
+GSR_E_PLY_PROPERTY = -8
+GSR_E_PLY_TRUNCATED = -9
+GSR_E_NONFINITE = -10
+GSR_PLY_NCOLS = 59
 
 
 class RenderError(Exception):
@@ -51,6 +56,22 @@ class GsrStats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class GsrPlyInfo(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64), ("body_offset", ctypes.c_int64),
+                ("body_bytes", ctypes.c_int64), ("n_props", ctypes.c_int32),
+                ("has_rest", ctypes.c_int32), ("col", ctypes.c_int32 * GSR_PLY_NCOLS),
+                ("reserved", ctypes.c_int32)]
+
+
+class GsrPlyStats(ctypes.Structure):
+    _fields_ = [("h2d_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
+                ("total_ms", ctypes.c_double), ("body_bytes", ctypes.c_int64),
+                ("scene_bytes", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 # (name, restype, argtypes); every symbol declared in include/gsr.h
 _vp, _i32, _i64, _dbl, _sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
 _P = ctypes.POINTER
@@ -63,6 +84,9 @@ SIGNATURES = [
     ("gsr_scene_count", _i64, [_vp]),
     ("gsr_scene_device_bytes", _i64, [_vp]),
     ("gsr_scene_sh_is_f32", _i32, [_vp]),
+    ("gsr_ply_parse_header", _i32, [_vp, _i64, _P(GsrPlyInfo)]),
+    ("gsr_scene_create_ply", _i32, [_P(_vp), _i32, _vp, _i64, _P(GsrPlyStats)]),
+    ("gsr_scene_read", _i32, [_vp, _i32, _vp]),
     ("gsr_ctx_create", _i32, [_P(_vp), _i32]),
     ("gsr_ctx_destroy", _i32, [_vp]),
     ("gsr_ctx_device_bytes", _i64, [_vp]),
@@ -131,6 +155,12 @@ def check(rc: int, what: str = "") -> None:
     if rc == GSR_E_TOO_SMALL:
         from .metrics import TooSmall
         raise TooSmall(msg)
+    if GSR_E_NONFINITE <= rc <= GSR_E_PLY_HEADER:  # model.py:40-57, reference messages
+        from . import model
+        cls = {GSR_E_PLY_HEADER: model.MalformedHeader, GSR_E_PLY_PROPERTY: model.MissingProperty,
+               GSR_E_PLY_TRUNCATED: model.TruncatedBody,
+               GSR_E_NONFINITE: model.NonFiniteAttribute}[rc]
+        raise cls(last_error())
     raise RenderError(msg or f"gsr error {rc}")
 
 

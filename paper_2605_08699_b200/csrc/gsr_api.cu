@@ -17,12 +17,13 @@
 
 #include "../../include/gsr.h"
 #include "kernels.cuh"
+#include "scene.cuh"
 
 namespace gsr {
 
 thread_local std::string g_err;
 
-static int fail(int code, const std::string &msg) {
+int fail(int code, const std::string &msg) {
     g_err = msg;
     return code;
 }
@@ -33,19 +34,7 @@ int fail_cuda(cudaError_t e, const char *what) {
     return e == cudaErrorMemoryAllocation ? GSR_E_OOM : GSR_E_CUDA;
 }
 
-struct DevBuf {
-    void *p = nullptr;
-    size_t bytes = 0;
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    template <typename T>
-    T *as() const {
-        return reinterpret_cast<T *>(p);
-    }
-};
-
-static int ensure(DevBuf &b, size_t bytes) {
+int ensure(DevBuf &b, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (b.bytes >= bytes) return GSR_OK;
     if (b.p) cudaFree(b.p);
@@ -56,21 +45,9 @@ static int ensure(DevBuf &b, size_t bytes) {
     return GSR_OK;
 }
 
-static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
-
 }  // namespace gsr
 
 using namespace gsr;
-
-struct gsr_scene {
-    int device = 0;
-    int64_t n = 0;
-    int64_t stride = 0;
-    int sh_f32 = 1;
-    int has_sh = 0;
-    DevBuf block;
-    SceneView view{};
-};
 
 struct SavedCall {
     const gsr_scene *scene = nullptr;
@@ -131,28 +108,7 @@ struct gsr_ctx {
 
 namespace {
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
 
-__global__ void rsq_kernel(const float *op32, const double *op64, int64_t n, double *rsq) {
-    // device fallback of render.py:476-481 (IEEE log; numpy may differ by 1 ulp)
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double floor_ = 1.0 / (255.0 * 32.0);
-    double o = op64[i];
-    o = o > floor_ ? o : floor_;
-    double r = 2.0 * log(o / floor_);
-    rsq[i] = r < 20.25 ? r : 20.25;
-    (void)op32;
-}
 
 int check_camera(const gsr_camera *cam) {
     if (!cam) return fail(GSR_E_INVALID, "camera is null");
@@ -613,24 +569,14 @@ int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means
             f32ok = (double)(float)sh_coeffs[i] == sh_coeffs[i];
     sc->sh_f32 = f32ok ? 1 : 0;
     const int64_t st = sc->stride;
-    const size_t sh_elem = sc->sh_f32 ? 4 : 8;
-    size_t off = 0;
-    auto take = [&](size_t bytes) {
-        size_t o = off;
-        off += round_up((int64_t)bytes, 256);
-        return o;
-    };
-    const size_t o_mean = take(3 * st * 8), o_scale = take(3 * st * 8), o_rot = take(4 * st * 8),
-                 o_rsq = take(st * 8), o_opac = take(st * 4), o_dc = take(3 * st * 4),
-                 o_op64 = take(st * 8),
-                 o_sh = take(sc->has_sh ? 48 * st * sh_elem : 16);
-    int rc = ensure(sc->block, off);
+    const SceneLayout L = scene_layout(st, sc->has_sh, sc->sh_f32);
+    int rc = ensure(sc->block, L.total);
     if (rc) {
         delete sc;
         return rc;
     }
     // host staging in planar (SoA) layout
-    std::vector<unsigned char> host(off, 0);
+    std::vector<unsigned char> host(L.total, 0);
     auto plane_d = [&](size_t o, const double *src, int k, int comps) {
         double *d = reinterpret_cast<double *>(host.data() + o) + (size_t)k * st;
         for (int64_t i = 0; i < n; i++) d[i] = src[i * comps + k];
@@ -640,47 +586,36 @@ int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means
         for (int64_t i = 0; i < n; i++) d[i] = (float)src[i * comps + k];
     };
     for (int k = 0; k < 3; k++) {
-        plane_d(o_mean, means, k, 3);
-        plane_d(o_scale, scales, k, 3);
-        plane_f(o_dc, colors_dc, k, 3);
+        plane_d(L.mean, means, k, 3);
+        plane_d(L.scale, scales, k, 3);
+        plane_f(L.dc, colors_dc, k, 3);
     }
-    for (int k = 0; k < 4; k++) plane_d(o_rot, rotations, k, 4);
-    plane_f(o_opac, opacities, 0, 1);
-    plane_d(o_op64, opacities, 0, 1);
-    if (rsq) plane_d(o_rsq, rsq, 0, 1);
+    for (int k = 0; k < 4; k++) plane_d(L.rot, rotations, k, 4);
+    plane_f(L.opac, opacities, 0, 1);
+    plane_d(L.op64, opacities, 0, 1);
+    if (rsq) plane_d(L.rsq, rsq, 0, 1);
     if (sc->has_sh) {
         for (int k = 0; k < 48; k++) {
-            if (sc->sh_f32) plane_f(o_sh, sh_coeffs, k, 48);
-            else plane_d(o_sh, sh_coeffs, k, 48);
+            if (sc->sh_f32) plane_f(L.sh, sh_coeffs, k, 48);
+            else plane_d(L.sh, sh_coeffs, k, 48);
         }
     }
     unsigned char *d = sc->block.as<unsigned char>();
-    cudaError_t e = cudaMemcpy(d, host.data(), off, cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMemcpy(d, host.data(), L.total, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         delete sc;
         return fail_cuda(e, "scene upload");
     }
     if (!rsq && n > 0) {
-        rsq_kernel<<<(unsigned)((n + 255) / 256), 256>>>(
-            reinterpret_cast<float *>(d + o_opac), reinterpret_cast<double *>(d + o_op64), n,
-            reinterpret_cast<double *>(d + o_rsq));
+        launch_rsq(reinterpret_cast<const double *>(d + L.op64), n,
+                   reinterpret_cast<double *>(d + L.rsq), nullptr);
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
             delete sc;
             return fail_cuda(e, "rsq kernel");
         }
     }
-    SceneView &v = sc->view;
-    v.n = n;
-    v.stride = st;
-    v.mean = reinterpret_cast<const double *>(d + o_mean);
-    v.scale = reinterpret_cast<const double *>(d + o_scale);
-    v.rot = reinterpret_cast<const double *>(d + o_rot);
-    v.rsq = reinterpret_cast<const double *>(d + o_rsq);
-    v.opac = reinterpret_cast<const float *>(d + o_opac);
-    v.dc = reinterpret_cast<const float *>(d + o_dc);
-    v.sh = d + o_sh;
-    v.sh_f32 = sc->sh_f32;
+    sc->bind(L);
     *out = sc;
     return GSR_OK;
 }

@@ -48,6 +48,7 @@ struct SceneView {
     const float *opac;    // [stride]     f32(opacity)
     const float *dc;      // [3][stride]  f32(colors_dc)
     const void *sh;       // [48][stride] f32 or f64, coefficient-major (k*3 + c)
+    const double *op64;   // [stride]     f64 opacity (rsq, read-back)
     int sh_f32;
 };
 

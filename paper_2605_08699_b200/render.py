@@ -129,9 +129,24 @@ class DeviceScene:
         self.lib = lib
         self._finalizer = weakref.finalize(self, lib.gsr_scene_destroy, h)
 
+    @classmethod
+    def from_handle(cls, handle, device: int) -> "DeviceScene":
+        """Wrap a scene the library created (gsr_scene_create_ply)."""
+        sc = cls.__new__(cls)
+        sc.lib = _lib.load()
+        sc.handle = handle
+        sc.device = int(device)
+        sc.count = int(sc.lib.gsr_scene_count(handle))
+        sc._finalizer = weakref.finalize(sc, sc.lib.gsr_scene_destroy, handle)
+        return sc
+
+    @property
+    def closed(self) -> bool:
+        return not self._finalizer.alive
+
     @property
     def device_bytes(self) -> int:
-        return int(self.lib.gsr_scene_device_bytes(self.handle))
+        return 0 if self.closed else int(self.lib.gsr_scene_device_bytes(self.handle))
 
     def close(self):
         self._finalizer()
@@ -152,6 +167,9 @@ def device_scene(prims, device: int = 0) -> DeviceScene:
     """Upload-once cache keyed by the primitives object (registry record)."""
     if isinstance(prims, DeviceScene):
         return prims
+    own = getattr(prims, "scene", None)  # model.DeviceActivatedPrimitives (load_ply)
+    if isinstance(own, DeviceScene) and own.device == device and not own.closed:
+        return own
     key = (id(prims), device)
     sig = _signature(prims)
     with _scene_lock:
@@ -166,6 +184,9 @@ def device_scene(prims, device: int = 0) -> DeviceScene:
 
 def evict(prims, device: int | None = None) -> None:
     """Free the device copy of `prims` (model.py:394-408 eviction)."""
+    own = getattr(prims, "scene", None)
+    if isinstance(own, DeviceScene) and (device is None or own.device == device):
+        prims.release_device()  # PLY-loaded: arrays are read back first, then freed
     with _scene_lock:
         for k in [k for k in _scenes if k[0] == id(prims) and (device is None or k[1] == device)]:
             _scenes.pop(k)[1].close()

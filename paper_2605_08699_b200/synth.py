@@ -76,6 +76,27 @@ def ply_round_trip(raw: GaussianPrimitiveSet) -> GaussianPrimitiveSet:
                                 sh_coeffs=f(raw.sh_coeffs))
 
 
+PLY_REQUIRED = ("x", "y", "z", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2",
+                "rot_3", "opacity", "f_dc_0", "f_dc_1", "f_dc_2")   # model.py:31-36
+PLY_REST = tuple(f"f_rest_{i}" for i in range(45))
+
+
+def serialize_ply(prims: GaussianPrimitiveSet, include_rest: bool = True) -> bytes:
+    """synth.py:40-64: binary little-endian splat PLY (f_rest channel-major)."""
+    names = list(PLY_REQUIRED) + (list(PLY_REST) if include_rest else [])
+    header = ["ply", "format binary_little_endian 1.0", f"element vertex {prims.count}"]
+    header += [f"property float {name}" for name in names] + ["end_header"]
+    n = prims.count
+    cols = [np.asarray(prims.means).reshape(n, 3), np.asarray(prims.log_scales).reshape(n, 3),
+            np.asarray(prims.quaternions).reshape(n, 4),
+            np.asarray(prims.opacity_logits).reshape(n, 1),
+            np.asarray(prims.sh_coeffs)[:, 0, :].reshape(n, 3)]
+    if include_rest:
+        cols.append(np.asarray(prims.sh_coeffs)[:, 1:, :].transpose(0, 2, 1).reshape(n, -1))
+    table = np.concatenate(cols, axis=1).astype("<f4")
+    return ("\n".join(header) + "\n").encode("ascii") + table.tobytes()
+
+
 def activate(prims: GaussianPrimitiveSet) -> ActivatedPrimitives:
     """model.py:223-252."""
     from scipy.special import expit
@@ -168,5 +189,5 @@ def base_intrinsics_1080p():
 
 
 __all__ = ["ActivatedPrimitives", "GaussianPrimitiveSet", "make_synthetic_set",
-           "ply_round_trip", "activate", "synthetic_scene", "scale_range_for",
+           "ply_round_trip", "serialize_ply", "activate", "synthetic_scene", "scale_range_for",
            "pose_trace", "trace_to_csv", "ladder_1080p", "base_intrinsics_1080p"]
