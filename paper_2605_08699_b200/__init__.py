@@ -15,6 +15,8 @@ from .render import (DeviceScene, EncodeFailure, Framebuffer, RenderError, Rende
                      RenderStats,
                      decode_image, device_scene, encode_jpeg, encode_png, evict,
                      framebuffer_to_u8, render_framebuffer, render_u8, render_view, set_device)
+from .model import (DeviceActivatedPrimitives, MalformedHeader, MissingProperty, ModelError,
+                    NonFiniteAttribute, TruncatedBody, load_ply, parse_ply_header)
 from .registry import DeviceRegistry
 from .synth import ActivatedPrimitives
 
@@ -26,4 +28,6 @@ __all__ = [
     "device_scene", "encode_jpeg", "encode_png", "evict", "framebuffer_to_u8", "ladder_ssim",
     "pose_from_degrees", "psnr", "render_framebuffer", "render_u8", "render_view",
     "scale_intrinsics", "set_device", "ssim", "upscale_to", "world_to_camera",
+    "DeviceActivatedPrimitives", "MalformedHeader", "MissingProperty", "ModelError",
+    "NonFiniteAttribute", "TruncatedBody", "load_ply", "parse_ply_header",
 ]
