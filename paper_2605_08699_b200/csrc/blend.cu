@@ -110,8 +110,8 @@ __device__ __forceinline__ float expf_blend(float x, const unsigned long long *t
     const double r = __fma_rn(K.inv_ln2n, xd, -kd);
     unsigned long long t;  // tab[ki & 31] through a precomputed shared-window address
     asm("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(tab_s + ((ki & 31u) << 3)));
-    t += (unsigned long long)ki << 47;
-    const double sc = __longlong_as_double((long long)t);
+    // t + (ki << 47): only the high word changes (the low word of ki << 47 is 0)
+    const double sc = __hiloint2double((int)((uint32_t)(t >> 32) + (ki << 15)), (int)(uint32_t)t);
     const double z = __fma_rn(K.c0, r, K.c1);
     const double r2 = __dmul_rn(r, r);
     double y = __fma_rn(K.c2, r, 1.0);
@@ -138,38 +138,42 @@ struct WarpBatch {         // one warp's current 32 splats
 };
 
 // Each lane walks its own covering splats of the batch in depth order
-// (render.py:405-421, reference operation order).  (Software-pipelining the
-// next splat's alpha against the transmittance chain was measured slower:
-// the kernel is issue-bound, not latency-bound.)
+// (render.py:405-421, reference operation order).  The body is branch-free:
+// a lane with no splat left (or saturated) evaluates slot 31 of the batch (a
+// finite record: the batch is zeroed at kernel start) and its state is kept
+// by selects -- weight 0, transmittance factor 1 -- which costs less than
+// the divergence bookkeeping of an `if`.  (Software-pipelining the next
+// splat's alpha against the transmittance chain was measured slower: the
+// kernel is issue-bound, not latency-bound.)
 template <bool kChecked>
 __device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, const float4 *col,
                                           float fx, const unsigned long long *tab, uint32_t tab_s,
                                           const ExpK &ek, float &T, float &cr, float &cg,
                                           float &cb, uint32_t &n_comp) {
-    // (a lane that saturates drops its remaining bits; the caller derives
-    //  `done` from T, and the composite count from the dropped bits)
+    // composites done = bits taken: popc(mine) minus what saturation drops
     n_comp += __popc(mine);
+    uint32_t dropped = 0u;
     while (__any_sync(0xffffffffu, mine != 0u)) {
-        if (mine) {
-            const int s = __ffs(mine) - 1;
-            mine &= mine - 1u;
-            const float4 g = geo[s];  // u, ia, ib_dy, cy_term
-            const float4 k = col[s];  // op, r, g, b
-            const float dx = fx - g.x;
-            const float power = -0.5f * (g.y * dx * dx + g.z * dx + g.w);
-            float alpha = k.x * expf_blend<kChecked>(power, tab, tab_s, ek);
-            if (alpha > kAlphaMax) alpha = kAlphaMax;
-            const float weight = T * alpha;
-            cr += weight * k.y;
-            cg += weight * k.z;
-            cb += weight * k.w;
-            T = T * (1.0f - alpha);
-            if (T < kTStop) {
-                n_comp -= __popc(mine);
-                mine = 0u;
-            }
+        const bool act = mine != 0u;
+        const int s = __ffs(mine | 0x80000000u) - 1;
+        mine &= mine - 1u;
+        const float4 g = geo[s];  // u, ia, ib_dy, cy_term
+        const float4 k = col[s];  // op, r, g, b
+        const float dx = fx - g.x;
+        const float power = -0.5f * (g.y * dx * dx + g.z * dx + g.w);
+        float alpha = k.x * expf_blend<kChecked>(power, tab, tab_s, ek);
+        if (alpha > kAlphaMax) alpha = kAlphaMax;
+        const float weight = act ? T * alpha : 0.0f;
+        cr += weight * k.y;
+        cg += weight * k.z;
+        cb += weight * k.w;
+        T = T * (act ? 1.0f - alpha : 1.0f);
+        if (T < kTStop) {  // the pixel is done (the caller derives `done` from T)
+            dropped = mine;
+            mine = 0u;
         }
     }
+    n_comp -= __popc(dropped);
 }
 
 // Persistent kernel: the work items are (tile, pixel-row pair) = one warp's
@@ -185,6 +189,11 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+    {   // finite records in every slot (inactive lanes read slot 31)
+        float4 *z = reinterpret_cast<float4 *>(s_b);
+        for (int i = threadIdx.x; i < (int)(sizeof(s_b) / sizeof(float4)); i += blockDim.x)
+            z[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
     __syncthreads();
 
     const int tiles_x = (width + kTile - 1) / kTile;
