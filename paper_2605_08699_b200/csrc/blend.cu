@@ -132,21 +132,28 @@ __device__ __forceinline__ bool exp_safe(const float4 &A, const float4 &B) {
            ic < 1e30f && fabsf(ib) < 1e30f && rsq >= 0.0f && rsq <= 21.0f && ib * ib <= ia * ic;
 }
 
-struct WarpBatch {         // one warp's current 32 splats
-    float4 geo[2][32];     // per pixel row of the warp: (u, ia, (2*ib)*dy, (ic*dy)*dy)
-    float4 col[32];        // (op, r, g, b)
+struct WarpBatch {         // one warp's current 32 splats in slots 1..32; slot 0: null
+    float4 geo[2][33];     // per pixel row of the warp: (u, ia, (2*ib)*dy, (ic*dy)*dy)
+    float4 col[33];        // (op, r, g, b)
 };
 
 // Each lane walks its own covering splats of the batch in depth order
 // (render.py:405-421, reference operation order).  The body is branch-free:
-// a lane with no splat left (or saturated) evaluates slot 31 of the batch (a
-// finite record: the batch is zeroed at kernel start) and its state is kept
-// by selects -- weight 0, transmittance factor 1 -- which costs less than
-// the divergence bookkeeping of an `if`.  (Software-pipelining the next
+// a lane with no splat left (or saturated) gets index -1, the null slot in
+// front of the batch (all zero: power -0, alpha = 0 * 1 = 0, so rgb += 0
+// and T *= 1 exactly), which costs less than the divergence bookkeeping of
+// an `if` or select.  (Software-pipelining the next
 // splat's alpha against the transmittance chain was measured slower: the
 // kernel is issue-bound, not latency-bound.)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
 template <bool kChecked>
-__device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, const float4 *col,
+__device__ __forceinline__ void composite(uint32_t mine, uint32_t geo, uint32_t col,
                                           float fx, const unsigned long long *tab, uint32_t tab_s,
                                           const ExpK &ek, float &T, float &cr, float &cg,
                                           float &cb, uint32_t &n_comp) {
@@ -154,20 +161,19 @@ __device__ __forceinline__ void composite(uint32_t mine, const float4 *geo, cons
     n_comp += __popc(mine);
     uint32_t dropped = 0u;
     while (__any_sync(0xffffffffu, mine != 0u)) {
-        const bool act = mine != 0u;
-        const int s = __ffs(mine | 0x80000000u) - 1;
+        const int s = __ffs(mine) - 1;  // -1: null slot
         mine &= mine - 1u;
-        const float4 g = geo[s];  // u, ia, ib_dy, cy_term
-        const float4 k = col[s];  // op, r, g, b
+        const float4 g = lds128(geo + 16u * (uint32_t)s);  // u, ia, ib_dy, cy_term
+        const float4 k = lds128(col + 16u * (uint32_t)s);  // op, r, g, b
         const float dx = fx - g.x;
         const float power = -0.5f * (g.y * dx * dx + g.z * dx + g.w);
         float alpha = k.x * expf_blend<kChecked>(power, tab, tab_s, ek);
         if (alpha > kAlphaMax) alpha = kAlphaMax;
-        const float weight = act ? T * alpha : 0.0f;
+        const float weight = T * alpha;
         cr += weight * k.y;
         cg += weight * k.z;
         cb += weight * k.w;
-        T = T * (act ? 1.0f - alpha : 1.0f);
+        T = T * (1.0f - alpha);
         if (T < kTStop) {  // the pixel is done (the caller derives `done` from T)
             dropped = mine;
             mine = 0u;
@@ -189,7 +195,7 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
-    {   // finite records in every slot (inactive lanes read slot 31)
+    {   // zero records (the null slot is never written afterwards)
         float4 *z = reinterpret_cast<float4 *>(s_b);
         for (int i = threadIdx.x; i < (int)(sizeof(s_b) / sizeof(float4)); i += blockDim.x)
             z[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -201,7 +207,11 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int prow = lane >> 4;
     WarpBatch &B_ = s_b[w];
-    const float4 *geo = B_.geo[prow];
+    // shared-window addresses of slot 0 of this lane's rows, opaque to the
+    // compiler so they stay in registers across the composite loop
+    uint32_t geo, bcol;
+    asm volatile("mov.u32 %0, %1;" : "=r"(geo) : "r"((uint32_t)__cvta_generic_to_shared(&B_.geo[prow][1])));
+    asm volatile("mov.u32 %0, %1;" : "=r"(bcol) : "r"((uint32_t)__cvta_generic_to_shared(&B_.col[1])));
     // (opaque to the compiler, so the table base stays in a register instead
     //  of being rebuilt from the CTA id in the inner loop)
     uint32_t tab_s;
@@ -257,18 +267,18 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
                     safe = exp_safe(A, B);
                     const float ib2 = 2.0f * A.w;
                     const float dy0 = py0 - A.y, dy1 = py1 - A.y;
-                    B_.geo[0][lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
-                    B_.geo[1][lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
-                    B_.col[lane] = make_float4(B.z, C.x, C.y, C.z);
+                    B_.geo[0][1 + lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
+                    B_.geo[1][1 + lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
+                    B_.col[1 + lane] = make_float4(B.z, C.x, C.y, C.z);
                 }
             }
             __syncwarp();
             uint32_t mine = transpose32(mask, lane);
             if (done) mine = 0u;
             if (__all_sync(0xffffffffu, safe))
-                composite<false>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
+                composite<false>(mine, geo, bcol, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
             else
-                composite<true>(mine, geo, B_.col, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
+                composite<true>(mine, geo, bcol, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
             done = done || T < kTStop;
             __syncwarp();
         }
