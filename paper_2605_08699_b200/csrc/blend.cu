@@ -81,7 +81,7 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 // glibc expf constants (see common.cuh), in constant memory so the DFMAs take
 // them as operands instead of rematerialising 64-bit immediates per call
 __constant__ double kExpK[4] = {
-    0x1.71547652b82fep+0 * 32.0,                       // InvLn2N
+    -0.5 * 0x1.71547652b82fep+0 * 32.0,                // -0.5 * InvLn2N (see expf_blend)
     0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0,         // C0
     0x1.ebfce50fac4f3p-3 / 32.0 / 32.0,                // C1
     0x1.62e42ff0c52d6p-1 / 32.0,                       // C2
@@ -98,16 +98,20 @@ struct ExpK {
     double inv_ln2n, c0, c1, c2;
 };
 
+// expf(-0.5f * q) for the quadratic form q.  -0.5f * q is exact in f32
+// (short of underflow, where both give 1.0f), so the factor is folded into
+// the f64 constant: InvLn2N * (-0.5 q) == (-0.5 InvLn2N) * q exactly, and
+// |-0.5 q| < 88 <=> |q| < 176.
 template <bool kChecked>
-__device__ __forceinline__ float expf_blend(float x, const unsigned long long *tab,
+__device__ __forceinline__ float expf_blend(float q, const unsigned long long *tab,
                                             uint32_t tab_s, const ExpK &K) {
-    if (kChecked && !(fabsf(x) < 88.0f)) return expf_special(x, tab);
+    if (kChecked && !(fabsf(q) < 176.0f)) return expf_special(-0.5f * q, tab);
     const double kShift = 0x1.8p+52;
-    const double xd = (double)x;
-    double kd = __fma_rn(K.inv_ln2n, xd, kShift);
+    const double qd = (double)q;
+    double kd = __fma_rn(K.inv_ln2n, qd, kShift);  // K.inv_ln2n = -0.5 * InvLn2N
     const uint32_t ki = (uint32_t)__double2loint(kd);
     kd = __dsub_rn(kd, kShift);
-    const double r = __fma_rn(K.inv_ln2n, xd, -kd);
+    const double r = __fma_rn(K.inv_ln2n, qd, -kd);
     unsigned long long t;  // tab[ki & 31] through a precomputed shared-window address
     asm("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(tab_s + ((ki & 31u) << 3)));
     // t + (ki << 47): only the high word changes (the low word of ki << 47 is 0)
@@ -132,7 +136,7 @@ __device__ __forceinline__ bool exp_safe(const float4 &A, const float4 &B) {
            ic < 1e30f && fabsf(ib) < 1e30f && rsq >= 0.0f && rsq <= 21.0f && ib * ib <= ia * ic;
 }
 
-struct WarpBatch {         // one warp's current 32 splats in slots 1..32; slot 0: null
+struct WarpBatch {         // one warp's current 32 splats, splat j in slot 32 - j; slot 0: null
     float4 geo[2][33];     // per pixel row of the warp: (u, ia, (2*ib)*dy, (ic*dy)*dy)
     float4 col[33];        // (op, r, g, b)
 };
@@ -161,13 +165,18 @@ __device__ __forceinline__ void composite(uint32_t mine, uint32_t geo, uint32_t 
     n_comp += __popc(mine);
     uint32_t dropped = 0u;
     while (__any_sync(0xffffffffu, mine != 0u)) {
-        const int s = __ffs(mine) - 1;  // -1: null slot
-        mine &= mine - 1u;
+        // mine is bit-reversed (splat j <-> bit 31 - j <-> slot 31 - j), so the
+        // next splat in depth order is the highest set bit; -1: null slot
+        const int s = 31 - __clz(mine);
+        uint32_t below;  // bits [0, s): clears bit s (mine = 0 stays 0)
+        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"((uint32_t)s));
+        mine &= below;
         const float4 g = lds128(geo + 16u * (uint32_t)s);  // u, ia, ib_dy, cy_term
         const float4 k = lds128(col + 16u * (uint32_t)s);  // op, r, g, b
         const float dx = fx - g.x;
-        const float power = -0.5f * (g.y * dx * dx + g.z * dx + g.w);
-        float alpha = k.x * expf_blend<kChecked>(power, tab, tab_s, ek);
+        // power = -0.5f * q (render.py:405-406), applied inside expf_blend
+        const float q = g.y * dx * dx + g.z * dx + g.w;
+        float alpha = k.x * expf_blend<kChecked>(q, tab, tab_s, ek);
         if (alpha > kAlphaMax) alpha = kAlphaMax;
         const float weight = T * alpha;
         cr += weight * k.y;
@@ -267,13 +276,13 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
                     safe = exp_safe(A, B);
                     const float ib2 = 2.0f * A.w;
                     const float dy0 = py0 - A.y, dy1 = py1 - A.y;
-                    B_.geo[0][1 + lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
-                    B_.geo[1][1 + lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
-                    B_.col[1 + lane] = make_float4(B.z, C.x, C.y, C.z);
+                    B_.geo[0][32 - lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
+                    B_.geo[1][32 - lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
+                    B_.col[32 - lane] = make_float4(B.z, C.x, C.y, C.z);
                 }
             }
             __syncwarp();
-            uint32_t mine = transpose32(mask, lane);
+            uint32_t mine = __brev(transpose32(mask, lane));
             if (done) mine = 0u;
             if (__all_sync(0xffffffffu, safe))
                 composite<false>(mine, geo, bcol, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
