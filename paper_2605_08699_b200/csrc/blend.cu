@@ -26,6 +26,7 @@
 // given splat covers).  Warps leave as soon as all their 32 pixels are
 // saturated (warp-vote early termination); no block barriers in the loop.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -339,6 +340,12 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel, kBlendThreads, 0);
+        // GSR_BLEND_CTAS_PER_SM (tuning): fewer resident CTAs leave room for
+        // other frames' kernels when several frames are in flight
+        if (const char *e = getenv("GSR_BLEND_CTAS_PER_SM")) {
+            const int v = atoi(e);
+            if (v > 0 && v < per_sm) per_sm = v;
+        }
         g_blend_grid = sms * (per_sm > 0 ? per_sm : 1);
     }
     const int tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);

@@ -73,7 +73,10 @@ void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_deg
 cudaError_t radix_init_attributes();
 constexpr int kRadixThreads = 256;
 // items per thread (8: keeps <= 64 registers, 4 blocks / 32 warps per SM)
-constexpr int radix_items(int key_bytes) { return key_bytes == 8 ? 8 : 8; }
+#ifndef GSR_RADIX_ITEMS
+#define GSR_RADIX_ITEMS 8
+#endif
+constexpr int radix_items(int key_bytes) { return key_bytes == 8 ? 8 : GSR_RADIX_ITEMS; }
 inline int64_t radix_tiles(int64_t n_cap, int key_bytes) {
     const int64_t tile = (int64_t)kRadixThreads * radix_items(key_bytes);
     return (n_cap + tile - 1) / tile;

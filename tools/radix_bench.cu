@@ -54,7 +54,7 @@ static void run(const char *name, int64_t n, int passes, bool drop, unsigned lon
         check(cudaMemcpy(v0, hv.data(), n * 4, cudaMemcpyHostToDevice), "c");
         cudaEventRecord(e0);
         launch_onesweep_sort<K>(k0, k1, v0, v1, false, drop, nd, n, n, passes, true, work, sched,
-                                nullptr, 148, 0);
+                                nullptr, 148, 0, KMark(), SpanKeys());
         cudaEventRecord(e1);
         check(cudaEventSynchronize(e1), "sync");
         float ms;
@@ -96,9 +96,8 @@ static void run(const char *name, int64_t n, int passes, bool drop, unsigned lon
 }
 
 int main() {
-    run<uint32_t>("u32 tile-like (13 bit)", 31000000, 2, false, 8191, 5);
-    run<uint32_t>("u32 tile-like 1 pass", 31000000, 1, false, 255, 5);
+    run<uint32_t>("u32 depth span keys (24 bit)", 2650000, 3, false, (1u << 24) - 1, 10);
+    run<uint32_t>("u32 span keys 6M", 5300000, 3, false, (1u << 24) - 1, 10);
     run<unsigned long long>("u64 depth-like (56 bit)", 3000000, 7, false, (1ull << 56) - 1, 5);
-    run<unsigned long long>("u64 depth-like 6M", 6000000, 7, false, (1ull << 56) - 1, 5);
     return 0;
 }
