@@ -18,3 +18,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --n
 python tools/launch_summary.py gpurun_out/launches.csv 1 | tee gpurun_out/launches.txt
 timeout 900 python bench.py --steps 200 --warmup 10 2>&1 | tail -1 > gpurun_out/bench.json
 cat gpurun_out/bench.json
+# K10 (PLY load): one ncu --set full capture of the activation kernel of a 3M load
+timeout 600 ncu --set full --clock-control none -k regex:ply_activate -s 3 -c 1 \
+  -o gpurun_out/ply_full -f python tools/ply_bench.py 3000000 1 > gpurun_out/ncu_ply.log 2>&1
+python tools/ncu_summary.py gpurun_out/ply_full.ncu-rep > gpurun_out/ncu_ply_summary.txt 2>&1
+head -40 gpurun_out/ncu_ply_summary.txt
