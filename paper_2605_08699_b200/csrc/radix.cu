@@ -110,20 +110,37 @@ __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
         shift = bits > a.span.bits ? bits - a.span.bits : 0;
         kcap = (1ull << a.span.bits) - 1ull;
     }
-    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        K k;
-        if (sizeof(K) == 4 && a.span.src) {  // span key of the depth bits
-            const unsigned long long k64 = a.span.src[i];
-            const unsigned long long q = (k64 - kmin) >> shift;
-            k = k64 == ~0ull ? sentinel<K>() : (K)(q < kcap ? q : kcap);
-            a.keys[0][i] = k;
-        } else {
-            k = keys[i];
-        }
-        if (a.drop_sentinel && k == sentinel<K>()) continue;
+    // kHU keys per thread per step, all loads issued before any use (the
+    // loop is otherwise one global latency per key)
+    constexpr int kHU = 8;
+    const int64_t stride = (int64_t)gridDim.x * RB;
+    for (int64_t i0 = (int64_t)blockIdx.x * RB + threadIdx.x; i0 < n; i0 += stride * kHU) {
+        K kk[kHU];
+        unsigned long long k64[kHU];
+        const bool span = sizeof(K) == 4 && a.span.src;
 #pragma unroll
-        for (int p = 0; p < (int)sizeof(K); p++)
-            if (p < a.passes) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 255u], 1u);
+        for (int u = 0; u < kHU; u++) {
+            const int64_t i = i0 + u * stride;
+            if (span) k64[u] = i < n ? a.span.src[i] : ~0ull;
+            else kk[u] = i < n ? keys[i] : sentinel<K>();
+        }
+#pragma unroll
+        for (int u = 0; u < kHU; u++) {
+            const int64_t i = i0 + u * stride;
+            if (i >= n) continue;
+            K k;
+            if (span) {  // span key of the depth bits
+                const unsigned long long q = (k64[u] - kmin) >> shift;
+                k = k64[u] == ~0ull ? sentinel<K>() : (K)(q < kcap ? q : kcap);
+                a.keys[0][i] = k;
+            } else {
+                k = kk[u];
+            }
+            if (a.drop_sentinel && k == sentinel<K>()) continue;
+#pragma unroll
+            for (int p = 0; p < (int)sizeof(K); p++)
+                if (p < a.passes) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 255u], 1u);
+        }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < a.passes * 256; j += RB) {
