@@ -507,18 +507,43 @@ __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
         for (uint32_t e = 0; e < n; e++) atomicOr(&mask[a0 + e], 1u << lane);
         __syncwarp();
         // 2: position = cursor + earlier (lower-rank) lanes covering the column
-        //    (and remember the columns this lane is the highest covering lane of)
-        uint32_t top = 0;
+        //    (and remember the columns this lane is the highest covering lane
+        //    of; the first kKeep of them with their new cursor, in registers)
+        constexpr int kKeep = 4;
+        uint32_t top = 0, kt[kKeep], kc[kKeep];
+        int nkeep = 0;
+#pragma unroll
+        for (int q = 0; q < kKeep; q++) kt[q] = kc[q] = 0u;
         for (uint32_t e = 0; e < n; e++) {
             const uint32_t t = a0 + e;
             const uint32_t m = mask[t];
-            const uint32_t pos = cur[t] + __popc(m & lt_mask);
+            const uint32_t c = cur[t];
+            const uint32_t pos = c + __popc(m & lt_mask);
             if ((int64_t)pos < a.cap_d) a.tile_vals[pos] = rank;
-            if ((m >> lane) == 1u) top |= e < 32 ? 1u << e : 0u;
+            if ((m >> lane) == 1u) {
+                if (nkeep < kKeep) {  // shift register (static indices)
+#pragma unroll
+                    for (int q = kKeep - 1; q > 0; q--) {
+                        kt[q] = kt[q - 1];
+                        kc[q] = kc[q - 1];
+                    }
+                    kt[0] = t;
+                    kc[0] = c + __popc(m);
+                    nkeep++;
+                } else {
+                    top |= e < 32 ? 1u << e : 0u;
+                }
+            }
         }
         __syncwarp();
         // 3: the highest covering lane of each column advances its cursor and
         //    clears its mask (only that lane touches the column in this phase)
+#pragma unroll
+        for (int q = 0; q < kKeep; q++)
+            if (q < nkeep) {
+                cur[kt[q]] = kc[q];
+                mask[kt[q]] = 0;
+            }
         for (uint32_t bits = top; bits; bits &= bits - 1u) {
             const uint32_t t = a0 + (uint32_t)(__ffs(bits) - 1);
             cur[t] += __popc(mask[t]);
