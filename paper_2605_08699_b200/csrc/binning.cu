@@ -35,8 +35,8 @@ namespace gsr {
 
 namespace {
 
-constexpr int BR = 256;          // depth ranks per block (stages 1a, 1c)
-constexpr int kPairCache = 4096; // per-block pair results kept in smem (1c)
+constexpr int BR = 512;          // depth ranks per block (stages 1a, 1c)
+constexpr int kPairCache = 6144; // per-block pair results kept in smem (1c)
 constexpr int kSeg = 1024;       // pairs per segment (stage 2)
 constexpr int kRowsMax = kMaxTileRows;
 
