@@ -2,6 +2,7 @@
 # the depth-tie / overflow paths: memcheck (device memory errors) and
 # racecheck / synccheck (shared-memory hazards, barrier misuse).
 mkdir -p gpurun_out
+rm -f gpurun_out/sanitizer_summary.txt
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 cat > /tmp/san_case.py <<'PY'
 import sys
@@ -22,6 +23,11 @@ for i in range(3):
     pipe.submit(prims, g.CameraPose(0.01 * i, 0.0))
 pipe.drain()
 pipe.close()
+# PLY load on the device (K10) + a render from the loaded scene
+from paper_2605_08699_b200.synth import make_synthetic_set, serialize_ply
+dp = g.load_ply(serialize_ply(make_synthetic_set(count=5000, seed=4, include_rest=True)))
+g.render_u8(dp, g.CameraPose(0.0, 0.0), intr, sh_degree=3)
+_ = dp.scales, dp.colors_dc, dp.sh_coeffs
 print("case ok", len(jp), round(s, 6))
 PY
 for tool in memcheck racecheck synccheck; do
