@@ -185,3 +185,26 @@ def test_gpu_load_ply_evict_keeps_arrays():
     arrays = _arrays()
     assert _same_bits(prims.scales, arrays["random_rest_33/scales"])
     assert render.device_scene(prims, prims.device) is not sc  # re-uploaded from host arrays
+
+
+@pytest.mark.gpu
+def test_gpu_load_ply_wide_rows_and_column_order():
+    """Rows too wide for shared-memory staging (> 384 properties: the direct
+    kernel variant), properties in a shuffled order with extras: bit-exact
+    vs the oracle."""
+    from paper_2605_08699_b200 import model
+    rng = np.random.default_rng(9)
+    names = list(oracle.PLY_REQUIRED + oracle.PLY_REST) + [f"extra_{i}" for i in range(360)]
+    rng.shuffle(names)
+    n = 3000
+    table = rng.normal(size=(n, len(names))).astype("<f4")
+    col = {p: i for i, p in enumerate(names)}
+    table[:, col["opacity"]] *= 6.0
+    header = ["ply", "format binary_little_endian 1.0", f"element vertex {n}"]
+    header += [f"property float {p}" for p in names] + ["end_header"]
+    data = ("\n".join(header) + "\n").encode("ascii") + table.tobytes()
+    prims = model.load_ply(data)
+    want = oracle.ply_load(data)
+    for a in ATTRS[:-1]:
+        assert _same_bits(getattr(prims, a), want[a]), a
+    assert _same_bits(_read(prims, 6), want["rsq"])
