@@ -71,8 +71,11 @@ void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_deg
 
 // radix.cu: Onesweep stable LSD sort (see radix.cu header)
 cudaError_t radix_init_attributes();
-constexpr int kRadixThreads = 256;
-// items per thread (8: keeps <= 64 registers, 4 blocks / 32 warps per SM)
+#ifndef GSR_RADIX_THREADS
+#define GSR_RADIX_THREADS 512
+#endif
+constexpr int kRadixThreads = GSR_RADIX_THREADS;  // >= 256 (one thread per digit)
+// items per thread (8: keeps <= 64 registers; 512 threads: 2 blocks / 32 warps per SM)
 #ifndef GSR_RADIX_ITEMS
 #define GSR_RADIX_ITEMS 8
 #endif
