@@ -62,10 +62,12 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
         const uint32_t *order = a.depth_sched[16] ? a.order1 : a.order0;
         const uint32_t i = __ldg(order + r);
         const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b);
-        a.srec[r].a = A;
-        a.srec[r].b = B;
         int lo, hi;
         row_range(A.y, B.w, a.height, lo, hi);
+        a.srec[r].a = A;
+        a.srec[r].b = make_float4(B.x, B.y, B.z,
+                                  pack_rows(lo, hi, a.height, splat_fast_ok(A.y, A.z, A.w),
+                                            exp_safe(A, B)));
         if (lo < hi)
             for (int ty = lo / kTile; ty <= (hi - 1) / kTile; ty++) atomicAdd(&cnt[ty], 1u);
     }
@@ -166,8 +168,9 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     int lo = 0, hi = 0;
     if (r < k) {
         const float4 A = __ldg(&a.srec[r].a), B = __ldg(&a.srec[r].b);
-        S.rinv[tid] = splat_fast_ok(A.y, A.z, A.w) ? __frcp_rn(A.z) : 0.0f;
-        row_range(A.y, B.w, a.height, lo, hi);
+        bool fast, esafe;
+        unpack_rows(B.w, lo, hi, fast, esafe);
+        S.rinv[tid] = fast ? __frcp_rn(A.z) : 0.0f;
         S.u[tid] = A.x;
         S.v[tid] = A.y;
         S.ia[tid] = A.z;

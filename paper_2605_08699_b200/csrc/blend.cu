@@ -125,17 +125,6 @@ __device__ __forceinline__ float expf_blend(float q, const unsigned long long *t
     return __double2float_rn(y);
 }
 
-// A splat whose record is finite with ia <= 4, rsq <= 21 and ib^2 <= ia*ic
-// cannot give |power| >= 88 on any pixel of its mask: on a pixel row, the
-// quadratic form is rsq at the interval ends (mid -+ span), the mask reaches at
-// most 1.5 px beyond them, and ia*span = sqrt(disc) <= sqrt(ia*rsq), so
-// Q <= rsq + 3*sqrt(ia*rsq) + 2.25*ia < 53, |power| < 27.  Batches of such
-// splats skip glibc's |x| >= 88 special cases.
-__device__ __forceinline__ bool exp_safe(const float4 &A, const float4 &B) {
-    const float u = A.x, v = A.y, ia = A.z, ib = A.w, ic = B.x, rsq = B.y;
-    return fabsf(u) < 1e30f && fabsf(v) < 1e30f && ia > 0.0f && ia <= 4.0f && ic > 0.0f &&
-           ic < 1e30f && fabsf(ib) < 1e30f && rsq >= 0.0f && rsq <= 21.0f && ib * ib <= ia * ic;
-}
 
 struct WarpBatch {         // one warp's current 32 splats, splat j in slot 32 - j; slot 0: null
     float4 geo[2][33];     // per pixel row of the warp: (u, ia, (2*ib)*dy, (ic*dy)*dy)
@@ -264,9 +253,9 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
                 const float4 A = __ldg(&srec[r].a);
                 const float4 B = __ldg(&srec[r].b);
                 const uint32_t gi = __ldg(order + r);  // issued with the record loads
-                int lo, hi;
-                row_range(A.y, B.w, height, lo, hi);
-                const bool fast = splat_fast_ok(A.y, A.z, A.w);
+                int lo, hi;  // precomputed per frame by bin_gather (SplatRec.b.w)
+                bool fast, esafe;
+                unpack_rows(B.w, lo, hi, fast, esafe);
                 const float rinv = fast ? __frcp_rn(A.z) : 0.0f;
                 n_rows += (uint32_t)(iy0 >= lo && iy0 < hi) +
                           (uint32_t)(iy0 + 1 >= lo && iy0 + 1 < hi);
@@ -274,7 +263,7 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
                        (row_mask(A, B, rinv, fast, iy0 + 1, lo, hi, X, width) << 16);
                 if (mask) {  // render.py:400-402 terms per pixel row
                     const float4 C = __ldg(col + gi);  // (r, g, b)
-                    safe = exp_safe(A, B);
+                    safe = esafe;
                     const float ib2 = 2.0f * A.w;
                     const float dy0 = py0 - A.y, dy1 = py1 - A.y;
                     B_.geo[0][32 - lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);

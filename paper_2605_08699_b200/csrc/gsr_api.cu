@@ -834,6 +834,9 @@ int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera 
         std::vector<SplatRec> r((size_t)k);
         std::vector<uint32_t> o((size_t)k);
         std::vector<float4> col((size_t)scene->n);
+        std::vector<SplatRec> geo((size_t)scene->n);  // by Gaussian index: b.w = ry
+        GSR_CUDA_OK(cudaMemcpy(geo.data(), ctx->geo.p, sizeof(SplatRec) * scene->n,
+                               cudaMemcpyDeviceToHost));
         const DevBuf &vb = ctx->vals[ctx->hsched[16] & 1u];
         GSR_CUDA_OK(cudaMemcpy(r.data(), ctx->srec.p, sizeof(SplatRec) * k, cudaMemcpyDeviceToHost));
         GSR_CUDA_OK(cudaMemcpy(o.data(), vb.p, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost));
@@ -844,7 +847,7 @@ int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera 
             const SplatRec &s = r[i];
             const float4 &cc = col[o[i]];
             p[0] = s.a.x; p[1] = s.a.y; p[2] = s.a.z; p[3] = s.a.w; p[4] = s.b.x; p[5] = s.b.y;
-            p[6] = cc.x; p[7] = cc.y; p[8] = cc.z; p[9] = s.b.z; p[10] = s.b.w;
+            p[6] = cc.x; p[7] = cc.y; p[8] = cc.z; p[9] = s.b.z; p[10] = geo[o[i]].b.w;
         }
     }
     fill_stats(ctx, scene, stats);
