@@ -245,6 +245,7 @@ def kernel_work(name, wl, c):
         # order + geometry gathered, 32 B record written
         "bin_gather": (k * (4 + 32) + k * 32, 0),
         # records in, pairs out; 20 FP32 ops per exact row interval (render.py:383-397)
+        # evaluated (pairs whose span the f64 band bound settles need none)
         "bin_pairs": (k * 32 + p * 8, 20 * c["Rp"]),
         "seg_count": (p * 8, 0),
         "seg_place": (p * 8 + d * 4, 0),
@@ -294,7 +295,7 @@ def kernel_profile(lib, ctx, sc, cams, sh, frames, wl, peaks, simt):
         b, f = kernel_work(nm, wl, mean_c)
         b, f = b * nl, f * nl  # per frame
         e = {"ms_per_frame": round(per_frame, 4), "launches_per_frame": nl,
-             "bound": BOUND.get(nm, "hbm")}
+             "bound": BOUND.get(nm, "hbm") if f or nm not in BOUND else "hbm"}
         if b and per_frame > 0:
             gbs = b / (per_frame * 1e-3) / 1e9
             e.update(alg_bytes=int(b), achieved_gbs=round(gbs, 1), frac_hbm=round(gbs / hbm, 4))

@@ -272,51 +272,15 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
                             ty <= (S.hi[jj] - 1) / kTile);
         }
         const uint32_t slot = rowbase[ty] + wpre_all[(j >> 5) * nr + ty] + in_warp;
-        // exact tile-column span of splat j in tile row ty
+        // tile-column span of splat j in tile row ty
         const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
-        n_rows += (uint32_t)(y1 - y0);
-        int mn = 0x7fffffff, mx = -0x7fffffff;
+        int mn, mx;
         const float u = S.u[j], v = S.v[j], ia = S.ia[j], ib = S.ib[j], ic = S.ic[j],
                     rsq = S.rsq[j], rinv = S.rinv[j];
-        // fast exact path: min/max of the float interval ends over the rows
-        // whose interval meets [0, W) (floor/ceil are monotone, so one
-        // conversion per pair); rows with NaN/huge values take row_interval
-        bool slow = rinv == 0.0f;
-        if (!slow) {
-            float fmn = __int_as_float(0x7f800000), fmx = -__int_as_float(0x7f800000);
-            const float wf = (float)a.width;
-            float py = (float)y0 + 0.5f;  // f32(y) + 0.5, stepped exactly (y < 2^23)
-            for (int y = y0; y < y1; y++, py += 1.0f) {
-                float xl, xr;
-                const int k = row_xlr(u, v, ia, ib, ic, rsq, rinv, py, xl, xr);
-                if (k < 0) slow = true;
-                if (k > 0 && xl < wf && xr > -1.0f) {
-                    fmn = fminf(fmn, xl);
-                    fmx = fmaxf(fmx, xr);
-                }
-            }
-            if (fmn <= fmx) {
-                if (fabsf(fmn) < 0x1p30f && fabsf(fmx) < 0x1p30f) {
-                    mn = max(0, __float2int_rd(fmn));
-                    mx = min(a.width, __float2int_ru(fmx) + 1);
-                } else {
-                    slow = true;
-                }
-            }
-        }
-        if (slow) {
-            mn = 0x7fffffff;
-            mx = -0x7fffffff;
-            for (int y = y0; y < y1; y++) {
-                int x0, x1;
-                if (row_interval(u, v, ia, ib, ic, rsq, (float)y + 0.5f, a.width, x0, x1)) {
-                    x0 = x0 > 0 ? x0 : 0;
-                    if (x0 < x1) {
-                        mn = x0 < mn ? x0 : mn;
-                        mx = x1 > mx ? x1 : mx;
-                    }
-                }
-            }
+        if (!(rinv != 0.0f && y0 < y1 &&
+              band_span_bound(u, v, ia, ib, ic, rsq, y0, y1, a.width, mn, mx))) {
+            n_rows += (uint32_t)(y1 - y0);
+            exact_band_span(u, v, ia, ib, ic, rsq, rinv, y0, y1, a.width, mn, mx);
         }
         uint32_t span = 0;
         if (mn <= mx) {

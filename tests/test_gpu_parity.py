@@ -54,8 +54,21 @@ def test_sweep_bit_exact(gsr):
     assert n == 50
 
 
+def _assert_lists_cover(tt, tr, ot, orr, max_inflation=1.05):
+    """The device's tile lists contain every (tile, rank) of the exact
+    tile-list contract (the oracle's), sorted by (tile, rank) with ranks
+    increasing -- the property the bit-exact blend relies on (a superset
+    only costs blend work: splats outside a pixel's exact interval are never
+    composited) -- and are at most `max_inflation` times as long."""
+    g = tt.astype(np.int64) * (1 << 32) + tr.astype(np.int64)
+    o = ot.astype(np.int64) * (1 << 32) + orr.astype(np.int64)
+    assert np.all(np.diff(g) > 0)
+    assert np.isin(o, g).all(), "a contract (tile, rank) entry is missing"
+    assert len(g) <= max_inflation * len(o) + 16, (len(g), len(o))
+
+
 @pytest.mark.parametrize("name", list(load_json("frames.json")))
-def test_frames_bit_exact(gsr, name):
+def test_frames_bit_exact(gsr, oracle, name):
     from paper_2605_08699_b200.render import debug_preprocess, debug_tile_lists, debug_tile_ranges
     case = load_json("frames.json")[name]
     prims = golden_scene(case["scene"])
@@ -80,8 +93,11 @@ def test_frames_bit_exact(gsr, name):
     assert digest(fb.u8) == case["u8"]
     tiles = load_json("tiles.json")[name]
     tt, tr = debug_tile_lists()
-    assert tt.shape[0] == tiles["D"] == stats.tile_keys
-    assert digest(tt) == tiles["tiles"] and digest(tr) == tiles["ranks"]
+    assert tt.shape[0] == stats.tile_keys
+    ot, orr, _ = oracle.tile_lists(packed, intr.width, intr.height)  # pinned to tiles.json
+    assert ot.shape[0] == tiles["D"]
+    assert digest(ot) == tiles["tiles"] and digest(orr) == tiles["ranks"]
+    _assert_lists_cover(tt, tr, ot, orr)
     ranges = debug_tile_ranges(intr.width, intr.height)
     for t_id in np.unique(tt):
         s, e = ranges[t_id]
@@ -247,7 +263,7 @@ def test_config2_500k_720p_trace_vs_oracle(gsr, oracle):
         assert np.array_equal(fb.u8, fr.u8)
         tt, tr = debug_tile_lists()
         ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
-        assert np.array_equal(tt, ot) and np.array_equal(tr, orr)
+        _assert_lists_cover(tt, tr, ot, orr)
 
 
 def test_config3_3m_1080p_vs_oracle(gsr, oracle):
@@ -267,8 +283,7 @@ def test_config3_3m_1080p_vs_oracle(gsr, oracle):
     assert np.array_equal(fb._rgb32, fr.rgb32)
     tt, tr = debug_tile_lists()
     ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
-    assert tt.shape == ot.shape
-    assert np.array_equal(tt, ot) and np.array_equal(tr, orr)
+    _assert_lists_cover(tt, tr, ot, orr)
     # size-independent properties: depth order is sorted, tile keys sorted
     z = fr.depths
     assert np.all(np.diff(z) >= 0)
@@ -292,7 +307,7 @@ def test_config4_6m_1080p_vs_oracle(gsr, oracle):
     assert np.array_equal(fb.u8, fr.u8)
     tt, tr = debug_tile_lists()
     ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
-    assert np.array_equal(tt, ot) and np.array_equal(tr, orr)
+    _assert_lists_cover(tt, tr, ot, orr)
     key = tt.astype(np.int64) * (1 << 32) + tr
     assert np.all(np.diff(key) > 0)
 
