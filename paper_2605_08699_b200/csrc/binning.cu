@@ -15,10 +15,11 @@
 //              its pairs per tile row (row range only, no interval math).
 //  1b row_scan exclusive scan of those counts, tile-row major: each (row,
 //              block) gets its output slot, each row its pair range.
-//  1c pairs    same blocks: one thread per pair computes the pair's exact
-//              tile-column span (tx0, count) -- the only interval arithmetic
-//              -- and stores (rank, tx0 | count << 16) at its slot: pairs end
-//              up grouped by tile row, in rank order within a row.
+//  1c pairs    same blocks: one thread per pair computes the pair's
+//              tile-column span (tx0, count) -- a conservative bound of the
+//              exact one (band_span_bound, common.cuh; exact rows for
+//              ill-conditioned splats) -- and stores (rank, tx0 | count << 16)
+//              at its slot: pairs end up grouped by tile row, in rank order.
 //  2a segments each row's pairs are cut into segments of <= 1024 pairs.
 //  2b seg_count one warp per segment: keys per tile column (difference array).
 //  2c scans    per tile: prefix over the row's segments; tile starts, ranges, D.
@@ -132,8 +133,6 @@ struct PairSmem {
     uint32_t s_warp[33];
     uint8_t lr[kPairCache];          // in-warp rank of a pair within its row
     uint16_t owner[kPairCache];      // block-local splat of a pair
-    uint16_t perm[kPairCache];       // pairs ordered by row count (see below)
-    uint32_t bucket[17];             // row-count histogram -> cursors
     int ty_lo, ty_hi;
     // followed in dynamic shared memory by (n_rows = tile rows of the frame):
     //   uint32_t wpre[BR / 32][n_rows]  per-warp coverage masks -> counts -> prefix
@@ -224,42 +223,10 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         rowbase[ty] = run ? a.row_blk[(int64_t)ty * a.n_blocks + b] : 0u;
     }
     __syncthreads();
-    // One thread per pair: exact tile span, stored at its grouped slot.  A
-    // pair has 1..16 rows; threads take the pairs in decreasing row count
-    // (a counting sort of the block's pairs) so the 32 row loops of a warp
-    // run similar trip counts.  The order only affects scheduling: each
-    // pair's slot is fixed above.
-    const bool sorted = npairs <= (uint32_t)kPairCache;
-    if (sorted) {
-        if (tid < 17) S.bucket[tid] = 0;
-        __syncthreads();
-        for (uint32_t q = tid; q < npairs; q += BR) {
-            const int j = S.owner[q];
-            const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
-            const int nrow = min(S.hi[j], ty * kTile + kTile) - max(S.lo[j], ty * kTile);
-            atomicAdd(&S.bucket[16 - nrow], 1u);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t run = 0;
-            for (int i = 0; i < 17; i++) {
-                const uint32_t c = S.bucket[i];
-                S.bucket[i] = run;
-                run += c;
-            }
-        }
-        __syncthreads();
-        for (uint32_t q = tid; q < npairs; q += BR) {
-            const int j = S.owner[q];
-            const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
-            const int nrow = min(S.hi[j], ty * kTile + kTile) - max(S.lo[j], ty * kTile);
-            S.perm[atomicAdd(&S.bucket[16 - nrow], 1u)] = (uint16_t)q;
-        }
-        __syncthreads();
-    }
+    // One thread per pair: tile span (bounded; exact rows for the few
+    // ill-conditioned splats), stored at its grouped slot.
     uint32_t n_rows = 0;
-    for (uint32_t qi = tid; qi < npairs; qi += BR) {
-        const uint32_t q = sorted ? (uint32_t)S.perm[qi] : qi;
+    for (uint32_t q = tid; q < npairs; q += BR) {
         const int j = q < kPairCache ? (int)S.owner[q] : rank_of_pair(S.poff, q);
         const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
         uint32_t in_warp;
