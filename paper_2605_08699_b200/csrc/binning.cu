@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
                                   pack_rows(lo, hi, a.height, splat_fast_ok(A.y, A.z, A.w),
                                             exp_safe(A, B)));
         if (lo < hi)
-            for (int ty = lo / kTile; ty <= (hi - 1) / kTile; ty++) atomicAdd(&cnt[ty], 1u);
+            for (int ty = lo / kTileH; ty <= (hi - 1) / kTileH; ty++) atomicAdd(&cnt[ty], 1u);
     }
     __syncthreads();
     const int64_t nb = a.n_blocks;
@@ -176,11 +176,11 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         S.ib[tid] = A.w;
         S.ic[tid] = B.x;
         S.rsq[tid] = B.y;
-        if (lo < hi) ntr = (uint32_t)((hi - 1) / kTile - lo / kTile + 1);
+        if (lo < hi) ntr = (uint32_t)((hi - 1) / kTileH - lo / kTileH + 1);
     }
     S.lo[tid] = lo;
     S.hi[tid] = hi;
-    const int t0 = ntr ? lo / kTile : 0x7fffffff, t1 = ntr ? (hi - 1) / kTile : -1;
+    const int t0 = ntr ? lo / kTileH : 0x7fffffff, t1 = ntr ? (hi - 1) / kTileH : -1;
     if (tid == 0) {
         S.ty_lo = 0x7fffffff;
         S.ty_hi = -1;
@@ -228,19 +228,19 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     uint32_t n_rows = 0;
     for (uint32_t q = tid; q < npairs; q += BR) {
         const int j = q < kPairCache ? (int)S.owner[q] : rank_of_pair(S.poff, q);
-        const int ty = S.lo[j] / kTile + (int)(q - S.poff[j]);
+        const int ty = S.lo[j] / kTileH + (int)(q - S.poff[j]);
         uint32_t in_warp;
         if (q < kPairCache) {
             in_warp = S.lr[q];
         } else {  // rare: recount covering splats of this warp before j
             in_warp = 0;
             for (int jj = j & ~31; jj < j; jj++)
-                in_warp += (S.lo[jj] < S.hi[jj] && ty >= S.lo[jj] / kTile &&
-                            ty <= (S.hi[jj] - 1) / kTile);
+                in_warp += (S.lo[jj] < S.hi[jj] && ty >= S.lo[jj] / kTileH &&
+                            ty <= (S.hi[jj] - 1) / kTileH);
         }
         const uint32_t slot = rowbase[ty] + wpre_all[(j >> 5) * nr + ty] + in_warp;
         // tile-column span of splat j in tile row ty
-        const int y0 = max(S.lo[j], ty * kTile), y1 = min(S.hi[j], ty * kTile + kTile);
+        const int y0 = max(S.lo[j], ty * kTileH), y1 = min(S.hi[j], ty * kTileH + kTileH);
         int mn, mx;
         const float u = S.u[j], v = S.v[j], ia = S.ia[j], ib = S.ib[j], ic = S.ic[j],
                     rsq = S.rsq[j], rinv = S.rinv[j];
@@ -251,8 +251,8 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
         }
         uint32_t span = 0;
         if (mn <= mx) {
-            const uint32_t tx0 = (uint32_t)(mn / kTile);
-            span = tx0 | (((uint32_t)((mx - 1) / kTile) - tx0 + 1u) << 16);
+            const uint32_t tx0 = (uint32_t)(mn / kTileW);
+            span = tx0 | (((uint32_t)((mx - 1) / kTileW) - tx0 + 1u) << 16);
         }
         if ((int64_t)slot < a.cap_p) a.pairs[slot] = make_uint2((uint32_t)(b * BR + j), span);
     }

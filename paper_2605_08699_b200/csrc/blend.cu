@@ -13,13 +13,13 @@
 // contributions per pixel are the reference's.  After the list: rgb += T*bg
 // (render.py:423-427), then the u8 conversion of render.py:470+484-485.
 //
-// Layout: a work item is one warp's 2x16 pixels, pixel rows 2w, 2w+1 of a
-// 16x16 tile (lane & 15 = column, lane >> 4 = row), taken from a work queue by
-// a persistent grid (see blend_kernel).  A warp walks the tile list 32
-// splats at a time: lane j loads splat j's record (128-bit loads), computes
-// its two row intervals (exact, row_xlr) as a 32-bit pixel-coverage mask and
-// stages the splat's per-row terms in shared memory (structure of arrays, so
-// any lane can read any splat without bank conflicts).  A 5-step shuffle
+// Layout: a work item is one warp's 32 pixels, pixel row w of a 32x16 tile
+// (lane = column), taken from a work queue by a persistent grid (see
+// blend_kernel).  A warp walks the tile list 32 splats at a time: lane j
+// loads splat j's record (128-bit loads), computes its row interval (exact,
+// row_xlr) as a 32-bit pixel-coverage mask and stages the splat's row terms
+// in shared memory (structure of arrays, so any lane can read any splat
+// without bank conflicts).  A 5-step shuffle
 // transpose turns the 32 splat masks into 32 per-pixel masks; each lane then
 // walks its OWN covering splats in depth order, so a warp iteration does
 // useful work on every lane that still has splats (not just on the lanes a
@@ -36,19 +36,20 @@ namespace {
 
 constexpr int kBlendThreads = 128;              // 4 warps: finer occupancy granularity
 constexpr int kWarps = kBlendThreads / 32;
-constexpr int kRowPairs = kTile / 2;           // work items per tile (2 pixel rows each)
+constexpr int kItemsPerTile = kTileH;           // work items per tile (one pixel row each)
 
 __device__ __forceinline__ uint32_t span_mask(int x0, int x1, int X) {
-    // columns [x0, x1) intersected with [X, X+16), as a 16-bit mask
+    // columns [x0, x1) intersected with [X, X+32), as a 32-bit mask
     int a = x0 - X, b = x1 - X;
     a = a < 0 ? 0 : a;
-    b = b > 16 ? 16 : b;
+    b = b > 32 ? 32 : b;
     if (a >= b) return 0u;
-    return ((1u << b) - 1u) & ~((1u << a) - 1u);
+    const uint32_t hi = b >= 32 ? 0xffffffffu : (1u << b) - 1u;
+    return hi & ~((1u << a) - 1u);
 }
 
 // Coverage of one pixel row of the tile by one splat (render.py:329-333 row
-// range, 383-397 interval), as a 16-bit column mask.
+// range, 383-397 interval), as a 32-bit column mask.
 __device__ __forceinline__ uint32_t row_mask(const float4 &A, const float4 &B, float rinv, bool fast,
                                              int iy, int lo, int hi, int X, int width) {
     if (iy < lo || iy >= hi) return 0u;
@@ -127,7 +128,7 @@ __device__ __forceinline__ float expf_blend(float q, const unsigned long long *t
 
 
 struct WarpBatch {         // one warp's current 32 splats, splat j in slot 32 - j; slot 0: null
-    float4 geo[2][33];     // per pixel row of the warp: (u, ia, (2*ib)*dy, (ic*dy)*dy)
+    float4 geo[33];        // for the item's pixel row: (u, ia, (2*ib)*dy, (ic*dy)*dy)
     float4 col[33];        // (op, r, g, b)
 };
 
@@ -201,15 +202,14 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
     }
     __syncthreads();
 
-    const int tiles_x = (width + kTile - 1) / kTile;
-    const int n_items = tiles_x * ((height + kTile - 1) / kTile) * kRowPairs;
+    const int tiles_x = (width + kTileW - 1) / kTileW;
+    const int n_items = tiles_x * ((height + kTileH - 1) / kTileH) * kItemsPerTile;
     const int lane = lane_id(), w = threadIdx.x >> 5;
-    const int prow = lane >> 4;
     WarpBatch &B_ = s_b[w];
     // shared-window addresses of slot 0 of this lane's rows, opaque to the
     // compiler so they stay in registers across the composite loop
     uint32_t geo, bcol;
-    asm volatile("mov.u32 %0, %1;" : "=r"(geo) : "r"((uint32_t)__cvta_generic_to_shared(&B_.geo[prow][1])));
+    asm volatile("mov.u32 %0, %1;" : "=r"(geo) : "r"((uint32_t)__cvta_generic_to_shared(&B_.geo[1])));
     asm volatile("mov.u32 %0, %1;" : "=r"(bcol) : "r"((uint32_t)__cvta_generic_to_shared(&B_.col[1])));
     // (opaque to the compiler, so the table base stays in a register instead
     //  of being rebuilt from the CTA id in the inner loop)
@@ -229,14 +229,13 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
         if (lane == 0) item = (int)atomicAdd(&ctr->blend_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= n_items) break;
-        const int tile = item / kRowPairs, wr = item % kRowPairs;
+        const int tile = item / kItemsPerTile, wr = item % kItemsPerTile;
         const int tx = tile % tiles_x, ty = tile / tiles_x;
-        const int X = tx * kTile;
-        const int iy0 = ty * kTile + 2 * wr;
-        const int iy = iy0 + prow;
-        const int ix = X + (lane & 15);
+        const int X = tx * kTileW;
+        const int iy = ty * kTileH + wr;
+        const int ix = X + lane;
         const bool inside = ix < width && iy < height;
-        const float py0 = (float)iy0 + 0.5f, py1 = (float)(iy0 + 1) + 0.5f;
+        const float py = (float)iy + 0.5f;
         const float fx = (float)ix + 0.5f;
 
         float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
@@ -257,17 +256,13 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
                 bool fast, esafe;
                 unpack_rows(B.w, lo, hi, fast, esafe);
                 const float rinv = fast ? __frcp_rn(A.z) : 0.0f;
-                n_rows += (uint32_t)(iy0 >= lo && iy0 < hi) +
-                          (uint32_t)(iy0 + 1 >= lo && iy0 + 1 < hi);
-                mask = row_mask(A, B, rinv, fast, iy0, lo, hi, X, width) |
-                       (row_mask(A, B, rinv, fast, iy0 + 1, lo, hi, X, width) << 16);
-                if (mask) {  // render.py:400-402 terms per pixel row
+                n_rows += (uint32_t)(iy >= lo && iy < hi);
+                mask = row_mask(A, B, rinv, fast, iy, lo, hi, X, width);
+                if (mask) {  // render.py:400-402 terms of the pixel row
                     const float4 C = __ldg(col + gi);  // (r, g, b)
                     safe = esafe;
-                    const float ib2 = 2.0f * A.w;
-                    const float dy0 = py0 - A.y, dy1 = py1 - A.y;
-                    B_.geo[0][32 - lane] = make_float4(A.x, A.z, ib2 * dy0, B.x * dy0 * dy0);
-                    B_.geo[1][32 - lane] = make_float4(A.x, A.z, ib2 * dy1, B.x * dy1 * dy1);
+                    const float dy = py - A.y;
+                    B_.geo[32 - lane] = make_float4(A.x, A.z, (2.0f * A.w) * dy, B.x * dy * dy);
                     B_.col[32 - lane] = make_float4(B.z, C.x, C.y, C.z);
                 }
             }
@@ -337,8 +332,8 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
         }
         g_blend_grid = sms * (per_sm > 0 ? per_sm : 1);
     }
-    const int tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
-    const int grid = std::min(g_blend_grid, tiles);
+    const int tiles = ((width + kTileW - 1) / kTileW) * ((height + kTileH - 1) / kTileH);
+    const int grid = std::min(g_blend_grid, tiles * kItemsPerTile);
     blend_kernel<<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges, width, height,
                                                 bg0, bg1, bg2, out, ctr);
     mark("blend");

@@ -114,7 +114,7 @@ int check_camera(const gsr_camera *cam) {
     if (!cam) return fail(GSR_E_INVALID, "camera is null");
     if (cam->width <= 0 || cam->height <= 0)
         return fail(GSR_E_INVALID, "image dimensions must be positive");
-    if (cam->width > 16 * kMaxTilesX || cam->height > 16 * kMaxTileRows)
+    if (cam->width > kTileW * kMaxTilesX || cam->height > kTileH * kMaxTileRows)
         return fail(GSR_E_INVALID, "image larger than 16384 x 8192 is not supported");
     if (!(cam->fx > 0) || !(cam->fy > 0)) return fail(GSR_E_INVALID, "focal lengths must be positive");
     return GSR_OK;
@@ -159,7 +159,7 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
     if ((rc = ensure(c->pairs, sizeof(uint2) * c->cap_p))) return rc;
     if ((rc = ensure(c->depth_work, depth_work64_bytes(c->cap_n)))) return rc;
     if ((rc = ensure(c->depth_work32, depth_work32_bytes(c->cap_n)))) return rc;
-    const int tiles_x = (W + kTile - 1) / kTile, n_rows = (H + kTile - 1) / kTile;
+    const int tiles_x = (W + kTileW - 1) / kTileW, n_rows = (H + kTileH - 1) / kTileH;
     const int ntiles = tiles_x * n_rows;
     if ((rc = ensure(c->ranges, sizeof(uint2) * (size_t)ntiles))) return rc;
     if ((rc = ensure(c->ttotal, sizeof(uint32_t) * (size_t)ntiles))) return rc;
@@ -207,7 +207,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     const CameraArgs ca = camera_args(cam);
     c->W = W;
     c->H = H;
-    c->ntiles = ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+    c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
     uint32_t *dsched = c->sched.as<uint32_t>();
     int launches = 2;  // frame init + blend
 
@@ -255,8 +255,8 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.ctr = ctr;
         ba.width = W;
         ba.height = H;
-        ba.tiles_x = (W + kTile - 1) / kTile;
-        ba.n_rows = (H + kTile - 1) / kTile;
+        ba.tiles_x = (W + kTileW - 1) / kTileW;
+        ba.n_rows = (H + kTileH - 1) / kTileH;
         ba.ntiles = c->ntiles;
         ba.n_blocks = bin_blocks(c->cap_n);
         ba.row_blk = c->row_blk.as<uint32_t>();

@@ -124,8 +124,8 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s,
                       const KMark &mark = KMark());  // returns kernels launched
 
 // binning.cu: sort-free tile lists (see binning.cu header)
-constexpr int kMaxTileRows = 512;   // height <= 8192
-constexpr int kMaxTilesX = 1024;    // width <= 16384
+constexpr int kMaxTileRows = 8192 / kTileH;   // height <= 8192
+constexpr int kMaxTilesX = 16384 / kTileW;   // width <= 16384
 struct BinArgs {
     const uint32_t *order0, *order1;  // depth sort result buffers
     const uint32_t *depth_sched;      // [16]: which of order0/order1 holds the result

@@ -35,7 +35,7 @@ ALPHA_MAX = 0.99
 TRANSMITTANCE_STOP = 1.0 / 255.0
 CUTOFF_SIGMA = 4.5
 TAIL_SAFETY = 32.0
-TILE = 16
+TILE_W, TILE_H = 32, 16  # tiles of the device's lists (csrc/common.cuh kTileW, kTileH)
 
 
 class EncodeFailure(RenderError):
@@ -465,7 +465,7 @@ def debug_tile_lists(*, device: int | None = None):
 def debug_tile_ranges(width: int, height: int, *, device: int | None = None) -> np.ndarray:
     dev = _default_device if device is None else device
     ctx = _lib.context(dev)
-    n_tiles = ((width + TILE - 1) // TILE) * ((height + TILE - 1) // TILE)
+    n_tiles = ((width + TILE_W - 1) // TILE_W) * ((height + TILE_H - 1) // TILE_H)
     ranges = np.empty((n_tiles, 2), dtype=np.int32)
     st = _lib.GsrStats()
     _lib.check(ctx.lib.gsr_debug_tile_lists(ctx.handle, None, None, _lib.ptr(ranges),

@@ -54,14 +54,18 @@ def test_sweep_bit_exact(gsr):
     assert n == 50
 
 
-def _assert_lists_cover(tt, tr, ot, orr, max_inflation=1.05):
-    """The device's tile lists contain every (tile, rank) of the exact
-    tile-list contract (the oracle's), sorted by (tile, rank) with ranks
-    increasing -- the property the bit-exact blend relies on (a superset
-    only costs blend work: splats outside a pixel's exact interval are never
-    composited) -- and are at most `max_inflation` times as long."""
+def _assert_lists_cover(tt, tr, ot, orr, width, max_inflation=1.05):
+    """The device's tile lists (32x16 tiles) contain every (tile, rank) of the
+    exact tile-list contract (the oracle's, 16x16 tiles: a contract tile
+    (tx, ty) lies in device tile (tx // 2, ty)), sorted by (tile, rank) with
+    ranks increasing -- the property the bit-exact blend relies on (a
+    superset only costs blend work: splats outside a pixel's exact interval
+    are never composited) -- and at most `max_inflation` times as long as the
+    contract mapped onto the device tiles."""
+    n16, n32 = (width + 15) // 16, (width + 31) // 32
     g = tt.astype(np.int64) * (1 << 32) + tr.astype(np.int64)
-    o = ot.astype(np.int64) * (1 << 32) + orr.astype(np.int64)
+    dev_tile = (ot // n16) * n32 + (ot % n16) // 2
+    o = np.unique(dev_tile.astype(np.int64) * (1 << 32) + orr.astype(np.int64))
     assert np.all(np.diff(g) > 0)
     assert np.isin(o, g).all(), "a contract (tile, rank) entry is missing"
     assert len(g) <= max_inflation * len(o) + 16, (len(g), len(o))
@@ -97,7 +101,7 @@ def test_frames_bit_exact(gsr, oracle, name):
     ot, orr, _ = oracle.tile_lists(packed, intr.width, intr.height)  # pinned to tiles.json
     assert ot.shape[0] == tiles["D"]
     assert digest(ot) == tiles["tiles"] and digest(orr) == tiles["ranks"]
-    _assert_lists_cover(tt, tr, ot, orr)
+    _assert_lists_cover(tt, tr, ot, orr, intr.width)
     ranges = debug_tile_ranges(intr.width, intr.height)
     for t_id in np.unique(tt):
         s, e = ranges[t_id]
@@ -263,7 +267,7 @@ def test_config2_500k_720p_trace_vs_oracle(gsr, oracle):
         assert np.array_equal(fb.u8, fr.u8)
         tt, tr = debug_tile_lists()
         ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
-        _assert_lists_cover(tt, tr, ot, orr)
+        _assert_lists_cover(tt, tr, ot, orr, intr.width)
 
 
 def test_config3_3m_1080p_vs_oracle(gsr, oracle):
@@ -283,7 +287,7 @@ def test_config3_3m_1080p_vs_oracle(gsr, oracle):
     assert np.array_equal(fb._rgb32, fr.rgb32)
     tt, tr = debug_tile_lists()
     ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
-    _assert_lists_cover(tt, tr, ot, orr)
+    _assert_lists_cover(tt, tr, ot, orr, intr.width)
     # size-independent properties: depth order is sorted, tile keys sorted
     z = fr.depths
     assert np.all(np.diff(z) >= 0)
@@ -307,7 +311,7 @@ def test_config4_6m_1080p_vs_oracle(gsr, oracle):
     assert np.array_equal(fb.u8, fr.u8)
     tt, tr = debug_tile_lists()
     ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
-    _assert_lists_cover(tt, tr, ot, orr)
+    _assert_lists_cover(tt, tr, ot, orr, intr.width)
     key = tt.astype(np.int64) * (1 << 32) + tr
     assert np.all(np.diff(key) > 0)
 
