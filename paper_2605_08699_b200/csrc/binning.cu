@@ -276,24 +276,23 @@ __global__ void __launch_bounds__(1024) seg_table_kernel(BinArgs a) {
         }
         uint32_t tot;
         const uint32_t ex = block_excl_scan_u32(ns, s_warp, &tot);
+        if (ty < a.n_rows) a.row_seg0[ty] = carry + ex;
         for (uint32_t s = 0; s < ns; s++) {
             const uint32_t g = carry + ex + s;
             if ((int64_t)g < a.cap_seg) a.seg_row[g] = (uint32_t)ty;
         }
         carry += tot;
     }
-    if (threadIdx.x == 0) a.ctr->nseg = carry;
+    if (threadIdx.x == 0) {
+        a.ctr->nseg = carry;
+        a.row_seg0[a.n_rows] = carry;
+    }
 }
 
-// first segment of tile row ty (seg_row is non-decreasing): binary search
+// first segment of tile row ty (written by seg_table)
 __device__ __forceinline__ int64_t first_seg_of_row(const BinArgs &a, uint32_t ty, int64_t nseg) {
-    int64_t lo = 0, hi = nseg;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (a.seg_row[mid] < ty) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
+    const int64_t f = (int64_t)a.row_seg0[ty];
+    return f < nseg ? f : nseg;
 }
 
 __device__ __forceinline__ void seg_bounds(const BinArgs &a, int64_t g, int64_t nseg,
@@ -341,34 +340,27 @@ __global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
 }
 
 // ---------------------------------------------------------------- 2c -------
-// thread per tile: exclusive prefix over its row's segments, tile total
-__global__ void seg_scan_kernel(BinArgs a) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+// warp per tile: exclusive prefix over its row's segments (32 at a time,
+// warp scan), tile total
+__global__ void __launch_bounds__(256) seg_scan_kernel(BinArgs a) {
+    const int t = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (t >= a.ntiles || overflowed(a)) return;
     const int tx_n = a.tiles_x;
     const int ty = t / tx_n, tx = t % tx_n;
     const uint32_t rs = a.row_start[ty], re = a.row_start[ty + 1];
     const uint32_t nrow = (re - rs + kSeg - 1) / kSeg;
     const int64_t lo = first_seg_of_row(a, (uint32_t)ty, seg_count_of(a));
-    uint32_t run = 0;
     uint32_t *base = a.seg_cnt + lo * tx_n + tx;
-    uint32_t s = 0;
-    for (; s + 8 <= nrow; s += 8) {  // 8 independent loads in flight
-        uint32_t c[8];
-#pragma unroll
-        for (int j = 0; j < 8; j++) c[j] = base[(int64_t)(s + j) * tx_n];
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            base[(int64_t)(s + j) * tx_n] = run;
-            run += c[j];
-        }
+    uint32_t carry = 0;
+    for (uint32_t s0 = 0; s0 < nrow; s0 += 32) {
+        const uint32_t si = s0 + lane;
+        const uint32_t v = si < nrow ? base[(int64_t)si * tx_n] : 0u;
+        const uint32_t inc = warp_incl_scan_u32(v);
+        if (si < nrow) base[(int64_t)si * tx_n] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    for (; s < nrow; s++) {
-        const uint32_t c = base[(int64_t)s * tx_n];
-        base[(int64_t)s * tx_n] = run;
-        run += c;
-    }
-    a.tile_total[t] = run;
+    if (lane == 0) a.tile_total[t] = carry;
 }
 
 // one block of 1024: tile starts (exclusive scan of totals), ranges, D
@@ -532,7 +524,7 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark) {
     const unsigned sb = (unsigned)((a.cap_seg + 7) / 8);
     seg_count_kernel<<<sb, 256, 8 * (a.tiles_x + 1) * sizeof(uint32_t), s>>>(a);
     mark("seg_count");
-    seg_scan_kernel<<<(unsigned)((a.ntiles + 255) / 256), 256, 0, s>>>(a);
+    seg_scan_kernel<<<(unsigned)((a.ntiles + 7) / 8), 256, 0, s>>>(a);
     mark("seg_scan");
     tile_scan_kernel<<<1, 1024, 0, s>>>(a);
     mark("tile_scan");

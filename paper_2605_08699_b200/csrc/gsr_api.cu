@@ -171,7 +171,7 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
                                        (size_t)(bin_scan_tiles(bin_blocks(c->cap_n), n_rows) + 1))))
         return rc;
     const int64_t cap_seg = bin_segments(c->cap_p, n_rows);
-    if ((rc = ensure(c->seg_row, sizeof(uint32_t) * (size_t)cap_seg))) return rc;
+    if ((rc = ensure(c->seg_row, sizeof(uint32_t) * (size_t)(cap_seg + n_rows + 2)))) return rc;
     if ((rc = ensure(c->seg_cnt, sizeof(uint32_t) * (size_t)cap_seg * tiles_x))) return rc;
     const int64_t px = (int64_t)W * H;
     if ((rc = ensure(c->frame_u8, (size_t)px * 3))) return rc;
@@ -266,6 +266,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.cap_p = c->cap_p;
         ba.seg_row = c->seg_row.as<uint32_t>();
         ba.cap_seg = bin_segments(c->cap_p, ba.n_rows);
+        ba.row_seg0 = ba.seg_row + ba.cap_seg;
         ba.seg_cnt = c->seg_cnt.as<uint32_t>();
         ba.tile_total = c->ttotal.as<uint32_t>();
         ba.tile_start = c->tstart.as<uint32_t>();

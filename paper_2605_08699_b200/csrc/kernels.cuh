@@ -140,6 +140,7 @@ struct BinArgs {
     uint2 *pairs;           // [cap_p] (rank, tx0 | count << 16), grouped by tile row
     int64_t cap_p;
     uint32_t *seg_row;      // [cap_seg] tile row of each segment
+    uint32_t *row_seg0;     // [n_rows + 1] first segment of each tile row
     int64_t cap_seg;
     uint32_t *seg_cnt;      // [cap_seg][tiles_x] keys per column -> offsets
     uint32_t *tile_total;   // [ntiles]
