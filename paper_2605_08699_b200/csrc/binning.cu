@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
 // segments: row ty's pairs [row_start[ty], row_start[ty+1]) in pieces of kSeg
 __global__ void __launch_bounds__(1024) seg_table_kernel(BinArgs a) {
     __shared__ uint32_t s_warp[33];
+    __shared__ uint32_t s_first[kRowsMax + 1];
     uint32_t carry = 0;
     const bool ov = overflowed(a);
     for (int base = 0; base < a.n_rows; base += 1024) {
@@ -276,16 +277,28 @@ __global__ void __launch_bounds__(1024) seg_table_kernel(BinArgs a) {
         }
         uint32_t tot;
         const uint32_t ex = block_excl_scan_u32(ns, s_warp, &tot);
-        if (ty < a.n_rows) a.row_seg0[ty] = carry + ex;
-        for (uint32_t s = 0; s < ns; s++) {
-            const uint32_t g = carry + ex + s;
-            if ((int64_t)g < a.cap_seg) a.seg_row[g] = (uint32_t)ty;
+        if (ty < a.n_rows) {
+            a.row_seg0[ty] = carry + ex;
+            s_first[ty] = carry + ex;
         }
         carry += tot;
     }
     if (threadIdx.x == 0) {
         a.ctr->nseg = carry;
         a.row_seg0[a.n_rows] = carry;
+        s_first[a.n_rows] = carry;
+    }
+    __syncthreads();
+    // segment -> tile row, all threads (binary search over the row starts)
+    const int64_t ns_all = carry < (uint64_t)a.cap_seg ? carry : a.cap_seg;
+    for (int64_t g = threadIdx.x; g < ns_all; g += 1024) {
+        int lo = 0, hi = a.n_rows;  // s_first[lo] <= g < s_first[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_first[mid] <= (uint32_t)g) lo = mid;
+            else hi = mid;
+        }
+        a.seg_row[g] = (uint32_t)lo;
     }
 }
 
