@@ -10,7 +10,7 @@ import threading
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, digest, golden_scene, load_json, sweep_scenes, textured
+from conftest import GOLDEN, ROOT, digest, golden_scene, load_json, sweep_scenes, textured
 
 pytestmark = pytest.mark.gpu
 
@@ -641,3 +641,18 @@ def test_device_registry_residency(gsr):
     assert len(key) >= 1
     assert reg.evict_inactive() == ["garden"]
     assert reg.device_bytes() == 0
+
+
+def test_span_bound_contains_exact_spans(tmp_path):
+    """The conservative tile-column span (band_span_bound) contains the exact
+    contract span on random splats -- realistic, elongated / huge / tiny, and
+    boundary-aligned (tools/span_check.cu, one batch: ~4e8 pairs)."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    exe = tmp_path / "span_check"
+    subprocess.run([nvcc, "-O3", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
+                    "-gencode", "arch=compute_100a,code=sm_100a", "-I", str(ROOT / "include"),
+                    "-o", str(exe), str(ROOT / "tools" / "span_check.cu")], check=True)
+    out = subprocess.run([str(exe), "1"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "OK: no violations" in out.stdout, out.stdout
