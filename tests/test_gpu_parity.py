@@ -55,16 +55,18 @@ def test_sweep_bit_exact(gsr):
 
 
 def _assert_lists_cover(tt, tr, ot, orr, width, max_inflation=1.05):
-    """The device's tile lists (32x16 tiles) contain every (tile, rank) of the
-    exact tile-list contract (the oracle's, 16x16 tiles: a contract tile
-    (tx, ty) lies in device tile (tx // 2, ty)), sorted by (tile, rank) with
+    """The device's tile lists (TILE_W x TILE_H tiles) contain every (tile,
+    rank) of the exact tile-list contract (the oracle's, 16x16 tiles: a
+    contract tile (tx, ty) lies in device tile (tx // (TILE_W / 16),
+    ty // (TILE_H / 16))), sorted by (tile, rank) with
     ranks increasing -- the property the bit-exact blend relies on (a
     superset only costs blend work: splats outside a pixel's exact interval
     are never composited) -- and at most `max_inflation` times as long as the
     contract mapped onto the device tiles."""
-    n16, n32 = (width + 15) // 16, (width + 31) // 32
+    from paper_2605_08699_b200.render import TILE_H, TILE_W
+    n16, nd = (width + 15) // 16, (width + TILE_W - 1) // TILE_W
     g = tt.astype(np.int64) * (1 << 32) + tr.astype(np.int64)
-    dev_tile = (ot // n16) * n32 + (ot % n16) // 2
+    dev_tile = (ot // n16) // (TILE_H // 16) * nd + (ot % n16) // (TILE_W // 16)
     o = np.unique(dev_tile.astype(np.int64) * (1 << 32) + orr.astype(np.int64))
     assert np.all(np.diff(g) > 0)
     assert np.isin(o, g).all(), "a contract (tile, rank) entry is missing"
