@@ -35,7 +35,7 @@ ALPHA_MAX = 0.99
 TRANSMITTANCE_STOP = 1.0 / 255.0
 CUTOFF_SIGMA = 4.5
 TAIL_SAFETY = 32.0
-TILE_W, TILE_H = 32, 32  # tiles of the device's lists (csrc/common.cuh kTileW, kTileH)
+TILE_W, TILE_H = 32, 64  # tiles of the device's lists (csrc/common.cuh kTileW, kTileH)
 
 
 class EncodeFailure(RenderError):
