@@ -36,7 +36,6 @@ namespace {
 
 constexpr int kBlendThreads = 128;              // 4 warps: finer occupancy granularity
 constexpr int kWarps = kBlendThreads / 32;
-constexpr int kItemsPerTile = kTileH;           // work items per tile (one pixel row each)
 
 __device__ __forceinline__ uint32_t span_mask(int x0, int x1, int X) {
     // columns [x0, x1) intersected with [X, X+32), as a 32-bit mask
@@ -128,7 +127,7 @@ __device__ __forceinline__ float expf_blend(float q, const unsigned long long *t
 
 
 struct WarpBatch {         // one warp's current 32 splats, splat j in slot 32 - j; slot 0: null
-    float4 geo[33];        // for the item's pixel row: (u, ia, (2*ib)*dy, (ic*dy)*dy)
+    float4 geo[2][33];     // per pixel row of the item: (u, ia, (2*ib)*dy, (ic*dy)*dy)
     float4 col[33];        // (op, r, g, b)
 };
 
@@ -188,10 +187,15 @@ __device__ __forceinline__ void composite(uint32_t mine, uint32_t geo, uint32_t 
 // as soon as its 32 pixels saturate, or walks the whole tile list if they
 // never do), so binding 8 warps to a CTA per tile would leave most of a CTA's
 // warps idle behind its slowest one; the queue keeps every warp busy.
-__global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
+// kSets pixel rows per item (one pixel per lane per row): the batch's loads
+// and per-splat set-up are shared by the item's rows, which are composited
+// one after the other from the same staged batch.
+template <int kSets>
+__global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kernel(
     const SplatRec *__restrict__ srec, const float4 *__restrict__ col, DepthOrder ord,
     const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
     int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *__restrict__ ctr) {
+    constexpr int kItems = kTileH / kSets;  // items per tile
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
@@ -203,13 +207,15 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
     __syncthreads();
 
     const int tiles_x = (width + kTileW - 1) / kTileW;
-    const int n_items = tiles_x * ((height + kTileH - 1) / kTileH) * kItemsPerTile;
+    const int n_items = tiles_x * ((height + kTileH - 1) / kTileH) * kItems;
     const int lane = lane_id(), w = threadIdx.x >> 5;
     WarpBatch &B_ = s_b[w];
-    // shared-window addresses of slot 0 of this lane's rows, opaque to the
-    // compiler so they stay in registers across the composite loop
-    uint32_t geo, bcol;
-    asm volatile("mov.u32 %0, %1;" : "=r"(geo) : "r"((uint32_t)__cvta_generic_to_shared(&B_.geo[1])));
+    // shared-window addresses of slot 0 of the rows, opaque to the compiler
+    // so they stay in registers across the composite loop
+    uint32_t geo[kSets], bcol;
+#pragma unroll
+    for (int h = 0; h < kSets; h++)
+        asm volatile("mov.u32 %0, %1;" : "=r"(geo[h]) : "r"((uint32_t)__cvta_generic_to_shared(&B_.geo[h][1])));
     asm volatile("mov.u32 %0, %1;" : "=r"(bcol) : "r"((uint32_t)__cvta_generic_to_shared(&B_.col[1])));
     // (opaque to the compiler, so the table base stays in a register instead
     //  of being rebuilt from the CTA id in the inner loop)
@@ -229,23 +235,33 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
         if (lane == 0) item = (int)atomicAdd(&ctr->blend_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= n_items) break;
-        const int tile = item / kItemsPerTile, wr = item % kItemsPerTile;
+        const int tile = item / kItems, wr = item % kItems;
         const int tx = tile % tiles_x, ty = tile / tiles_x;
         const int X = tx * kTileW;
-        const int iy = ty * kTileH + wr;
+        const int iy0 = ty * kTileH + kSets * wr;
         const int ix = X + lane;
-        const bool inside = ix < width && iy < height;
-        const float py = (float)iy + 0.5f;
         const float fx = (float)ix + 0.5f;
 
-        float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-        bool done = !inside;
+        float T[kSets], cr[kSets], cg[kSets], cb[kSets];
+        bool inside[kSets], done[kSets];
+#pragma unroll
+        for (int h = 0; h < kSets; h++) {
+            T[h] = 1.0f;
+            cr[h] = cg[h] = cb[h] = 0.0f;
+            inside[h] = ix < width && iy0 + h < height;
+            done[h] = !inside[h];
+        }
         const uint2 rg = ranges[tile];
 
         for (uint32_t c = rg.x; c < rg.y; c += 32) {
-            if (__all_sync(0xffffffffu, done)) break;
+            bool all_done = true;
+#pragma unroll
+            for (int h = 0; h < kSets; h++) all_done = all_done && done[h];
+            if (__all_sync(0xffffffffu, all_done)) break;
             const uint32_t j = c + lane;
-            uint32_t mask = 0;
+            uint32_t mask[kSets];
+#pragma unroll
+            for (int h = 0; h < kSets; h++) mask[h] = 0u;
             bool safe = true;
             if (j < rg.y) {
                 const uint32_t r = __ldg(tile_vals + j);  // depth rank
@@ -255,40 +271,57 @@ __global__ void __launch_bounds__(kBlendThreads, 9) blend_kernel(
                 int lo, hi;  // precomputed per frame by bin_gather (SplatRec.b.w)
                 bool fast, esafe;
                 unpack_rows(B.w, lo, hi, fast, esafe);
-                const float rinv = fast ? __frcp_rn(A.z) : 0.0f;
-                n_rows += (uint32_t)(iy >= lo && iy < hi);
-                mask = row_mask(A, B, rinv, fast, iy, lo, hi, X, width);
-                if (mask) {  // render.py:400-402 terms of the pixel row
-                    const float4 C = __ldg(col + gi);  // (r, g, b)
-                    safe = esafe;
-                    const float dy = py - A.y;
-                    B_.geo[32 - lane] = make_float4(A.x, A.z, (2.0f * A.w) * dy, B.x * dy * dy);
-                    B_.col[32 - lane] = make_float4(B.z, C.x, C.y, C.z);
+                if (iy0 + kSets > lo && iy0 < hi) {
+                    const float rinv = fast ? __frcp_rn(A.z) : 0.0f;
+                    uint32_t any = 0u;
+#pragma unroll
+                    for (int h = 0; h < kSets; h++) {
+                        n_rows += (uint32_t)(iy0 + h >= lo && iy0 + h < hi);
+                        mask[h] = row_mask(A, B, rinv, fast, iy0 + h, lo, hi, X, width);
+                        any |= mask[h];
+                    }
+                    if (any) {  // render.py:400-402 terms per pixel row
+                        const float4 C = __ldg(col + gi);  // (r, g, b)
+                        safe = esafe;
+#pragma unroll
+                        for (int h = 0; h < kSets; h++) {
+                            const float dy = ((float)(iy0 + h) + 0.5f) - A.y;
+                            B_.geo[h][32 - lane] =
+                                make_float4(A.x, A.z, (2.0f * A.w) * dy, B.x * dy * dy);
+                        }
+                        B_.col[32 - lane] = make_float4(B.z, C.x, C.y, C.z);
+                    }
                 }
             }
             __syncwarp();
-            uint32_t mine = __brev(transpose32(mask, lane));
-            if (done) mine = 0u;
-            if (__all_sync(0xffffffffu, safe))
-                composite<false>(mine, geo, bcol, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
-            else
-                composite<true>(mine, geo, bcol, fx, s_tab, tab_s, ek, T, cr, cg, cb, n_comp);
-            done = done || T < kTStop;
+            const bool all_safe = __all_sync(0xffffffffu, safe);
+#pragma unroll
+            for (int h = 0; h < kSets; h++) {
+                uint32_t mine = __brev(transpose32(mask[h], lane));
+                if (done[h]) mine = 0u;
+                if (all_safe)
+                    composite<false>(mine, geo[h], bcol, fx, s_tab, tab_s, ek, T[h], cr[h], cg[h],
+                                     cb[h], n_comp);
+                else
+                    composite<true>(mine, geo[h], bcol, fx, s_tab, tab_s, ek, T[h], cr[h], cg[h],
+                                    cb[h], n_comp);
+                done[h] = done[h] || T[h] < kTStop;
+            }
             __syncwarp();
         }
-        if (inside) {
-            cr += T * bg0;
-            cg += T * bg1;
-            cb += T * bg2;
-            const int64_t p = (int64_t)iy * width + ix;
+#pragma unroll
+        for (int h = 0; h < kSets; h++) {
+            if (!inside[h]) continue;
+            const float rr = cr[h] + T[h] * bg0, gg = cg[h] + T[h] * bg1, bb = cb[h] + T[h] * bg2;
+            const int64_t p = (int64_t)(iy0 + h) * width + ix;
             if (out.rgb) {
-                out.rgb[3 * p + 0] = cr;
-                out.rgb[3 * p + 1] = cg;
-                out.rgb[3 * p + 2] = cb;
+                out.rgb[3 * p + 0] = rr;
+                out.rgb[3 * p + 1] = gg;
+                out.rgb[3 * p + 2] = bb;
             }
-            if (out.trans) out.trans[p] = T;
+            if (out.trans) out.trans[p] = T[h];
             // render.py:470 + 484-485: trunc(clip(clip(f64(c), 0, 1) * 255 + 0.5, 0, 255))
-            const float ch[3] = {cr, cg, cb};
+            const float ch[3] = {rr, gg, bb};
 #pragma unroll
             for (int k = 0; k < 3; k++) {
                 double d = (double)ch[k];
@@ -319,11 +352,19 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
                   const uint32_t *tile_vals, const uint2 *ranges, int width,
                   int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
                   cudaStream_t s, const KMark &mark) {
+    static int sets = 0;
+    if (!sets) {
+        const char *e = getenv("GSR_BLEND_SETS");
+        sets = (e && atoi(e) == 1) ? 1 : 2;
+    }
     if (!g_blend_grid) {  // persistent grid: every SM full
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel, kBlendThreads, 0);
+        if (sets == 1)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<1>, kBlendThreads, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2>, kBlendThreads, 0);
         // GSR_BLEND_CTAS_PER_SM (tuning): fewer resident CTAs leave room for
         // other frames' kernels when several frames are in flight
         if (const char *e = getenv("GSR_BLEND_CTAS_PER_SM")) {
@@ -333,9 +374,13 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
         g_blend_grid = sms * (per_sm > 0 ? per_sm : 1);
     }
     const int tiles = ((width + kTileW - 1) / kTileW) * ((height + kTileH - 1) / kTileH);
-    const int grid = std::min(g_blend_grid, tiles * kItemsPerTile);
-    blend_kernel<<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges, width, height,
-                                                bg0, bg1, bg2, out, ctr);
+    const int grid = std::min(g_blend_grid, tiles * kTileH);
+    if (sets == 1)
+        blend_kernel<1><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges, width,
+                                                       height, bg0, bg1, bg2, out, ctr);
+    else
+        blend_kernel<2><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges, width,
+                                                       height, bg0, bg1, bg2, out, ctr);
     mark("blend");
 }
 
