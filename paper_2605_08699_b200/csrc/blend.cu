@@ -13,8 +13,8 @@
 // contributions per pixel are the reference's.  After the list: rgb += T*bg
 // (render.py:423-427), then the u8 conversion of render.py:470+484-485.
 //
-// Layout: a work item is one warp's 32 pixels, pixel row w of a 32x16 tile
-// (lane = column), taken from a work queue by a persistent grid (see
+// Layout: a work item is one warp's kSets x 32 pixels, pixel rows of a
+// 32x64 tile (lane = column; rows composited one after the other), taken from a work queue by a persistent grid (see
 // blend_kernel).  A warp walks the tile list 32 splats at a time: lane j
 // loads splat j's record (128-bit loads), computes its row interval (exact,
 // row_xlr) as a 32-bit pixel-coverage mask and stages the splat's row terms
