@@ -181,6 +181,57 @@ __device__ __forceinline__ void composite(uint32_t mine, uint32_t geo, uint32_t 
     n_comp -= __popc(dropped);
 }
 
+// The two pixel rows of an item interleaved: each iteration composites the
+// next covering splat of the lane's pixel in row 0 and of its pixel in row
+// 1 (two independent chains; a pixel with nothing left reads the null slot
+// of its row, alpha 0), so the loop runs max over lanes of max(count0,
+// count1) iterations instead of max count0 + max count1.
+template <bool kChecked>
+__device__ __forceinline__ void composite_pair(uint32_t m0, uint32_t m1, uint32_t geo0,
+                                               uint32_t geo1, uint32_t col, float fx,
+                                               const unsigned long long *tab, uint32_t tab_s,
+                                               const ExpK &ek, float *T, float *cr, float *cg,
+                                               float *cb, uint32_t &n_comp) {
+    n_comp += __popc(m0) + __popc(m1);
+    uint32_t dropped = 0u;
+    while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
+        const int s0 = 31 - __clz(m0), s1 = 31 - __clz(m1);
+        uint32_t b0, b1;
+        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(b0) : "r"((uint32_t)s0));
+        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(b1) : "r"((uint32_t)s1));
+        m0 &= b0;
+        m1 &= b1;
+        const float4 g0 = lds128(geo0 + 16u * (uint32_t)s0), g1 = lds128(geo1 + 16u * (uint32_t)s1);
+        const float4 k0 = lds128(col + 16u * (uint32_t)s0), k1 = lds128(col + 16u * (uint32_t)s1);
+        const float dx0 = fx - g0.x, dx1 = fx - g1.x;
+        // power = -0.5f * q (render.py:405-406), applied inside expf_blend
+        const float q0 = g0.y * dx0 * dx0 + g0.z * dx0 + g0.w;
+        const float q1 = g1.y * dx1 * dx1 + g1.z * dx1 + g1.w;
+        float a0 = k0.x * expf_blend<kChecked>(q0, tab, tab_s, ek);
+        float a1 = k1.x * expf_blend<kChecked>(q1, tab, tab_s, ek);
+        if (a0 > kAlphaMax) a0 = kAlphaMax;
+        if (a1 > kAlphaMax) a1 = kAlphaMax;
+        const float w0 = T[0] * a0, w1 = T[1] * a1;
+        cr[0] += w0 * k0.y;
+        cg[0] += w0 * k0.z;
+        cb[0] += w0 * k0.w;
+        cr[1] += w1 * k1.y;
+        cg[1] += w1 * k1.z;
+        cb[1] += w1 * k1.w;
+        T[0] = T[0] * (1.0f - a0);
+        T[1] = T[1] * (1.0f - a1);
+        if (T[0] < kTStop) {
+            dropped += __popc(m0);
+            m0 = 0u;
+        }
+        if (T[1] < kTStop) {
+            dropped += __popc(m1);
+            m1 = 0u;
+        }
+    }
+    n_comp -= dropped;
+}
+
 // Persistent kernel: the work items are (tile, pixel-row pair) = one warp's
 // 2x16 pixels; warps take items from a frame-global queue (ctr->blend_next)
 // until it is empty.  Item lengths vary by orders of magnitude (a warp leaves
@@ -190,7 +241,7 @@ __device__ __forceinline__ void composite(uint32_t mine, uint32_t geo, uint32_t 
 // kSets pixel rows per item (one pixel per lane per row): the batch's loads
 // and per-splat set-up are shared by the item's rows, which are composited
 // one after the other from the same staged batch.
-template <int kSets>
+template <int kSets, bool kPairLoop>
 __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kernel(
     const SplatRec *__restrict__ srec, const float4 *__restrict__ col, DepthOrder ord,
     const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
@@ -295,17 +346,32 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             }
             __syncwarp();
             const bool all_safe = __all_sync(0xffffffffu, safe);
-#pragma unroll
-            for (int h = 0; h < kSets; h++) {
-                uint32_t mine = __brev(transpose32(mask[h], lane));
-                if (done[h]) mine = 0u;
+            if (kSets == 2 && kPairLoop) {
+                uint32_t m0 = __brev(transpose32(mask[0], lane));
+                uint32_t m1 = __brev(transpose32(mask[kSets - 1], lane));
+                if (done[0]) m0 = 0u;
+                if (done[kSets - 1]) m1 = 0u;
                 if (all_safe)
-                    composite<false>(mine, geo[h], bcol, fx, s_tab, tab_s, ek, T[h], cr[h], cg[h],
-                                     cb[h], n_comp);
+                    composite_pair<false>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab, tab_s,
+                                          ek, T, cr, cg, cb, n_comp);
                 else
-                    composite<true>(mine, geo[h], bcol, fx, s_tab, tab_s, ek, T[h], cr[h], cg[h],
-                                    cb[h], n_comp);
-                done[h] = done[h] || T[h] < kTStop;
+                    composite_pair<true>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab, tab_s,
+                                         ek, T, cr, cg, cb, n_comp);
+#pragma unroll
+                for (int h = 0; h < kSets; h++) done[h] = done[h] || T[h] < kTStop;
+            } else {
+#pragma unroll
+                for (int h = 0; h < kSets; h++) {
+                    uint32_t mine = __brev(transpose32(mask[h], lane));
+                    if (done[h]) mine = 0u;
+                    if (all_safe)
+                        composite<false>(mine, geo[h], bcol, fx, s_tab, tab_s, ek, T[h], cr[h],
+                                         cg[h], cb[h], n_comp);
+                    else
+                        composite<true>(mine, geo[h], bcol, fx, s_tab, tab_s, ek, T[h], cr[h],
+                                        cg[h], cb[h], n_comp);
+                    done[h] = done[h] || T[h] < kTStop;
+                }
             }
             __syncwarp();
         }
@@ -355,16 +421,20 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
     static int sets = 0;
     if (!sets) {
         const char *e = getenv("GSR_BLEND_SETS");
-        sets = (e && atoi(e) == 1) ? 1 : 2;
+        // tuning: 1 = one row per item, 2 = two rows one after the other,
+        // 3 (default) = two rows interleaved (composite_pair)
+        sets = (e && atoi(e) >= 1 && atoi(e) <= 3) ? atoi(e) : 3;
     }
     if (!g_blend_grid) {  // persistent grid: every SM full
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sets == 1)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<1>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<1, false>, kBlendThreads, 0);
+        else if (sets == 3)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, true>, kBlendThreads, 0);
         else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, false>, kBlendThreads, 0);
         // GSR_BLEND_CTAS_PER_SM (tuning): fewer resident CTAs leave room for
         // other frames' kernels when several frames are in flight
         if (const char *e = getenv("GSR_BLEND_CTAS_PER_SM")) {
@@ -376,11 +446,14 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
     const int tiles = ((width + kTileW - 1) / kTileW) * ((height + kTileH - 1) / kTileH);
     const int grid = std::min(g_blend_grid, tiles * kTileH);
     if (sets == 1)
-        blend_kernel<1><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges, width,
-                                                       height, bg0, bg1, bg2, out, ctr);
+        blend_kernel<1, false><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
+                                                              width, height, bg0, bg1, bg2, out, ctr);
+    else if (sets == 3)
+        blend_kernel<2, true><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
+                                                             width, height, bg0, bg1, bg2, out, ctr);
     else
-        blend_kernel<2><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges, width,
-                                                       height, bg0, bg1, bg2, out, ctr);
+        blend_kernel<2, false><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
+                                                              width, height, bg0, bg1, bg2, out, ctr);
     mark("blend");
 }
 
