@@ -74,9 +74,11 @@ typedef struct gsr_stats {
     int32_t overflow_frames;  /* frames since the last finish whose tile keys overflowed */
     /* work counters of the last frame (roofline units) */
     int64_t pairs;              /* P: (splat, 16-row tile row) pairs */
-    int64_t composited;         /* E: composited (pixel, splat) evaluations */
-    int64_t row_evals_blend;    /* (splat, pixel row) interval evaluations in the blend */
+    int64_t composited;         /* E: composited (pixel, splat) evaluations (*) */
+    int64_t row_evals_blend;    /* (splat, pixel row) interval evaluations in the blend (*) */
     int64_t row_evals_binning;  /* (splat, pixel row) interval evaluations in the binning */
+    /* (*) counted only while gsr_ctx_set_kernel_timing is on (the counting
+     *     costs blend instructions), else 0 */
 } gsr_stats;
 
 GSR_API int gsr_abi_version(void);

@@ -146,7 +146,7 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
     return v;
 }
 
-template <bool kChecked>
+template <bool kChecked, bool kCount = true>
 __device__ __forceinline__ void composite(uint32_t mine, uint32_t geo, uint32_t col,
                                           float fx, const unsigned long long *tab, uint32_t tab_s,
                                           const ExpK &ek, float &T, float &cr, float &cg,
@@ -186,13 +186,13 @@ __device__ __forceinline__ void composite(uint32_t mine, uint32_t geo, uint32_t 
 // 1 (two independent chains; a pixel with nothing left reads the null slot
 // of its row, alpha 0), so the loop runs max over lanes of max(count0,
 // count1) iterations instead of max count0 + max count1.
-template <bool kChecked>
+template <bool kChecked, bool kCount>
 __device__ __forceinline__ void composite_pair(uint32_t m0, uint32_t m1, uint32_t geo0,
                                                uint32_t geo1, uint32_t col, float fx,
                                                const unsigned long long *tab, uint32_t tab_s,
                                                const ExpK &ek, float *T, float *cr, float *cg,
                                                float *cb, uint32_t &n_comp) {
-    n_comp += __popc(m0) + __popc(m1);
+    if (kCount) n_comp += __popc(m0) + __popc(m1);
     uint32_t dropped = 0u;
     while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
         const int s0 = 31 - __clz(m0), s1 = 31 - __clz(m1);
@@ -221,15 +221,15 @@ __device__ __forceinline__ void composite_pair(uint32_t m0, uint32_t m1, uint32_
         T[0] = T[0] * (1.0f - a0);
         T[1] = T[1] * (1.0f - a1);
         if (T[0] < kTStop) {
-            dropped += __popc(m0);
+            if (kCount) dropped += __popc(m0);
             m0 = 0u;
         }
         if (T[1] < kTStop) {
-            dropped += __popc(m1);
+            if (kCount) dropped += __popc(m1);
             m1 = 0u;
         }
     }
-    n_comp -= dropped;
+    if (kCount) n_comp -= dropped;
 }
 
 // Persistent kernel: the work items are (tile, pixel-row pair) = one warp's
@@ -241,7 +241,7 @@ __device__ __forceinline__ void composite_pair(uint32_t m0, uint32_t m1, uint32_
 // kSets pixel rows per item (one pixel per lane per row): the batch's loads
 // and per-splat set-up are shared by the item's rows, which are composited
 // one after the other from the same staged batch.
-template <int kSets, bool kPairLoop>
+template <int kSets, bool kPairLoop, bool kCount>
 __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kernel(
     const SplatRec *__restrict__ srec, const float4 *__restrict__ col, DepthOrder ord,
     const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
@@ -352,11 +352,11 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                 if (done[0]) m0 = 0u;
                 if (done[kSets - 1]) m1 = 0u;
                 if (all_safe)
-                    composite_pair<false>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab, tab_s,
-                                          ek, T, cr, cg, cb, n_comp);
+                    composite_pair<false, kCount>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab,
+                                                  tab_s, ek, T, cr, cg, cb, n_comp);
                 else
-                    composite_pair<true>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab, tab_s,
-                                         ek, T, cr, cg, cb, n_comp);
+                    composite_pair<true, kCount>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab,
+                                                 tab_s, ek, T, cr, cg, cb, n_comp);
 #pragma unroll
                 for (int h = 0; h < kSets; h++) done[h] = done[h] || T[h] < kTStop;
             } else {
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
         e += __shfl_xor_sync(0xffffffffu, e, o);
         r += __shfl_xor_sync(0xffffffffu, r, o);
     }
-    if (lane == 0) {
+    if (lane == 0 && kCount) {
         atomicAdd(&ctr->E, e);
         atomicAdd(&ctr->Rb, r);
     }
@@ -417,7 +417,7 @@ int g_blend_grid = 0;
 void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
                   const uint32_t *tile_vals, const uint2 *ranges, int width,
                   int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
-                  cudaStream_t s, const KMark &mark) {
+                  cudaStream_t s, const KMark &mark, bool count) {
     static int sets = 0;
     if (!sets) {
         const char *e = getenv("GSR_BLEND_SETS");
@@ -430,11 +430,11 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sets == 1)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<1, false>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<1, false, true>, kBlendThreads, 0);
         else if (sets == 3)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, true>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, true, false>, kBlendThreads, 0);
         else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, false>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, false, true>, kBlendThreads, 0);
         // GSR_BLEND_CTAS_PER_SM (tuning): fewer resident CTAs leave room for
         // other frames' kernels when several frames are in flight
         if (const char *e = getenv("GSR_BLEND_CTAS_PER_SM")) {
@@ -446,13 +446,16 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
     const int tiles = ((width + kTileW - 1) / kTileW) * ((height + kTileH - 1) / kTileH);
     const int grid = std::min(g_blend_grid, tiles * kTileH);
     if (sets == 1)
-        blend_kernel<1, false><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
+        blend_kernel<1, false, true><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
                                                               width, height, bg0, bg1, bg2, out, ctr);
-    else if (sets == 3)
-        blend_kernel<2, true><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
-                                                             width, height, bg0, bg1, bg2, out, ctr);
+    else if (sets == 3 && count)
+        blend_kernel<2, true, true><<<grid, kBlendThreads, 0, s>>>(
+            srec, col, ord, tile_vals, ranges, width, height, bg0, bg1, bg2, out, ctr);
+    else if (sets == 3)  // work counters (E, Rb) only when kernel timing asks for them
+        blend_kernel<2, true, false><<<grid, kBlendThreads, 0, s>>>(
+            srec, col, ord, tile_vals, ranges, width, height, bg0, bg1, bg2, out, ctr);
     else
-        blend_kernel<2, false><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
+        blend_kernel<2, false, true><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
                                                               width, height, bg0, bg1, bg2, out, ctr);
     mark("blend");
 }

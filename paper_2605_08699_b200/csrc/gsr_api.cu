@@ -285,7 +285,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
     launch_blend(c->srec.as<SplatRec>(), c->col.as<float4>(), ord, c->tile_vals.as<uint32_t>(),
                  c->ranges.as<uint2>(), W, H,
-                 bg[0], bg[1], bg[2], out, ctr, s, mark);
+                 bg[0], bg[1], bg[2], out, ctr, s, mark, c->ktime != 0);
     cudaEventRecord(c->ev[5], s);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(c->hsched, dsched, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);

@@ -170,7 +170,8 @@ struct DepthOrder {  // depth rank -> Gaussian index (the depth sort's result bu
 void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
                   const uint32_t *tile_vals, const uint2 *ranges, int width,
                   int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
-                  cudaStream_t s, const KMark &mark = KMark());
+                  cudaStream_t s, const KMark &mark = KMark(),
+                  bool count = true);  // count: fill the E / Rb work counters
 
 // jpeg.cu: baseline JPEG of a device u8 frame (Pillow / libjpeg-turbo exact)
 struct JpegLayout {
