@@ -75,7 +75,7 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->pad2 = 0;
 }
 
-__global__ void __launch_bounds__(256) preprocess_geo_kernel(
+__global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
     SceneView sc, CameraArgs cam, int do_cull, unsigned long long *__restrict__ keys,
     GeoRec *__restrict__ geo, uint8_t *__restrict__ keep_out,
     FrameCounters *ctr) {
