@@ -10,7 +10,7 @@
 //
 // Every splat covers a run of tile rows and, in each, one contiguous run of
 // tile columns.  So the lists are built from (splat, tile row) pairs:
-//  1a gather   block of 256 depth ranks: gathers the depth-sorted geometry
+//  1a gather   block of 512 depth ranks: gathers the depth-sorted geometry
 //              records (sort_splats' column gathers, render.py:295-302) and counts
 //              its pairs per tile row (row range only, no interval math).
 //  1b row_scan exclusive scan of those counts, tile-row major: each (row,

@@ -1,4 +1,4 @@
-// blend.cu -- K6: per-16x16-tile front-to-back alpha blending.
+// blend.cu -- K6: per-tile (32x64) front-to-back alpha blending.
 //
 // Restates _composite_kernel's per-pixel arithmetic (render.py:383-427) with
 // its exact f32 operation order and glibc expf, so frames are float-identical
@@ -233,7 +233,7 @@ __device__ __forceinline__ void composite_pair(uint32_t m0, uint32_t m1, uint32_
 }
 
 // Persistent kernel: the work items are (tile, pixel-row pair) = one warp's
-// 2x16 pixels; warps take items from a frame-global queue (ctr->blend_next)
+// 2x32 pixels; warps take items from a frame-global queue (ctr->blend_next)
 // until it is empty.  Item lengths vary by orders of magnitude (a warp leaves
 // as soon as its 32 pixels saturate, or walks the whole tile list if they
 // never do), so binding 8 warps to a CTA per tile would leave most of a CTA's
