@@ -173,9 +173,11 @@ GSR_API int gsr_ctx_kernel_times(gsr_ctx *ctx, int max, char *names, float *ms, 
 
 /* ---- the hot path: render_framebuffer (render.py:516-524) ----------------
  * project (render.py:163-290) -> stable f64 depth sort (293-302) -> tile
- * binning -> tile sort -> 16x16 front-to-back blend (430-473) -> u8
- * (484-485).  Outputs are optional host buffers:
- *   out_u8   (H,W,3) u8   = framebuffer_to_u8(fb)
+ * lists in depth order (32x64 device tiles) -> front-to-back blend
+ * (430-473) -> u8 (484-485).  Outputs are optional host buffers:
+ *   out_u8   (H,W,3) u8   = framebuffer_to_u8(fb); page-locked memory with
+ *                           W % 32 == 0 is written by the blend kernel
+ *                           directly (GSR_ZERO_COPY=0: copied instead)
  *   out_rgb  (H,W,3) f32  = rgb before the reference's clip (render.py:470)
  *   out_T    (H,W)   f32  = transmittance (alpha = 1 - T)
  * Synchronous: returns after the frame (and copies) completed. */

@@ -232,6 +232,15 @@ __device__ __forceinline__ void composite_pair(uint32_t m0, uint32_t m1, uint32_
     if (kCount) n_comp -= dropped;
 }
 
+// render.py:470 + 484-485: trunc(clip(clip(f64(c), 0, 1) * 255 + 0.5, 0, 255))
+__device__ __forceinline__ uint32_t to_u8(float c) {
+    double d = (double)c;
+    d = d < 0.0 ? 0.0 : (d > 1.0 ? 1.0 : d);
+    double q = d * 255.0 + 0.5;
+    q = q < 0.0 ? 0.0 : (q > 255.0 ? 255.0 : q);
+    return (uint32_t)(int)q;
+}
+
 // Persistent kernel: the work items are (tile, pixel-row pair) = one warp's
 // 2x32 pixels; warps take items from a frame-global queue (ctr->blend_next)
 // until it is empty.  Item lengths vary by orders of magnitude (a warp leaves
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
         }
 #pragma unroll
         for (int h = 0; h < kSets; h++) {
-            if (!inside[h]) continue;
+            if (!inside[h]) continue;  // warp-uniform when out.packed
             const float rr = cr[h] + T[h] * bg0, gg = cg[h] + T[h] * bg1, bb = cb[h] + T[h] * bg2;
             const int64_t p = (int64_t)(iy0 + h) * width + ix;
             if (out.rgb) {
@@ -386,15 +395,26 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                 out.rgb[3 * p + 2] = bb;
             }
             if (out.trans) out.trans[p] = T[h];
-            // render.py:470 + 484-485: trunc(clip(clip(f64(c), 0, 1) * 255 + 0.5, 0, 255))
-            const float ch[3] = {rr, gg, bb};
-#pragma unroll
-            for (int k = 0; k < 3; k++) {
-                double d = (double)ch[k];
-                d = d < 0.0 ? 0.0 : (d > 1.0 ? 1.0 : d);
-                double q = d * 255.0 + 0.5;
-                q = q < 0.0 ? 0.0 : (q > 255.0 ? 255.0 : q);
-                out.u8[3 * p + k] = (uint8_t)(int)q;
+            const uint32_t px = to_u8(rr) | (to_u8(gg) << 8) | (to_u8(bb) << 16);
+            if (out.packed) {
+                // the warp's 32 pixels are 96 contiguous bytes: lane l < 24
+                // stores bytes 4l..4l+3 (pixels 4l/3 and (4l+3)/3) as one word,
+                // so a row is three full 32 B sectors (and full-sector writes
+                // when the copy goes to mapped host memory)
+                const int a = (4 * lane) / 3, b = min((4 * lane + 3) / 3, 31);
+                const uint32_t pa = __shfl_sync(0xffffffffu, px, a);
+                const uint32_t pb = __shfl_sync(0xffffffffu, px, b);
+                const unsigned long long both = (unsigned long long)pa | ((unsigned long long)pb << 24);
+                const uint32_t word = (uint32_t)(both >> (8 * (lane % 3)));
+                const int64_t wofs = (3 * (p - lane)) / 4 + lane;
+                if (lane < 24) {
+                    reinterpret_cast<uint32_t *>(out.u8)[wofs] = word;
+                    if (out.host) reinterpret_cast<uint32_t *>(out.host)[wofs] = word;
+                }
+            } else {
+                out.u8[3 * p + 0] = (uint8_t)(px & 0xffu);
+                out.u8[3 * p + 1] = (uint8_t)((px >> 8) & 0xffu);
+                out.u8[3 * p + 2] = (uint8_t)(px >> 16);
             }
         }
     }

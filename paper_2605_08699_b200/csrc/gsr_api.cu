@@ -9,6 +9,8 @@
 // overflow the buffer grows and the frame is re-rendered once).
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -91,6 +93,10 @@ struct gsr_ctx {
     int tile_passes = 0;
     SavedCall saved;
     uint8_t *saved_out = nullptr;  // host destination of an enqueued frame (gsr_render_enqueue)
+    // gsr_render: device view of the caller's mapped pinned frame; the blend
+    // stores the u8 frame there directly (zc_used), so no copy follows it
+    uint8_t *zc_host = nullptr;
+    bool zc_used = false;
     bool saved_full64 = false;  // depth order via the full 64-bit sort (long key runs)
     bool pending = false;
     int retries = 0;
@@ -280,8 +286,11 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     }
     cudaEventRecord(c->ev[3], s);
     cudaEventRecord(c->ev[4], s);
+    const bool packed = W % kTileW == 0 && ((uintptr_t)c->zc_host & 3u) == 0;
+    c->zc_used = packed && c->zc_host != nullptr;
     BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
-                 want_rgb ? c->frame_t.as<float>() : nullptr};
+                 want_rgb ? c->frame_t.as<float>() : nullptr, c->zc_used ? c->zc_host : nullptr,
+                 packed};
     DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
     launch_blend(c->srec.as<SplatRec>(), c->col.as<float4>(), ord, c->tile_vals.as<uint32_t>(),
                  c->ranges.as<uint2>(), W, H,
@@ -786,6 +795,26 @@ int gsr_ctx_finish(gsr_ctx *ctx, uint8_t *out_u8, gsr_stats *stats) {
     return GSR_OK;
 }
 
+namespace {
+// Device view of `p` when it is page-locked host memory mapped into the
+// device address space (cudaHostAlloc / cudaHostRegister / torch pin_memory),
+// else null.  Probed per call: a cached answer could outlive the allocation.
+// GSR_ZERO_COPY=0 turns the direct store off (the frame is then copied).
+uint8_t *mapped_host(uint8_t *p) {
+    static const int enabled = [] {
+        const char *e = getenv("GSR_ZERO_COPY");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    if (!enabled) return nullptr;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? static_cast<uint8_t *>(at.devicePointer) : nullptr;
+}
+}  // namespace
+
 int gsr_render(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
                const float background[3], int sh_degree, int frustum_cull, uint8_t *out_u8,
                float *out_rgb, float *out_T, gsr_stats *stats) {
@@ -793,12 +822,14 @@ int gsr_render(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
     DeviceGuard g(ctx->device);
     const float zero[3] = {0, 0, 0};
     const bool want_rgb = out_rgb || out_T;
+    ctx->zc_host = out_u8 ? mapped_host(out_u8) : nullptr;
     int rc = enqueue_frame(ctx, scene, cam, background ? background : zero, sh_degree,
                            frustum_cull, want_rgb, false);
+    ctx->zc_host = nullptr;  // a re-render (complete_frame) writes the device frame only
     if (rc) return rc;
     const size_t px = (size_t)cam->width * cam->height;
     // copies ride the stream; if the frame overflows they are redone below
-    if (out_u8)
+    if (out_u8 && !ctx->zc_used)
         GSR_CUDA_OK(cudaMemcpyAsync(out_u8, ctx->frame_u8.p, px * 3, cudaMemcpyDeviceToHost,
                                     ctx->stream));
     if ((rc = complete_frame(ctx))) return rc;

@@ -162,6 +162,8 @@ struct BlendOut {
     uint8_t *u8;    // (H,W,3)
     float *rgb;     // (H,W,3) or null
     float *trans;   // (H,W) or null
+    uint8_t *host;  // device view of a mapped pinned (H,W,3) host frame, or null (needs packed)
+    bool packed;    // W % 32 == 0 and u8/host 4-byte aligned: one 96 B row segment per warp store
 };
 struct DepthOrder {  // depth rank -> Gaussian index (the depth sort's result buffer)
     const uint32_t *order0, *order1;

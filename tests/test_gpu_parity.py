@@ -426,6 +426,46 @@ def test_render_pipeline_matches_render_u8(gsr):
             assert np.array_equal(f, r)
 
 
+def test_render_u8_into_pinned_frame(gsr, oracle):
+    """A page-locked output frame is written by the blend kernel directly
+    (mapped host memory, widths that are multiples of 32) instead of copied
+    after it: same bytes as a pageable output, also for a frame re-rendered
+    with the 64-bit depth sort, and for widths that take the copy path."""
+    from paper_2605_08699_b200 import _lib
+    from paper_2605_08699_b200.synth import ActivatedPrimitives
+    ctx = _lib.context(0)
+    prims = golden_scene((20000, 3, (0.01, 0.05), 1))
+    for w, h in ((1920, 1080), (320, 240), (333, 217), (64, 1)):
+        intr = gsr.Intrinsics(fx=0.9 * w, fy=0.9 * w, cx=w / 2, cy=h / 2, width=w, height=h)
+        for k in range(2):
+            pose = gsr.CameraPose(0.03 * k, -0.02, (0.0, 0.0, 0.1 * k))
+            ref = gsr.render_u8(prims, pose, intr, sh_degree=3).copy()
+            pin = ctx.pinned(f"test_frame_{w}", (h, w, 3), np.uint8)
+            pin[...] = 0xAB
+            got = gsr.render_u8(prims, pose, intr, sh_degree=3, out=pin)
+            assert got is pin and np.array_equal(pin, ref), (w, h, k)
+    # a run of 200 equal depths: the frame is re-rendered with the full sort
+    rng = np.random.default_rng(11)
+    n = 2000
+    z = rng.uniform(2.0, 6.0, n)
+    z[:200] = 3.0
+    means = np.column_stack([rng.uniform(-1.5, 1.5, n), rng.uniform(-1.5, 1.5, n), z])
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    prims = ActivatedPrimitives(means, rng.uniform(0.01, 0.05, (n, 3)), q,
+                                rng.uniform(0.2, 0.99, n), rng.uniform(0, 1, (n, 3)),
+                                rng.normal(0, 0.2, (n, 16, 3)))
+    intr = gsr.Intrinsics(fx=120.0, fy=120.0, cx=64.0, cy=64.0, width=128, height=128)
+    rot, w2c = oracle.world_to_camera(0.0, 0.0, (0.0, 0.0, 0.0))
+    fr = oracle.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                       prims.colors_dc, prims.sh_coeffs, w2c, rot, intr.fx, intr.fy, intr.cx,
+                       intr.cy, intr.width, intr.height, (0.0, 0.0, 0.0), 0)
+    pin = ctx.pinned("test_frame_runs", (128, 128, 3), np.uint8)
+    pin[...] = 0xAB
+    gsr.render_u8(prims, gsr.CameraPose(0.0, 0.0), intr, out=pin)
+    assert np.array_equal(pin, fr.u8)
+
+
 def _pil_jpeg(img, quality):
     import io
     from PIL import Image
