@@ -763,6 +763,26 @@ int gsr_render_async(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam
                          false, false);
 }
 
+namespace {
+// Device view of `p` when it is page-locked host memory mapped into the
+// device address space (cudaHostAlloc / cudaHostRegister / torch pin_memory),
+// else null.  Probed per call: a cached answer could outlive the allocation.
+// GSR_ZERO_COPY=0 turns the direct store off (the frame is then copied).
+uint8_t *mapped_host(uint8_t *p) {
+    static const int enabled = [] {
+        const char *e = getenv("GSR_ZERO_COPY");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    if (!enabled) return nullptr;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? static_cast<uint8_t *>(at.devicePointer) : nullptr;
+}
+}  // namespace
+
 int gsr_render_enqueue(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
                        const float background[3], int sh_degree, int frustum_cull,
                        uint8_t *out_u8) {
@@ -771,6 +791,8 @@ int gsr_render_enqueue(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *c
     int rc = complete_frame(ctx);  // a ctx holds one frame in flight
     if (rc) return rc;
     const float zero[3] = {0, 0, 0};
+    // the frame is copied after the blend (a copy engine transfer overlaps the
+    // other contexts' kernels; storing from the blend measured no faster here)
     rc = enqueue_frame(ctx, scene, cam, background ? background : zero, sh_degree, frustum_cull,
                        false, false);
     if (rc) return rc;
@@ -795,25 +817,6 @@ int gsr_ctx_finish(gsr_ctx *ctx, uint8_t *out_u8, gsr_stats *stats) {
     return GSR_OK;
 }
 
-namespace {
-// Device view of `p` when it is page-locked host memory mapped into the
-// device address space (cudaHostAlloc / cudaHostRegister / torch pin_memory),
-// else null.  Probed per call: a cached answer could outlive the allocation.
-// GSR_ZERO_COPY=0 turns the direct store off (the frame is then copied).
-uint8_t *mapped_host(uint8_t *p) {
-    static const int enabled = [] {
-        const char *e = getenv("GSR_ZERO_COPY");
-        return e && e[0] == '0' ? 0 : 1;
-    }();
-    if (!enabled) return nullptr;
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    return at.type == cudaMemoryTypeHost ? static_cast<uint8_t *>(at.devicePointer) : nullptr;
-}
-}  // namespace
 
 int gsr_render(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera *cam,
                const float background[3], int sh_degree, int frustum_cull, uint8_t *out_u8,

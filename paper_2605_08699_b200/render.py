@@ -290,8 +290,9 @@ class RenderPipeline:
     copy and launch gaps of one frame overlap the kernels of the next.  Once
     `depth` frames are in flight, `submit` first completes the oldest and
     returns it as (tag, frame); `drain` completes the rest.  A returned frame
-    is a view of a pinned slot, valid until that slot is reused (`depth`
-    submits later): copy it to keep it.  Results are the same frames
+    is a view of a pinned slot (depth + 1 slots rotate, so the frame enqueued
+    by the same `submit` never lands in the slot it returns); it stays valid
+    until the next `submit`: copy it to keep it.  Results are the same frames
     render_u8 returns, in submission order."""
 
     def __init__(self, intr, sh_degree: int = 0, background=(0.0, 0.0, 0.0), depth: int = 2,
@@ -302,37 +303,41 @@ class RenderPipeline:
         self.bg = _bg(background)
         self.ctxs = [_lib.Context(self.device) for _ in range(max(1, int(depth)))]
         shape = (int(intr.height), int(intr.width), 3)
-        self.slots = [c.pinned("pipeline", shape, np.uint8) for c in self.ctxs]
-        self.inflight = []  # (ctx index, tag), oldest first
+        d = len(self.ctxs)
+        self.slots = [self.ctxs[k % d].pinned(f"pipeline{k // d}", shape, np.uint8)
+                      for k in range(d + 1)]
+        self.inflight = []  # (ctx index, slot index, tag), oldest first
         self.next = 0
+        self.next_slot = 0
 
-    def _finish(self, i):
+    def _finish(self, i, j):
         ctx = self.ctxs[i]
         _lib.check(ctx.lib.gsr_ctx_finish(ctx.handle, None, None), "gsr_ctx_finish")
-        return self.slots[i]
+        return self.slots[j]
 
     def submit(self, prims, pose, tag=None):
         done = None
         if len(self.inflight) == len(self.ctxs):
-            i, t = self.inflight.pop(0)
-            done = (t, self._finish(i))
-        i = self.next
+            i, j, t = self.inflight.pop(0)
+            done = (t, self._finish(i, j))
+        i, j = self.next, self.next_slot
         self.next = (self.next + 1) % len(self.ctxs)
+        self.next_slot = (self.next_slot + 1) % len(self.slots)
         sc = device_scene(prims, self.device)
         _check_sh(self.sh_degree, sc.count)
         cam = make_camera(pose, self.intr)
         ctx = self.ctxs[i]
         _lib.check(ctx.lib.gsr_render_enqueue(ctx.handle, sc.handle, ctypes.byref(cam), self.bg,
-                                              self.sh_degree, 1, _lib.ptr(self.slots[i])),
+                                              self.sh_degree, 1, _lib.ptr(self.slots[j])),
                    "gsr_render_enqueue")
-        self.inflight.append((i, tag))
+        self.inflight.append((i, j, tag))
         return done
 
     def drain(self):
         out = []
         while self.inflight:
-            i, t = self.inflight.pop(0)
-            out.append((t, self._finish(i)))
+            i, j, t = self.inflight.pop(0)
+            out.append((t, self._finish(i, j)))
         return out
 
     def close(self):
