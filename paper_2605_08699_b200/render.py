@@ -207,12 +207,8 @@ def make_camera(pose, intr) -> _lib.GsrCamera:
     """Host pose math exactly as the reference (camera.py:101-108, render.py:276)."""
     view = world_to_camera(pose)
     cam = _lib.GsrCamera()
-    w = np.ascontiguousarray(view.world_to_camera[:3, :], dtype=np.float64).ravel()
-    for i in range(12):
-        cam.w2c[i] = float(w[i])
-    cp = camera_position(view)
-    for i in range(3):
-        cam.campos[i] = float(cp[i])
+    cam.w2c[:] = view.world_to_camera[:3, :].ravel().tolist()
+    cam.campos[:] = camera_position(view).tolist()
     cam.fx, cam.fy, cam.cx, cam.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
     cam.width, cam.height = int(intr.width), int(intr.height)
     return cam
