@@ -157,10 +157,14 @@ _scenes: dict = {}  # (id(prims), device) -> (weakref(prims), DeviceScene, signa
 
 
 def _signature(prims):
-    arrs = [prims.means, prims.scales, prims.rotations, prims.opacities, prims.colors_dc,
-            getattr(prims, "sh_coeffs", None)]
-    return tuple((id(a), None if a is None else (a.__array_interface__["data"][0], a.shape))
-                 for a in arrs)
+    # the attribute arrays themselves: a cached upload is reused only while
+    # the record still holds these very objects (compared with `is`)
+    return (prims.means, prims.scales, prims.rotations, prims.opacities, prims.colors_dc,
+            getattr(prims, "sh_coeffs", None))
+
+
+def _same(a, b):
+    return all(x is y for x, y in zip(a, b))
 
 
 def device_scene(prims, device: int = 0) -> DeviceScene:
@@ -174,7 +178,7 @@ def device_scene(prims, device: int = 0) -> DeviceScene:
     sig = _signature(prims)
     with _scene_lock:
         ent = _scenes.get(key)
-        if ent is not None and ent[0]() is prims and ent[2] == sig:
+        if ent is not None and ent[0]() is prims and _same(ent[2], sig):
             return ent[1]
     sc = DeviceScene(prims, device)
     with _scene_lock:
