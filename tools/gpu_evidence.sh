@@ -4,6 +4,7 @@
 mkdir -p gpurun_out tools/_build
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3 | tee gpurun_out/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 | tee gpurun_out/smoke.txt
 nvcc -O3 -fmad=false -gencode arch=compute_100a,code=sm_100a tools/peaks.cu -o tools/_build/peaks && \
   tools/_build/peaks > gpurun_out/measured_simt_peaks.json
 cat gpurun_out/measured_simt_peaks.json
