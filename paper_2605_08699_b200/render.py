@@ -218,8 +218,18 @@ def make_camera(pose, intr) -> _lib.GsrCamera:
     return cam
 
 
+_bg_cache: dict = {}
+
+
 def _bg(background):
-    return (ctypes.c_float * 3)(*[float(np.float32(b)) for b in background])
+    """float[3] background (f32, as rasterize packs it), cached per value."""
+    key = tuple(background)
+    arr = _bg_cache.get(key)
+    if arr is None:
+        arr = (ctypes.c_float * 3)(*[float(np.float32(b)) for b in background])
+        if len(_bg_cache) < 64:
+            _bg_cache[key] = arr
+    return arr
 
 
 def _check_sh(sh_degree, n):
