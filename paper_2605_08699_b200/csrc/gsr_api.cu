@@ -228,9 +228,11 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     launch_frame_init(ctr, s);
     mark("frame_init");
     if (n > 0) {
-        launch_preprocess(sc->view, ca, sh_degree, cull, c->keys[0].as<unsigned long long>(),
-                          c->geo.as<GeoRec>(), c->col.as<float4>(),
-                          want_keep ? c->keep.as<uint8_t>() : nullptr, ctr, s, mark);
+        launch_preprocess_geo(sc->view, ca, cull, c->keys[0].as<unsigned long long>(),
+                              c->geo.as<GeoRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr,
+                              ctr, s, mark);
+        launch_preprocess_color(sc->view, ca, sh_degree, c->keys[0].as<unsigned long long>(),
+                                c->col.as<float4>(), s, mark);
         launches += 2;
     }
     cudaEventRecord(c->ev[1], s);

@@ -64,10 +64,15 @@ struct CameraArgs {
 // preprocess.cu (2 kernels)
 using GeoRec = SplatRec;  // by Gaussian index (preprocess), by depth rank (gather)
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
-void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                       int frustum_cull, unsigned long long *keys, GeoRec *geo,
-                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s,
-                       const KMark &mark = KMark());
+// K1a: projection, culling, depth keys, packed geometry (render.py:163-290)
+void launch_preprocess_geo(const SceneView &scene, const CameraArgs &cam, int frustum_cull,
+                           unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
+                           FrameCounters *ctr, cudaStream_t s, const KMark &mark = KMark());
+// K1b: SH colours of the kept Gaussians (render.py:126-160); needs the keys
+// of K1a, read only by the blend, so it may run beside the depth sort
+void launch_preprocess_color(const SceneView &scene, const CameraArgs &cam, int sh_degree,
+                             const unsigned long long *keys, float4 *col, cudaStream_t s,
+                             const KMark &mark = KMark());
 
 // radix.cu: Onesweep stable LSD sort (see radix.cu header)
 cudaError_t radix_init_attributes();

@@ -240,16 +240,23 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
     frame_init_kernel<<<1, 1, 0, s>>>(ctr);
 }
 
-void launch_preprocess(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                       int frustum_cull, unsigned long long *keys, GeoRec *geo,
-                       float4 *col, uint8_t *keep_out, FrameCounters *ctr, cudaStream_t s,
-                       const KMark &mark) {
+void launch_preprocess_geo(const SceneView &scene, const CameraArgs &cam, int frustum_cull,
+                           unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
+                           FrameCounters *ctr, cudaStream_t s, const KMark &mark) {
     if (scene.n == 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
     preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, cam, frustum_cull, keys, geo,
                                                      keep_out, ctr);
     mark("preprocess_geo");
+}
+
+void launch_preprocess_color(const SceneView &scene, const CameraArgs &cam, int sh_degree,
+                             const unsigned long long *keys, float4 *col, cudaStream_t s,
+                             const KMark &mark) {
+    if (scene.n == 0) return;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
 #define GSR_COLOR(T, D)                                                                   \
     preprocess_color_kernel<T, D><<<blocks, threads, 0, s>>>(scene, cam, keys, col)
     if (sh_degree == 0) GSR_COLOR(float, 0);
