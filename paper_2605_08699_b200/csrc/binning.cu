@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     // rank of each (splat, row) among the block's splats covering that row:
     // per-warp coverage bitmasks per tile row (shared atomics, one per pair)
     // give the in-warp rank, a prefix of the popcounts over warps the rest
-    const int ylo = S.ty_lo, yhi = S.ty_hi;
+    // a block whose splats cover no row (all ranges empty) keeps ty_lo at its
+    // sentinel: start the loops at 0 so `ylo + lane` cannot overflow
+    const int yhi = S.ty_hi, ylo = yhi >= 0 ? S.ty_lo : 0;
     const uint32_t lt_mask = (1u << lane) - 1u;
     uint32_t *wm = wpre_all + w * nr;
     for (int ty = ylo + lane; ty <= yhi; ty += 32) wm[ty] = 0u;
