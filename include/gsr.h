@@ -71,14 +71,19 @@ typedef struct gsr_stats {
     float ms_device;          /* CUDA-event time of the whole device pipeline */
     float ms_preprocess, ms_depth_sort, ms_binning, ms_tile_sort, ms_blend;
     int32_t kernel_launches;  /* kernels this ctx launched since the last finish/render */
-    int32_t overflow_frames;  /* frames since the last finish whose tile keys overflowed */
+    int32_t overflow_frames;  /* frames since the last finish whose pair/tile buffers overflowed
+                                 (re-rendered when completed through finish/render) */
     /* work counters of the last frame (roofline units) */
-    int64_t pairs;              /* P: (splat, 16-row tile row) pairs */
+    int64_t pairs;              /* P: (splat, 64-row tile row) pairs of the render path */
     int64_t composited;         /* E: composited (pixel, splat) evaluations (*) */
     int64_t row_evals_blend;    /* (splat, pixel row) interval evaluations in the blend (*) */
     int64_t row_evals_binning;  /* (splat, pixel row) interval evaluations in the binning */
     /* (*) counted only while gsr_ctx_set_kernel_timing is on (the counting
      *     costs blend instructions), else 0 */
+    int32_t long_run_frames;  /* frames since the last finish whose 32-bit depth keys had a
+                                 run too long for the fix-up (re-rendered with the 64-bit
+                                 sort when completed through finish/render) */
+    int32_t reserved;
 } gsr_stats;
 
 GSR_API int gsr_abi_version(void);
@@ -214,6 +219,22 @@ GSR_API int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr
  * query sizes through stats->tile_keys. */
 GSR_API int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_ranks,
                          int32_t *out_ranges, gsr_stats *stats);
+/* The exact tile-list contract (a depth rank is listed in a
+ * tile x tile tile iff some row of the tile row has a non-empty reference
+ * interval, render.py:329-333 + 384-397, reaching that tile column) of the
+ * last render on ctx, built on the device from 64-bit (tile | rank) keys, a
+ * radix sort and per-tile range identification (north_star item 2).  The
+ * render path itself blends from conservative 32 x 64 superset lists
+ * (gsr_debug_tile_lists); this entry exists so the contract can be compared
+ * bit for bit with the reference's rows.  First call (outputs NULL) builds
+ * the lists and returns *out_count = D; later calls for the same frame and
+ * tile size copy them out: out_tiles/out_ranks (D,) sorted by (tile, rank),
+ * out_ranges (n_tiles, 2) [start, end) with n_tiles = ceil(W/tile) *
+ * ceil(H/tile).  *out_ms (nullable): device time of the key, sort and range
+ * kernels.  1 <= tile <= 256. */
+GSR_API int gsr_debug_contract_tiles(gsr_ctx *ctx, int tile, int64_t *out_count,
+                         int32_t *out_tiles, int32_t *out_ranks, int32_t *out_ranges,
+                         float *out_ms);
 
 /* ---- ladder resample: metrics.upscale_to (metrics.py:125-130), Pillow
  * BILINEAR bit-exact.  Host (h,w,3) u8 in, host (H,W,3) u8 out. ---------- */

@@ -50,7 +50,8 @@ class GsrStats(ctypes.Structure):
                 ("ms_blend", ctypes.c_float), ("kernel_launches", ctypes.c_int32),
                 ("overflow_frames", ctypes.c_int32), ("pairs", ctypes.c_int64),
                 ("composited", ctypes.c_int64), ("row_evals_blend", ctypes.c_int64),
-                ("row_evals_binning", ctypes.c_int64)]
+                ("row_evals_binning", ctypes.c_int64), ("long_run_frames", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -101,6 +102,8 @@ SIGNATURES = [
     ("gsr_debug_preprocess", _i32, [_vp, _vp, _P(GsrCamera), _i32, _i32, _vp, _vp, _vp,
                                     _P(GsrStats)]),
     ("gsr_debug_tile_lists", _i32, [_vp, _vp, _vp, _vp, _P(GsrStats)]),
+    ("gsr_debug_contract_tiles", _i32, [_vp, _i32, _P(_i64), _vp, _vp, _vp,
+                                        _P(ctypes.c_float)]),
     ("gsr_resample_bilinear_u8", _i32, [_vp, _vp, _i32, _i32, _vp, _i32, _i32]),
     ("gsr_ssim_u8", _i32, [_vp, _vp, _vp, _i32, _i32, _P(_dbl)]),
     ("gsr_ssim_luma_f64", _i32, [_vp, _vp, _vp, _i32, _i32, _P(_dbl)]),
@@ -186,23 +189,20 @@ class Context:
         self._pinned = {}
 
     def pinned(self, key: str, shape, dtype) -> np.ndarray:
-        """A page-locked host array (reused per key) for fast readback."""
+        """A page-locked host array (reused per key) for fast readback.  The
+        memory belongs to a PinnedBlock that every returned view references
+        (through numpy's base chain), so it is freed only when the context
+        has dropped it (close, or a larger request for the key) AND the last
+        view is gone: arrays returned from here never dangle."""
         nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
-        cur = self._pinned.get(key)
-        if cur is None or cur[1] < nbytes:
-            if cur is not None:
-                self.lib.gsr_host_free(cur[0])
-            p = ctypes.c_void_p()
-            check(self.lib.gsr_host_alloc(ctypes.byref(p), max(nbytes, 1)), "gsr_host_alloc")
-            cur = (p, max(nbytes, 1))
-            self._pinned[key] = cur
-        buf = (ctypes.c_uint8 * cur[1]).from_address(cur[0].value)
-        return np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
+        blk = self._pinned.get(key)
+        if blk is None or blk.nbytes < nbytes:
+            blk = PinnedBlock(self.lib, max(nbytes, 1))
+            self._pinned[key] = blk  # the old block lives on in its views, if any
+        return np.asarray(blk)[:nbytes].view(dtype).reshape(shape)
 
     def close(self):
         if getattr(self, "handle", None) is not None:
-            for p, _ in self._pinned.values():
-                self.lib.gsr_host_free(p)
             self._pinned = {}
             self.lib.gsr_ctx_destroy(self.handle)
             self.handle = None
@@ -210,6 +210,31 @@ class Context:
     def __del__(self):  # pragma: no cover - interpreter shutdown order
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class PinnedBlock:
+    """cudaHostAlloc'd bytes (gsr_host_alloc) freed when the block object
+    dies; numpy arrays made from it keep it alive via __array_interface__."""
+
+    def __init__(self, lib, nbytes: int):
+        self.lib = lib
+        self.nbytes = int(nbytes)
+        p = ctypes.c_void_p()
+        check(lib.gsr_host_alloc(ctypes.byref(p), self.nbytes), "gsr_host_alloc")
+        self.ptr = p
+
+    @property
+    def __array_interface__(self):
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr.value, False),
+                "version": 3}
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            if self.ptr is not None and self.ptr.value:
+                self.lib.gsr_host_free(self.ptr)
+                self.ptr = None
         except Exception:
             pass
 

@@ -44,7 +44,8 @@ __global__ void depth_fixup_kernel(DepthArgs a) {
     while (e < K && e - i <= kMaxRun && ks[e] == c) e++;
     const int len = (int)(e - i);
     if (len > kMaxRun) {
-        atomicOr(&a.ctr->long_runs, 1u);
+        if (atomicOr(&a.ctr->long_runs, 1u) == 0u && a.long_run_sticky)
+            atomicAdd(a.long_run_sticky, 1u);
         return;
     }
     uint32_t idx[kMaxRun];

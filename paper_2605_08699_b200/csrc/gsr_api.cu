@@ -52,7 +52,11 @@ int ensure(DevBuf &b, size_t bytes) {
 using namespace gsr;
 
 struct SavedCall {
+    // the scene of the frame in flight, needed only to re-render it inside
+    // complete_frame; cleared once the frame completes (the caller may free
+    // the scene as soon as its frame is finished)
     const gsr_scene *scene = nullptr;
+    int64_t scene_n = 0;
     gsr_camera cam{};
     float bg[3] = {0, 0, 0};
     int sh_degree = 0;
@@ -73,8 +77,14 @@ struct gsr_ctx {
     DevBuf row_blk, row_start, scan_work, pairs, seg_row, seg_cnt, ttotal, tstart, tile_vals;
     DevBuf ranges;
     DevBuf frame_u8, frame_rgb, frame_t;
-    DevBuf ctr, sticky;
+    // device FrameCounters followed by two sticky per-context counters
+    // (frames whose pair/tile buffers overflowed, frames that needed the
+    // 64-bit depth re-sort); one D2H copy per frame brings all of them back
+    DevBuf ctr;
     FrameCounters *hctr = nullptr;
+    uint32_t sticky_seen[2] = {0, 0};  // sticky values reported by the last fill_stats
+    uint32_t *dsticky() { return reinterpret_cast<uint32_t *>(ctr.as<FrameCounters>() + 1); }
+    const uint32_t *hsticky() const { return reinterpret_cast<const uint32_t *>(hctr + 1); }
     int64_t launches = 0;  // kernels enqueued since the last finish/render
     cudaEvent_t ev[8] = {};
     // per-kernel event timeline of the last frame (gsr_ctx_set_kernel_timing)
@@ -86,6 +96,12 @@ struct gsr_ctx {
     // ladder / resample / ssim scratch
     DevBuf base_u8, up_u8, tmp_u8, src_u8, dst_u8, coefs, ssim_part, ssim_misc, ssim_w;
     DevBuf jpeg_ws;                  // jpeg.cu workspace
+    // contract tile lists of the last frame (gsr_debug_contract_tiles, contract.cu)
+    DevBuf ckeys[2], cvals[2], cwork, csched, cranges, cdcount;
+    int64_t cap_c = 0, contract_d = 0;
+    int contract_tile = 0;  // tile size of the lists built for the last frame, 0 = none
+    int contract_buf = 0;   // which of ckeys holds the sorted keys
+    float contract_ms = 0.0f;
     uint32_t *hjpeg = nullptr;       // pinned [bits, stuffed bytes]
     double *hssim = nullptr;
     // last frame
@@ -106,7 +122,8 @@ struct gsr_ctx {
                                &geo, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
-                               &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws};
+                               &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
+                               &cvals[0], &cvals[1], &cwork, &csched, &cranges, &cdcount};
         for (auto *b : all) s += (int64_t)b->bytes;
         return s;
     }
@@ -213,6 +230,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     const CameraArgs ca = camera_args(cam);
     c->W = W;
     c->H = H;
+    c->contract_tile = 0;
     c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
     uint32_t *dsched = c->sched.as<uint32_t>();
     int launches = 2;  // frame init + blend
@@ -250,6 +268,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         da.work64 = c->depth_work.p;
         da.sched = dsched;
         da.full64 = c->saved_full64;
+        da.long_run_sticky = c->dsticky() + 1;
         launches += launch_depth_sort(da, c->sms, s, mark);
     }
     cudaEventRecord(c->ev[2], s);
@@ -281,7 +300,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.ranges = c->ranges.as<uint2>();
         ba.tile_vals = c->tile_vals.as<uint32_t>();
         ba.cap_d = c->cap_d;
-        ba.overflow_sticky = c->sticky.as<uint32_t>();
+        ba.overflow_sticky = c->dsticky();
         launches += launch_binning(ba, s, mark);
     } else {
         cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
@@ -298,11 +317,13 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
                  c->ranges.as<uint2>(), W, H,
                  bg[0], bg[1], bg[2], out, ctr, s, mark, c->ktime != 0);
     cudaEventRecord(c->ev[5], s);
-    cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters) + 2 * sizeof(uint32_t),
+                    cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(c->hsched, dsched, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     GSR_CUDA_OK(cudaGetLastError());
     c->launches += launches;
     c->saved.scene = sc;
+    c->saved.scene_n = n;
     c->saved.cam = *cam;
     for (int i = 0; i < 3; i++) c->saved.bg[i] = bg[i];
     c->saved.sh_degree = sh_degree;
@@ -374,10 +395,12 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     st->ms_blend = t[5];
     st->kernel_launches = (int32_t)c->launches;
     c->launches = 0;
-    uint32_t ov = 0;
-    if (cudaMemcpy(&ov, c->sticky.p, sizeof(ov), cudaMemcpyDeviceToHost) == cudaSuccess && ov)
-        cudaMemset(c->sticky.p, 0, sizeof(ov));
-    st->overflow_frames = (int32_t)ov;
+    // sticky counters as of the last completed frame's copy (no extra sync)
+    const uint32_t *hs = c->hsticky();
+    st->overflow_frames = (int32_t)(hs[0] - c->sticky_seen[0]);
+    st->long_run_frames = (int32_t)(hs[1] - c->sticky_seen[1]);
+    c->sticky_seen[0] = hs[0];
+    c->sticky_seen[1] = hs[1];
     st->pairs = (int64_t)c->hctr->P;
     st->composited = (int64_t)c->hctr->E;
     st->row_evals_blend = (int64_t)c->hctr->Rb;
@@ -664,7 +687,8 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     if (e == cudaSuccess) e = binning_init_attributes();
     for (int i = 0; i < 8 && e == cudaSuccess; i++) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i <= gsr_ctx::kMaxMarks && e == cudaSuccess; i++) e = cudaEventCreate(&c->kev[i]);
-    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters));
+    if (e == cudaSuccess)
+        e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters) + 4 * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hssim, sizeof(double) * 64);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hsched, sizeof(uint32_t) * 64);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hjpeg, sizeof(uint32_t) * 4);
@@ -673,13 +697,13 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
         gsr_ctx_destroy(c);
         return rc;
     }
-    int rc = ensure(c->ctr, sizeof(FrameCounters));
-    if (!rc) rc = ensure(c->sticky, sizeof(uint32_t));
+    int rc = ensure(c->ctr, sizeof(FrameCounters) + 4 * sizeof(uint32_t));
     if (!rc) rc = ensure(c->sched, 64 * sizeof(uint32_t));
     if (!rc && cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
-    if (!rc && cudaMemset(c->sticky.p, 0, sizeof(uint32_t)) != cudaSuccess)
+    if (!rc && cudaMemset(c->ctr.p, 0, c->ctr.bytes) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
+    if (!rc) std::memset(c->hctr, 0, sizeof(FrameCounters) + 4 * sizeof(uint32_t));
     if (!rc) rc = ensure(c->ssim_misc, 64);
     if (!rc) rc = ensure(c->ssim_w, sizeof(double) * 11);
     if (rc) {
@@ -915,6 +939,100 @@ int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_ranks,
     if (stats) {
         stats->tile_keys = ctx->hctr->D;
         stats->splats_drawn = ctx->hctr->K;
+    }
+    return GSR_OK;
+}
+
+namespace {
+// Builds the contract lists of the last frame (contract.cu): keys, then --
+// once their count is known on the host -- the 64-bit radix sort and the
+// ranges.  Two attempts: the first with the capacity of the previous frame.
+int build_contract(gsr_ctx *c, int tile) {
+    const int64_t k = (int64_t)c->hctr->K;
+    const int tiles_x = (c->W + tile - 1) / tile, ntiles = tiles_x * ((c->H + tile - 1) / tile);
+    int rc;
+    if (c->cap_c == 0) c->cap_c = round_up(std::max<int64_t>(int64_t(1) << 20, 8 * k), 4096);
+    if ((rc = ensure(c->cdcount, sizeof(unsigned long long)))) return rc;
+    if ((rc = ensure(c->csched, 64 * sizeof(uint32_t)))) return rc;
+    if ((rc = ensure(c->cranges, sizeof(uint2) * (size_t)std::max(ntiles, 1)))) return rc;
+    float t_keys = 0.0f, t_sort = 0.0f;
+    unsigned long long d = 0;
+    for (int attempt = 0;; attempt++) {
+        for (int i = 0; i < 2; i++) {
+            if ((rc = ensure(c->ckeys[i], sizeof(unsigned long long) * c->cap_c))) return rc;
+            if ((rc = ensure(c->cvals[i], sizeof(uint32_t) * c->cap_c))) return rc;
+        }
+        ContractArgs a;
+        a.srec = c->srec.as<SplatRec>();
+        a.ctr = c->ctr.as<FrameCounters>();
+        a.width = c->W;
+        a.tile = tile;
+        a.tiles_x = tiles_x;
+        a.keys = c->ckeys[0].as<unsigned long long>();
+        a.cap = c->cap_c;
+        a.d_count = c->cdcount.as<unsigned long long>();
+        GSR_CUDA_OK(cudaMemsetAsync(a.d_count, 0, sizeof(unsigned long long), c->stream));
+        cudaEventRecord(c->ev[6], c->stream);
+        launch_contract_keys(a, k, c->stream);
+        cudaEventRecord(c->ev[7], c->stream);
+        GSR_CUDA_OK(cudaMemcpyAsync(&d, a.d_count, sizeof(d), cudaMemcpyDeviceToHost, c->stream));
+        GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
+        GSR_CUDA_OK(cudaEventElapsedTime(&t_keys, c->ev[6], c->ev[7]));
+        if ((int64_t)d <= c->cap_c) break;
+        if (attempt == 1) return fail(GSR_E_OOM, "contract key buffer overflow");
+        if (d >= (1ull << 30)) return fail(GSR_E_OOM, "contract lists exceed 2^30 entries");
+        c->cap_c = round_up((int64_t)d + (int64_t)d / 8 + 4096, 4096);
+    }
+    if ((rc = ensure(c->cwork, sort_work_bytes(std::max<int64_t>((int64_t)d, 1), 8, 8)))) return rc;
+    cudaEventRecord(c->ev[6], c->stream);
+    launch_onesweep_sort<unsigned long long>(
+        c->ckeys[0].as<unsigned long long>(), c->ckeys[1].as<unsigned long long>(),
+        c->cvals[0].as<uint32_t>(), c->cvals[1].as<uint32_t>(), true, false, nullptr,
+        (int64_t)d, (int64_t)d, 8, false, c->cwork.p, c->csched.as<uint32_t>(), nullptr, c->sms,
+        c->stream);
+    launch_contract_ranges(c->ckeys[0].as<unsigned long long>(),
+                           c->ckeys[1].as<unsigned long long>(), c->csched.as<uint32_t>(),
+                           c->cdcount.as<unsigned long long>(), c->cap_c,
+                           c->cranges.as<uint2>(), ntiles, c->sms, c->stream);
+    cudaEventRecord(c->ev[7], c->stream);
+    GSR_CUDA_OK(cudaMemcpyAsync(c->hsched, c->csched.p, 64 * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, c->stream));
+    GSR_CUDA_OK(cudaStreamSynchronize(c->stream));
+    GSR_CUDA_OK(cudaEventElapsedTime(&t_sort, c->ev[6], c->ev[7]));
+    c->contract_buf = (int)(c->hsched[16] & 1u);
+    c->contract_d = (int64_t)d;
+    c->contract_ms = t_keys + t_sort;
+    c->contract_tile = tile;
+    return GSR_OK;
+}
+}  // namespace
+
+int gsr_debug_contract_tiles(gsr_ctx *ctx, int tile, int64_t *out_count, int32_t *out_tiles,
+                             int32_t *out_ranks, int32_t *out_ranges, float *out_ms) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    if (tile < 1 || tile > 256) return fail(GSR_E_INVALID, "tile size must be in 1..256");
+    DeviceGuard g(ctx->device);
+    int rc = complete_frame(ctx);
+    if (rc) return rc;
+    if (ctx->W <= 0 || ctx->H <= 0) return fail(GSR_E_INVALID, "no frame rendered on this context");
+    if (ctx->contract_tile != tile && (rc = build_contract(ctx, tile))) return rc;
+    const int64_t d = ctx->contract_d;
+    if (out_count) *out_count = d;
+    if (out_ms) *out_ms = ctx->contract_ms;
+    if ((out_tiles || out_ranks) && d > 0) {
+        std::vector<unsigned long long> keys((size_t)d);
+        const DevBuf &kb = ctx->ckeys[ctx->contract_buf];
+        GSR_CUDA_OK(cudaMemcpy(keys.data(), kb.p, sizeof(unsigned long long) * d,
+                               cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < d; i++) {
+            if (out_tiles) out_tiles[i] = (int32_t)(keys[i] >> 32);
+            if (out_ranks) out_ranks[i] = (int32_t)(keys[i] & 0xffffffffu);
+        }
+    }
+    if (out_ranges) {
+        const int ntiles = ((ctx->W + tile - 1) / tile) * ((ctx->H + tile - 1) / tile);
+        GSR_CUDA_OK(cudaMemcpy(out_ranges, ctx->cranges.p, sizeof(uint2) * (size_t)ntiles,
+                               cudaMemcpyDeviceToHost));
     }
     return GSR_OK;
 }

@@ -122,6 +122,7 @@ struct DepthArgs {
     void *work32, *work64;
     uint32_t *sched;    // sort schedule: sched[16] = buffer of vals holding the order
     bool full64;        // full 64-bit key sort (after a frame reported long runs)
+    uint32_t *long_run_sticky;  // per-context count of frames that reported long runs
 };
 size_t depth_work32_bytes(int64_t n_cap);
 size_t depth_work64_bytes(int64_t n_cap);
@@ -161,6 +162,22 @@ int64_t bin_segments(int64_t cap_p, int n_rows);
 cudaError_t binning_init_attributes();
 int launch_binning(const BinArgs &a, cudaStream_t s,
                    const KMark &mark = KMark());  // returns kernels launched
+
+// contract.cu: the exact tile-list contract on tile x tile tiles via
+// (tile | rank) keys, a radix sort and range identification (parity path)
+struct ContractArgs {
+    const SplatRec *srec;            // depth-ranked records of the frame (bin_gather)
+    const FrameCounters *ctr;        // K
+    int width, tile, tiles_x;
+    unsigned long long *keys;        // [cap] (ty * tiles_x + tx) << 32 | rank
+    int64_t cap;
+    unsigned long long *d_count;     // keys reserved (may exceed cap)
+};
+int launch_contract_keys(const ContractArgs &a, int64_t cap_n, cudaStream_t s);
+// ranges of the sorted keys (keys0 or keys1 by sched[16], the sort's result buffer)
+int launch_contract_ranges(const unsigned long long *keys0, const unsigned long long *keys1,
+                           const uint32_t *sched, const unsigned long long *d_count, int64_t cap,
+                           uint2 *ranges, int ntiles, int sms, cudaStream_t s);
 
 // blend.cu
 struct BlendOut {

@@ -133,8 +133,8 @@ class _Lease:
 def _scene_bytes(prims) -> int:
     """Device bytes gsr_scene_create will allocate (SoA planes, f32 SH)."""
     own = getattr(prims, "scene", None)  # load_ply: already resident
-    if own is not None and hasattr(own, "device_bytes"):
-        return int(own.device_bytes)
+    if own is not None and hasattr(own, "device_bytes") and not getattr(own, "closed", False):
+        return int(own.device_bytes)  # (once evicted, the re-upload's size is estimated below)
     n = int(prims.means.shape[0])
     stride = (max(n, 1) + 31) // 32 * 32
     sh = getattr(prims, "sh_coeffs", None)

@@ -2,8 +2,10 @@
 
 ``render_framebuffer`` / ``render_view`` keep the reference's signatures and
 return types (render.py:516-541); the work runs in libgsr.so (sm_100a CUDA):
-f64 projection + SH + packing, stable f64 radix depth sort, 16x16 tile
-binning and sort, per-tile front-to-back blend, u8 conversion.  Host work is
+f64 projection + SH + packing, stable f64 radix depth sort, sort-free
+binning into conservative 32x64 tile lists (a superset of the exact 16x16
+tile-list contract, which ``debug_contract_tiles`` emits on the device for
+parity), per-tile front-to-back blend, u8 conversion.  Host work is
 only the reference's own pose math (camera.py) and, at scene upload, the
 view-independent cutoff radius (render.py:476-481) in numpy.
 
@@ -301,8 +303,12 @@ class RenderPipeline:
     `depth` frames are in flight, `submit` first completes the oldest and
     returns it as (tag, frame); `drain` completes the rest.  A returned frame
     is a view of a pinned slot (depth + 1 slots rotate, so the frame enqueued
-    by the same `submit` never lands in the slot it returns); it stays valid
-    until the next `submit`: copy it to keep it.  Results are the same frames
+    by the same `submit` never lands in the slot it returns); its contents
+    stay valid until the next `submit` (copy it to keep them), and its memory
+    stays allocated as long as the array lives, even after close().  Every
+    frame in flight holds a reference to its scene, so a caller (or the
+    registry's eviction) dropping the primitives cannot free the scene under
+    a frame that may still be re-rendered.  Results are the same frames
     render_u8 returns, in submission order."""
 
     def __init__(self, intr, sh_degree: int = 0, background=(0.0, 0.0, 0.0), depth: int = 2,
@@ -316,7 +322,7 @@ class RenderPipeline:
         d = len(self.ctxs)
         self.slots = [self.ctxs[k % d].pinned(f"pipeline{k // d}", shape, np.uint8)
                       for k in range(d + 1)]
-        self.inflight = []  # (ctx index, slot index, tag), oldest first
+        self.inflight = []  # (ctx index, slot index, tag, scene), oldest first
         self.next = 0
         self.next_slot = 0
 
@@ -328,7 +334,7 @@ class RenderPipeline:
     def submit(self, prims, pose, tag=None):
         done = None
         if len(self.inflight) == len(self.ctxs):
-            i, j, t = self.inflight.pop(0)
+            i, j, t, _sc = self.inflight.pop(0)
             done = (t, self._finish(i, j))
         i, j = self.next, self.next_slot
         self.next = (self.next + 1) % len(self.ctxs)
@@ -340,13 +346,13 @@ class RenderPipeline:
         _lib.check(ctx.lib.gsr_render_enqueue(ctx.handle, sc.handle, ctypes.byref(cam), self.bg,
                                               self.sh_degree, 1, _lib.ptr(self.slots[j])),
                    "gsr_render_enqueue")
-        self.inflight.append((i, j, tag))
+        self.inflight.append((i, j, tag, sc))  # sc stays alive until the frame completes
         return done
 
     def drain(self):
         out = []
         while self.inflight:
-            i, j, t = self.inflight.pop(0)
+            i, j, t, _sc = self.inflight.pop(0)
             out.append((t, self._finish(i, j)))
         return out
 
@@ -477,6 +483,31 @@ def debug_tile_lists(*, device: int | None = None):
     return tiles[:d].copy(), ranks[:d].copy()
 
 
+def debug_contract_tiles(width: int, height: int, tile: int = 16, *,
+                         device: int | None = None):
+    """The exact tile-list contract of the calling thread's last render
+    (SURVEY.md A.4 on tile x tile tiles, oracle.tile_lists' definition), built
+    on the device from 64-bit (tile | depth rank) keys, a radix sort and
+    per-tile range identification (contract.cu).  Returns (tiles (D,) int32,
+    ranks (D,) int32, ranges (n_tiles, 2) int32, device ms)."""
+    dev = _default_device if device is None else device
+    ctx = _lib.context(dev)
+    d = ctypes.c_int64(0)
+    ms = ctypes.c_float(0.0)
+    _lib.check(ctx.lib.gsr_debug_contract_tiles(ctx.handle, int(tile), ctypes.byref(d), None,
+                                                 None, None, ctypes.byref(ms)),
+               "gsr_debug_contract_tiles")
+    n = int(d.value)
+    tiles = np.empty(max(n, 1), dtype=np.int32)
+    ranks = np.empty(max(n, 1), dtype=np.int32)
+    n_tiles = ((int(width) + tile - 1) // tile) * ((int(height) + tile - 1) // tile)
+    ranges = np.empty((n_tiles, 2), dtype=np.int32)
+    _lib.check(ctx.lib.gsr_debug_contract_tiles(ctx.handle, int(tile), None, _lib.ptr(tiles),
+                                                 _lib.ptr(ranks), _lib.ptr(ranges), None),
+               "gsr_debug_contract_tiles")
+    return tiles[:n].copy(), ranks[:n].copy(), ranges, float(ms.value)
+
+
 def debug_tile_ranges(width: int, height: int, *, device: int | None = None) -> np.ndarray:
     dev = _default_device if device is None else device
     ctx = _lib.context(dev)
@@ -493,4 +524,5 @@ __all__ = ["Framebuffer", "RenderStats", "RenderError", "EncodeFailure", "Device
            "device_scene", "evict", "set_device", "render_framebuffer", "render_u8",
            "render_view", "framebuffer_to_u8", "encode_jpeg", "encode_png", "decode_image",
            "cutoff_radius_sq", "make_camera", "debug_preprocess", "debug_tile_lists",
+           "debug_contract_tiles",
            "debug_tile_ranges", "Intrinsics"]

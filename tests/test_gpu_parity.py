@@ -73,6 +73,22 @@ def _assert_lists_cover(tt, tr, ot, orr, width, max_inflation=1.05):
     assert len(g) <= max_inflation * len(o) + 16, (len(g), len(o))
 
 
+def _assert_contract_exact(oracle, packed, width, height):
+    """The device-built 16x16 contract lists of the last frame ((tile | rank)
+    keys, radix sort, range identification: contract.cu) equal the oracle's
+    tile_lists over the same packed table, entry for entry, ranges included."""
+    from paper_2605_08699_b200.render import debug_contract_tiles
+    ct, cr, crg, ms = debug_contract_tiles(width, height)
+    ot, orr, org = oracle.tile_lists(packed, width, height)
+    assert ct.shape == ot.shape, (ct.shape, ot.shape)
+    assert np.array_equal(ct, ot) and np.array_equal(cr, orr)
+    full = org[:, 1] > org[:, 0]
+    assert np.array_equal(crg[full], org[full].astype(np.int32))
+    assert np.all(crg[~full, 0] == crg[~full, 1])
+    assert ms > 0.0 or ct.shape[0] == 0
+    return ct, cr
+
+
 @pytest.mark.parametrize("name", list(load_json("frames.json")))
 def test_frames_bit_exact(gsr, oracle, name):
     from paper_2605_08699_b200.render import debug_preprocess, debug_tile_lists, debug_tile_ranges
@@ -104,6 +120,10 @@ def test_frames_bit_exact(gsr, oracle, name):
     assert ot.shape[0] == tiles["D"]
     assert digest(ot) == tiles["tiles"] and digest(orr) == tiles["ranks"]
     _assert_lists_cover(tt, tr, ot, orr, intr.width)
+    # the exact 16x16 contract emitted by the device itself, vs the golden digests
+    ct, cr = _assert_contract_exact(oracle, packed, intr.width, intr.height)
+    assert ct.shape[0] == tiles["D"]
+    assert digest(ct) == tiles["tiles"] and digest(cr) == tiles["ranks"]
     ranges = debug_tile_ranges(intr.width, intr.height)
     for t_id in np.unique(tt):
         s, e = ranges[t_id]
@@ -270,6 +290,7 @@ def test_config2_500k_720p_trace_vs_oracle(gsr, oracle):
         tt, tr = debug_tile_lists()
         ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
         _assert_lists_cover(tt, tr, ot, orr, intr.width)
+        _assert_contract_exact(oracle, fr.packed, intr.width, intr.height)
 
 
 def test_config3_3m_1080p_vs_oracle(gsr, oracle):
@@ -290,6 +311,7 @@ def test_config3_3m_1080p_vs_oracle(gsr, oracle):
     tt, tr = debug_tile_lists()
     ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
     _assert_lists_cover(tt, tr, ot, orr, intr.width)
+    _assert_contract_exact(oracle, fr.packed, intr.width, intr.height)
     # size-independent properties: depth order is sorted, tile keys sorted
     z = fr.depths
     assert np.all(np.diff(z) >= 0)
@@ -314,6 +336,7 @@ def test_config4_6m_1080p_vs_oracle(gsr, oracle):
     tt, tr = debug_tile_lists()
     ot, orr, _ = oracle.tile_lists(fr.packed, intr.width, intr.height)
     _assert_lists_cover(tt, tr, ot, orr, intr.width)
+    _assert_contract_exact(oracle, fr.packed, intr.width, intr.height)
     key = tt.astype(np.int64) * (1 << 32) + tr
     assert np.all(np.diff(key) > 0)
 
@@ -424,6 +447,24 @@ def test_render_pipeline_matches_render_u8(gsr):
         assert [t for t, _ in got] == list(range(len(poses)))
         for (_, f), r in zip(got, ref):
             assert np.array_equal(f, r)
+    # the frame a submit returns is not overwritten by the frames still in
+    # flight: compare it only after drain() has completed all of them (the
+    # slot rotation of 5a35778), and it outlives close() and the pipeline
+    def last_submitted(depth):
+        pipe = gsr.RenderPipeline(intr, sh_degree=3, depth=depth)
+        keep = None
+        for i, p in enumerate(poses):
+            r = pipe.submit(prims, p, tag=i)
+            if r is not None:
+                keep = r
+        rest = pipe.drain()
+        pipe.close()
+        return keep, rest
+    for depth in (1, 2, 3):
+        (t, f), rest = last_submitted(depth)
+        assert np.array_equal(f, ref[t]), (depth, t)
+        for t2, f2 in rest:
+            assert np.array_equal(f2, ref[t2]), (depth, t2)
 
 
 def test_render_u8_into_pinned_frame(gsr, oracle):
