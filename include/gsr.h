@@ -78,8 +78,8 @@ typedef struct gsr_stats {
     int64_t composited;         /* E: composited (pixel, splat) evaluations (*) */
     int64_t row_evals_blend;    /* (splat, pixel row) interval evaluations in the blend (*) */
     int64_t row_evals_binning;  /* (splat, pixel row) interval evaluations in the binning */
-    /* (*) counted only while gsr_ctx_set_kernel_timing is on (the counting
-     *     costs blend instructions), else 0 */
+    /* (*) counted only while gsr_ctx_set_kernel_timing has GSR_TIMING_COUNTERS
+     *     on (the counting costs blend instructions), else 0 */
     int32_t long_run_frames;  /* frames since the last finish whose 32-bit depth keys had a
                                  run too long for the fix-up (re-rendered with the 64-bit
                                  sort when completed through finish/render) */
@@ -168,11 +168,16 @@ GSR_API int64_t gsr_ctx_device_bytes(const gsr_ctx *ctx);
 GSR_API const uint8_t *gsr_ctx_frame_u8(const gsr_ctx *ctx);
 /* the ctx's cudaStream_t (as void*), e.g. to record timing events on it */
 GSR_API void *gsr_ctx_stream(const gsr_ctx *ctx);
-/* Per-kernel timing (profiling; off by default): when enabled, a CUDA event is
- * recorded on the ctx stream after every kernel of a frame.
+/* Per-kernel timing (profiling; off by default).  `enable` is a bit set:
+ * GSR_TIMING_EVENTS records a CUDA event on the ctx stream after every kernel
+ * of a frame; GSR_TIMING_COUNTERS switches the blend to its counting variant,
+ * which fills the (*) work counters of gsr_stats (and costs blend time, so
+ * time the kernels with EVENTS alone and count in a separate frame).
  * gsr_ctx_kernel_times waits for the last frame and returns, for each kernel
  * launch in order, its name (NUL-terminated, 48-byte slots in names) and its
  * device time in ms (event after it minus event before it). */
+#define GSR_TIMING_EVENTS 1
+#define GSR_TIMING_COUNTERS 2
 GSR_API int gsr_ctx_set_kernel_timing(gsr_ctx *ctx, int enable);
 GSR_API int gsr_ctx_kernel_times(gsr_ctx *ctx, int max, char *names, float *ms, int *n);
 

@@ -89,7 +89,8 @@ struct gsr_ctx {
     cudaEvent_t ev[8] = {};
     // per-kernel event timeline of the last frame (gsr_ctx_set_kernel_timing)
     static constexpr int kMaxMarks = 64;
-    bool ktime = false;
+    bool ktime = false;   // per-kernel event marks
+    bool kcount = false;  // blend work counters (E, Rb): the counting blend variant
     int nmarks = 0;
     cudaEvent_t kev[kMaxMarks + 1] = {};
     const char *kname[kMaxMarks] = {};
@@ -315,7 +316,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
     launch_blend(c->srec.as<SplatRec>(), c->col.as<float4>(), ord, c->tile_vals.as<uint32_t>(),
                  c->ranges.as<uint2>(), W, H,
-                 bg[0], bg[1], bg[2], out, ctr, s, mark, c->ktime != 0);
+                 bg[0], bg[1], bg[2], out, ctr, s, mark, c->kcount);
     cudaEventRecord(c->ev[5], s);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters) + 2 * sizeof(uint32_t),
                     cudaMemcpyDeviceToHost, s);
@@ -755,7 +756,8 @@ void *gsr_ctx_stream(const gsr_ctx *ctx) { return ctx ? (void *)ctx->stream : nu
 
 int gsr_ctx_set_kernel_timing(gsr_ctx *ctx, int enable) {
     if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
-    ctx->ktime = enable != 0;
+    ctx->ktime = (enable & GSR_TIMING_EVENTS) != 0;
+    ctx->kcount = (enable & GSR_TIMING_COUNTERS) != 0;
     ctx->nmarks = 0;
     return GSR_OK;
 }
