@@ -312,8 +312,10 @@ class RenderPipeline:
     render_u8 returns, in submission order."""
 
     def __init__(self, intr, sh_degree: int = 0, background=(0.0, 0.0, 0.0), depth: int = 2,
-                 device: int | None = None):
+                 device: int | None = None, record_stats: bool = False):
         self.device = _default_device if device is None else device
+        # record_stats: device time (ms, CUDA events) of every completed frame
+        self.frame_ms = [] if record_stats else None
         self.intr = intr
         self.sh_degree = int(sh_degree)
         self.bg = _bg(background)
@@ -328,7 +330,13 @@ class RenderPipeline:
 
     def _finish(self, i, j):
         ctx = self.ctxs[i]
-        _lib.check(ctx.lib.gsr_ctx_finish(ctx.handle, None, None), "gsr_ctx_finish")
+        if self.frame_ms is None:
+            _lib.check(ctx.lib.gsr_ctx_finish(ctx.handle, None, None), "gsr_ctx_finish")
+        else:
+            st = _lib.GsrStats()
+            _lib.check(ctx.lib.gsr_ctx_finish(ctx.handle, None, ctypes.byref(st)),
+                       "gsr_ctx_finish")
+            self.frame_ms.append(float(st.ms_device))
         return self.slots[j]
 
     def submit(self, prims, pose, tag=None):

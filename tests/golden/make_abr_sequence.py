@@ -37,14 +37,11 @@ from splatstream.abr import LatencyAbr, ladder_from_config  # noqa: E402
 from splatstream.harness import (DEFAULT_VIRTUAL_RTT, BandwidthEntry, BandwidthTrace,  # noqa: E402
                                  MovementEntry, TokenBucketShaper, _is_panning)
 
-from paper_2605_08699_b200.synth import pose_trace  # noqa: E402
+from paper_2605_08699_b200.synth import ladder_1080p, pose_trace  # noqa: E402
 
 N_SESSIONS = 64
 FRAMES = 300
-RUNGS = [dict(width=1920, height=1080, jpeg_quality=90, expected_kb=540.0),
-         dict(width=1280, height=720, jpeg_quality=90, expected_kb=240.0),
-         dict(width=960, height=540, jpeg_quality=65, expected_kb=55.0),
-         dict(width=640, height=360, jpeg_quality=35, expected_kb=20.0)]
+RUNGS = ladder_1080p()
 
 
 def bandwidth_trace(seed: int, seconds: float) -> BandwidthTrace:

@@ -739,3 +739,38 @@ def test_span_bound_contains_exact_spans(tmp_path):
                     "-o", str(exe), str(ROOT / "tools" / "span_check.cu")], check=True)
     out = subprocess.run([str(exe), "1"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "OK: no violations" in out.stdout, out.stdout
+
+
+def test_config5_sessions_spot_check(gsr, oracle):
+    """Config 5 serving: frames of 3 sessions (scene sizes k = 0, 1, 2 of the
+    14, each its own pose trace) through RenderPipeline at 1080p, bit-exact vs
+    the oracle, and each session's ABR rung (tests/golden/abr_sequence.json)
+    through render_view: JPEG bytes equal Pillow's encode of the oracle frame."""
+    import io
+    from PIL import Image
+    from paper_2605_08699_b200.sessions import config5_sessions
+    from paper_2605_08699_b200.synth import base_intrinsics_1080p, pose_trace, synthetic_scene
+    fx = load_json("abr_sequence.json")
+    intr = base_intrinsics_1080p()
+    pipe = gsr.RenderPipeline(intr, sh_degree=3, depth=2)
+    for s in config5_sessions(64)[:3]:
+        prims = synthetic_scene(s.gaussians, seed=s.scene, sh_degree=3)
+        t = 7
+        tp = pose_trace(t + 1, seed=s.index)[t]
+        pose = gsr.pose_from_degrees(tp.azimuth_deg, tp.elevation_deg, tp.translation)
+        pipe.submit(prims, pose)
+        (_, u8), = pipe.drain()
+        assert np.array_equal(u8, _oracle_frame(oracle, prims, pose, intr, 3).u8), s.index
+        rung = fx["rungs"][int(fx["sessions"][s.index]["levels"][t])]
+
+        class Profile:
+            width, height, jpeg_quality = rung["width"], rung["height"], rung["jpeg_quality"]
+
+        payload, _ = gsr.render_view(prims, pose, intr, Profile, sh_degree=3)
+        ri = gsr.scale_intrinsics(intr, rung["width"], rung["height"])
+        ref = _oracle_frame(oracle, prims, pose, ri, 3).u8
+        buf = io.BytesIO()
+        Image.fromarray(ref, "RGB").save(buf, format="JPEG", quality=rung["jpeg_quality"],
+                                         subsampling=2 if rung["jpeg_quality"] < 90 else 0)
+        assert payload == buf.getvalue(), (s.index, rung)
+    pipe.close()

@@ -69,3 +69,41 @@ def test_shard_is_partition(world):
     assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
     with pytest.raises(ValueError):
         shard(sess, world, world)
+
+
+def _bench_dry(*extra):
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--dry-run", "--steps", "8",
+                        "--warmup", "3", *extra], capture_output=True, text=True, timeout=300,
+                       cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints one JSON line
+    return json.loads(lines[0])
+
+
+def test_bench_gpus2_launches_two_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself
+    with two ranks (torch.distributed.run, 127.0.0.1); each rank owns its own
+    session trace and rank 0 reports n_gpus = 2 after the max-over-ranks."""
+    line = _bench_dry("--gpus", "2")
+    assert line["n_gpus"] == 2 and line["dry_run"] is True
+    assert line["sessions_by_rank"] == [[0], [1]]
+
+
+def test_bench_config5w_weak_sharding_two_ranks():
+    """config 5w: 8 sessions per GPU, session i -> GPU i mod N."""
+    line = _bench_dry("--gpus", "2", "--workload", "config5w")
+    assert line["n_gpus"] == 2 and line["sessions"] == 16
+    assert line["sessions_by_rank"] == [list(range(0, 16, 2)), list(range(1, 16, 2))]
+
+
+def test_bench_single_process_dry_run():
+    line = _bench_dry()
+    assert line["n_gpus"] == 1 and line["sessions_by_rank"] == [[0]]
