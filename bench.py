@@ -856,9 +856,13 @@ def run_config5(args, wl):
                                  sh_degree=3) for k in scenes_for(mine)}
     intr = base_intrinsics_1080p()
     K, W, S = args.steps, args.warmup, max(1, args.streams)
-    per_session = W + (K + len(mine) - 1) // len(mine) + 1
-    traces = {s.index: poses_for(s.index, per_session) for s in mine}
-    order = [(mine[i % len(mine)], W + i // len(mine)) for i in range(K)]
+    # a session's k-th timed frame is step W + k * stride of its 300-step
+    # trace, so the ABR-mixed run samples the whole controller trajectory
+    # (it starts at the worst rung) rather than its first frames
+    per = (K + len(mine) - 1) // len(mine)
+    stride = max(1, (300 - W) // max(per, 1))
+    traces = {s.index: poses_for(s.index, 300) for s in mine}
+    order = [(mine[i % len(mine)], min(299, W + (i // len(mine)) * stride)) for i in range(K)]
 
     # ---- all-1080p through RenderPipeline ----
     pipe = g.RenderPipeline(intr, sh_degree=3, depth=S, device=local_rank, record_stats=True)

@@ -237,6 +237,13 @@ GSR_API int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_
  * out_ranges (n_tiles, 2) [start, end) with n_tiles = ceil(W/tile) *
  * ceil(H/tile).  *out_ms (nullable): device time of the key, sort and range
  * kernels.  1 <= tile <= 256. */
+/* Raw device counters of the last frame on ctx, in this order: K, D, P, E,
+ * Rb, Rp (gsr_stats), then the blend's instrumentation -- list entries walked
+ * by all work items, entries whose row range meets the item's rows, 32-entry
+ * batches, composite-loop iterations x 32, useful (pixel, iteration) slots,
+ * work items.  E, Rb and the blend entries need GSR_TIMING_COUNTERS. */
+#define GSR_NCOUNTERS 12
+GSR_API int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n);
 GSR_API int gsr_debug_contract_tiles(gsr_ctx *ctx, int tile, int64_t *out_count,
                          int32_t *out_tiles, int32_t *out_ranks, int32_t *out_ranges,
                          float *out_ms);

@@ -191,10 +191,15 @@ __device__ __forceinline__ void composite_pair(uint32_t m0, uint32_t m1, uint32_
                                                uint32_t geo1, uint32_t col, float fx,
                                                const unsigned long long *tab, uint32_t tab_s,
                                                const ExpK &ek, float *T, float *cr, float *cg,
-                                               float *cb, uint32_t &n_comp) {
+                                               float *cb, uint32_t &n_comp, uint32_t &n_it,
+                                               uint32_t &n_lanes) {
     if (kCount) n_comp += __popc(m0) + __popc(m1);
     uint32_t dropped = 0u;
     while (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
+        if (kCount) {  // instrumentation: warp iterations and useful lanes (2 per pixel pair)
+            n_it += 1u;
+            n_lanes += (m0 != 0u) + (m1 != 0u);
+        }
         const int s0 = 31 - __clz(m0), s1 = 31 - __clz(m1);
         uint32_t b0, b1;
         asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(b0) : "r"((uint32_t)s0));
@@ -288,6 +293,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c1) : "d"(kExpK[2]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c2) : "d"(kExpK[3]));
     uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
+    uint32_t n_walk = 0, n_hit = 0, n_batch = 0, n_it = 0, n_lanes = 0, n_done = 0;
     const uint32_t *__restrict__ order = ord.sched[16] ? ord.order1 : ord.order0;
 
     while (true) {
@@ -295,6 +301,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
         if (lane == 0) item = (int)atomicAdd(&ctr->blend_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= n_items) break;
+        if (kCount) n_done += (lane == 0);
         const int tile = item / kItems, wr = item % kItems;
         const int tx = tile % tiles_x, ty = tile / tiles_x;
         const int X = tx * kTileW;
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             for (int h = 0; h < kSets; h++) all_done = all_done && done[h];
             if (__all_sync(0xffffffffu, all_done)) break;
             const uint32_t j = c + lane;
+            if (kCount) n_batch += (lane == 0);
             uint32_t mask[kSets];
 #pragma unroll
             for (int h = 0; h < kSets; h++) mask[h] = 0u;
@@ -331,7 +339,9 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                 int lo, hi;  // precomputed per frame by bin_gather (SplatRec.b.w)
                 bool fast, esafe;
                 unpack_rows(B.w, lo, hi, fast, esafe);
+                if (kCount) n_walk++;
                 if (iy0 + kSets > lo && iy0 < hi) {
+                    if (kCount) n_hit++;
                     const float rinv = fast ? __frcp_rn(A.z) : 0.0f;
                     uint32_t any = 0u;
 #pragma unroll
@@ -362,10 +372,10 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                 if (done[kSets - 1]) m1 = 0u;
                 if (all_safe)
                     composite_pair<false, kCount>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab,
-                                                  tab_s, ek, T, cr, cg, cb, n_comp);
+                                                  tab_s, ek, T, cr, cg, cb, n_comp, n_it, n_lanes);
                 else
                     composite_pair<true, kCount>(m0, m1, geo[0], geo[kSets - 1], bcol, fx, s_tab,
-                                                 tab_s, ek, T, cr, cg, cb, n_comp);
+                                                 tab_s, ek, T, cr, cg, cb, n_comp, n_it, n_lanes);
 #pragma unroll
                 for (int h = 0; h < kSets; h++) done[h] = done[h] || T[h] < kTStop;
             } else {
@@ -418,15 +428,22 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             }
         }
     }
-    unsigned long long e = n_comp, r = n_rows;
+    if (kCount) {
+        unsigned long long v[8] = {n_comp, n_rows, n_walk, n_hit, n_batch, n_it, n_lanes, n_done};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        e += __shfl_xor_sync(0xffffffffu, e, o);
-        r += __shfl_xor_sync(0xffffffffu, r, o);
-    }
-    if (lane == 0 && kCount) {
-        atomicAdd(&ctr->E, e);
-        atomicAdd(&ctr->Rb, r);
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < 8; i++) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+        if (lane == 0) {
+            atomicAdd(&ctr->E, v[0]);
+            atomicAdd(&ctr->Rb, v[1]);
+            atomicAdd(&ctr->b_walked, v[2]);
+            atomicAdd(&ctr->b_hit, v[3]);
+            atomicAdd(&ctr->b_batches, v[4]);
+            atomicAdd(&ctr->b_iters, v[5]);   // counted by every lane: warp-uniform
+            atomicAdd(&ctr->b_lanes, v[6]);
+            atomicAdd(&ctr->b_items, v[7]);
+        }
     }
 }
 

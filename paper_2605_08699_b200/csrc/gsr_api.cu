@@ -1039,6 +1039,18 @@ int gsr_debug_contract_tiles(gsr_ctx *ctx, int tile, int64_t *out_count, int32_t
     return GSR_OK;
 }
 
+int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n) {
+    if (!ctx || !out) return fail(GSR_E_INVALID, "null argument");
+    DeviceGuard g(ctx->device);
+    int rc = complete_frame(ctx);
+    if (rc) return rc;
+    const FrameCounters &f = *ctx->hctr;
+    const uint64_t v[GSR_NCOUNTERS] = {f.K, f.D, f.P, f.E, f.Rb, f.Rp, f.b_walked, f.b_hit,
+                                       f.b_batches, f.b_iters, f.b_lanes, f.b_items};
+    for (int i = 0; i < n && i < GSR_NCOUNTERS; i++) out[i] = v[i];
+    return GSR_OK;
+}
+
 int gsr_resample_bilinear_u8(gsr_ctx *ctx, const uint8_t *src, int src_w, int src_h, uint8_t *dst,
                              int dst_w, int dst_h) {
     if (!ctx || !src || !dst) return fail(GSR_E_INVALID, "null argument");

@@ -35,6 +35,13 @@ struct FrameCounters {
     unsigned long long Rp;      // binning: (splat, pixel row) interval evaluations
     uint32_t blend_next;        // blend work queue: next (tile, pixel-row pair) item
     uint32_t pad2;
+    // blend instrumentation (counting variant only; gsr_debug_frame_counters)
+    unsigned long long b_walked;   // list entries loaded by items (all items of all tiles)
+    unsigned long long b_hit;      // ... of which the splat's row range meets the item's rows
+    unsigned long long b_batches;  // 32-entry batches processed (warp level)
+    unsigned long long b_iters;    // composite-loop iterations (warp level)
+    unsigned long long b_lanes;    // sum over iterations of lanes with a splat to composite
+    unsigned long long b_items;    // work items processed
 };
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.
