@@ -241,9 +241,14 @@ GSR_API int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_
  * Rb, Rp (gsr_stats), then the blend's instrumentation -- list entries walked
  * by all work items, entries whose row range meets the item's rows, 32-entry
  * batches, composite-loop iterations x 32, useful (pixel, iteration) slots,
- * work items.  E, Rb and the blend entries need GSR_TIMING_COUNTERS. */
-#define GSR_NCOUNTERS 12
+ * work items, distinct splats whose colour the blend read.  E, Rb and the
+ * blend entries need GSR_TIMING_COUNTERS. */
+#define GSR_NCOUNTERS 13
 GSR_API int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n);
+/* Per blend work item (tile-major, 32 items of two pixel rows per 32 x 64
+ * tile) of the last frame rendered with GSR_TIMING_COUNTERS: the deepest
+ * depth rank it walked, | 1 << 31 if all its pixels saturated (T < 1/255). */
+GSR_API int gsr_debug_blend_items(gsr_ctx *ctx, uint32_t *out, int64_t n);
 GSR_API int gsr_debug_contract_tiles(gsr_ctx *ctx, int tile, int64_t *out_count,
                          int32_t *out_tiles, int32_t *out_ranks, int32_t *out_ranges,
                          float *out_ms);

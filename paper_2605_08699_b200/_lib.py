@@ -103,6 +103,7 @@ SIGNATURES = [
                                     _P(GsrStats)]),
     ("gsr_debug_tile_lists", _i32, [_vp, _vp, _vp, _vp, _P(GsrStats)]),
     ("gsr_debug_frame_counters", _i32, [_vp, _vp, _i32]),
+    ("gsr_debug_blend_items", _i32, [_vp, _vp, _i64]),
     ("gsr_debug_contract_tiles", _i32, [_vp, _i32, _P(_i64), _vp, _vp, _vp,
                                         _P(ctypes.c_float)]),
     ("gsr_resample_bilinear_u8", _i32, [_vp, _vp, _i32, _i32, _vp, _i32, _i32]),

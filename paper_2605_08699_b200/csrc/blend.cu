@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             done[h] = !inside[h];
         }
         const uint2 rg = ranges[tile];
+        uint32_t last_r = 0;  // instrumentation: deepest rank this item walked
 
         for (uint32_t c = rg.x; c < rg.y; c += 32) {
             bool all_done = true;
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             bool safe = true;
             if (j < rg.y) {
                 const uint32_t r = __ldg(tile_vals + j);  // depth rank
+                if (kCount) last_r = max(last_r, r);
                 const float4 A = __ldg(&srec[r].a);
                 const float4 B = __ldg(&srec[r].b);
                 const uint32_t gi = __ldg(order + r);  // issued with the record loads
@@ -352,6 +354,8 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                     }
                     if (any) {  // render.py:400-402 terms per pixel row
                         const float4 C = __ldg(col + gi);  // (r, g, b)
+                        if (kCount && out.used && atomicExch(out.used + r, 1u) == 0u)
+                            atomicAdd(&ctr->b_used, 1ull);
                         safe = esafe;
 #pragma unroll
                         for (int h = 0; h < kSets; h++) {
@@ -393,6 +397,15 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                 }
             }
             __syncwarp();
+        }
+        if (kCount && out.item_info) {
+            bool sat = true;
+#pragma unroll
+            for (int h = 0; h < kSets; h++) sat = sat && done[h];
+            sat = __all_sync(0xffffffffu, sat);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) last_r = max(last_r, __shfl_xor_sync(0xffffffffu, last_r, o));
+            if (lane == 0) out.item_info[item] = (last_r & 0x7fffffffu) | ((uint32_t)sat << 31);
         }
 #pragma unroll
         for (int h = 0; h < kSets; h++) {

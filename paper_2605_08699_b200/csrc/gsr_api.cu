@@ -97,6 +97,7 @@ struct gsr_ctx {
     // ladder / resample / ssim scratch
     DevBuf base_u8, up_u8, tmp_u8, src_u8, dst_u8, coefs, ssim_part, ssim_misc, ssim_w;
     DevBuf jpeg_ws;                  // jpeg.cu workspace
+    DevBuf used;                     // blend instrumentation (GSR_TIMING_COUNTERS only)
     // contract tile lists of the last frame (gsr_debug_contract_tiles, contract.cu)
     DevBuf ckeys[2], cvals[2], cwork, csched, cranges, cdcount;
     int64_t cap_c = 0, contract_d = 0;
@@ -124,7 +125,7 @@ struct gsr_ctx {
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
-                               &cvals[0], &cvals[1], &cwork, &csched, &cranges, &cdcount};
+                               &cvals[0], &cvals[1], &cwork, &csched, &cranges, &cdcount, &used};
         for (auto *b : all) s += (int64_t)b->bytes;
         return s;
     }
@@ -313,6 +314,13 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
                  want_rgb ? c->frame_t.as<float>() : nullptr, c->zc_used ? c->zc_host : nullptr,
                  packed};
+    const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
+    if (c->kcount &&
+        ensure(c->used, sizeof(uint32_t) * ((size_t)c->cap_n + n_items)) == GSR_OK) {
+        cudaMemsetAsync(c->used.p, 0, sizeof(uint32_t) * ((size_t)c->cap_n + n_items), s);
+        out.used = c->used.as<uint32_t>();
+        out.item_info = out.used + c->cap_n;
+    }
     DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
     launch_blend(c->srec.as<SplatRec>(), c->col.as<float4>(), ord, c->tile_vals.as<uint32_t>(),
                  c->ranges.as<uint2>(), W, H,
@@ -1039,6 +1047,19 @@ int gsr_debug_contract_tiles(gsr_ctx *ctx, int tile, int64_t *out_count, int32_t
     return GSR_OK;
 }
 
+int gsr_debug_blend_items(gsr_ctx *ctx, uint32_t *out, int64_t n) {
+    if (!ctx || !out) return fail(GSR_E_INVALID, "null argument");
+    DeviceGuard g(ctx->device);
+    int rc = complete_frame(ctx);
+    if (rc) return rc;
+    const int64_t have = (int64_t)ctx->ntiles * (kTileH / 2);
+    if (!ctx->kcount || ctx->used.bytes < sizeof(uint32_t) * (size_t)(ctx->cap_n + have))
+        return fail(GSR_E_INVALID, "blend item info needs GSR_TIMING_COUNTERS on the last frame");
+    GSR_CUDA_OK(cudaMemcpy(out, ctx->used.as<uint32_t>() + ctx->cap_n,
+                           sizeof(uint32_t) * (size_t)std::min(n, have), cudaMemcpyDeviceToHost));
+    return GSR_OK;
+}
+
 int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n) {
     if (!ctx || !out) return fail(GSR_E_INVALID, "null argument");
     DeviceGuard g(ctx->device);
@@ -1046,7 +1067,7 @@ int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n) {
     if (rc) return rc;
     const FrameCounters &f = *ctx->hctr;
     const uint64_t v[GSR_NCOUNTERS] = {f.K, f.D, f.P, f.E, f.Rb, f.Rp, f.b_walked, f.b_hit,
-                                       f.b_batches, f.b_iters, f.b_lanes, f.b_items};
+                                       f.b_batches, f.b_iters, f.b_lanes, f.b_items, f.b_used};
     for (int i = 0; i < n && i < GSR_NCOUNTERS; i++) out[i] = v[i];
     return GSR_OK;
 }

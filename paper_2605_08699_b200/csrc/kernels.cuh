@@ -42,6 +42,7 @@ struct FrameCounters {
     unsigned long long b_iters;    // composite-loop iterations (warp level)
     unsigned long long b_lanes;    // sum over iterations of lanes with a splat to composite
     unsigned long long b_items;    // work items processed
+    unsigned long long b_used;     // distinct splats whose colour the blend read
 };
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.
@@ -193,6 +194,8 @@ struct BlendOut {
     float *trans;   // (H,W) or null
     uint8_t *host;  // device view of a mapped pinned (H,W,3) host frame, or null (needs packed)
     bool packed;    // W % 32 == 0 and u8/host 4-byte aligned: one 96 B row segment per warp store
+    uint32_t *used = nullptr;  // instrumentation (counting variant): per-rank "colour read" flags
+    uint32_t *item_info = nullptr;  // ... per work item: last depth rank walked | saturated << 31
 };
 struct DepthOrder {  // depth rank -> Gaussian index (the depth sort's result buffer)
     const uint32_t *order0, *order1;

@@ -73,7 +73,7 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->Rp = 0ull;
     ctr->blend_next = 0;
     ctr->pad2 = 0;
-    ctr->b_walked = ctr->b_hit = ctr->b_batches = ctr->b_iters = ctr->b_lanes = ctr->b_items = 0ull;
+    ctr->b_walked = ctr->b_hit = ctr->b_batches = ctr->b_iters = ctr->b_lanes = ctr->b_items = ctr->b_used = 0ull;
 }
 
 __global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(

@@ -21,7 +21,7 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 
 NAMES = ["K", "D", "P", "E", "Rb", "Rp", "walked", "hit", "batches", "iters_x32", "lanes",
-         "items"]
+         "items", "used"]
 
 
 def main():
@@ -42,8 +42,8 @@ def main():
     for c in cams[:3]:
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(c), bg, wl["sh"], 1, None,
                                   None, None, ctypes.byref(st)))
-    rows, blend_ms = [], []
-    out = (ctypes.c_uint64 * 12)()
+    rows, blend_ms, items = [], [], []
+    out = (ctypes.c_uint64 * 13)()
     for c in cams[3:]:
         _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 0))
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(c), bg, wl["sh"], 1, None,
@@ -52,8 +52,12 @@ def main():
         _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 2))
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(c), bg, wl["sh"], 1, None,
                                   None, None, ctypes.byref(st)))
-        _lib.check(lib.gsr_debug_frame_counters(ctx.handle, out, 12))
+        _lib.check(lib.gsr_debug_frame_counters(ctx.handle, out, 13))
         rows.append([int(x) for x in out])
+        n_items = ((intr.width + 31) // 32) * ((intr.height + 63) // 64) * 32
+        info = np.empty(n_items, dtype=np.uint32)
+        _lib.check(lib.gsr_debug_blend_items(ctx.handle, info.ctypes.data, n_items))
+        items.append(info)
     lib.gsr_ctx_set_kernel_timing(ctx.handle, 0)
     m = {k: float(np.mean([r[i] for r in rows])) for i, k in enumerate(NAMES)}
     iters = m["iters_x32"] / 32.0
@@ -72,7 +76,17 @@ def main():
         "lane_efficiency": m["lanes"] / (2.0 * m["iters_x32"]),
         "composites_per_iteration": m["E"] / iters,
         "composites_per_batch": m["E"] / m["batches"],
+        "splats_colour_read_fraction_of_K": m["used"] / m["K"],
     }
+    sat = np.concatenate([(x >> 31) == 1 for x in items])
+    last = np.concatenate([(x & 0x7fffffff) for x in items]).astype(np.float64)
+    kk = np.concatenate([np.full(len(x), r[0], dtype=np.float64) for x, r in zip(items, rows)])
+    frac = last / kk
+    res["items_unsaturated_fraction"] = float(1.0 - sat.mean())
+    res["saturated_items_last_rank_fraction_of_K"] = {
+        q: float(np.percentile(frac[sat], q)) for q in (50, 90, 99, 99.9, 100)} if sat.any() else None
+    res["unsaturated_items_last_rank_fraction_of_K"] = {
+        q: float(np.percentile(frac[~sat], q)) for q in (50, 90, 100)} if (~sat).any() else None
     print(json.dumps(res, indent=1))
 
 
