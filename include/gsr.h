@@ -83,7 +83,9 @@ typedef struct gsr_stats {
     int32_t long_run_frames;  /* frames since the last finish whose 32-bit depth keys had a
                                  run too long for the fix-up (re-rendered with the 64-bit
                                  sort when completed through finish/render) */
-    int32_t reserved;
+    float ms_slice_b;         /* depth-sliced frames: device time of the second slice (its
+                                 filter, sort, colours, lists and blend); the stage times above
+                                 are then those of the first slice.  0 for one-pass frames */
 } gsr_stats;
 
 GSR_API int gsr_abi_version(void);
@@ -176,6 +178,13 @@ GSR_API void *gsr_ctx_stream(const gsr_ctx *ctx);
  * gsr_ctx_kernel_times waits for the last frame and returns, for each kernel
  * launch in order, its name (NUL-terminated, 48-byte slots in names) and its
  * device time in ms (event after it minus event before it). */
+/* Depth-sliced frames (slice.cu): scenes with at least min_gaussians
+ * Gaussians are rendered as a front slice of about front_fraction of the
+ * kept splats, then the splats behind it that can still reach an unsaturated
+ * pixel; frames are identical to a one-pass render.  min_gaussians < 0 and
+ * front_fraction 0 restore the defaults (GSR_SLICE_MIN, 262144;
+ * GSR_SLICE_FRAC, 0.15); a huge min_gaussians renders every frame in one pass. */
+GSR_API int gsr_ctx_set_slicing(gsr_ctx *ctx, int64_t min_gaussians, float front_fraction);
 #define GSR_TIMING_EVENTS 1
 #define GSR_TIMING_COUNTERS 2
 GSR_API int gsr_ctx_set_kernel_timing(gsr_ctx *ctx, int enable);

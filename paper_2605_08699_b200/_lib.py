@@ -51,7 +51,7 @@ class GsrStats(ctypes.Structure):
                 ("overflow_frames", ctypes.c_int32), ("pairs", ctypes.c_int64),
                 ("composited", ctypes.c_int64), ("row_evals_blend", ctypes.c_int64),
                 ("row_evals_binning", ctypes.c_int64), ("long_run_frames", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("ms_slice_b", ctypes.c_float)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -61,7 +61,7 @@ class GsrPlyInfo(ctypes.Structure):
     _fields_ = [("count", ctypes.c_int64), ("body_offset", ctypes.c_int64),
                 ("body_bytes", ctypes.c_int64), ("n_props", ctypes.c_int32),
                 ("has_rest", ctypes.c_int32), ("col", ctypes.c_int32 * GSR_PLY_NCOLS),
-                ("reserved", ctypes.c_int32)]
+                ("ms_slice_b", ctypes.c_float)]
 
 
 class GsrPlyStats(ctypes.Structure):
@@ -94,6 +94,7 @@ SIGNATURES = [
     ("gsr_ctx_frame_u8", _vp, [_vp]),
     ("gsr_ctx_stream", _vp, [_vp]),
     ("gsr_ctx_set_kernel_timing", _i32, [_vp, _i32]),
+    ("gsr_ctx_set_slicing", _i32, [_vp, _i64, ctypes.c_float]),
     ("gsr_ctx_kernel_times", _i32, [_vp, _i32, _vp, _vp, _P(_i32)]),
     ("gsr_render", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32, _vp, _vp, _vp, _P(GsrStats)]),
     ("gsr_render_async", _i32, [_vp, _vp, _P(GsrCamera), _vp, _i32, _i32]),

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
     __shared__ uint32_t cnt[kRowsMax];
     const int tid = threadIdx.x;
     const int64_t b = blockIdx.x;
-    const int64_t k = a.ctr->K;
+    const int64_t k = *a.count;
     const int64_t r = b * BR + tid;
     for (int t = tid; t < a.n_rows; t += BR) cnt[t] = 0;
     __syncthreads();
@@ -120,6 +120,8 @@ __global__ void __launch_bounds__(256) row_scan_kernel(BinArgs a) {
     if (threadIdx.x == 255 && (tile + 1) * kScanTile >= n) {  // last tile: totals
         const unsigned long long p = pre + ex;
         a.ctr->P = p;
+        a.ctr->Ptot += p;  // one thread of one block per pass
+        a.ctr->Pmax = p > a.ctr->Pmax ? p : a.ctr->Pmax;
         a.row_start[a.n_rows] = (uint32_t)(p < 0xffffffffull ? p : 0xffffffffull);
         if (p > (unsigned long long)a.cap_p) atomicAdd(a.overflow_sticky, 1u);
     }
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     uint32_t *rowbase = wpre_all + (BR / 32) * nr;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t b = blockIdx.x;
-    const int64_t k = a.ctr->K;
+    const int64_t k = *a.count;
     if (b * BR >= k || overflowed(a)) return;
     const int64_t r = b * BR + tid;
     uint32_t ntr = 0;
@@ -398,6 +400,8 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(BinArgs a) {
     const bool overflow = ov_p || (int64_t)carry > a.cap_d;
     if (threadIdx.x == 0) {
         a.ctr->D = (uint32_t)(carry < 0xffffffffull ? carry : 0xffffffffull);
+        a.ctr->Dtot += carry;
+        a.ctr->Dmax = carry > a.ctr->Dmax ? carry : a.ctr->Dmax;
         if ((int64_t)carry > a.cap_d) atomicAdd(a.overflow_sticky, 1u);
     }
     if (overflow)  // lists are not placed: empty ranges keep the blend in bounds

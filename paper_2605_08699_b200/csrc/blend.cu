@@ -255,11 +255,16 @@ __device__ __forceinline__ uint32_t to_u8(float c) {
 // kSets pixel rows per item (one pixel per lane per row): the batch's loads
 // and per-splat set-up are shared by the item's rows, which are composited
 // one after the other from the same staged batch.
-template <int kSets, bool kPairLoop, bool kCount>
+// kMode 0: one pass over the frame's lists.  1: slice A (slice.cu) -- an
+// item whose pixels all saturate writes them; any other saves (T, r, g, b)
+// per pixel in `state` and sets its bit in unsat[tile].  2: slice B -- only
+// the items with their unsat bit, continuing from `state`.
+template <int kSets, bool kPairLoop, bool kCount, int kMode>
 __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kernel(
-    const SplatRec *__restrict__ srec, const float4 *__restrict__ col, DepthOrder ord,
+    const SplatRec *__restrict__ srec, const float4 *__restrict__ colr,
     const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
-    int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *__restrict__ ctr) {
+    int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *__restrict__ ctr,
+    float4 *__restrict__ state, uint32_t *__restrict__ unsat) {
     constexpr int kItems = kTileH / kSets;  // items per tile
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
@@ -294,7 +299,6 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c2) : "d"(kExpK[3]));
     uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
     uint32_t n_walk = 0, n_hit = 0, n_batch = 0, n_it = 0, n_lanes = 0, n_done = 0;
-    const uint32_t *__restrict__ order = ord.sched[16] ? ord.order1 : ord.order0;
 
     while (true) {
         int item = 0;
@@ -309,6 +313,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
         const int ix = X + lane;
         const float fx = (float)ix + 0.5f;
 
+        if (kMode == 2 && !((__ldg(unsat + tile) >> wr) & 1u)) continue;  // saturated in A
         float T[kSets], cr[kSets], cg[kSets], cb[kSets];
         bool inside[kSets], done[kSets];
 #pragma unroll
@@ -316,7 +321,14 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             T[h] = 1.0f;
             cr[h] = cg[h] = cb[h] = 0.0f;
             inside[h] = ix < width && iy0 + h < height;
-            done[h] = !inside[h];
+            if (kMode == 2 && inside[h]) {
+                const float4 st = state[(int64_t)(iy0 + h) * width + ix];
+                T[h] = st.x;
+                cr[h] = st.y;
+                cg[h] = st.z;
+                cb[h] = st.w;
+            }
+            done[h] = !inside[h] || (kMode == 2 && T[h] < kTStop);
         }
         const uint2 rg = ranges[tile];
         uint32_t last_r = 0;  // instrumentation: deepest rank this item walked
@@ -337,7 +349,6 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                 if (kCount) last_r = max(last_r, r);
                 const float4 A = __ldg(&srec[r].a);
                 const float4 B = __ldg(&srec[r].b);
-                const uint32_t gi = __ldg(order + r);  // issued with the record loads
                 int lo, hi;  // precomputed per frame by bin_gather (SplatRec.b.w)
                 bool fast, esafe;
                 unpack_rows(B.w, lo, hi, fast, esafe);
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                         any |= mask[h];
                     }
                     if (any) {  // render.py:400-402 terms per pixel row
-                        const float4 C = __ldg(col + gi);  // (r, g, b)
+                        const float4 C = __ldg(colr + r);  // (r, g, b) by depth rank
                         if (kCount && out.used && atomicExch(out.used + r, 1u) == 0u)
                             atomicAdd(&ctr->b_used, 1ull);
                         safe = esafe;
@@ -406,6 +417,19 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) last_r = max(last_r, __shfl_xor_sync(0xffffffffu, last_r, o));
             if (lane == 0) out.item_info[item] = (last_r & 0x7fffffffu) | ((uint32_t)sat << 31);
+        }
+        if (kMode == 1) {  // slice A: saturated items finish, the others wait for B
+            bool sat = true;
+#pragma unroll
+            for (int h = 0; h < kSets; h++) sat = sat && (done[h] || T[h] < kTStop);
+            if (!__all_sync(0xffffffffu, sat)) {
+#pragma unroll
+                for (int h = 0; h < kSets; h++)
+                    if (inside[h])
+                        state[(int64_t)(iy0 + h) * width + ix] = make_float4(T[h], cr[h], cg[h], cb[h]);
+                if (lane == 0) atomicOr(unsat + tile, 1u << wr);
+                continue;
+            }
         }
 #pragma unroll
         for (int h = 0; h < kSets; h++) {
@@ -462,29 +486,37 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
 
 int g_blend_grid = 0;
 
-}  // namespace
-
-void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
-                  const uint32_t *tile_vals, const uint2 *ranges, int width,
-                  int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
-                  cudaStream_t s, const KMark &mark, bool count) {
+// tuning: 1 = one row per item, 2 = two rows one after the other,
+// 3 (default) = two rows interleaved (composite_pair); only 3 has the
+// slice modes
+int blend_sets() {
     static int sets = 0;
     if (!sets) {
         const char *e = getenv("GSR_BLEND_SETS");
-        // tuning: 1 = one row per item, 2 = two rows one after the other,
-        // 3 (default) = two rows interleaved (composite_pair)
         sets = (e && atoi(e) >= 1 && atoi(e) <= 3) ? atoi(e) : 3;
     }
+    return sets;
+}
+
+}  // namespace
+
+bool blend_has_slices() { return blend_sets() == 3; }
+
+void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
+                  const uint2 *ranges, int width, int height, float bg0, float bg1, float bg2,
+                  BlendOut out, FrameCounters *ctr, cudaStream_t s, const KMark &mark, bool count,
+                  int mode, float4 *state, uint32_t *unsat) {
+    const int sets = blend_sets();
     if (!g_blend_grid) {  // persistent grid: every SM full
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sets == 1)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<1, false, true>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<1, false, true, 0>, kBlendThreads, 0);
         else if (sets == 3)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, true, false>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, true, false, 0>, kBlendThreads, 0);
         else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, false, true>, kBlendThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_kernel<2, false, true, 0>, kBlendThreads, 0);
         // GSR_BLEND_CTAS_PER_SM (tuning): fewer resident CTAs leave room for
         // other frames' kernels when several frames are in flight
         if (const char *e = getenv("GSR_BLEND_CTAS_PER_SM")) {
@@ -495,19 +527,18 @@ void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
     }
     const int tiles = ((width + kTileW - 1) / kTileW) * ((height + kTileH - 1) / kTileH);
     const int grid = std::min(g_blend_grid, tiles * kTileH);
-    if (sets == 1)
-        blend_kernel<1, false, true><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
-                                                              width, height, bg0, bg1, bg2, out, ctr);
-    else if (sets == 3 && count)
-        blend_kernel<2, true, true><<<grid, kBlendThreads, 0, s>>>(
-            srec, col, ord, tile_vals, ranges, width, height, bg0, bg1, bg2, out, ctr);
-    else if (sets == 3)  // work counters (E, Rb) only when kernel timing asks for them
-        blend_kernel<2, true, false><<<grid, kBlendThreads, 0, s>>>(
-            srec, col, ord, tile_vals, ranges, width, height, bg0, bg1, bg2, out, ctr);
-    else
-        blend_kernel<2, false, true><<<grid, kBlendThreads, 0, s>>>(srec, col, ord, tile_vals, ranges,
-                                                              width, height, bg0, bg1, bg2, out, ctr);
-    mark("blend");
+#define GSR_BLEND(S, P, C, M)                                                                 \
+    blend_kernel<S, P, C, M><<<grid, kBlendThreads, 0, s>>>(srec, colr, tile_vals, ranges, width, \
+                                                           height, bg0, bg1, bg2, out, ctr,   \
+                                                           state, unsat)
+    if (sets == 1) GSR_BLEND(1, false, true, 0);  // tuning variants: one pass only
+    else if (sets == 2) GSR_BLEND(2, false, true, 0);
+    else if (mode == 1) { if (count) GSR_BLEND(2, true, true, 1); else GSR_BLEND(2, true, false, 1); }
+    else if (mode == 2) { if (count) GSR_BLEND(2, true, true, 2); else GSR_BLEND(2, true, false, 2); }
+    else if (count) GSR_BLEND(2, true, true, 0);  // work counters (E, Rb) only when asked
+    else GSR_BLEND(2, true, false, 0);
+#undef GSR_BLEND
+    mark(mode == 1 ? "blend_a" : mode == 2 ? "blend_b" : "blend");
 }
 
 }  // namespace gsr

@@ -55,7 +55,7 @@ __device__ __forceinline__ void band_tiles(const SplatRec &r, int band, int tile
 __global__ void __launch_bounds__(CB) contract_keys_kernel(ContractArgs a) {
     __shared__ uint32_t s_warp[33];
     __shared__ unsigned long long s_base;
-    const int64_t k = a.ctr->K;
+    const int64_t k = *a.count;
     const int64_t s = (int64_t)blockIdx.x * CB + threadIdx.x;
     if ((int64_t)blockIdx.x * CB >= k) return;
     SplatRec r;

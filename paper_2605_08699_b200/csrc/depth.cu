@@ -28,11 +28,11 @@ namespace {
 constexpr int kMaxRun = 16;
 // Span key width: 24 bits = 3 radix passes.  At 3M kept splats a bucket holds
 // 0.2 splats on average; the fix-up resolves the resulting short runs.
-constexpr int kSpanBits = 24;
+constexpr int kSpanBits = kSpanKeyBits;
 
 __global__ void depth_fixup_kernel(DepthArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t K = a.ctr->K;
+    const int64_t K = *a.count;
     if (i >= K) return;
     const uint32_t b = a.sched[16];
     const uint32_t *ks = b ? a.keys32[1] : a.keys32[0];
@@ -79,16 +79,19 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &
     if (a.n <= 0) return 0;
     if (a.full64)  // exact for any input: 8 passes over the raw f64 key bits
         return launch_onesweep_sort<unsigned long long>(
-            a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, &a.ctr->K, a.n, a.n, 8,
+            a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, a.count, a.n, a.n, 8,
             true, a.work64, a.sched, &a.ctr->npass_fb, sms, s, mark);
     const unsigned g = (unsigned)((a.n + 255) / 256);
     SpanKeys span;  // the histogram kernel writes the span keys (step 1)
-    span.src = a.keys64[0];
-    span.kmin = &a.ctr->kmin;
-    span.kmax = &a.ctr->kmax;
-    span.bits = kSpanBits;
+    if (!a.keys_given) {
+        span.src = a.keys64[0];
+        span.kmin = &a.ctr->kmin;
+        span.kmax = &a.ctr->kmax;
+        span.bits = kSpanBits;
+        span.limit = a.limit;
+    }
     int launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
-                                                  true, true, &a.ctr->K, a.n, a.n, kSpanBits / 8,
+                                                  true, true, a.count, a.n, a.n, kSpanBits / 8,
                                                   true, a.work32, a.sched, &a.ctr->npass, sms, s,
                                                   mark, span);
     depth_fixup_kernel<<<g, 256, 0, s>>>(a);

@@ -47,6 +47,27 @@ int ensure(DevBuf &b, size_t bytes) {
     return GSR_OK;
 }
 
+// Depth-sliced frames (slice.cu): scenes of at least GSR_SLICE_MIN Gaussians
+// (default 262144; 0 disables slicing) are rendered in two slices, the first
+// holding about GSR_SLICE_FRAC (default 0.15) of the kept splats.
+int64_t slice_min() {
+    static const int64_t v = [] {
+        const char *e = getenv("GSR_SLICE_MIN");
+        if (!e) return (int64_t)262144;
+        const long long x = atoll(e);
+        return x <= 0 ? (int64_t)1 << 62 : (int64_t)x;
+    }();
+    return v;
+}
+float slice_frac() {
+    static const float v = [] {
+        const char *e = getenv("GSR_SLICE_FRAC");
+        const float x = e ? (float)atof(e) : 0.15f;
+        return x > 0.0f && x <= 1.0f ? x : 0.15f;
+    }();
+    return v;
+}
+
 }  // namespace gsr
 
 using namespace gsr;
@@ -69,7 +90,7 @@ struct gsr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int64_t cap_n = 0, cap_d = 0, cap_p = 0;
-    DevBuf keys[2], vals[2], keys32[2], geo, col, srec, keep;
+    DevBuf keys[2], vals[2], keys32[2], geo, srec, keep;
     int sms = 148;
     DevBuf depth_work, depth_work32, sched;  // depth-sort scratch; sched[16] = result buffer
     uint32_t *hsched = nullptr;   // pinned host copy of sched
@@ -77,6 +98,12 @@ struct gsr_ctx {
     DevBuf row_blk, row_start, scan_work, pairs, seg_row, seg_cnt, ttotal, tstart, tile_vals;
     DevBuf ranges;
     DevBuf frame_u8, frame_rgb, frame_t;
+    DevBuf colr;          // colours by depth rank of the current pass
+    DevBuf state, unsat;  // depth-sliced frames: pixel state after slice A, unsaturated items
+    bool force_full = false;   // next enqueue: one pass over all kept splats (debug entries)
+    int64_t slice_min_n = -1;  // gsr_ctx_set_slicing (-1: the GSR_SLICE_MIN default)
+    float slice_frac_v = 0.0f; // ... (0: the GSR_SLICE_FRAC default)
+    bool last_sliced = false;  // the last frame was rendered in two slices
     // device FrameCounters followed by two sticky per-context counters
     // (frames whose pair/tile buffers overflowed, frames that needed the
     // 64-bit depth re-sort); one D2H copy per frame brings all of them back
@@ -121,7 +148,7 @@ struct gsr_ctx {
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &col, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+                               &geo, &colr, &state, &unsat, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
@@ -173,7 +200,7 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
             if ((rc = ensure(c->keys32[i], sizeof(uint32_t) * cap))) return rc;
         }
         if ((rc = ensure(c->geo, sizeof(GeoRec) * cap))) return rc;
-        if ((rc = ensure(c->col, sizeof(float4) * cap))) return rc;
+        if ((rc = ensure(c->colr, sizeof(float4) * cap))) return rc;
         if ((rc = ensure(c->srec, sizeof(SplatRec) * cap))) return rc;
         c->cap_n = cap;
     }
@@ -235,7 +262,20 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     c->contract_tile = 0;
     c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
     uint32_t *dsched = c->sched.as<uint32_t>();
-    int launches = 2;  // frame init + blend
+    int launches = 1;  // frame init
+
+    // depth-sliced frame (slice.cu) unless a stage output of the whole
+    // frame is wanted (debug entries), the 64-bit sort is needed, the scene
+    // is small or a blend tuning variant without slice modes is selected
+    const int64_t smin = c->slice_min_n >= 0 ? c->slice_min_n : slice_min();
+    const bool slice = !want_keep && !c->force_full && !c->saved_full64 && n >= smin &&
+                       blend_has_slices();
+    c->last_sliced = slice;
+    if (slice) {
+        int r2;
+        if ((r2 = ensure(c->state, sizeof(float4) * (size_t)W * H))) return r2;
+        if ((r2 = ensure(c->unsat, sizeof(uint32_t) * (size_t)c->ntiles))) return r2;
+    }
 
     KMark mark;
     if (c->ktime) {
@@ -243,21 +283,15 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         mark.self = c;
         c->nmarks = 0;
     }
-    cudaEventRecord(c->ev[0], s);
-    if (c->ktime) cudaEventRecord(c->kev[0], s);
-    launch_frame_init(ctr, s);
-    mark("frame_init");
-    if (n > 0) {
-        launch_preprocess_geo(sc->view, ca, cull, c->keys[0].as<unsigned long long>(),
-                              c->geo.as<GeoRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr,
-                              ctr, s, mark);
-        launch_preprocess_color(sc->view, ca, sh_degree, c->keys[0].as<unsigned long long>(),
-                                c->col.as<float4>(), s, mark);
-        launches += 2;
-    }
-    cudaEventRecord(c->ev[1], s);
-    if (n > 0) {
-        // stable f64 depth order; the first radix pass compacts (drops culled sentinels)
+    const bool packed = W % kTileW == 0 && ((uintptr_t)c->zc_host & 3u) == 0;
+    c->zc_used = packed && c->zc_host != nullptr;
+    BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
+                 want_rgb ? c->frame_t.as<float>() : nullptr, c->zc_used ? c->zc_host : nullptr,
+                 packed};
+    const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
+    DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
+    // one depth-ordered pass over `count` splats: sort, colour, bin
+    auto sort_color_bin = [&](uint32_t *count, const uint32_t *limit, bool keys_given) {
         DepthArgs da;
         for (int i = 0; i < 2; i++) {
             da.keys64[i] = c->keys[i].as<unsigned long long>();
@@ -271,11 +305,16 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         da.sched = dsched;
         da.full64 = c->saved_full64;
         da.long_run_sticky = c->dsticky() + 1;
+        da.count = count;
+        da.limit = limit;
+        da.keys_given = keys_given;
         launches += launch_depth_sort(da, c->sms, s, mark);
-    }
-    cudaEventRecord(c->ev[2], s);
-    if (n > 0) {
+        launch_color_ranked(sc->view, ca, sh_degree, ord, count, c->cap_n, c->colr.as<float4>(),
+                            s, mark);
+        launches += 1;
+        if (!keys_given) cudaEventRecord(c->ev[2], s);
         BinArgs ba;
+        ba.count = count;
         ba.order0 = c->vals[0].as<uint32_t>();
         ba.order1 = c->vals[1].as<uint32_t>();
         ba.depth_sched = dsched;
@@ -304,27 +343,74 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.cap_d = c->cap_d;
         ba.overflow_sticky = c->dsticky();
         launches += launch_binning(ba, s, mark);
-    } else {
-        cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
-    }
-    cudaEventRecord(c->ev[3], s);
-    cudaEventRecord(c->ev[4], s);
-    const bool packed = W % kTileW == 0 && ((uintptr_t)c->zc_host & 3u) == 0;
-    c->zc_used = packed && c->zc_host != nullptr;
-    BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
-                 want_rgb ? c->frame_t.as<float>() : nullptr, c->zc_used ? c->zc_host : nullptr,
-                 packed};
-    const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
+    };
+    auto blend = [&](int mode) {
+        launch_blend(c->srec.as<SplatRec>(), c->colr.as<float4>(), c->tile_vals.as<uint32_t>(),
+                     c->ranges.as<uint2>(), W, H, bg[0], bg[1], bg[2], out, ctr, s, mark,
+                     c->kcount, mode, slice ? c->state.as<float4>() : nullptr,
+                     slice ? c->unsat.as<uint32_t>() : nullptr);
+        launches += 1;
+    };
+
+    cudaEventRecord(c->ev[0], s);
+    if (c->ktime) cudaEventRecord(c->kev[0], s);
+    launch_frame_init(ctr, s);
+    mark("frame_init");
     if (c->kcount &&
         ensure(c->used, sizeof(uint32_t) * ((size_t)c->cap_n + n_items)) == GSR_OK) {
         cudaMemsetAsync(c->used.p, 0, sizeof(uint32_t) * ((size_t)c->cap_n + n_items), s);
         out.used = c->used.as<uint32_t>();
         out.item_info = out.used + c->cap_n;
     }
-    DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
-    launch_blend(c->srec.as<SplatRec>(), c->col.as<float4>(), ord, c->tile_vals.as<uint32_t>(),
-                 c->ranges.as<uint2>(), W, H,
-                 bg[0], bg[1], bg[2], out, ctr, s, mark, c->kcount);
+    if (n > 0) {
+        launch_preprocess_geo(sc->view, ca, cull, c->keys[0].as<unsigned long long>(),
+                              c->geo.as<GeoRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr,
+                              ctr, s, mark);
+        launches += 1;
+        if (slice) {
+            launch_slice_plan(c->keys[0].as<unsigned long long>(), n, ctr,
+                              c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac(), c->sms,
+                              s, mark);
+            launches += 2;
+        }
+    }
+    cudaEventRecord(c->ev[1], s);
+    if (n == 0) {
+        cudaEventRecord(c->ev[2], s);
+        cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
+        cudaEventRecord(c->ev[3], s);
+        blend(0);
+        cudaEventRecord(c->ev[4], s);
+    } else if (!slice) {
+        // stable f64 depth order of all kept splats (the first radix pass
+        // compacts: drops the culled sentinels), colours, lists, blend
+        sort_color_bin(&ctr->K, nullptr, false);
+        cudaEventRecord(c->ev[3], s);
+        blend(0);
+        cudaEventRecord(c->ev[4], s);
+    } else {
+        // slice A: the front of the depth order
+        sort_color_bin(&ctr->KA, &ctr->tau, false);
+        cudaEventRecord(c->ev[3], s);
+        cudaMemsetAsync(c->unsat.p, 0, sizeof(uint32_t) * (size_t)c->ntiles, s);
+        blend(1);
+        cudaEventRecord(c->ev[4], s);
+        // slice B: the splats behind it that can reach an unsaturated item
+        SliceBArgs sb;
+        sb.keys64 = c->keys[0].as<unsigned long long>();
+        sb.geo = c->geo.as<GeoRec>();
+        sb.n = n;
+        sb.ctr = ctr;
+        sb.unsat = c->unsat.as<uint32_t>();
+        sb.width = W;
+        sb.height = H;
+        sb.tiles_x = (W + kTileW - 1) / kTileW;
+        sb.keysB = c->keys32[0].as<uint32_t>();
+        launch_slice_b_filter(sb, s, mark);
+        launches += 1;
+        sort_color_bin(&ctr->KB, nullptr, true);
+        blend(2);
+    }
     cudaEventRecord(c->ev[5], s);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters) + 2 * sizeof(uint32_t),
                     cudaMemcpyDeviceToHost, s);
@@ -355,7 +441,7 @@ int complete_frame(gsr_ctx *c) {
     c->retries = 0;
     uint8_t *out = c->saved_out;
     for (int round = 0;; round++) {
-        const int64_t d = (int64_t)c->hctr->D, p = (int64_t)c->hctr->P;
+        const int64_t d = (int64_t)c->hctr->Dmax, p = (int64_t)c->hctr->Pmax;
         const bool ov_p = p > c->cap_p, ov_d = !ov_p && d > c->cap_d;
         const bool long_runs = c->hctr->long_runs != 0 && !c->saved_full64;
         if (!ov_p && !ov_d && !long_runs) break;
@@ -386,7 +472,7 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     if (!st) return;
     st->splats_drawn = c->hctr->K;
     st->splats_culled = sc ? sc->n - (int64_t)c->hctr->K : 0;
-    st->tile_keys = c->hctr->D;
+    st->tile_keys = (int64_t)c->hctr->Dtot;
     st->depth_passes = (int32_t)(c->hctr->npass + c->hctr->npass_fb);
     st->retries = c->retries;
     float t[6] = {0, 0, 0, 0, 0, 0};
@@ -397,11 +483,12 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     cudaEventElapsedTime(&t[4], c->ev[3], c->ev[4]);
     cudaEventElapsedTime(&t[5], c->ev[4], c->ev[5]);
     st->ms_device = t[0];
-    st->ms_preprocess = t[1];
-    st->ms_depth_sort = t[2];
-    st->ms_binning = t[3];
-    st->ms_tile_sort = t[4];
-    st->ms_blend = t[5];
+    st->ms_preprocess = t[1];   // projection (+ slice plan)
+    st->ms_depth_sort = t[2];   // depth sort + colours (of slice A)
+    st->ms_binning = t[3];      // tile lists (of slice A)
+    st->ms_tile_sort = 0.0f;    // (no tile sort: sort-free lists)
+    st->ms_blend = t[4];        // blend (of slice A)
+    st->ms_slice_b = t[5];      // slice B: filter, sort, colours, lists, blend (0: one pass)
     st->kernel_launches = (int32_t)c->launches;
     c->launches = 0;
     // sticky counters as of the last completed frame's copy (no extra sync)
@@ -410,7 +497,7 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     st->long_run_frames = (int32_t)(hs[1] - c->sticky_seen[1]);
     c->sticky_seen[0] = hs[0];
     c->sticky_seen[1] = hs[1];
-    st->pairs = (int64_t)c->hctr->P;
+    st->pairs = (int64_t)c->hctr->Ptot;
     st->composited = (int64_t)c->hctr->E;
     st->row_evals_blend = (int64_t)c->hctr->Rb;
     st->row_evals_binning = (int64_t)c->hctr->Rp;
@@ -638,10 +725,12 @@ int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means
     plane_f(L.opac, opacities, 0, 1);
     plane_d(L.op64, opacities, 0, 1);
     if (rsq) plane_d(L.rsq, rsq, 0, 1);
-    if (sc->has_sh) {
-        for (int k = 0; k < 48; k++) {
-            if (sc->sh_f32) plane_f(L.sh, sh_coeffs, k, 48);
-            else plane_d(L.sh, sh_coeffs, k, 48);
+    if (sc->has_sh) {  // rows of 48 coefficients (SceneView.sh)
+        if (sc->sh_f32) {
+            float *d = reinterpret_cast<float *>(host.data() + L.sh);
+            for (int64_t i = 0; i < n * 48; i++) d[i] = (float)sh_coeffs[i];
+        } else {
+            std::memcpy(host.data() + L.sh, sh_coeffs, sizeof(double) * (size_t)(n * 48));
         }
     }
     unsigned char *d = sc->block.as<unsigned char>();
@@ -767,6 +856,15 @@ int gsr_ctx_set_kernel_timing(gsr_ctx *ctx, int enable) {
     ctx->ktime = (enable & GSR_TIMING_EVENTS) != 0;
     ctx->kcount = (enable & GSR_TIMING_COUNTERS) != 0;
     ctx->nmarks = 0;
+    return GSR_OK;
+}
+
+int gsr_ctx_set_slicing(gsr_ctx *ctx, int64_t min_gaussians, float front_fraction) {
+    if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
+    if (!(front_fraction >= 0.0f && front_fraction <= 1.0f))
+        return fail(GSR_E_INVALID, "front_fraction must be in [0, 1]");
+    ctx->slice_min_n = min_gaussians < 0 ? -1 : min_gaussians;
+    ctx->slice_frac_v = front_fraction;
     return GSR_OK;
 }
 
@@ -904,19 +1002,19 @@ int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera 
     if (out_packed && k > 0) {
         std::vector<SplatRec> r((size_t)k);
         std::vector<uint32_t> o((size_t)k);
-        std::vector<float4> col((size_t)scene->n);
+        std::vector<float4> col((size_t)k);  // colours by depth rank
         std::vector<SplatRec> geo((size_t)scene->n);  // by Gaussian index: b.w = ry
         GSR_CUDA_OK(cudaMemcpy(geo.data(), ctx->geo.p, sizeof(SplatRec) * scene->n,
                                cudaMemcpyDeviceToHost));
         const DevBuf &vb = ctx->vals[ctx->hsched[16] & 1u];
         GSR_CUDA_OK(cudaMemcpy(r.data(), ctx->srec.p, sizeof(SplatRec) * k, cudaMemcpyDeviceToHost));
         GSR_CUDA_OK(cudaMemcpy(o.data(), vb.p, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost));
-        GSR_CUDA_OK(cudaMemcpy(col.data(), ctx->col.p, sizeof(float4) * scene->n,
+        GSR_CUDA_OK(cudaMemcpy(col.data(), ctx->colr.p, sizeof(float4) * k,
                                cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < k; i++) {
             float *p = out_packed + 11 * i;
             const SplatRec &s = r[i];
-            const float4 &cc = col[o[i]];
+            const float4 &cc = col[i];
             p[0] = s.a.x; p[1] = s.a.y; p[2] = s.a.z; p[3] = s.a.w; p[4] = s.b.x; p[5] = s.b.y;
             p[6] = cc.x; p[7] = cc.y; p[8] = cc.z; p[9] = s.b.z; p[10] = geo[o[i]].b.w;
         }
@@ -925,11 +1023,28 @@ int gsr_debug_preprocess(gsr_ctx *ctx, const gsr_scene *scene, const gsr_camera 
     return GSR_OK;
 }
 
+namespace {
+// The debug entries that read the frame's depth-ranked records or lists need
+// a one-pass frame (all kept splats ranked): re-render the last call that way.
+int ensure_one_pass(gsr_ctx *c) {
+    int rc = complete_frame(c);
+    if (rc || !c->last_sliced) return rc;
+    SavedCall sv = c->saved;
+    if (!sv.scene) return fail(GSR_E_INVALID, "the last frame's scene is gone");
+    c->force_full = true;
+    rc = enqueue_frame(c, sv.scene, &sv.cam, sv.bg, sv.sh_degree, sv.cull, sv.want_rgb,
+                       sv.want_keep);
+    c->force_full = false;
+    if (rc) return rc;
+    return complete_frame(c);
+}
+}  // namespace
+
 int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_ranks,
                          int32_t *out_ranges, gsr_stats *stats) {
     if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
     DeviceGuard g(ctx->device);
-    int rc = complete_frame(ctx);
+    int rc = ensure_one_pass(ctx);
     if (rc) return rc;
     const int64_t d = std::min<int64_t>(ctx->hctr->D, ctx->cap_d);
     std::vector<uint2> rg((size_t)ctx->ntiles);
@@ -958,7 +1073,7 @@ namespace {
 // once their count is known on the host -- the 64-bit radix sort and the
 // ranges.  Two attempts: the first with the capacity of the previous frame.
 int build_contract(gsr_ctx *c, int tile) {
-    const int64_t k = (int64_t)c->hctr->K;
+    const int64_t k = (int64_t)c->hctr->K;  // one-pass frame: all kept splats ranked
     const int tiles_x = (c->W + tile - 1) / tile, ntiles = tiles_x * ((c->H + tile - 1) / tile);
     int rc;
     if (c->cap_c == 0) c->cap_c = round_up(std::max<int64_t>(int64_t(1) << 20, 8 * k), 4096);
@@ -974,7 +1089,7 @@ int build_contract(gsr_ctx *c, int tile) {
         }
         ContractArgs a;
         a.srec = c->srec.as<SplatRec>();
-        a.ctr = c->ctr.as<FrameCounters>();
+        a.count = &c->ctr.as<FrameCounters>()->K;
         a.width = c->W;
         a.tile = tile;
         a.tiles_x = tiles_x;
@@ -1022,9 +1137,9 @@ int gsr_debug_contract_tiles(gsr_ctx *ctx, int tile, int64_t *out_count, int32_t
     if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
     if (tile < 1 || tile > 256) return fail(GSR_E_INVALID, "tile size must be in 1..256");
     DeviceGuard g(ctx->device);
-    int rc = complete_frame(ctx);
-    if (rc) return rc;
     if (ctx->W <= 0 || ctx->H <= 0) return fail(GSR_E_INVALID, "no frame rendered on this context");
+    int rc = ctx->contract_tile == tile ? complete_frame(ctx) : ensure_one_pass(ctx);
+    if (rc) return rc;
     if (ctx->contract_tile != tile && (rc = build_contract(ctx, tile))) return rc;
     const int64_t d = ctx->contract_d;
     if (out_count) *out_count = d;

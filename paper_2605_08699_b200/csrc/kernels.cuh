@@ -43,7 +43,39 @@ struct FrameCounters {
     unsigned long long b_lanes;    // sum over iterations of lanes with a splat to composite
     unsigned long long b_items;    // work items processed
     unsigned long long b_used;     // distinct splats whose colour the blend read
+    // depth-sliced frames (slice.cu): per-pass item counts, slice threshold,
+    // per-pass binning sizes summed / maximised over the passes
+    uint32_t KA;                   // items of the first pass (the slice, or all K)
+    uint32_t KB;                   // splats of the second pass
+    uint32_t tau;                  // slice: span keys <= tau
+    uint32_t pad3;
+    unsigned long long Dtot, Ptot; // tile keys / pairs over the passes
+    unsigned long long Dmax, Pmax; // largest pass (buffer capacities)
+    uint32_t slice_hist[256];      // top 8 bits of the kept span keys
 };
+
+// The depth sort's 24-bit span key of a kept splat's f64 depth bits k64
+// (depth.cu): k32 = min((k64 - kmin) >> shift, 2^24 - 1), shift chosen from
+// [kmin, kmax] so the span fits 24 bits.  Monotone in k64.
+constexpr int kSpanKeyBits = 24;
+struct SpanMap {
+    unsigned long long kmin, kcap;
+    int shift;
+};
+__device__ __forceinline__ SpanMap span_map(unsigned long long kmin, unsigned long long kmax,
+                                            int bits = kSpanKeyBits) {
+    SpanMap m;
+    const unsigned long long range = kmax > kmin ? kmax - kmin : 0ull;
+    const int b = range ? 64 - __clzll((long long)range) : 0;
+    m.kmin = kmin;
+    m.shift = b > bits ? b - bits : 0;
+    m.kcap = (1ull << bits) - 1ull;
+    return m;
+}
+__device__ __forceinline__ uint32_t span_key(const SpanMap &m, unsigned long long k64) {
+    const unsigned long long q = (k64 - m.kmin) >> m.shift;
+    return (uint32_t)(q < m.kcap ? q : m.kcap);
+}
 
 // Scene in HBM, structure-of-arrays, each plane padded to `stride` elements.
 struct SceneView {
@@ -55,7 +87,9 @@ struct SceneView {
     const double *rsq;    // [stride]     render.py:476-481, f64
     const float *opac;    // [stride]     f32(opacity)
     const float *dc;      // [3][stride]  f32(colors_dc)
-    const void *sh;       // [48][stride] f32 or f64, coefficient-major (k*3 + c)
+    const void *sh;       // [stride][48] f32 or f64: one 192 B (384 B) row per Gaussian,
+                          // coefficient k*3 + c; rows so a gather by depth rank reads
+                          // whole sectors (colour only for the splats a pass blends)
     const double *op64;   // [stride]     f64 opacity (rsq, read-back)
     int sh_f32;
 };
@@ -69,6 +103,11 @@ struct CameraArgs {
     int iwidth, iheight;
 };
 
+struct DepthOrder {  // depth rank -> Gaussian index (the depth sort's result buffer)
+    const uint32_t *order0, *order1;
+    const uint32_t *sched;  // sched[16]: which buffer holds the result
+};
+
 // preprocess.cu (2 kernels)
 using GeoRec = SplatRec;  // by Gaussian index (preprocess), by depth rank (gather)
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
@@ -76,12 +115,6 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 void launch_preprocess_geo(const SceneView &scene, const CameraArgs &cam, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
                            FrameCounters *ctr, cudaStream_t s, const KMark &mark = KMark());
-// K1b: SH colours of the kept Gaussians (render.py:126-160); needs the keys
-// of K1a, read only by the blend, so it may run beside the depth sort
-void launch_preprocess_color(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                             const unsigned long long *keys, float4 *col, cudaStream_t s,
-                             const KMark &mark = KMark());
-
 // radix.cu: Onesweep stable LSD sort (see radix.cu header)
 cudaError_t radix_init_attributes();
 #ifndef GSR_RADIX_THREADS
@@ -107,6 +140,7 @@ struct SpanKeys {
     const unsigned long long *src = nullptr;
     const unsigned long long *kmin = nullptr, *kmax = nullptr;
     int bits = 24;
+    const uint32_t *limit = nullptr;  // span keys above *limit become sentinels (slice A)
 };
 // Sorts (keys0, vals0) over `passes` 8-bit digits; the result lands in buffer
 // sched[16] (0 or 1).  First pass: n_first items (>= 0) or *n_dev (n_first <
@@ -131,6 +165,9 @@ struct DepthArgs {
     uint32_t *sched;    // sort schedule: sched[16] = buffer of vals holding the order
     bool full64;        // full 64-bit key sort (after a frame reported long runs)
     uint32_t *long_run_sticky;  // per-context count of frames that reported long runs
+    uint32_t *count = nullptr;         // items after compaction (K, the slice's KA, or KB)
+    const uint32_t *limit = nullptr;   // slice A: span keys <= *limit only
+    bool keys_given = false;  // keys32[0] already holds the span keys / sentinels (slice B)
 };
 size_t depth_work32_bytes(int64_t n_cap);
 size_t depth_work64_bytes(int64_t n_cap);
@@ -141,6 +178,7 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s,
 constexpr int kMaxTileRows = 8192 / kTileH;   // height <= 8192
 constexpr int kMaxTilesX = 16384 / kTileW;   // width <= 16384
 struct BinArgs {
+    const uint32_t *count;            // depth-ranked items of this pass
     const uint32_t *order0, *order1;  // depth sort result buffers
     const uint32_t *depth_sched;      // [16]: which of order0/order1 holds the result
     const GeoRec *geo;                // packed geometry by Gaussian index (preprocess)
@@ -175,7 +213,7 @@ int launch_binning(const BinArgs &a, cudaStream_t s,
 // (tile | rank) keys, a radix sort and range identification (parity path)
 struct ContractArgs {
     const SplatRec *srec;            // depth-ranked records of the frame (bin_gather)
-    const FrameCounters *ctr;        // K
+    const uint32_t *count;           // ranked items (K of a one-pass frame)
     int width, tile, tiles_x;
     unsigned long long *keys;        // [cap] (ty * tiles_x + tx) << 32 | rank
     int64_t cap;
@@ -187,6 +225,12 @@ int launch_contract_ranges(const unsigned long long *keys0, const unsigned long 
                            const uint32_t *sched, const unsigned long long *d_count, int64_t cap,
                            uint2 *ranges, int ntiles, int sms, cudaStream_t s);
 
+// preprocess.cu, K1b: SH colours (render.py:126-160) of the ranks [0, *count)
+// of a pass's depth order, stored by rank: colr[r] = (r, g, b, 0)
+void launch_color_ranked(const SceneView &scene, const CameraArgs &cam, int sh_degree,
+                         DepthOrder ord, const uint32_t *count, int64_t cap, float4 *colr,
+                         cudaStream_t s, const KMark &mark = KMark());
+
 // blend.cu
 struct BlendOut {
     uint8_t *u8;    // (H,W,3)
@@ -197,15 +241,29 @@ struct BlendOut {
     uint32_t *used = nullptr;  // instrumentation (counting variant): per-rank "colour read" flags
     uint32_t *item_info = nullptr;  // ... per work item: last depth rank walked | saturated << 31
 };
-struct DepthOrder {  // depth rank -> Gaussian index (the depth sort's result buffer)
-    const uint32_t *order0, *order1;
-    const uint32_t *sched;  // sched[16]: which buffer holds the result
+bool blend_has_slices();  // the selected blend variant has modes 1 and 2
+// mode: 0 one pass; 1 slice A (saturated items write the frame, the others
+// save their pixels' state and set their unsat bit); 2 slice B (unsat items
+// only, from the saved state)
+void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
+                  const uint2 *ranges, int width, int height, float bg0, float bg1, float bg2,
+                  BlendOut out, FrameCounters *ctr, cudaStream_t s, const KMark &mark = KMark(),
+                  bool count = true, int mode = 0, float4 *state = nullptr,
+                  uint32_t *unsat = nullptr);  // count: fill the E / Rb work counters
+
+// slice.cu: depth-sliced frames
+struct SliceBArgs {
+    const unsigned long long *keys64;  // preprocess keys (sentinel ~0 = culled)
+    const GeoRec *geo;                 // records by Gaussian index
+    int64_t n;
+    FrameCounters *ctr;                // kmin, kmax, tau; KB counted here
+    const uint32_t *unsat;             // [ntiles] items of slice A left unsaturated
+    int width, height, tiles_x;
+    uint32_t *keysB;                   // out: span key of a slice-B member, else ~0
 };
-void launch_blend(const SplatRec *srec, const float4 *col, DepthOrder ord,
-                  const uint32_t *tile_vals, const uint2 *ranges, int width,
-                  int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *ctr,
-                  cudaStream_t s, const KMark &mark = KMark(),
-                  bool count = true);  // count: fill the E / Rb work counters
+void launch_slice_plan(const unsigned long long *keys64, int64_t n, FrameCounters *ctr,
+                       float frac, int sms, cudaStream_t s, const KMark &mark = KMark());
+void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark = KMark());
 
 // jpeg.cu: baseline JPEG of a device u8 frame (Pillow / libjpeg-turbo exact)
 struct JpegLayout {

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kPlyThreads) ply_activate_kernel(
         for (int k = 0; k < 3; k++) {
             dc[k] = at(11 + k);
             if (!finite32(dc[k])) bad |= kBadSh;
-            o.sh[(int64_t)k * st + g] = dc[k];  // sh[:, 0, c] (model.py:193)
+            o.sh[g * 48 + k] = dc[k];  // sh[:, 0, c] (model.py:193)
         }
         // sh[:, 1 + i, c] = f_rest_{15 c + i} (channel-major on disk, model.py:197-198)
 #pragma unroll 5
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kPlyThreads) ply_activate_kernel(
                     v = at(kRequired + 15 * c + i);
                     if (!finite32(v)) bad |= kBadSh;
                 }
-                o.sh[(int64_t)(3 * (1 + i) + c) * st + g] = v;
+                o.sh[g * 48 + 3 * (1 + i) + c] = v;
             }
         }
         // activation (model.py:211-252)
@@ -396,12 +396,15 @@ __global__ void rsq_kernel(const double *__restrict__ op64, int64_t n, double *_
 }
 
 // planes -> row-major f64 (ActivatedPrimitives layout)
+// plane: SoA planes (k * stride + row) unless row_width > 0: rows of
+// row_width values (row * row_width + k, the SH rows)
 __global__ void scene_read_kernel(const void *plane, int f32, int64_t stride, int comps,
-                                  int64_t n0, int64_t rows, int colors, double *__restrict__ out) {
+                                  int64_t n0, int64_t rows, int colors, int row_width,
+                                  double *__restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows * comps) return;
     const int64_t r = i / comps, k = i % comps;
-    const int64_t src = k * stride + n0 + r;
+    const int64_t src = row_width ? (n0 + r) * row_width + k : k * stride + n0 + r;
     double v = f32 ? (double)reinterpret_cast<const float *>(plane)[src]
                    : reinterpret_cast<const double *>(plane)[src];
     if (colors) {  // colors_dc from f_dc (model.py:227)
@@ -682,7 +685,7 @@ int scene_read(const gsr_scene *sc, int attr, double *host) {
     if (!host && sc->n > 0) return fail(GSR_E_INVALID, "output is null");
     const SceneView &v = sc->view;
     const void *plane = nullptr;
-    int comps = 0, f32 = 0, colors = 0;
+    int comps = 0, f32 = 0, colors = 0, row_width = 0;
     switch (attr) {
         case GSR_ATTR_MEANS: plane = v.mean; comps = 3; break;
         case GSR_ATTR_SCALES: plane = v.scale; comps = 3; break;
@@ -691,11 +694,11 @@ int scene_read(const gsr_scene *sc, int attr, double *host) {
         case GSR_ATTR_COLORS_DC:
             if (!sc->from_ply)
                 return fail(GSR_E_INVALID, "colors_dc is stored as f32 only for this scene");
-            plane = v.sh; comps = 3; f32 = 1; colors = 1;
+            plane = v.sh; comps = 3; f32 = 1; colors = 1; row_width = 48;
             break;
         case GSR_ATTR_SH:
             if (!sc->has_sh) return fail(GSR_E_INVALID, "scene has no SH coefficients");
-            plane = v.sh; comps = 48; f32 = sc->sh_f32;
+            plane = v.sh; comps = 48; f32 = sc->sh_f32; row_width = 48;
             break;
         case GSR_ATTR_RSQ: plane = v.rsq; comps = 1; break;
         default: return fail(GSR_E_INVALID, "unknown attribute");
@@ -709,8 +712,8 @@ int scene_read(const gsr_scene *sc, int attr, double *host) {
     for (int64_t n0 = 0; n0 < sc->n; n0 += chunk) {
         const int64_t rows = std::min(chunk, sc->n - n0);
         const int64_t items = rows * comps;
-        scene_read_kernel<<<(unsigned)((items + 255) / 256), 256>>>(plane, f32, sc->stride, comps, n0,
-                                                                    rows, colors, tmp.as<double>());
+        scene_read_kernel<<<(unsigned)((items + 255) / 256), 256>>>(
+            plane, f32, sc->stride, comps, n0, rows, colors, row_width, tmp.as<double>());
         cudaError_t e = cudaMemcpy(host + n0 * comps, tmp.p, (size_t)(items * 8), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return fail_cuda(e, "scene read");
     }

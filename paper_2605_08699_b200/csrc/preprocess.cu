@@ -58,7 +58,9 @@ __device__ __forceinline__ double sh_channel(const T *v, int c, double x, double
     return r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);  // np.clip(result + 0.5, 0, 1)
 }
 
-__global__ void frame_init_kernel(FrameCounters *ctr) {
+__global__ void __launch_bounds__(256) frame_init_kernel(FrameCounters *ctr) {
+    ctr->slice_hist[threadIdx.x] = 0u;
+    if (threadIdx.x) return;
     ctr->K = 0;
     ctr->D = 0;
     ctr->npass = 0;
@@ -73,7 +75,10 @@ __global__ void frame_init_kernel(FrameCounters *ctr) {
     ctr->Rp = 0ull;
     ctr->blend_next = 0;
     ctr->pad2 = 0;
-    ctr->b_walked = ctr->b_hit = ctr->b_batches = ctr->b_iters = ctr->b_lanes = ctr->b_items = ctr->b_used = 0ull;
+    ctr->b_walked = ctr->b_hit = ctr->b_batches = ctr->b_iters = ctr->b_lanes = 0ull;
+    ctr->b_items = ctr->b_used = 0ull;
+    ctr->KA = ctr->KB = ctr->tau = ctr->pad3 = 0u;
+    ctr->Dtot = ctr->Ptot = ctr->Dmax = ctr->Pmax = 0ull;
 }
 
 __global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
@@ -198,14 +203,19 @@ __global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
     }
 }
 
-// All of a Gaussian's loads are issued before any arithmetic (one memory
-// round trip per thread instead of one per SH degree block).
+// Colour of the splat at depth rank r of a pass (order[r] = Gaussian index):
+// the Gaussian's SH row (rows of 48 coefficients, 12 x 16 B loads) and mean,
+// every load before any arithmetic (one memory round trip).  Only the ranks
+// a pass sorted are coloured, so splats behind the front slice that no
+// unsaturated pixel reaches never read their 192 B of SH.
 template <typename ShT, int DEG>
-__global__ void __launch_bounds__(256) preprocess_color_kernel(
-    SceneView sc, CameraArgs cam, const unsigned long long *__restrict__ keys,
-    float4 *__restrict__ col) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= sc.n || __ldg(keys + i) == ~0ull) return;  // culled: no colour needed
+__global__ void __launch_bounds__(256) color_ranked_kernel(
+    SceneView sc, CameraArgs cam, DepthOrder ord, const uint32_t *__restrict__ count,
+    float4 *__restrict__ colr) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= (int64_t)*count) return;
+    const uint32_t *order = ord.sched[16] ? ord.order1 : ord.order0;
+    const int64_t i = __ldg(order + r);
     const int64_t st = sc.stride;
     float cr, cg, cbl;
     if (DEG == 0) {  // render.py:129-130
@@ -214,10 +224,27 @@ __global__ void __launch_bounds__(256) preprocess_color_kernel(
         cbl = __ldg(sc.dc + 2 * st + i);
     } else {  // render.py:134-160
         constexpr int NC = (DEG + 1) * (DEG + 1) * 3;
-        const ShT *sh = (const ShT *)sc.sh;
         ShT v[NC];
+        if (sizeof(ShT) == 4) {  // f32 rows: 192 B, 16 B aligned
+            constexpr int N4 = (NC + 3) / 4;
+            const float4 *row = reinterpret_cast<const float4 *>(sc.sh) + i * 12;
+            float4 q[N4];
 #pragma unroll
-        for (int k = 0; k < NC; k++) v[k] = __ldg(sh + (int64_t)k * st + i);
+            for (int k = 0; k < N4; k++) q[k] = __ldg(row + k);
+#pragma unroll
+            for (int k = 0; k < NC; k++) {
+                const float4 &w = q[k >> 2];
+                v[k] = (ShT)((k & 3) == 0 ? w.x : (k & 3) == 1 ? w.y : (k & 3) == 2 ? w.z : w.w);
+            }
+        } else {  // f64 rows: 384 B
+            constexpr int N2 = (NC + 1) / 2;
+            const double2 *row = reinterpret_cast<const double2 *>(sc.sh) + i * 24;
+            double2 q[N2];
+#pragma unroll
+            for (int k = 0; k < N2; k++) q[k] = __ldg(row + k);
+#pragma unroll
+            for (int k = 0; k < NC; k++) v[k] = (ShT)((k & 1) ? q[k >> 1].y : q[k >> 1].x);
+        }
         const double mx = __ldg(sc.mean + i), my = __ldg(sc.mean + st + i),
                      mz = __ldg(sc.mean + 2 * st + i);
         const double dx = mx - cam.campos[0];
@@ -232,13 +259,13 @@ __global__ void __launch_bounds__(256) preprocess_color_kernel(
         cg = (float)sh_channel<DEG>(v, 1, ux, uy, uz, xx, yy, zz, xy, yz, xz);
         cbl = (float)sh_channel<DEG>(v, 2, ux, uy, uz, xx, yy, zz, xy, yz, xz);
     }
-    col[i] = make_float4(cr, cg, cbl, 0.0f);
+    colr[r] = make_float4(cr, cg, cbl, 0.0f);
 }
 
 }  // namespace
 
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
-    frame_init_kernel<<<1, 1, 0, s>>>(ctr);
+    frame_init_kernel<<<1, 256, 0, s>>>(ctr);
 }
 
 void launch_preprocess_geo(const SceneView &scene, const CameraArgs &cam, int frustum_cull,
@@ -252,14 +279,14 @@ void launch_preprocess_geo(const SceneView &scene, const CameraArgs &cam, int fr
     mark("preprocess_geo");
 }
 
-void launch_preprocess_color(const SceneView &scene, const CameraArgs &cam, int sh_degree,
-                             const unsigned long long *keys, float4 *col, cudaStream_t s,
-                             const KMark &mark) {
-    if (scene.n == 0) return;
+void launch_color_ranked(const SceneView &scene, const CameraArgs &cam, int sh_degree,
+                         DepthOrder ord, const uint32_t *count, int64_t cap, float4 *colr,
+                         cudaStream_t s, const KMark &mark) {
+    if (cap <= 0) return;
     const int threads = 256;
-    const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
+    const unsigned blocks = (unsigned)((cap + threads - 1) / threads);
 #define GSR_COLOR(T, D)                                                                   \
-    preprocess_color_kernel<T, D><<<blocks, threads, 0, s>>>(scene, cam, keys, col)
+    color_ranked_kernel<T, D><<<blocks, threads, 0, s>>>(scene, cam, ord, count, colr)
     if (sh_degree == 0) GSR_COLOR(float, 0);
     else if (scene.sh_f32 && sh_degree == 1) GSR_COLOR(float, 1);
     else if (scene.sh_f32 && sh_degree == 2) GSR_COLOR(float, 2);
@@ -268,7 +295,7 @@ void launch_preprocess_color(const SceneView &scene, const CameraArgs &cam, int 
     else if (sh_degree == 2) GSR_COLOR(double, 2);
     else GSR_COLOR(double, 3);
 #undef GSR_COLOR
-    mark("preprocess_color");
+    mark("color_ranked");
 }
 
 }  // namespace gsr

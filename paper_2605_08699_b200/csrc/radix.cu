@@ -99,16 +99,11 @@ __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
     __syncthreads();
     const int64_t n = first_count(a);
     const K *keys = a.keys[0];
-    unsigned long long kmin = 0;
-    int shift = 0;
-    unsigned long long kcap = 0;
+    SpanMap sm{0ull, 0ull, 0};
+    uint32_t limit = 0xffffffffu;
     if (sizeof(K) == 4 && a.span.src) {
-        kmin = *a.span.kmin;
-        const unsigned long long kmax = *a.span.kmax;
-        const unsigned long long range = kmax > kmin ? kmax - kmin : 0ull;
-        const int bits = range ? 64 - __clzll((long long)range) : 0;
-        shift = bits > a.span.bits ? bits - a.span.bits : 0;
-        kcap = (1ull << a.span.bits) - 1ull;
+        sm = span_map(*a.span.kmin, *a.span.kmax, a.span.bits);
+        if (a.span.limit) limit = *a.span.limit;
     }
     // kHU keys per thread per step, all loads issued before any use (the
     // loop is otherwise one global latency per key)
@@ -129,9 +124,9 @@ __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
             const int64_t i = i0 + u * stride;
             if (i >= n) continue;
             K k;
-            if (span) {  // span key of the depth bits
-                const unsigned long long q = (k64[u] - kmin) >> shift;
-                k = k64[u] == ~0ull ? sentinel<K>() : (K)(q < kcap ? q : kcap);
+            if (span) {  // span key of the depth bits (slice A: above the limit -> dropped)
+                const uint32_t q = span_key(sm, k64[u]);
+                k = (k64[u] == ~0ull || q > limit) ? sentinel<K>() : (K)q;
                 a.keys[0][i] = k;
             } else {
                 k = kk[u];

@@ -491,6 +491,19 @@ def debug_tile_lists(*, device: int | None = None):
     return tiles[:d].copy(), ranks[:d].copy()
 
 
+def set_slicing(min_gaussians: int = -1, front_fraction: float = 0.0, *,
+                device: int | None = None) -> None:
+    """Depth-sliced frames for the calling thread's context (gsr_ctx_set_slicing,
+    slice.cu): scenes of >= min_gaussians Gaussians render the front
+    front_fraction of the depth order first, then only the splats that can
+    reach a pixel still unsaturated.  Frames are identical either way;
+    (-1, 0.0) restores the defaults, a huge min_gaussians disables slicing."""
+    dev = _default_device if device is None else device
+    ctx = _lib.context(dev)
+    _lib.check(ctx.lib.gsr_ctx_set_slicing(ctx.handle, int(min_gaussians),
+                                           float(front_fraction)), "gsr_ctx_set_slicing")
+
+
 def debug_contract_tiles(width: int, height: int, tile: int = 16, *,
                          device: int | None = None):
     """The exact tile-list contract of the calling thread's last render
@@ -532,5 +545,5 @@ __all__ = ["Framebuffer", "RenderStats", "RenderError", "EncodeFailure", "Device
            "device_scene", "evict", "set_device", "render_framebuffer", "render_u8",
            "render_view", "framebuffer_to_u8", "encode_jpeg", "encode_png", "decode_image",
            "cutoff_radius_sq", "make_camera", "debug_preprocess", "debug_tile_lists",
-           "debug_contract_tiles",
+           "debug_contract_tiles", "set_slicing",
            "debug_tile_ranges", "Intrinsics"]

@@ -774,3 +774,36 @@ def test_config5_sessions_spot_check(gsr, oracle):
                                          subsampling=2 if rung["jpeg_quality"] < 90 else 0)
         assert payload == buf.getvalue(), (s.index, rung)
     pipe.close()
+
+
+@pytest.mark.parametrize("frac", [0.01, 0.05, 0.15, 0.5, 1.0])
+def test_depth_sliced_frames_equal_one_pass(gsr, oracle, frac):
+    """Depth-sliced frames (slice.cu: front slice, then only the splats that
+    can reach an unsaturated item, from the saved pixel state) equal the
+    one-pass frame and the oracle float for float, for slices from 1 % to
+    all of the kept splats, with rgb/T planes, backgrounds and SH degrees."""
+    from paper_2605_08699_b200.render import set_slicing
+    from paper_2605_08699_b200.synth import synthetic_scene
+    cases = [(40_000, 3, 0, (320, 240), (0.0, 0.0, 0.0)),
+             (60_000, 5, 3, (333, 217), (0.25, 0.5, 0.75)),
+             (30_000, 9, 1, (640, 360), (1.0, 1.0, 1.0))]
+    try:
+        for n, seed, sh, (w, h), bg in cases:
+            prims = synthetic_scene(n, seed=seed, sh_degree=3)
+            intr = gsr.Intrinsics(fx=0.9 * w, fy=0.9 * w, cx=w / 2, cy=h / 2, width=w, height=h)
+            for k in range(3):
+                pose = gsr.CameraPose(0.05 * k - 0.04, 0.02 * k, (0.02 * k, -0.01, 0.2 * k))
+                set_slicing(1 << 40)  # one pass
+                one = gsr.render_framebuffer(prims, pose, intr, bg, sh)
+                set_slicing(1, frac)
+                st = gsr.RenderStats()
+                sl = gsr.render_framebuffer(prims, pose, intr, bg, sh, st)
+                assert np.array_equal(sl._rgb32, one._rgb32), (n, k, frac)
+                assert np.array_equal(sl._t32, one._t32)
+                assert np.array_equal(sl.u8, one.u8)
+                u8 = gsr.render_u8(prims, pose, intr, bg, sh)
+                assert np.array_equal(u8, one.u8)
+                if k == 0:
+                    assert np.array_equal(sl.u8, _oracle_frame(oracle, prims, pose, intr, sh, bg).u8)
+    finally:
+        set_slicing()
