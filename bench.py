@@ -393,30 +393,35 @@ def load_simt_peaks():
 
 
 def kernel_work(name, wl, c):
-    """Algorithmic units of ONE launch of a kernel:
-    (bytes, fp32 ops)."""
+    """Algorithmic units of a kernel over ONE frame, all its launches
+    (DESIGN.md section 4): (bytes, fp32 ops).  KA / KB: splats sorted by the
+    first / second depth slice (K, 0 for a one-pass frame)."""
     n, k, d, p = wl["n"], c["K"], c["D"], c["P"]
+    ks = c["KA"] + c["KB"]  # splats ranked, coloured and binned over the slices
     sh_bytes = 12 * (wl["sh"] + 1) ** 2 if wl["sh"] else 12
     px = wl["w"] * wl["h"]
+    sliced = c["KB"] > 0 or c["KA"] < k
     table = {
         # mean/scale/rotation/rsq f64 + opacity f32 in; key for all N; record of kept
         "preprocess_geo": (n * 92 + n * 8 + k * 32, 0),
-        # key of all N; mean f64 + SH f32 (or DC) of kept in; colour out
-        "preprocess_color": (n * 8 + k * (24 + sh_bytes) + k * 16, 0),
-        # reads the f64 depth key of all N, writes the 32-bit span key
-        "radix32_hist": (n * 12, 0),
-        "radix32_pass": (k * 16, 0),  # per pass: key + index read and written
-        "depth_fixup": (k * 4, 0),
+        "slice_hist": (n * 8, 0),
+        # order + mean f64 + SH row (or DC) of each ranked splat in; colour out
+        "color_ranked": (ks * (4 + 24 + sh_bytes + 16), 0),
+        # f64 depth key of all N in, span key out (slice B: span keys in)
+        "radix32_hist": (n * 12 + (n * 4 if sliced else 0), 0),
+        "radix32_pass": (3 * ks * 16, 0),  # per pass: key + index read and written
+        "depth_fixup": (ks * 4, 0),
+        "slice_b_filter": (n * (8 + 32 + 4), 0),
         # order + geometry gathered, 32 B record written
-        "bin_gather": (k * (4 + 32) + k * 32, 0),
+        "bin_gather": (ks * (4 + 32 + 32), 0),
         # records in, pairs out; 20 FP32 ops per exact row interval (render.py:383-397)
         # evaluated (pairs whose span the f64 band bound settles need none)
-        "bin_pairs": (k * 32 + p * 8, 20 * c["Rp"]),
+        "bin_pairs": (ks * 32 + p * 8, 20 * c["Rp"]),
         "seg_count": (p * 8, 0),
         "seg_place": (p * 8 + d * 4, 0),
-        # lists + each record (and colour) once + u8 frame; 20 FP32 ops per
+        # lists + each record and colour once + u8 frame; 20 FP32 ops per
         # composited evaluation (render.py:405-421) and per row interval (383-397)
-        "blend": (d * 4 + k * 52 + 3 * px, 20 * (c["E"] + c["Rb"])),
+        "blend": (d * 4 + ks * 48 + 3 * px, 20 * (c["E"] + c["Rb"])),
     }
     return table.get(name, (0, 0))
 
@@ -451,9 +456,10 @@ def kernel_profile(lib, ctx, sc, cams, sh, frames, wl, peaks, simt):
         for cam in cams[:frames]:
             _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cam), _bg((0, 0, 0)), sh,
                                       1, None, None, None, ctypes.byref(st)))
-            counters.append({"K": st.splats_drawn, "D": st.tile_keys, "P": st.pairs,
-                             "E": st.composited, "Rb": st.row_evals_blend,
-                             "Rp": st.row_evals_binning})
+            raw = (ctypes.c_uint64 * 15)()
+            _lib.check(lib.gsr_debug_frame_counters(ctx.handle, raw, 15))
+            counters.append({"K": raw[0], "D": raw[1], "P": raw[2], "E": raw[3], "Rb": raw[4],
+                             "Rp": raw[5], "KA": raw[13], "KB": raw[14]})
     finally:
         lib.gsr_ctx_set_kernel_timing(ctx.handle, 0)
     nf = max(1, len(counters))  # same frames for both passes
@@ -461,11 +467,13 @@ def kernel_profile(lib, ctx, sc, cams, sh, frames, wl, peaks, simt):
     hbm = float(peaks["hbm_gbs"])
     fp32 = float(simt["fp32_tops"])
     out = {}
+    if "blend_a" in agg:  # the two slices' blends, as one kernel for the roofline
+        agg["blend"] = agg.get("blend_a", 0.0) + agg.get("blend_b", 0.0)
+        launches["blend"] = launches.get("blend_a", 0) + launches.get("blend_b", 0)
     for nm, tot in agg.items():
         per_frame = tot / nf
         nl = launches[nm] / nf
-        b, f = kernel_work(nm, wl, mean_c)
-        b, f = b * nl, f * nl  # per frame
+        b, f = kernel_work(nm, wl, mean_c)  # per frame
         e = {"ms_per_frame": round(per_frame, 4), "launches_per_frame": nl,
              "bound": BOUND.get(nm, "hbm") if f or nm not in BOUND else "hbm"}
         if b and per_frame > 0:
@@ -640,12 +648,13 @@ def run_gsr(args, wl):
                                   None, None, None, ctypes.byref(st)))
         stage_stats.append(st.as_dict())
     stages = {k[3:]: round(float(np.mean([x[k] for x in stage_stats])), 4)
-              for k in ["ms_preprocess", "ms_depth_sort", "ms_binning", "ms_blend"]}
+              for k in ["ms_preprocess", "ms_depth_sort", "ms_binning", "ms_blend", "ms_slice_b"]}
     peaks, peak_kind = load_peaks()
     simt = load_simt_peaks()
     kernels, counters = kernel_profile(lib, ctx, sc, cams[W:], wl["sh"], min(K, 30), wl, peaks,
                                        simt)
-    dom = max(kernels, key=lambda x: kernels[x]["ms_per_frame"])
+    dom = max((x for x in kernels if x not in ("blend_a", "blend_b")),
+              key=lambda x: kernels[x]["ms_per_frame"])
     dk = kernels[dom]
     if dk["bound"] == "fp32":
         roof = {"bound": "fp32", "kernel": dom, "achieved": dk["achieved_tflops"],
@@ -657,7 +666,8 @@ def run_gsr(args, wl):
                 "peak_source": peak_kind}
     roof["traffic"] = TRAFFIC.get(dom)
     roof["alg_per_frame"] = dk.get("alg_fp32_ops") or dk.get("alg_bytes")
-    roof["ms_per_launch"] = dk["ms_per_frame"] / max(dk["launches_per_frame"], 1)
+    roof["ms_per_frame"] = dk["ms_per_frame"]
+    roof["launches_per_frame"] = dk["launches_per_frame"]
     roof["timed_variant"] = "serving (no work counters); counters from separate frames"
     if roof["bound"] == "fp32":
         # the contract's two bounds are hbm / tensor; this kernel is bound by

@@ -29,6 +29,8 @@
 //              so each list comes out in increasing rank order.
 // Only 4-byte ranks are written per list entry; there is no key array and
 // no radix pass.  Counts stay on the device (no host synchronisation).
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "scan.cuh"
 
@@ -322,16 +324,10 @@ __device__ __forceinline__ void seg_bounds(const BinArgs &a, int64_t g, int64_t 
 }
 
 // ---------------------------------------------------------------- 2b -------
-// one warp per segment: keys per tile column via a difference array
-__global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
-    extern __shared__ __align__(16) uint32_t diff_all[];  // [8][tiles_x + 1]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t g = (int64_t)blockIdx.x * 8 + w;
-    if (overflowed(a)) return;
-    const int64_t nseg = seg_count_of(a);
-    if (g >= nseg) return;
+__device__ __forceinline__ void seg_count_one(const BinArgs &a, int64_t g, int64_t nseg,
+                                              uint32_t *diff, int lane) {
     const int tx_n = a.tiles_x;
-    uint32_t *diff = diff_all + w * (tx_n + 1);
+    __syncwarp();  // the warp's previous segment is done with diff
     for (int t = lane; t <= tx_n; t += 32) diff[t] = 0;
     __syncwarp();
     uint32_t ty, p0, p1;
@@ -354,6 +350,16 @@ __global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
         if (t < tx_n) a.seg_cnt[g * tx_n + t] = inc;
         carry = __shfl_sync(0xffffffffu, inc, 31);
     }
+}
+
+// one warp per segment: keys per tile column via a difference array
+__global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
+    extern __shared__ __align__(16) uint32_t diff_all[];  // [8][tiles_x + 1]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (overflowed(a)) return;
+    const int64_t nseg = seg_count_of(a);
+    for (int64_t g = (int64_t)blockIdx.x * 8 + w; g < nseg; g += (int64_t)gridDim.x * 8)
+        seg_count_one(a, g, nseg, diff_all + w * (a.tiles_x + 1), lane);
 }
 
 // ---------------------------------------------------------------- 2c -------
@@ -409,17 +415,11 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(BinArgs a) {
 }
 
 // ---------------------------------------------------------------- 2d -------
-__global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
-    // per warp: column cursors [tiles_x] and coverage masks [tiles_x]
-    extern __shared__ __align__(16) uint32_t place_smem[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t g = (int64_t)blockIdx.x * 8 + w;
-    if (overflowed(a)) return;
-    const int64_t nseg = seg_count_of(a);
-    if (g >= nseg) return;
+__device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64_t nseg,
+                                              uint32_t *cur, int lane) {
     const int tx_n = a.tiles_x;
-    uint32_t *cur = place_smem + w * 2 * tx_n;
     uint32_t *mask = cur + tx_n;
+    __syncwarp();  // the warp's previous segment is done with cur / mask
     uint32_t ty, p0, p1;
     seg_bounds(a, g, nseg, ty, p0, p1);
     const uint32_t *tstart = a.tile_start + (int64_t)ty * tx_n;
@@ -506,6 +506,17 @@ __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
     }
 }
 
+__global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
+    // per warp: column cursors [tiles_x] and coverage masks [tiles_x]
+    extern __shared__ __align__(16) uint32_t place_smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (overflowed(a)) return;
+    const int64_t nseg = seg_count_of(a);
+    for (int64_t g = (int64_t)blockIdx.x * 8 + w; g < nseg; g += (int64_t)gridDim.x * 8)
+        seg_place_one(a, g, nseg, place_smem + w * 2 * a.tiles_x, lane);
+}
+
+
 }  // namespace
 
 int64_t bin_blocks(int64_t n_cap) { return (n_cap + BR - 1) / BR; }
@@ -540,7 +551,9 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark) {
     mark("bin_pairs");
     seg_table_kernel<<<1, 1024, 0, s>>>(a);
     mark("seg_table");
-    const unsigned sb = (unsigned)((a.cap_seg + 7) / 8);
+    // segment kernels loop over the frame's segments: the grid covers the
+    // capacity up to 2048 blocks (a small slice's pass exits early)
+    const unsigned sb = (unsigned)std::min<int64_t>((a.cap_seg + 7) / 8, 2048);
     seg_count_kernel<<<sb, 256, 8 * (a.tiles_x + 1) * sizeof(uint32_t), s>>>(a);
     mark("seg_count");
     seg_scan_kernel<<<(unsigned)((a.ntiles + 7) / 8), 256, 0, s>>>(a);

@@ -263,8 +263,9 @@ template <int kSets, bool kPairLoop, bool kCount, int kMode>
 __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kernel(
     const SplatRec *__restrict__ srec, const float4 *__restrict__ colr,
     const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
-    int height, float bg0, float bg1, float bg2, BlendOut out, FrameCounters *__restrict__ ctr,
-    float4 *__restrict__ state, uint32_t *__restrict__ unsat) {
+    int height, BlendOut out, FrameCounters *__restrict__ ctr, SliceState ss) {
+    const float bg0 = out.fp->bg[0], bg1 = out.fp->bg[1], bg2 = out.fp->bg[2];
+    uint8_t *const host = out.fp->host;
     constexpr int kItems = kTileH / kSets;  // items per tile
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
@@ -300,11 +301,14 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
     uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
     uint32_t n_walk = 0, n_hit = 0, n_batch = 0, n_it = 0, n_lanes = 0, n_done = 0;
 
+    // slice B: only the items slice A left unsaturated (its list)
+    const int n_queue = kMode == 2 ? (int)ctr->n_unsat : n_items;
     while (true) {
         int item = 0;
         if (lane == 0) item = (int)atomicAdd(&ctr->blend_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= n_items) break;
+        if (item >= n_queue) break;
+        if (kMode == 2) item = (int)__ldg(ss.unsat_items + item);
         if (kCount) n_done += (lane == 0);
         const int tile = item / kItems, wr = item % kItems;
         const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -313,7 +317,6 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
         const int ix = X + lane;
         const float fx = (float)ix + 0.5f;
 
-        if (kMode == 2 && !((__ldg(unsat + tile) >> wr) & 1u)) continue;  // saturated in A
         float T[kSets], cr[kSets], cg[kSets], cb[kSets];
         bool inside[kSets], done[kSets];
 #pragma unroll
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             cr[h] = cg[h] = cb[h] = 0.0f;
             inside[h] = ix < width && iy0 + h < height;
             if (kMode == 2 && inside[h]) {
-                const float4 st = state[(int64_t)(iy0 + h) * width + ix];
+                const float4 st = ss.state[(int64_t)(iy0 + h) * width + ix];
                 T[h] = st.x;
                 cr[h] = st.y;
                 cg[h] = st.z;
@@ -426,8 +429,12 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
 #pragma unroll
                 for (int h = 0; h < kSets; h++)
                     if (inside[h])
-                        state[(int64_t)(iy0 + h) * width + ix] = make_float4(T[h], cr[h], cg[h], cb[h]);
-                if (lane == 0) atomicOr(unsat + tile, 1u << wr);
+                        ss.state[(int64_t)(iy0 + h) * width + ix] =
+                            make_float4(T[h], cr[h], cg[h], cb[h]);
+                if (lane == 0) {
+                    atomicOr(ss.unsat + tile, 1u << wr);
+                    ss.unsat_items[atomicAdd(&ctr->n_unsat, 1u)] = (uint32_t)item;
+                }
                 continue;
             }
         }
@@ -456,7 +463,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                 const int64_t wofs = (3 * (p - lane)) / 4 + lane;
                 if (lane < 24) {
                     reinterpret_cast<uint32_t *>(out.u8)[wofs] = word;
-                    if (out.host) reinterpret_cast<uint32_t *>(out.host)[wofs] = word;
+                    if (host) reinterpret_cast<uint32_t *>(host)[wofs] = word;
                 }
             } else {
                 out.u8[3 * p + 0] = (uint8_t)(px & 0xffu);
@@ -502,12 +509,10 @@ int blend_sets() {
 
 bool blend_has_slices() { return blend_sets() == 3; }
 
-void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
-                  const uint2 *ranges, int width, int height, float bg0, float bg1, float bg2,
-                  BlendOut out, FrameCounters *ctr, cudaStream_t s, const KMark &mark, bool count,
-                  int mode, float4 *state, uint32_t *unsat) {
+// persistent grid: every SM full (computed once; call before any graph capture)
+int blend_grid(int width, int height) {
     const int sets = blend_sets();
-    if (!g_blend_grid) {  // persistent grid: every SM full
+    if (!g_blend_grid) {
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -526,11 +531,17 @@ void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile
         g_blend_grid = sms * (per_sm > 0 ? per_sm : 1);
     }
     const int tiles = ((width + kTileW - 1) / kTileW) * ((height + kTileH - 1) / kTileH);
-    const int grid = std::min(g_blend_grid, tiles * kTileH);
+    return std::max(1, std::min(g_blend_grid, tiles * kTileH));
+}
+
+void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
+                  const uint2 *ranges, int width, int height, BlendOut out, FrameCounters *ctr,
+                  cudaStream_t s, const KMark &mark, bool count, int mode, SliceState ss) {
+    const int grid = blend_grid(width, height);
+    const int sets = blend_sets();
 #define GSR_BLEND(S, P, C, M)                                                                 \
     blend_kernel<S, P, C, M><<<grid, kBlendThreads, 0, s>>>(srec, colr, tile_vals, ranges, width, \
-                                                           height, bg0, bg1, bg2, out, ctr,   \
-                                                           state, unsat)
+                                                           height, out, ctr, ss)
     if (sets == 1) GSR_BLEND(1, false, true, 0);  // tuning variants: one pass only
     else if (sets == 2) GSR_BLEND(2, false, true, 0);
     else if (mode == 1) { if (count) GSR_BLEND(2, true, true, 1); else GSR_BLEND(2, true, false, 1); }

@@ -54,12 +54,13 @@ __global__ void depth_fixup_kernel(DepthArgs a) {
         idx[j] = vs[i + j];
         key[j] = a.keys64[0][idx[j]];
     }
-    // stable insertion sort by key (indices enter in increasing order)
+    // insertion sort by (key, index): the argsort tie order whatever order
+    // the run's indices arrive in (slice B's are appended unordered)
     for (int j = 1; j < len; j++) {
         const uint32_t xi = idx[j];
         const unsigned long long xk = key[j];
         int m = j - 1;
-        while (m >= 0 && key[m] > xk) {
+        while (m >= 0 && (key[m] > xk || (key[m] == xk && idx[m] > xi))) {
             key[m + 1] = key[m];
             idx[m + 1] = idx[m];
             m--;
@@ -81,19 +82,27 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &
         return launch_onesweep_sort<unsigned long long>(
             a.keys64[0], a.keys64[1], a.vals[0], a.vals[1], true, true, a.count, a.n, a.n, 8,
             true, a.work64, a.sched, &a.ctr->npass_fb, sms, s, mark);
-    const unsigned g = (unsigned)((a.n + 255) / 256);
-    SpanKeys span;  // the histogram kernel writes the span keys (step 1)
-    if (!a.keys_given) {
+    int launches;
+    unsigned g;
+    if (a.keys_given) {  // slice B: appended (span key, index) pairs, no sentinels
+        g = (unsigned)((a.cap + 255) / 256);
+        launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
+                                                  false, false, a.count, -1, a.cap,
+                                                  kSpanBits / 8, false, a.work32, a.sched,
+                                                  &a.ctr->npass, sms, s, mark);
+    } else {
+        g = (unsigned)((a.n + 255) / 256);
+        SpanKeys span;  // the histogram kernel writes the span keys (step 1)
         span.src = a.keys64[0];
         span.kmin = &a.ctr->kmin;
         span.kmax = &a.ctr->kmax;
         span.bits = kSpanBits;
         span.limit = a.limit;
-    }
-    int launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
+        launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
                                                   true, true, a.count, a.n, a.n, kSpanBits / 8,
                                                   true, a.work32, a.sched, &a.ctr->npass, sms, s,
                                                   mark, span);
+    }
     depth_fixup_kernel<<<g, 256, 0, s>>>(a);
     mark("depth_fixup");
     return launches + 1;

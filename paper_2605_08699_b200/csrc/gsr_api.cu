@@ -72,6 +72,25 @@ float slice_frac() {
 
 using namespace gsr;
 
+// Frame configuration: everything a frame's launch sequence depends on
+// besides the per-frame parameters (camera, background, mapped host frame),
+// which the kernels read from c->params.  Frames with equal keys replay one
+// CUDA graph.
+struct FrameKey {
+    SceneView view;
+    int W, H, sh_degree, cull, want_rgb, want_keep, slice, kcount, full64, packed;
+    uint64_t gen;  // buffer generation of the context (reallocation -> new graphs)
+    bool operator==(const FrameKey &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+
+struct FrameGraph {
+    FrameKey key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t params_node = nullptr;
+    uint64_t last_use = 0;
+};
+
 struct SavedCall {
     // the scene of the frame in flight, needed only to re-render it inside
     // complete_frame; cleared once the frame completes (the caller may free
@@ -99,7 +118,15 @@ struct gsr_ctx {
     DevBuf ranges;
     DevBuf frame_u8, frame_rgb, frame_t;
     DevBuf colr;          // colours by depth rank of the current pass
-    DevBuf state, unsat;  // depth-sliced frames: pixel state after slice A, unsaturated items
+    // depth-sliced frames: pixel state after slice A, unsaturated items (bits, list)
+    DevBuf state, unsat, unsat_items;
+    DevBuf params;        // FrameParams of the frame being rendered
+    // CUDA graphs of this context's frame configurations (record_frame)
+    static constexpr int kMaxGraphs = 32;
+    std::vector<FrameGraph> graphs;
+    uint64_t graph_clock = 0, graph_builds = 0;
+    uint64_t gen = 0;                  // bumped when a frame buffer is reallocated
+    cudaStream_t cap_stream = nullptr; // captures the conditional bodies
     bool force_full = false;   // next enqueue: one pass over all kept splats (debug entries)
     int64_t slice_min_n = -1;  // gsr_ctx_set_slicing (-1: the GSR_SLICE_MIN default)
     float slice_frac_v = 0.0f; // ... (0: the GSR_SLICE_FRAC default)
@@ -148,7 +175,7 @@ struct gsr_ctx {
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &colr, &state, &unsat, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+                               &geo, &colr, &state, &unsat, &unsat_items, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
@@ -161,6 +188,15 @@ struct gsr_ctx {
 namespace {
 
 
+
+// grow-only allocation of a frame buffer; a reallocation invalidates the
+// context's frame graphs (they hold the old addresses)
+int cens(gsr_ctx *c, DevBuf &b, size_t bytes) {
+    void *old = b.p;
+    const int rc = ensure(b, bytes);
+    if (b.p != old) c->gen++;
+    return rc;
+}
 
 int check_camera(const gsr_camera *cam) {
     if (!cam) return fail(GSR_E_INVALID, "camera is null");
@@ -195,41 +231,41 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
     if (n > c->cap_n) {
         const int64_t cap = round_up(n + n / 8 + 1024, 4096);
         for (int i = 0; i < 2; i++) {
-            if ((rc = ensure(c->keys[i], sizeof(unsigned long long) * cap))) return rc;
-            if ((rc = ensure(c->vals[i], sizeof(uint32_t) * cap))) return rc;
-            if ((rc = ensure(c->keys32[i], sizeof(uint32_t) * cap))) return rc;
+            if ((rc = cens(c, c->keys[i], sizeof(unsigned long long) * cap))) return rc;
+            if ((rc = cens(c, c->vals[i], sizeof(uint32_t) * cap))) return rc;
+            if ((rc = cens(c, c->keys32[i], sizeof(uint32_t) * cap))) return rc;
         }
-        if ((rc = ensure(c->geo, sizeof(GeoRec) * cap))) return rc;
-        if ((rc = ensure(c->colr, sizeof(float4) * cap))) return rc;
-        if ((rc = ensure(c->srec, sizeof(SplatRec) * cap))) return rc;
+        if ((rc = cens(c, c->geo, sizeof(GeoRec) * cap))) return rc;
+        if ((rc = cens(c, c->colr, sizeof(float4) * cap))) return rc;
+        if ((rc = cens(c, c->srec, sizeof(SplatRec) * cap))) return rc;
         c->cap_n = cap;
     }
-    if (want_keep && (rc = ensure(c->keep, (size_t)c->cap_n))) return rc;
+    if (want_keep && (rc = cens(c, c->keep, (size_t)c->cap_n))) return rc;
     if (c->cap_d == 0) c->cap_d = round_up(std::max<int64_t>(int64_t(1) << 22, 16 * n), 4096);
     if (c->cap_p == 0) c->cap_p = round_up(std::max<int64_t>(int64_t(1) << 20, 6 * n), 4096);
-    if ((rc = ensure(c->tile_vals, sizeof(uint32_t) * c->cap_d))) return rc;
-    if ((rc = ensure(c->pairs, sizeof(uint2) * c->cap_p))) return rc;
-    if ((rc = ensure(c->depth_work, depth_work64_bytes(c->cap_n)))) return rc;
-    if ((rc = ensure(c->depth_work32, depth_work32_bytes(c->cap_n)))) return rc;
+    if ((rc = cens(c, c->tile_vals, sizeof(uint32_t) * c->cap_d))) return rc;
+    if ((rc = cens(c, c->pairs, sizeof(uint2) * c->cap_p))) return rc;
+    if ((rc = cens(c, c->depth_work, depth_work64_bytes(c->cap_n)))) return rc;
+    if ((rc = cens(c, c->depth_work32, depth_work32_bytes(c->cap_n)))) return rc;
     const int tiles_x = (W + kTileW - 1) / kTileW, n_rows = (H + kTileH - 1) / kTileH;
     const int ntiles = tiles_x * n_rows;
-    if ((rc = ensure(c->ranges, sizeof(uint2) * (size_t)ntiles))) return rc;
-    if ((rc = ensure(c->ttotal, sizeof(uint32_t) * (size_t)ntiles))) return rc;
-    if ((rc = ensure(c->tstart, sizeof(uint32_t) * (size_t)ntiles))) return rc;
-    if ((rc = ensure(c->row_blk, sizeof(uint32_t) * (size_t)n_rows * bin_blocks(c->cap_n))))
+    if ((rc = cens(c, c->ranges, sizeof(uint2) * (size_t)ntiles))) return rc;
+    if ((rc = cens(c, c->ttotal, sizeof(uint32_t) * (size_t)ntiles))) return rc;
+    if ((rc = cens(c, c->tstart, sizeof(uint32_t) * (size_t)ntiles))) return rc;
+    if ((rc = cens(c, c->row_blk, sizeof(uint32_t) * (size_t)n_rows * bin_blocks(c->cap_n))))
         return rc;
-    if ((rc = ensure(c->row_start, sizeof(uint32_t) * (size_t)(n_rows + 1)))) return rc;
-    if ((rc = ensure(c->scan_work, sizeof(unsigned long long) *
+    if ((rc = cens(c, c->row_start, sizeof(uint32_t) * (size_t)(n_rows + 1)))) return rc;
+    if ((rc = cens(c, c->scan_work, sizeof(unsigned long long) *
                                        (size_t)(bin_scan_tiles(bin_blocks(c->cap_n), n_rows) + 1))))
         return rc;
     const int64_t cap_seg = bin_segments(c->cap_p, n_rows);
-    if ((rc = ensure(c->seg_row, sizeof(uint32_t) * (size_t)(cap_seg + n_rows + 2)))) return rc;
-    if ((rc = ensure(c->seg_cnt, sizeof(uint32_t) * (size_t)cap_seg * tiles_x))) return rc;
+    if ((rc = cens(c, c->seg_row, sizeof(uint32_t) * (size_t)(cap_seg + n_rows + 2)))) return rc;
+    if ((rc = cens(c, c->seg_cnt, sizeof(uint32_t) * (size_t)cap_seg * tiles_x))) return rc;
     const int64_t px = (int64_t)W * H;
-    if ((rc = ensure(c->frame_u8, (size_t)px * 3))) return rc;
+    if ((rc = cens(c, c->frame_u8, (size_t)px * 3))) return rc;
     if (want_rgb) {
-        if ((rc = ensure(c->frame_rgb, sizeof(float) * (size_t)px * 3))) return rc;
-        if ((rc = ensure(c->frame_t, sizeof(float) * (size_t)px))) return rc;
+        if ((rc = cens(c, c->frame_rgb, sizeof(float) * (size_t)px * 3))) return rc;
+        if ((rc = cens(c, c->frame_t, sizeof(float) * (size_t)px))) return rc;
     }
     return GSR_OK;
 }
@@ -241,57 +277,40 @@ void kmark_cb(void *self, const char *kernel) {
     cudaEventRecord(c->kev[++c->nmarks], c->stream);
 }
 
-// Enqueue one full frame on c->stream (no host synchronisation).
-int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const float bg[3],
-                  int sh_degree, int cull, bool want_rgb, bool want_keep) {
-    int rc;
-    if ((rc = check_camera(cam))) return rc;
-    if (!sc) return fail(GSR_E_INVALID, "scene is null");
-    if (sh_degree < 0 || sh_degree > 3) return fail(GSR_E_INVALID, "SH degree must be in 0..3");
-    if (sh_degree > 0 && !sc->has_sh)
-        return fail(GSR_E_INVALID, "scene was created without SH coefficients");
-    if (sc->device != c->device) return fail(GSR_E_INVALID, "scene and context are on different devices");
-    const int W = cam->width, H = cam->height;
-    const int64_t n = sc->n;
-    if ((rc = ensure_capacity(c, n, W, H, want_rgb, want_keep))) return rc;
+// Records one frame on stream s: launches directly, or -- while s is being
+// captured (graph) -- builds the graph; slice B's work then sits in a switch
+// node whose body is chosen on the device from slice B's size.
+int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_degree, int cull,
+                 bool want_rgb, bool want_keep, bool slice, bool graph) {
     cudaStream_t s = c->stream;
     FrameCounters *ctr = c->ctr.as<FrameCounters>();
-    const CameraArgs ca = camera_args(cam);
-    c->W = W;
-    c->H = H;
-    c->contract_tile = 0;
-    c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
+    FrameParams *dfp = c->params.as<FrameParams>();
+    const int W = c->W, H = c->H;
+    const int64_t n = sc->n;
     uint32_t *dsched = c->sched.as<uint32_t>();
-    int launches = 1;  // frame init
-
-    // depth-sliced frame (slice.cu) unless a stage output of the whole
-    // frame is wanted (debug entries), the 64-bit sort is needed, the scene
-    // is small or a blend tuning variant without slice modes is selected
-    const int64_t smin = c->slice_min_n >= 0 ? c->slice_min_n : slice_min();
-    const bool slice = !want_keep && !c->force_full && !c->saved_full64 && n >= smin &&
-                       blend_has_slices();
-    c->last_sliced = slice;
-    if (slice) {
-        int r2;
-        if ((r2 = ensure(c->state, sizeof(float4) * (size_t)W * H))) return r2;
-        if ((r2 = ensure(c->unsat, sizeof(uint32_t) * (size_t)c->ntiles))) return r2;
-    }
+    const unsigned evflags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+    int launches = 2;  // frame params + frame init
 
     KMark mark;
-    if (c->ktime) {
+    if (c->ktime && !graph) {
         mark.fn = kmark_cb;
         mark.self = c;
         c->nmarks = 0;
     }
-    const bool packed = W % kTileW == 0 && ((uintptr_t)c->zc_host & 3u) == 0;
-    c->zc_used = packed && c->zc_host != nullptr;
+    const bool packed = W % kTileW == 0;
     BlendOut out{c->frame_u8.as<uint8_t>(), want_rgb ? c->frame_rgb.as<float>() : nullptr,
-                 want_rgb ? c->frame_t.as<float>() : nullptr, c->zc_used ? c->zc_host : nullptr,
-                 packed};
+                 want_rgb ? c->frame_t.as<float>() : nullptr, dfp, packed};
     const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
     DepthOrder ord{c->vals[0].as<uint32_t>(), c->vals[1].as<uint32_t>(), dsched};
-    // one depth-ordered pass over `count` splats: sort, colour, bin
-    auto sort_color_bin = [&](uint32_t *count, const uint32_t *limit, bool keys_given) {
+    SliceState ss;
+    if (slice) {
+        ss.state = c->state.as<float4>();
+        ss.unsat = c->unsat.as<uint32_t>();
+        ss.unsat_items = c->unsat_items.as<uint32_t>();
+    }
+    // one depth-ordered pass over *count splats (at most cap): sort, colour, bin
+    auto sort_color_bin = [&](cudaStream_t st, uint32_t *count, const uint32_t *limit,
+                              bool keys_given, int64_t cap) {
         DepthArgs da;
         for (int i = 0; i < 2; i++) {
             da.keys64[i] = c->keys[i].as<unsigned long long>();
@@ -308,11 +327,12 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         da.count = count;
         da.limit = limit;
         da.keys_given = keys_given;
-        launches += launch_depth_sort(da, c->sms, s, mark);
-        launch_color_ranked(sc->view, ca, sh_degree, ord, count, c->cap_n, c->colr.as<float4>(),
-                            s, mark);
+        da.cap = cap;
+        launches += launch_depth_sort(da, c->sms, st, mark);
+        launch_color_ranked(sc->view, dfp, sh_degree, ord, count, cap, c->colr.as<float4>(), st,
+                            mark);
         launches += 1;
-        if (!keys_given) cudaEventRecord(c->ev[2], s);
+        if (!keys_given) cudaEventRecordWithFlags(c->ev[2], st, evflags);
         BinArgs ba;
         ba.count = count;
         ba.order0 = c->vals[0].as<uint32_t>();
@@ -326,7 +346,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.tiles_x = (W + kTileW - 1) / kTileW;
         ba.n_rows = (H + kTileH - 1) / kTileH;
         ba.ntiles = c->ntiles;
-        ba.n_blocks = bin_blocks(c->cap_n);
+        ba.n_blocks = bin_blocks(cap);
         ba.row_blk = c->row_blk.as<uint32_t>();
         ba.row_start = c->row_start.as<uint32_t>();
         ba.scan_work = c->scan_work.as<unsigned long long>();
@@ -342,18 +362,17 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         ba.tile_vals = c->tile_vals.as<uint32_t>();
         ba.cap_d = c->cap_d;
         ba.overflow_sticky = c->dsticky();
-        launches += launch_binning(ba, s, mark);
+        launches += launch_binning(ba, st, mark);
     };
     auto blend = [&](int mode) {
         launch_blend(c->srec.as<SplatRec>(), c->colr.as<float4>(), c->tile_vals.as<uint32_t>(),
-                     c->ranges.as<uint2>(), W, H, bg[0], bg[1], bg[2], out, ctr, s, mark,
-                     c->kcount, mode, slice ? c->state.as<float4>() : nullptr,
-                     slice ? c->unsat.as<uint32_t>() : nullptr);
+                     c->ranges.as<uint2>(), W, H, out, ctr, s, mark, c->kcount, mode, ss);
         launches += 1;
     };
 
-    cudaEventRecord(c->ev[0], s);
-    if (c->ktime) cudaEventRecord(c->kev[0], s);
+    cudaEventRecordWithFlags(c->ev[0], s, evflags);
+    if (c->ktime && !graph) cudaEventRecord(c->kev[0], s);
+    launch_frame_params(fp, dfp, s);
     launch_frame_init(ctr, s);
     mark("frame_init");
     if (c->kcount &&
@@ -363,7 +382,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         out.item_info = out.used + c->cap_n;
     }
     if (n > 0) {
-        launch_preprocess_geo(sc->view, ca, cull, c->keys[0].as<unsigned long long>(),
+        launch_preprocess_geo(sc->view, dfp, cull, c->keys[0].as<unsigned long long>(),
                               c->geo.as<GeoRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr,
                               ctr, s, mark);
         launches += 1;
@@ -374,27 +393,27 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
             launches += 2;
         }
     }
-    cudaEventRecord(c->ev[1], s);
+    cudaEventRecordWithFlags(c->ev[1], s, evflags);
     if (n == 0) {
-        cudaEventRecord(c->ev[2], s);
+        cudaEventRecordWithFlags(c->ev[2], s, evflags);
         cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
-        cudaEventRecord(c->ev[3], s);
+        cudaEventRecordWithFlags(c->ev[3], s, evflags);
         blend(0);
-        cudaEventRecord(c->ev[4], s);
+        cudaEventRecordWithFlags(c->ev[4], s, evflags);
     } else if (!slice) {
         // stable f64 depth order of all kept splats (the first radix pass
         // compacts: drops the culled sentinels), colours, lists, blend
-        sort_color_bin(&ctr->K, nullptr, false);
-        cudaEventRecord(c->ev[3], s);
+        sort_color_bin(s, &ctr->K, nullptr, false, c->cap_n);
+        cudaEventRecordWithFlags(c->ev[3], s, evflags);
         blend(0);
-        cudaEventRecord(c->ev[4], s);
+        cudaEventRecordWithFlags(c->ev[4], s, evflags);
     } else {
         // slice A: the front of the depth order
-        sort_color_bin(&ctr->KA, &ctr->tau, false);
-        cudaEventRecord(c->ev[3], s);
+        sort_color_bin(s, &ctr->KA, &ctr->tau, false, c->cap_n);
+        cudaEventRecordWithFlags(c->ev[3], s, evflags);
         cudaMemsetAsync(c->unsat.p, 0, sizeof(uint32_t) * (size_t)c->ntiles, s);
         blend(1);
-        cudaEventRecord(c->ev[4], s);
+        cudaEventRecordWithFlags(c->ev[4], s, evflags);
         // slice B: the splats behind it that can reach an unsaturated item
         SliceBArgs sb;
         sb.keys64 = c->keys[0].as<unsigned long long>();
@@ -406,17 +425,219 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         sb.height = H;
         sb.tiles_x = (W + kTileW - 1) / kTileW;
         sb.keysB = c->keys32[0].as<uint32_t>();
+        sb.valsB = c->vals[0].as<uint32_t>();
         launch_slice_b_filter(sb, s, mark);
         launches += 1;
-        sort_color_bin(&ctr->KB, nullptr, true);
+        auto class_cap = [&](int k) {
+            return k < kSliceClasses - 1 ? std::min<int64_t>(slice_class_cap(k), c->cap_n)
+                                         : c->cap_n;
+        };
+        if (graph) {
+            // switch node: body k sorts / colours / bins with class-k grids
+            cudaStreamCaptureStatus cs;
+            cudaGraph_t g = nullptr;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t nd = 0;
+            GSR_CUDA_OK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+            cudaGraphConditionalHandle h;
+            GSR_CUDA_OK(cudaGraphConditionalHandleCreate(&h, g, kSliceClasses,
+                                                         cudaGraphCondAssignDefault));
+            launch_slice_b_decide(ctr, h, s);
+            GSR_CUDA_OK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+            std::vector<cudaGraphNode_t> dv(deps, deps + nd);
+            cudaGraphNodeParams cp{};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeSwitch;
+            cp.conditional.size = kSliceClasses;
+            cudaGraphNode_t cn;
+            GSR_CUDA_OK(cudaGraphAddNode(&cn, g, dv.data(), dv.size(), &cp));
+            for (int k = 0; k < kSliceClasses; k++) {
+                GSR_CUDA_OK(cudaStreamBeginCaptureToGraph(c->cap_stream, cp.conditional.phGraph_out[k],
+                                                          nullptr, nullptr, 0,
+                                                          cudaStreamCaptureModeThreadLocal));
+                sort_color_bin(c->cap_stream, &ctr->KB, nullptr, true, class_cap(k));
+                cudaGraph_t body = nullptr;
+                GSR_CUDA_OK(cudaStreamEndCapture(c->cap_stream, &body));
+            }
+            GSR_CUDA_OK(cudaStreamUpdateCaptureDependencies(s, &cn, 1,
+                                                            cudaStreamSetCaptureDependencies));
+        } else {
+            // direct launches: slice B's size read back, its class chosen on the host
+            uint32_t kb = 0;
+            GSR_CUDA_OK(cudaMemcpyAsync(&c->hctr->KB, &ctr->KB, sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, s));
+            GSR_CUDA_OK(cudaStreamSynchronize(s));
+            kb = c->hctr->KB;
+            int k = kSliceClasses - 1;
+            for (int j = kSliceClasses - 2; j >= 0; j--)
+                if ((int64_t)kb <= slice_class_cap(j)) k = j;
+            if (kb > 0) sort_color_bin(s, &ctr->KB, nullptr, true, class_cap(k));
+        }
         blend(2);
     }
-    cudaEventRecord(c->ev[5], s);
+    cudaEventRecordWithFlags(c->ev[5], s, evflags);
     cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters) + 2 * sizeof(uint32_t),
                     cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(c->hsched, dsched, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     GSR_CUDA_OK(cudaGetLastError());
     c->launches += launches;
+    return GSR_OK;
+}
+
+bool graphs_enabled() {
+    static const bool v = [] {
+        const char *e = getenv("GSR_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+void destroy_graph(FrameGraph &fg) {
+    if (fg.exec) cudaGraphExecDestroy(fg.exec);
+    if (fg.graph) cudaGraphDestroy(fg.graph);
+    fg.exec = nullptr;
+    fg.graph = nullptr;
+}
+
+// The context's graph for `key`, captured and instantiated on first use
+// (least recently used of kMaxGraphs evicted).
+int frame_graph(gsr_ctx *c, const FrameKey &key, const gsr_scene *sc, const FrameParams &fp,
+                int sh_degree, int cull, bool want_rgb, bool want_keep, bool slice,
+                FrameGraph **out) {
+    c->graph_clock++;
+    for (auto &fg : c->graphs)
+        if (fg.exec && fg.key == key) {
+            fg.last_use = c->graph_clock;
+            *out = &fg;
+            return GSR_OK;
+        }
+    if (!c->cap_stream)
+        GSR_CUDA_OK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    blend_grid(c->W, c->H);  // occupancy query before capture
+    FrameGraph fg;
+    fg.key = key;
+    GSR_CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t launches_before = c->launches;
+    int rc = record_frame(c, sc, fp, sh_degree, cull, want_rgb, want_keep, slice, true);
+    c->launches = launches_before;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return fail_cuda(e, "frame graph capture");
+    fg.graph = g;
+    const cudaError_t ei = cudaGraphInstantiate(&fg.exec, g, 0);
+    if (ei != cudaSuccess) {
+        destroy_graph(fg);
+        return fail_cuda(ei, "frame graph instantiate");
+    }
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp{};
+        if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
+            kp.func == frame_params_kernel_fn()) {
+            fg.params_node = nd;
+            break;
+        }
+    }
+    if (!fg.params_node) {
+        destroy_graph(fg);
+        return fail(GSR_E_CUDA, "frame graph: parameter node not found");
+    }
+    fg.last_use = c->graph_clock;
+    // evict the least recently used graph when full
+    if ((int)c->graphs.size() >= gsr_ctx::kMaxGraphs) {
+        size_t lru = 0;
+        for (size_t i = 1; i < c->graphs.size(); i++)
+            if (c->graphs[i].last_use < c->graphs[lru].last_use) lru = i;
+        destroy_graph(c->graphs[lru]);
+        c->graphs[lru] = fg;
+        *out = &c->graphs[lru];
+    } else {
+        c->graphs.push_back(fg);
+        *out = &c->graphs.back();
+    }
+    c->graph_builds++;
+    return GSR_OK;
+}
+
+// Enqueue one full frame on c->stream (no host synchronisation in the graph
+// path: one parameter-node update and one graph launch).
+int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const float bg[3],
+                  int sh_degree, int cull, bool want_rgb, bool want_keep) {
+    int rc;
+    if ((rc = check_camera(cam))) return rc;
+    if (!sc) return fail(GSR_E_INVALID, "scene is null");
+    if (sh_degree < 0 || sh_degree > 3) return fail(GSR_E_INVALID, "SH degree must be in 0..3");
+    if (sh_degree > 0 && !sc->has_sh)
+        return fail(GSR_E_INVALID, "scene was created without SH coefficients");
+    if (sc->device != c->device) return fail(GSR_E_INVALID, "scene and context are on different devices");
+    const int W = cam->width, H = cam->height;
+    const int64_t n = sc->n;
+    if ((rc = ensure_capacity(c, n, W, H, want_rgb, want_keep))) return rc;
+    c->W = W;
+    c->H = H;
+    c->contract_tile = 0;
+    c->ntiles = ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
+    // depth-sliced frame (slice.cu) unless a stage output of the whole
+    // frame is wanted (debug entries), the 64-bit sort is needed, the scene
+    // is small or a blend tuning variant without slice modes is selected
+    const int64_t smin = c->slice_min_n >= 0 ? c->slice_min_n : slice_min();
+    const bool slice = !want_keep && !c->force_full && !c->saved_full64 && n >= smin &&
+                       blend_has_slices();
+    c->last_sliced = slice;
+    if (slice) {
+        const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
+        if ((rc = cens(c, c->state, sizeof(float4) * (size_t)W * H))) return rc;
+        if ((rc = cens(c, c->unsat, sizeof(uint32_t) * (size_t)c->ntiles))) return rc;
+        if ((rc = cens(c, c->unsat_items, sizeof(uint32_t) * n_items))) return rc;
+    }
+    FrameParams fp;
+    fp.cam = camera_args(cam);
+    for (int i = 0; i < 3; i++) fp.bg[i] = bg[i];
+    const bool packed = W % kTileW == 0 && ((uintptr_t)c->zc_host & 3u) == 0;
+    c->zc_used = packed && c->zc_host != nullptr;
+    fp.host = c->zc_used ? c->zc_host : nullptr;
+    if (graphs_enabled() && !c->ktime && !c->kcount) {
+        FrameKey key;
+        std::memset(&key, 0, sizeof(key));
+        key.view = sc->view;
+        key.W = W;
+        key.H = H;
+        key.sh_degree = sh_degree;
+        key.cull = cull;
+        key.want_rgb = want_rgb;
+        key.want_keep = want_keep;
+        key.slice = slice;
+        key.kcount = c->kcount;
+        key.full64 = c->saved_full64;
+        key.packed = W % kTileW == 0;
+        key.gen = c->gen;
+        FrameGraph *fg = nullptr;
+        if ((rc = frame_graph(c, key, sc, fp, sh_degree, cull, want_rgb, want_keep, slice, &fg)))
+            return rc;
+        cudaKernelNodeParams kp{};
+        FrameParams *dfp = c->params.as<FrameParams>();
+        void *args[2] = {&fp, &dfp};
+        kp.func = const_cast<void *>(frame_params_kernel_fn());
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        GSR_CUDA_OK(cudaGraphExecKernelNodeSetParams(fg->exec, fg->params_node, &kp));
+        GSR_CUDA_OK(cudaGraphLaunch(fg->exec, c->stream));
+        c->launches += 1;  // one graph launch (its kernels are this context's)
+    } else {
+        if ((rc = record_frame(c, sc, fp, sh_degree, cull, want_rgb, want_keep, slice, false)))
+            return rc;
+    }
     c->saved.scene = sc;
     c->saved.scene_n = n;
     c->saved.cam = *cam;
@@ -796,6 +1017,7 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
         return rc;
     }
     int rc = ensure(c->ctr, sizeof(FrameCounters) + 4 * sizeof(uint32_t));
+    if (!rc) rc = ensure(c->params, sizeof(FrameParams));
     if (!rc) rc = ensure(c->sched, 64 * sizeof(uint32_t));
     if (!rc && cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
@@ -838,6 +1060,8 @@ int gsr_ctx_destroy(gsr_ctx *ctx) {
     if (ctx->hssim) cudaFreeHost(ctx->hssim);
     if (ctx->hsched) cudaFreeHost(ctx->hsched);
     if (ctx->hjpeg) cudaFreeHost(ctx->hjpeg);
+    for (auto &fg : ctx->graphs) destroy_graph(fg);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return GSR_OK;
@@ -1181,8 +1405,10 @@ int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n) {
     int rc = complete_frame(ctx);
     if (rc) return rc;
     const FrameCounters &f = *ctx->hctr;
-    const uint64_t v[GSR_NCOUNTERS] = {f.K, f.D, f.P, f.E, f.Rb, f.Rp, f.b_walked, f.b_hit,
-                                       f.b_batches, f.b_iters, f.b_lanes, f.b_items, f.b_used};
+    const bool sliced = ctx->last_sliced;
+    const uint64_t v[GSR_NCOUNTERS] = {f.K, f.Dtot, f.Ptot, f.E, f.Rb, f.Rp, f.b_walked, f.b_hit,
+                                       f.b_batches, f.b_iters, f.b_lanes, f.b_items, f.b_used,
+                                       sliced ? f.KA : f.K, sliced ? f.KB : 0u};
     for (int i = 0; i < n && i < GSR_NCOUNTERS; i++) out[i] = v[i];
     return GSR_OK;
 }

@@ -48,7 +48,7 @@ struct FrameCounters {
     uint32_t KA;                   // items of the first pass (the slice, or all K)
     uint32_t KB;                   // splats of the second pass
     uint32_t tau;                  // slice: span keys <= tau
-    uint32_t pad3;
+    uint32_t n_unsat;              // work items slice A left unsaturated
     unsigned long long Dtot, Ptot; // tile keys / pairs over the passes
     unsigned long long Dmax, Pmax; // largest pass (buffer capacities)
     uint32_t slice_hist[256];      // top 8 bits of the kept span keys
@@ -108,11 +108,23 @@ struct DepthOrder {  // depth rank -> Gaussian index (the depth sort's result bu
     const uint32_t *sched;  // sched[16]: which buffer holds the result
 };
 
+// Per-frame parameters in device memory (one block per context): the
+// kernels read the camera, background and the mapped host frame from here,
+// so a frame's launch sequence is the same for every pose and is replayed as
+// a CUDA graph; load_frame_params (its only by-value use) stores them.
+struct FrameParams {
+    CameraArgs cam;
+    float bg[3];
+    uint8_t *host;  // device view of a mapped pinned (H,W,3) frame (zero copy), or null
+};
+void launch_frame_params(const FrameParams &p, FrameParams *dst, cudaStream_t s);
+const void *frame_params_kernel_fn();  // its function (graph node updates)
+
 // preprocess.cu (2 kernels)
 using GeoRec = SplatRec;  // by Gaussian index (preprocess), by depth rank (gather)
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 // K1a: projection, culling, depth keys, packed geometry (render.py:163-290)
-void launch_preprocess_geo(const SceneView &scene, const CameraArgs &cam, int frustum_cull,
+void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
                            FrameCounters *ctr, cudaStream_t s, const KMark &mark = KMark());
 // radix.cu: Onesweep stable LSD sort (see radix.cu header)
@@ -167,7 +179,9 @@ struct DepthArgs {
     uint32_t *long_run_sticky;  // per-context count of frames that reported long runs
     uint32_t *count = nullptr;         // items after compaction (K, the slice's KA, or KB)
     const uint32_t *limit = nullptr;   // slice A: span keys <= *limit only
-    bool keys_given = false;  // keys32[0] already holds the span keys / sentinels (slice B)
+    bool keys_given = false;  // slice B: keys32[0] / vals[0] hold *count appended
+                              // (span key, Gaussian index) pairs, at most `cap` of them
+    int64_t cap = 0;
 };
 size_t depth_work32_bytes(int64_t n_cap);
 size_t depth_work64_bytes(int64_t n_cap);
@@ -227,7 +241,7 @@ int launch_contract_ranges(const unsigned long long *keys0, const unsigned long 
 
 // preprocess.cu, K1b: SH colours (render.py:126-160) of the ranks [0, *count)
 // of a pass's depth order, stored by rank: colr[r] = (r, g, b, 0)
-void launch_color_ranked(const SceneView &scene, const CameraArgs &cam, int sh_degree,
+void launch_color_ranked(const SceneView &scene, const FrameParams *fp, int sh_degree,
                          DepthOrder ord, const uint32_t *count, int64_t cap, float4 *colr,
                          cudaStream_t s, const KMark &mark = KMark());
 
@@ -236,20 +250,25 @@ struct BlendOut {
     uint8_t *u8;    // (H,W,3)
     float *rgb;     // (H,W,3) or null
     float *trans;   // (H,W) or null
-    uint8_t *host;  // device view of a mapped pinned (H,W,3) host frame, or null (needs packed)
+    const FrameParams *fp;  // background; fp->host: mapped pinned host frame (needs packed)
     bool packed;    // W % 32 == 0 and u8/host 4-byte aligned: one 96 B row segment per warp store
     uint32_t *used = nullptr;  // instrumentation (counting variant): per-rank "colour read" flags
     uint32_t *item_info = nullptr;  // ... per work item: last depth rank walked | saturated << 31
 };
 bool blend_has_slices();  // the selected blend variant has modes 1 and 2
+int blend_grid(int width, int height);  // its persistent grid (host query, cached)
 // mode: 0 one pass; 1 slice A (saturated items write the frame, the others
-// save their pixels' state and set their unsat bit); 2 slice B (unsat items
-// only, from the saved state)
+// save their pixels' state, set their unsat bit and are listed in
+// unsat_items); 2 slice B (the listed items only, from the saved state)
+struct SliceState {
+    float4 *state = nullptr;        // (H, W) pixel (T, r, g, b) after slice A
+    uint32_t *unsat = nullptr;      // [ntiles] unsaturated items of slice A (bits)
+    uint32_t *unsat_items = nullptr;  // [n_items] their ids; count in FrameCounters.n_unsat
+};
 void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
-                  const uint2 *ranges, int width, int height, float bg0, float bg1, float bg2,
-                  BlendOut out, FrameCounters *ctr, cudaStream_t s, const KMark &mark = KMark(),
-                  bool count = true, int mode = 0, float4 *state = nullptr,
-                  uint32_t *unsat = nullptr);  // count: fill the E / Rb work counters
+                  const uint2 *ranges, int width, int height, BlendOut out, FrameCounters *ctr,
+                  cudaStream_t s, const KMark &mark = KMark(), bool count = true, int mode = 0,
+                  SliceState ss = SliceState());  // count: fill the E / Rb work counters
 
 // slice.cu: depth-sliced frames
 struct SliceBArgs {
@@ -259,11 +278,19 @@ struct SliceBArgs {
     FrameCounters *ctr;                // kmin, kmax, tau; KB counted here
     const uint32_t *unsat;             // [ntiles] items of slice A left unsaturated
     int width, height, tiles_x;
-    uint32_t *keysB;                   // out: span key of a slice-B member, else ~0
+    uint32_t *keysB, *valsB;           // out: slice B's (span key, Gaussian index), appended
 };
+// slice-B size classes: the second slice's sort / colour / lists run with
+// grids for at most kSliceClassCap[c] splats (class 2: all)
+constexpr int kSliceClasses = 3;
+__host__ __device__ constexpr int64_t slice_class_cap(int c) { return c == 0 ? 4096 : 65536; }
 void launch_slice_plan(const unsigned long long *keys64, int64_t n, FrameCounters *ctr,
                        float frac, int sms, cudaStream_t s, const KMark &mark = KMark());
 void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark = KMark());
+// sets `handle` (a graph's switch) to slice B's size class, kSliceClasses
+// (no body) when slice B is empty
+void launch_slice_b_decide(const FrameCounters *ctr, cudaGraphConditionalHandle handle,
+                           cudaStream_t s);
 
 // jpeg.cu: baseline JPEG of a device u8 frame (Pillow / libjpeg-turbo exact)
 struct JpegLayout {

@@ -77,14 +77,21 @@ __global__ void __launch_bounds__(256) frame_init_kernel(FrameCounters *ctr) {
     ctr->pad2 = 0;
     ctr->b_walked = ctr->b_hit = ctr->b_batches = ctr->b_iters = ctr->b_lanes = 0ull;
     ctr->b_items = ctr->b_used = 0ull;
-    ctr->KA = ctr->KB = ctr->tau = ctr->pad3 = 0u;
+    ctr->KA = ctr->KB = ctr->tau = ctr->n_unsat = 0u;
     ctr->Dtot = ctr->Ptot = ctr->Dmax = ctr->Pmax = 0ull;
 }
 
+__global__ void frame_params_kernel(FrameParams p, FrameParams *dst) { *dst = p; }
+
 __global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
-    SceneView sc, CameraArgs cam, int do_cull, unsigned long long *__restrict__ keys,
-    GeoRec *__restrict__ geo, uint8_t *__restrict__ keep_out,
-    FrameCounters *ctr) {
+    SceneView sc, const FrameParams *__restrict__ fp, int do_cull,
+    unsigned long long *__restrict__ keys, GeoRec *__restrict__ geo,
+    uint8_t *__restrict__ keep_out, FrameCounters *ctr) {
+    __shared__ CameraArgs cam;  // this frame's camera (FrameParams), staged once per block
+    if (threadIdx.x < sizeof(CameraArgs) / 8)
+        reinterpret_cast<unsigned long long *>(&cam)[threadIdx.x] =
+            reinterpret_cast<const unsigned long long *>(&fp->cam)[threadIdx.x];
+    __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t st = sc.stride;
     bool kept = false;
@@ -210,10 +217,11 @@ __global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
 // unsaturated pixel reaches never read their 192 B of SH.
 template <typename ShT, int DEG>
 __global__ void __launch_bounds__(256) color_ranked_kernel(
-    SceneView sc, CameraArgs cam, DepthOrder ord, const uint32_t *__restrict__ count,
-    float4 *__restrict__ colr) {
+    SceneView sc, const FrameParams *__restrict__ fp, DepthOrder ord,
+    const uint32_t *__restrict__ count, float4 *__restrict__ colr) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= (int64_t)*count) return;
+    const CameraArgs &cam = fp->cam;
     const uint32_t *order = ord.sched[16] ? ord.order1 : ord.order0;
     const int64_t i = __ldg(order + r);
     const int64_t st = sc.stride;
@@ -268,25 +276,31 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
     frame_init_kernel<<<1, 256, 0, s>>>(ctr);
 }
 
-void launch_preprocess_geo(const SceneView &scene, const CameraArgs &cam, int frustum_cull,
+void launch_frame_params(const FrameParams &p, FrameParams *dst, cudaStream_t s) {
+    frame_params_kernel<<<1, 1, 0, s>>>(p, dst);
+}
+
+const void *frame_params_kernel_fn() { return (const void *)frame_params_kernel; }
+
+void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
                            FrameCounters *ctr, cudaStream_t s, const KMark &mark) {
     if (scene.n == 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
-    preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, cam, frustum_cull, keys, geo,
+    preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, fp, frustum_cull, keys, geo,
                                                      keep_out, ctr);
     mark("preprocess_geo");
 }
 
-void launch_color_ranked(const SceneView &scene, const CameraArgs &cam, int sh_degree,
+void launch_color_ranked(const SceneView &scene, const FrameParams *fp, int sh_degree,
                          DepthOrder ord, const uint32_t *count, int64_t cap, float4 *colr,
                          cudaStream_t s, const KMark &mark) {
     if (cap <= 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((cap + threads - 1) / threads);
 #define GSR_COLOR(T, D)                                                                   \
-    color_ranked_kernel<T, D><<<blocks, threads, 0, s>>>(scene, cam, ord, count, colr)
+    color_ranked_kernel<T, D><<<blocks, threads, 0, s>>>(scene, fp, ord, count, colr)
     if (sh_degree == 0) GSR_COLOR(float, 0);
     else if (scene.sh_f32 && sh_degree == 1) GSR_COLOR(float, 1);
     else if (scene.sh_f32 && sh_degree == 2) GSR_COLOR(float, 2);

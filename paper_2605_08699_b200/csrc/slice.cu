@@ -68,14 +68,16 @@ __global__ void __launch_bounds__(256) slice_plan_kernel(FrameCounters *ctr, flo
     }
 }
 
-// Splats behind the slice that may reach an unsaturated item: span key of
-// the splat, else the sentinel (dropped by the first radix pass).
+// Splats behind the slice that may reach an unsaturated item, appended as
+// (span key, Gaussian index).  The append order depends on scheduling; the
+// sort and the fix-up order by (span key, f64 key, index), so the order of
+// the slice does not.
 __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) a.ctr->blend_next = 0u;  // blend A has finished (stream order)
     bool member = false;
     uint32_t out = 0xffffffffu;
-    if (i < a.n) {
+    if (i < a.n && a.ctr->n_unsat) {
         const unsigned long long k64 = __ldg(a.keys64 + i);
         if (k64 != ~0ull) {
             const SpanMap m = span_map(a.ctr->kmin, a.ctr->kmax);
@@ -108,10 +110,30 @@ __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
                 if (member) out = k32;
             }
         }
-        a.keysB[i] = out;
     }
-    const uint32_t c = __popc(__ballot_sync(0xffffffffu, member));
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&a.ctr->KB, c);
+    // warp-aggregated append
+    const uint32_t ballot = __ballot_sync(0xffffffffu, member);
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == 0 && ballot) base = atomicAdd(&a.ctr->KB, (uint32_t)__popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (member) {
+        const uint32_t pos = base + __popc(ballot & ((1u << lane) - 1u));
+        a.keysB[pos] = out;
+        a.valsB[pos] = (uint32_t)i;
+    }
+}
+
+__global__ void slice_b_decide_kernel(const FrameCounters *ctr,
+                                      cudaGraphConditionalHandle handle) {
+    const uint32_t kb = ctr->KB;
+    unsigned int v = kSliceClasses;  // no body: slice B is empty
+    if (kb > 0) {
+        v = kSliceClasses - 1;
+        for (int c = kSliceClasses - 2; c >= 0; c--)
+            if ((int64_t)kb <= slice_class_cap(c)) v = (unsigned int)c;
+    }
+    cudaGraphSetConditional(handle, v);
 }
 
 }  // namespace
@@ -131,6 +153,11 @@ void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mar
     if (a.n <= 0) return;
     slice_b_filter_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
     mark("slice_b_filter");
+}
+
+void launch_slice_b_decide(const FrameCounters *ctr, cudaGraphConditionalHandle handle,
+                           cudaStream_t s) {
+    slice_b_decide_kernel<<<1, 1, 0, s>>>(ctr, handle);
 }
 
 }  // namespace gsr

@@ -21,7 +21,7 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 
 NAMES = ["K", "D", "P", "E", "Rb", "Rp", "walked", "hit", "batches", "iters_x32", "lanes",
-         "items", "used"]
+         "items", "used", "KA", "KB"]
 
 
 def main():
@@ -43,7 +43,7 @@ def main():
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(c), bg, wl["sh"], 1, None,
                                   None, None, ctypes.byref(st)))
     rows, blend_ms, items = [], [], []
-    out = (ctypes.c_uint64 * 13)()
+    out = (ctypes.c_uint64 * 15)()
     for c in cams[3:]:
         _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 0))
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(c), bg, wl["sh"], 1, None,
@@ -52,7 +52,7 @@ def main():
         _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 2))
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(c), bg, wl["sh"], 1, None,
                                   None, None, ctypes.byref(st)))
-        _lib.check(lib.gsr_debug_frame_counters(ctx.handle, out, 13))
+        _lib.check(lib.gsr_debug_frame_counters(ctx.handle, out, 15))
         rows.append([int(x) for x in out])
         n_items = ((intr.width + 31) // 32) * ((intr.height + 63) // 64) * 32
         info = np.empty(n_items, dtype=np.uint32)
