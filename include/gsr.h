@@ -251,10 +251,10 @@ GSR_API int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_
  * by all work items, entries whose row range meets the item's rows, 32-entry
  * batches, composite-loop iterations x 32, useful (pixel, iteration) slots,
  * work items, distinct splats whose colour the blend read; then the splats
- * sorted by the first and second slice (K and 0 for a one-pass frame).  E, Rb
- * and the blend entries need GSR_TIMING_COUNTERS; D and P are summed over
- * the slices. */
-#define GSR_NCOUNTERS 15
+ * sorted by the first and second slice (K and 0 for a one-pass frame) and the
+ * work items the first slice left unsaturated.  E, Rb and the blend entries
+ * need GSR_TIMING_COUNTERS; D and P are summed over the slices. */
+#define GSR_NCOUNTERS 16
 GSR_API int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n);
 /* Per blend work item (tile-major, 32 items of two pixel rows per 32 x 64
  * tile) of the last frame rendered with GSR_TIMING_COUNTERS: the deepest

@@ -333,7 +333,9 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
             }
             done[h] = !inside[h] || (kMode == 2 && T[h] < kTStop);
         }
-        const uint2 rg = ranges[tile];
+        // slice B with no splats: its lists were never built (the switch ran
+        // no body), so the items only finish from the saved state
+        const uint2 rg = (kMode == 2 && ctr->KB == 0u) ? make_uint2(0u, 0u) : ranges[tile];
         uint32_t last_r = 0;  // instrumentation: deepest rank this item walked
 
         for (uint32_t c = rg.x; c < rg.y; c += 32) {

@@ -79,6 +79,7 @@ using namespace gsr;
 struct FrameKey {
     SceneView view;
     int W, H, sh_degree, cull, want_rgb, want_keep, slice, kcount, full64, packed;
+    float frac;    // the front slice's fraction (a slice_plan kernel parameter)
     uint64_t gen;  // buffer generation of the context (reallocation -> new graphs)
     bool operator==(const FrameKey &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
@@ -620,6 +621,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         key.kcount = c->kcount;
         key.full64 = c->saved_full64;
         key.packed = W % kTileW == 0;
+        key.frac = slice ? (c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac()) : 0.0f;
         key.gen = c->gen;
         FrameGraph *fg = nullptr;
         if ((rc = frame_graph(c, key, sc, fp, sh_degree, cull, want_rgb, want_keep, slice, &fg)))
@@ -1408,7 +1410,8 @@ int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n) {
     const bool sliced = ctx->last_sliced;
     const uint64_t v[GSR_NCOUNTERS] = {f.K, f.Dtot, f.Ptot, f.E, f.Rb, f.Rp, f.b_walked, f.b_hit,
                                        f.b_batches, f.b_iters, f.b_lanes, f.b_items, f.b_used,
-                                       sliced ? f.KA : f.K, sliced ? f.KB : 0u};
+                                       sliced ? f.KA : f.K, sliced ? f.KB : 0u,
+                                       sliced ? f.n_unsat : 0u};
     for (int i = 0; i < n && i < GSR_NCOUNTERS; i++) out[i] = v[i];
     return GSR_OK;
 }

@@ -782,11 +782,18 @@ def test_depth_sliced_frames_equal_one_pass(gsr, oracle, frac):
     can reach an unsaturated item, from the saved pixel state) equal the
     one-pass frame and the oracle float for float, for slices from 1 % to
     all of the kept splats, with rgb/T planes, backgrounds and SH degrees."""
+    import ctypes
+    from paper_2605_08699_b200 import _lib
     from paper_2605_08699_b200.render import set_slicing
     from paper_2605_08699_b200.synth import synthetic_scene
+    seen = set()
+    # dense scenes (most items saturate in the front slice) and a sparse one
+    # (many items never saturate: slice B non-empty for small fractions,
+    # empty -- no lists built -- when the front slice holds everything)
     cases = [(40_000, 3, 0, (320, 240), (0.0, 0.0, 0.0)),
              (60_000, 5, 3, (333, 217), (0.25, 0.5, 0.75)),
-             (30_000, 9, 1, (640, 360), (1.0, 1.0, 1.0))]
+             (30_000, 9, 1, (640, 360), (1.0, 1.0, 1.0)),
+             (1_500, 4, 3, (320, 240), (0.0, 0.0, 0.0))]
     try:
         for n, seed, sh, (w, h), bg in cases:
             prims = synthetic_scene(n, seed=seed, sh_degree=3)
@@ -798,6 +805,10 @@ def test_depth_sliced_frames_equal_one_pass(gsr, oracle, frac):
                 set_slicing(1, frac)
                 st = gsr.RenderStats()
                 sl = gsr.render_framebuffer(prims, pose, intr, bg, sh, st)
+                raw = (ctypes.c_uint64 * 16)()
+                _lib.check(_lib.context(0).lib.gsr_debug_frame_counters(
+                    _lib.context(0).handle, raw, 16))
+                seen.add((raw[14] > 0, raw[15] > 0))  # (slice B non-empty, items unsaturated)
                 assert np.array_equal(sl._rgb32, one._rgb32), (n, k, frac)
                 assert np.array_equal(sl._t32, one._t32)
                 assert np.array_equal(sl.u8, one.u8)
@@ -807,3 +818,5 @@ def test_depth_sliced_frames_equal_one_pass(gsr, oracle, frac):
                     assert np.array_equal(sl.u8, _oracle_frame(oracle, prims, pose, intr, sh, bg).u8)
     finally:
         set_slicing()
+    # the sparse scene leaves items unsaturated, with and without slice-B splats
+    assert (False, True) in seen if frac == 1.0 else (True, True) in seen, seen
