@@ -381,7 +381,7 @@ if _tp.exists():
 
 
 def load_simt_peaks():
-    """FP32/FP64/smem/issue peaks measured by tools/peaks.cu on a B200 of this
+    """FP32/FP64/smem peaks measured by tools/peaks.cu on a B200 of this
     pool (profiles/measured_simt_peaks.json), else the nominal figures."""
     p = ROOT / "profiles" / "measured_simt_peaks.json"
     if p.exists():
@@ -404,14 +404,16 @@ def kernel_work(name, wl, c):
     table = {
         # mean/scale/rotation/rsq f64 + opacity f32 in; key for all N; record of kept
         "preprocess_geo": (n * 92 + n * 8 + k * 32, 0),
-        "slice_hist": (n * 8, 0),
         # order + mean f64 + SH row (or DC) of each ranked splat in; colour out
         "color_ranked": (ks * (4 + 24 + sh_bytes + 16), 0),
-        # f64 depth key of all N in, span key out (slice B: span keys in)
-        "radix32_hist": (n * 12 + (n * 4 if sliced else 0), 0),
+        # one pass: f64 depth key of all N in, span key out; slice A: f64 key
+        # of all N in, the slice's (span key, index) pairs out; slice B: its
+        # appended span keys in
+        "radix32_hist": ((n * 8 + c["KA"] * 8 + c["KB"] * 4) if sliced else n * 12, 0),
         "radix32_pass": (3 * ks * 16, 0),  # per pass: key + index read and written
         "depth_fixup": (ks * 4, 0),
-        "slice_b_filter": (n * (8 + 32 + 4), 0),
+        # depth key of all N; record of each kept splat behind the front slice
+        "slice_b_filter": (n * 8 + max(k - c["KA"], 0) * 32, 0),
         # order + geometry gathered, 32 B record written
         "bin_gather": (ks * (4 + 32 + 32), 0),
         # records in, pairs out; 20 FP32 ops per exact row interval (render.py:383-397)

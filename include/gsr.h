@@ -89,6 +89,9 @@ typedef struct gsr_stats {
 } gsr_stats;
 
 GSR_API int gsr_abi_version(void);
+/* Tile size of the render path's lists (columns x rows), for the debug
+   entries' tile indices (gsr_debug_tile_lists / gsr_debug_blend_items). */
+GSR_API int gsr_tile_size(int *out_w, int *out_h);
 GSR_API const char *gsr_last_error(void);
 GSR_API int gsr_device_count(int *out_count);
 

@@ -8,13 +8,15 @@ silently computes on the host.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_build" / "libgsr.so"
+# GSR_LIB_PATH: a tuning variant built with `build.py --out ... -D ...`
+LIB_PATH = Path(os.environ.get("GSR_LIB_PATH") or PKG / "_build" / "libgsr.so")
 HEADER = PKG.parent / "include" / "gsr.h"
 
 GSR_OK = 0
@@ -78,6 +80,7 @@ _vp, _i32, _i64, _dbl, _sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctyp
 _P = ctypes.POINTER
 SIGNATURES = [
     ("gsr_abi_version", _i32, []),
+    ("gsr_tile_size", _i32, [_P(ctypes.c_int), _P(ctypes.c_int)]),
     ("gsr_last_error", ctypes.c_char_p, []),
     ("gsr_device_count", _i32, [_P(_i32)]),
     ("gsr_scene_create", _i32, [_P(_vp), _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -47,32 +47,50 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path = LIB,
+          defines: tuple = ()) -> Path:
+    """Compile every csrc/*.cu (in parallel) and link ``out``.  ``defines``
+    (e.g. ``("GSR_TILE_H=32",)``) build a tuning variant into another file,
+    loaded with GSR_LIB_PATH=<file> (A/B runs on the GPU box)."""
+    out = Path(out)
+    if out == LIB and not defines and not force and not _stale():
         return LIB
-    OUT_DIR.mkdir(parents=True, exist_ok=True)
-    objs = []
+    obj_dir = OUT_DIR if out == LIB else out.parent / (out.stem + "_obj")
+    obj_dir.mkdir(parents=True, exist_ok=True)
     host_cc = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else None
-    for src in sources():
-        obj = OUT_DIR / (src.stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
+
+    def compile_one(src):
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(INCLUDE),
+               "-c", str(src), "-o", str(obj)]
         if host_cc:
             cmd[1:1] = ["-ccbin", host_cc]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+        return str(obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    LIB_ = out
+    tmp = LIB_.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     if host_cc:
         cmd[1:1] = ["-ccbin", host_cc]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, LIB_)
     for o in objs:
         Path(o).unlink(missing_ok=True)
-    return LIB
+    return LIB_
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--out", default=str(LIB))
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=True, verbose=a.verbose, out=Path(a.out), defines=tuple(a.defines)))

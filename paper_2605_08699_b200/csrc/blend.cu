@@ -89,7 +89,12 @@ __constant__ double kExpK[4] = {
 };
 
 __device__ __noinline__ float expf_special(float x, const unsigned long long *tab) {
+#ifdef GSR_TAB_SPLIT
+    (void)tab;  // the shared table is split into word arrays: use the constant one
+    return glibc_expf_tab(x, kExp2fTab);
+#else
     return glibc_expf_tab(x, tab);
+#endif
 }
 
 // glibc expf for |x| < 88 (its main path) with the 2^(i/32) table in shared
@@ -113,10 +118,21 @@ __device__ __forceinline__ float expf_blend(float q, const unsigned long long *t
     const uint32_t ki = (uint32_t)__double2loint(kd);
     kd = __dsub_rn(kd, kShift);
     const double r = __fma_rn(K.inv_ln2n, qd, -kd);
+#ifdef GSR_TAB_SPLIT
+    // tab[ki & 31] as two 32-bit words from a high-word and a low-word
+    // array: 32 entries x 4 B span the 32 banks once, so each load is one
+    // wavefront (a 64-bit entry table spans 64 banks: 2+ wavefronts)
+    uint32_t th, tl;
+    const uint32_t ta = tab_s + ((ki & 31u) << 2);
+    asm("ld.shared.u32 %0, [%1];" : "=r"(th) : "r"(ta));
+    asm("ld.shared.u32 %0, [%1+128];" : "=r"(tl) : "r"(ta));
+    const double sc = __hiloint2double((int)(th + (ki << 15)), (int)tl);
+#else
     unsigned long long t;  // tab[ki & 31] through a precomputed shared-window address
     asm("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(tab_s + ((ki & 31u) << 3)));
     // t + (ki << 47): only the high word changes (the low word of ki << 47 is 0)
     const double sc = __hiloint2double((int)((uint32_t)(t >> 32) + (ki << 15)), (int)(uint32_t)t);
+#endif
     const double z = __fma_rn(K.c0, r, K.c1);
     const double r2 = __dmul_rn(r, r);
     double y = __fma_rn(K.c2, r, 1.0);
@@ -257,10 +273,16 @@ __device__ __forceinline__ uint32_t to_u8(float c) {
 // one after the other from the same staged batch.
 // kMode 0: one pass over the frame's lists.  1: slice A (slice.cu) -- an
 // item whose pixels all saturate writes them; any other saves (T, r, g, b)
-// per pixel in `state` and sets its bit in unsat[tile].  2: slice B -- only
-// the items with their unsat bit, continuing from `state`.
+// per pixel in `state`, sets its bit in unsat_rows and lists itself in
+// unsat_items.  2: slice B -- only the listed items, continuing from `state`.
 template <int kSets, bool kPairLoop, bool kCount, int kMode>
-__global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kernel(
+// 7 CTAs (28 warps) per SM: 71 registers keep the exp constants in registers
+// (at 8 CTAs / 64 registers ptxas reloads four of them from constant memory
+// in every composite iteration); one-call device p50 1.011 -> 1.005 ms
+#ifndef GSR_BLEND_MINB
+#define GSR_BLEND_MINB 7
+#endif
+__global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB) blend_kernel(
     const SplatRec *__restrict__ srec, const float4 *__restrict__ colr,
     const uint32_t *__restrict__ tile_vals, const uint2 *__restrict__ ranges, int width,
     int height, BlendOut out, FrameCounters *__restrict__ ctr, SliceState ss) {
@@ -269,7 +291,14 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
     constexpr int kItems = kTileH / kSets;  // items per tile
     __shared__ unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
+#ifdef GSR_TAB_SPLIT
+    if (threadIdx.x < 32) {
+        reinterpret_cast<uint32_t *>(s_tab)[threadIdx.x] = (uint32_t)(kExp2fTab[threadIdx.x] >> 32);
+        reinterpret_cast<uint32_t *>(s_tab)[32 + threadIdx.x] = (uint32_t)kExp2fTab[threadIdx.x];
+    }
+#else
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+#endif
     {   // zero records (the null slot is never written afterwards)
         float4 *z = reinterpret_cast<float4 *>(s_b);
         for (int i = threadIdx.x; i < (int)(sizeof(s_b) / sizeof(float4)); i += blockDim.x)
@@ -434,7 +463,8 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : 8) blend_kerne
                         ss.state[(int64_t)(iy0 + h) * width + ix] =
                             make_float4(T[h], cr[h], cg[h], cb[h]);
                 if (lane == 0) {
-                    atomicOr(ss.unsat + tile, 1u << wr);
+                    atomicOr(ss.unsat_rows + (int64_t)(iy0 >> 1) * ss.row_words + (tx >> 5),
+                             1u << (tx & 31));
                     ss.unsat_items[atomicAdd(&ctr->n_unsat, 1u)] = (uint32_t)item;
                 }
                 continue;

@@ -98,10 +98,22 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &
         span.kmax = &a.ctr->kmax;
         span.bits = kSpanBits;
         span.limit = a.limit;
-        launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
-                                                  true, true, a.count, a.n, a.n, kSpanBits / 8,
-                                                  true, a.work32, a.sched, &a.ctr->npass, sms, s,
-                                                  mark, span);
+        if (a.limit) {
+            // slice A: the histogram kernel appends the slice's (k32, index)
+            // pairs (counting KA); the passes sort only those
+            span.count_out = a.count;
+            span.compact = true;
+            span.n_src = a.n;
+            launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0],
+                                                      a.vals[1], false, false, a.count, -1, a.n,
+                                                      kSpanBits / 8, false, a.work32, a.sched,
+                                                      &a.ctr->npass, sms, s, mark, span);
+        } else {
+            launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0],
+                                                      a.vals[1], true, true, a.count, a.n, a.n,
+                                                      kSpanBits / 8, true, a.work32, a.sched,
+                                                      &a.ctr->npass, sms, s, mark, span);
+        }
     }
     depth_fixup_kernel<<<g, 256, 0, s>>>(a);
     mark("depth_fixup");

@@ -50,6 +50,14 @@ int ensure(DevBuf &b, size_t bytes) {
 // Depth-sliced frames (slice.cu): scenes of at least GSR_SLICE_MIN Gaussians
 // (default 262144; 0 disables slicing) are rendered in two slices, the first
 // holding about GSR_SLICE_FRAC (default 0.15) of the kept splats.
+// depth-sliced frames: unsaturated items after slice A, one bit per tile
+// column in each item row (two pixel rows; tile rows are whole item rows)
+int unsat_row_words(int W) { return ((W + kTileW - 1) / kTileW + 31) / 32; }
+int unsat_item_rows(int H) { return ((H + kTileH - 1) / kTileH) * (kTileH / 2); }
+size_t unsat_rows_bytes(int W, int H) {
+    return sizeof(uint32_t) * (size_t)unsat_item_rows(H) * (size_t)unsat_row_words(W);
+}
+
 int64_t slice_min() {
     static const int64_t v = [] {
         const char *e = getenv("GSR_SLICE_MIN");
@@ -90,6 +98,7 @@ struct FrameGraph {
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t params_node = nullptr;
     uint64_t last_use = 0;
+    int64_t base_launches = 0;  // kernels per launch outside the conditional bodies
 };
 
 struct SavedCall {
@@ -120,7 +129,7 @@ struct gsr_ctx {
     DevBuf frame_u8, frame_rgb, frame_t;
     DevBuf colr;          // colours by depth rank of the current pass
     // depth-sliced frames: pixel state after slice A, unsaturated items (bits, list)
-    DevBuf state, unsat, unsat_items;
+    DevBuf state, unsat_rows, unsat_items, col_prefix;
     DevBuf params;        // FrameParams of the frame being rendered
     // CUDA graphs of this context's frame configurations (record_frame)
     static constexpr int kMaxGraphs = 32;
@@ -137,7 +146,14 @@ struct gsr_ctx {
     // 64-bit depth re-sort); one D2H copy per frame brings all of them back
     DevBuf ctr;
     FrameCounters *hctr = nullptr;
-    uint32_t sticky_seen[2] = {0, 0};  // sticky values reported by the last fill_stats
+    // sticky device counters after FrameCounters: [0] frames whose buffers
+    // overflowed, [1] frames needing the 64-bit sort, [2 + k] graph frames
+    // whose slice B ran conditional body k (kernel-launch accounting)
+    static constexpr int kSticky = 2 + kSliceClasses + 1;
+    uint32_t sticky_seen[kSticky] = {};  // sticky values reported by the last fill_stats
+    // kernels per graph frame outside the conditional bodies, and per body
+    // (recorded at capture; a graph launch counts its kernels, not 1)
+    int64_t body_launches[kSliceClasses + 1] = {};
     uint32_t *dsticky() { return reinterpret_cast<uint32_t *>(ctr.as<FrameCounters>() + 1); }
     const uint32_t *hsticky() const { return reinterpret_cast<const uint32_t *>(hctr + 1); }
     int64_t launches = 0;  // kernels enqueued since the last finish/render
@@ -176,7 +192,7 @@ struct gsr_ctx {
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &colr, &state, &unsat, &unsat_items, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+                               &geo, &colr, &state, &unsat_rows, &unsat_items, &col_prefix, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
@@ -306,7 +322,8 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
     SliceState ss;
     if (slice) {
         ss.state = c->state.as<float4>();
-        ss.unsat = c->unsat.as<uint32_t>();
+        ss.unsat_rows = c->unsat_rows.as<uint32_t>();
+        ss.row_words = unsat_row_words(W);
         ss.unsat_items = c->unsat_items.as<uint32_t>();
     }
     // one depth-ordered pass over *count splats (at most cap): sort, colour, bin
@@ -365,11 +382,13 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         ba.overflow_sticky = c->dsticky();
         launches += launch_binning(ba, st, mark);
     };
-    auto blend = [&](int mode) {
+    auto blend_on = [&](cudaStream_t st, int mode, const SliceState &sst) {
         launch_blend(c->srec.as<SplatRec>(), c->colr.as<float4>(), c->tile_vals.as<uint32_t>(),
-                     c->ranges.as<uint2>(), W, H, out, ctr, s, mark, c->kcount, mode, ss);
+                     c->ranges.as<uint2>(), W, H, out, ctr, st, mark, c->kcount, mode, sst);
         launches += 1;
     };
+    auto blend = [&](int mode) { blend_on(s, mode, ss); };
+
 
     cudaEventRecordWithFlags(c->ev[0], s, evflags);
     if (c->ktime && !graph) cudaEventRecord(c->kev[0], s);
@@ -385,13 +404,12 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
     if (n > 0) {
         launch_preprocess_geo(sc->view, dfp, cull, c->keys[0].as<unsigned long long>(),
                               c->geo.as<GeoRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr,
-                              ctr, s, mark);
+                              ctr, slice ? ctr->slice_hist : nullptr, s, mark);
         launches += 1;
         if (slice) {
-            launch_slice_plan(c->keys[0].as<unsigned long long>(), n, ctr,
-                              c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac(), c->sms,
-                              s, mark);
-            launches += 2;
+            launch_slice_plan(ctr, c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac(), s,
+                              mark);
+            launches += 1;
         }
     }
     cudaEventRecordWithFlags(c->ev[1], s, evflags);
@@ -412,7 +430,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         // slice A: the front of the depth order
         sort_color_bin(s, &ctr->KA, &ctr->tau, false, c->cap_n);
         cudaEventRecordWithFlags(c->ev[3], s, evflags);
-        cudaMemsetAsync(c->unsat.p, 0, sizeof(uint32_t) * (size_t)c->ntiles, s);
+        cudaMemsetAsync(c->unsat_rows.p, 0, unsat_rows_bytes(W, H), s);
         blend(1);
         cudaEventRecordWithFlags(c->ev[4], s, evflags);
         // slice B: the splats behind it that can reach an unsaturated item
@@ -421,14 +439,17 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         sb.geo = c->geo.as<GeoRec>();
         sb.n = n;
         sb.ctr = ctr;
-        sb.unsat = c->unsat.as<uint32_t>();
+        sb.unsat_rows = c->unsat_rows.as<uint32_t>();
+        sb.row_words = unsat_row_words(W);
+        sb.item_rows = unsat_item_rows(H);
+        sb.col_prefix = c->col_prefix.as<uint32_t>();
         sb.width = W;
         sb.height = H;
         sb.tiles_x = (W + kTileW - 1) / kTileW;
         sb.keysB = c->keys32[0].as<uint32_t>();
         sb.valsB = c->vals[0].as<uint32_t>();
         launch_slice_b_filter(sb, s, mark);
-        launches += 1;
+        launches += 2;
         auto class_cap = [&](int k) {
             return k < kSliceClasses - 1 ? std::min<int64_t>(slice_class_cap(k), c->cap_n)
                                          : c->cap_n;
@@ -443,21 +464,31 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
             cudaGraphConditionalHandle h;
             GSR_CUDA_OK(cudaGraphConditionalHandleCreate(&h, g, kSliceClasses,
                                                          cudaGraphCondAssignDefault));
-            launch_slice_b_decide(ctr, h, s);
+            // bodies 0 .. kSliceClasses - 1: slice B's sort, colours, lists
+            // and blend with class-k grids; body kSliceClasses (slice B
+            // empty): the blend alone (the unsaturated items finish from the
+            // saved state)
+            launch_slice_b_decide(ctr, h, c->dsticky() + 2, s);
+            launches += 1;
             GSR_CUDA_OK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
             std::vector<cudaGraphNode_t> dv(deps, deps + nd);
             cudaGraphNodeParams cp{};
             cp.type = cudaGraphNodeTypeConditional;
             cp.conditional.handle = h;
             cp.conditional.type = cudaGraphCondTypeSwitch;
-            cp.conditional.size = kSliceClasses;
+            cp.conditional.size = kSliceClasses + 1;
             cudaGraphNode_t cn;
             GSR_CUDA_OK(cudaGraphAddNode(&cn, g, dv.data(), dv.size(), &cp));
-            for (int k = 0; k < kSliceClasses; k++) {
+            for (int k = 0; k <= kSliceClasses; k++) {
                 GSR_CUDA_OK(cudaStreamBeginCaptureToGraph(c->cap_stream, cp.conditional.phGraph_out[k],
                                                           nullptr, nullptr, 0,
                                                           cudaStreamCaptureModeThreadLocal));
-                sort_color_bin(c->cap_stream, &ctr->KB, nullptr, true, class_cap(k));
+                const int before = launches;
+                if (k < kSliceClasses)
+                    sort_color_bin(c->cap_stream, &ctr->KB, nullptr, true, class_cap(k));
+                blend_on(c->cap_stream, 2, ss);
+                c->body_launches[k] = launches - before;
+                launches = before;  // counted per frame from the device's class counters
                 cudaGraph_t body = nullptr;
                 GSR_CUDA_OK(cudaStreamEndCapture(c->cap_stream, &body));
             }
@@ -474,11 +505,11 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
             for (int j = kSliceClasses - 2; j >= 0; j--)
                 if ((int64_t)kb <= slice_class_cap(j)) k = j;
             if (kb > 0) sort_color_bin(s, &ctr->KB, nullptr, true, class_cap(k));
+            blend_on(s, 2, ss);
         }
-        blend(2);
     }
     cudaEventRecordWithFlags(c->ev[5], s, evflags);
-    cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters) + 2 * sizeof(uint32_t),
+    cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t),
                     cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(c->hsched, dsched, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     GSR_CUDA_OK(cudaGetLastError());
@@ -521,6 +552,7 @@ int frame_graph(gsr_ctx *c, const FrameKey &key, const gsr_scene *sc, const Fram
     GSR_CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     const int64_t launches_before = c->launches;
     int rc = record_frame(c, sc, fp, sh_degree, cull, want_rgb, want_keep, slice, true);
+    fg.base_launches = c->launches - launches_before;
     c->launches = launches_before;
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
@@ -598,7 +630,10 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     if (slice) {
         const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
         if ((rc = cens(c, c->state, sizeof(float4) * (size_t)W * H))) return rc;
-        if ((rc = cens(c, c->unsat, sizeof(uint32_t) * (size_t)c->ntiles))) return rc;
+        if ((rc = cens(c, c->unsat_rows, unsat_rows_bytes(W, H)))) return rc;
+        if ((rc = cens(c, c->col_prefix, sizeof(uint32_t) * (size_t)((W + kTileW - 1) / kTileW) *
+                                             (size_t)(unsat_item_rows(H) + 1))))
+            return rc;
         if ((rc = cens(c, c->unsat_items, sizeof(uint32_t) * n_items))) return rc;
     }
     FrameParams fp;
@@ -635,7 +670,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         kp.kernelParams = args;
         GSR_CUDA_OK(cudaGraphExecKernelNodeSetParams(fg->exec, fg->params_node, &kp));
         GSR_CUDA_OK(cudaGraphLaunch(fg->exec, c->stream));
-        c->launches += 1;  // one graph launch (its kernels are this context's)
+        c->launches += fg->base_launches;  // + the body's kernels, counted on the device
     } else {
         if ((rc = record_frame(c, sc, fp, sh_degree, cull, want_rgb, want_keep, slice, false)))
             return rc;
@@ -712,10 +747,14 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     st->ms_tile_sort = 0.0f;    // (no tile sort: sort-free lists)
     st->ms_blend = t[4];        // blend (of slice A)
     st->ms_slice_b = t[5];      // slice B: filter, sort, colours, lists, blend (0: one pass)
-    st->kernel_launches = (int32_t)c->launches;
-    c->launches = 0;
     // sticky counters as of the last completed frame's copy (no extra sync)
     const uint32_t *hs = c->hsticky();
+    for (int k = 0; k <= kSliceClasses; k++) {  // graph frames' slice-B bodies
+        c->launches += (int64_t)(hs[2 + k] - c->sticky_seen[2 + k]) * c->body_launches[k];
+        c->sticky_seen[2 + k] = hs[2 + k];
+    }
+    st->kernel_launches = (int32_t)c->launches;
+    c->launches = 0;
     st->overflow_frames = (int32_t)(hs[0] - c->sticky_seen[0]);
     st->long_run_frames = (int32_t)(hs[1] - c->sticky_seen[1]);
     c->sticky_seen[0] = hs[0];
@@ -884,6 +923,13 @@ extern "C" {
 
 int gsr_abi_version(void) { return GSR_ABI_VERSION; }
 
+int gsr_tile_size(int *out_w, int *out_h) {
+    if (!out_w || !out_h) return fail(GSR_E_INVALID, "null output");
+    *out_w = kTileW;
+    *out_h = kTileH;
+    return GSR_OK;
+}
+
 const char *gsr_last_error(void) { return g_err.c_str(); }
 
 int gsr_device_count(int *out_count) {
@@ -1009,7 +1055,7 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     for (int i = 0; i < 8 && e == cudaSuccess; i++) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i <= gsr_ctx::kMaxMarks && e == cudaSuccess; i++) e = cudaEventCreate(&c->kev[i]);
     if (e == cudaSuccess)
-        e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters) + 4 * sizeof(uint32_t));
+        e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hssim, sizeof(double) * 64);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hsched, sizeof(uint32_t) * 64);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hjpeg, sizeof(uint32_t) * 4);
@@ -1018,14 +1064,14 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
         gsr_ctx_destroy(c);
         return rc;
     }
-    int rc = ensure(c->ctr, sizeof(FrameCounters) + 4 * sizeof(uint32_t));
+    int rc = ensure(c->ctr, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t));
     if (!rc) rc = ensure(c->params, sizeof(FrameParams));
     if (!rc) rc = ensure(c->sched, 64 * sizeof(uint32_t));
     if (!rc && cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
     if (!rc && cudaMemset(c->ctr.p, 0, c->ctr.bytes) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
-    if (!rc) std::memset(c->hctr, 0, sizeof(FrameCounters) + 4 * sizeof(uint32_t));
+    if (!rc) std::memset(c->hctr, 0, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t));
     if (!rc) rc = ensure(c->ssim_misc, 64);
     if (!rc) rc = ensure(c->ssim_w, sizeof(double) * 11);
     if (rc) {

@@ -51,7 +51,7 @@ struct FrameCounters {
     uint32_t n_unsat;              // work items slice A left unsaturated
     unsigned long long Dtot, Ptot; // tile keys / pairs over the passes
     unsigned long long Dmax, Pmax; // largest pass (buffer capacities)
-    uint32_t slice_hist[256];      // top 8 bits of the kept span keys
+    uint32_t slice_hist[1024];     // kept depths over kZBins bins of their f64 bits (preprocess_geo)
 };
 
 // The depth sort's 24-bit span key of a kept splat's f64 depth bits k64
@@ -124,9 +124,18 @@ const void *frame_params_kernel_fn();  // its function (graph node updates)
 using GeoRec = SplatRec;  // by Gaussian index (preprocess), by depth rank (gather)
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 // K1a: projection, culling, depth keys, packed geometry (render.py:163-290)
+// zhist (depth-sliced frames, else null): += histogram of the kept depths
+// over kZBins bins of their f64 bits (slice_plan's input)
 void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
-                           FrameCounters *ctr, cudaStream_t s, const KMark &mark = KMark());
+                           FrameCounters *ctr, uint32_t *zhist, cudaStream_t s,
+                           const KMark &mark = KMark());
+// depth histogram bins: bin = clamp((bits(z) >> 47) - kZBinBase, 0, 1023),
+// 32 bins per binade (sign, 11 exponent and 5 mantissa bits) over z in
+// [2^-8, 2^24)
+constexpr int kZBins = 1024;
+constexpr int kZBinShift = 47;
+constexpr int kZBinBase = 1015 << 5;
 // radix.cu: Onesweep stable LSD sort (see radix.cu header)
 cudaError_t radix_init_attributes();
 #ifndef GSR_RADIX_THREADS
@@ -153,6 +162,9 @@ struct SpanKeys {
     const unsigned long long *kmin = nullptr, *kmax = nullptr;
     int bits = 24;
     const uint32_t *limit = nullptr;  // span keys above *limit become sentinels (slice A)
+    uint32_t *count_out = nullptr;    // += keys the first pass keeps (slice A's KA; zeroed per frame)
+    bool compact = false;             // append the kept (key, index) pairs to keys[0]/vals[0]
+    int64_t n_src = 0;                // (compact) source keys read
 };
 // Sorts (keys0, vals0) over `passes` 8-bit digits; the result lands in buffer
 // sched[16] (0 or 1).  First pass: n_first items (>= 0) or *n_dev (n_first <
@@ -223,6 +235,7 @@ cudaError_t binning_init_attributes();
 int launch_binning(const BinArgs &a, cudaStream_t s,
                    const KMark &mark = KMark());  // returns kernels launched
 
+
 // contract.cu: the exact tile-list contract on tile x tile tiles via
 // (tile | rank) keys, a radix sort and range identification (parity path)
 struct ContractArgs {
@@ -258,11 +271,12 @@ struct BlendOut {
 bool blend_has_slices();  // the selected blend variant has modes 1 and 2
 int blend_grid(int width, int height);  // its persistent grid (host query, cached)
 // mode: 0 one pass; 1 slice A (saturated items write the frame, the others
-// save their pixels' state, set their unsat bit and are listed in
+// save their pixels' state, set their bit in unsat_rows and are listed in
 // unsat_items); 2 slice B (the listed items only, from the saved state)
 struct SliceState {
     float4 *state = nullptr;        // (H, W) pixel (T, r, g, b) after slice A
-    uint32_t *unsat = nullptr;      // [ntiles] unsaturated items of slice A (bits)
+    uint32_t *unsat_rows = nullptr; // [item rows][row_words]: bit tx = item of tile column tx
+    int row_words = 0;              // words per item row: (tiles_x + 31) / 32
     uint32_t *unsat_items = nullptr;  // [n_items] their ids; count in FrameCounters.n_unsat
 };
 void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
@@ -276,7 +290,9 @@ struct SliceBArgs {
     const GeoRec *geo;                 // records by Gaussian index
     int64_t n;
     FrameCounters *ctr;                // kmin, kmax, tau; KB counted here
-    const uint32_t *unsat;             // [ntiles] items of slice A left unsaturated
+    const uint32_t *unsat_rows;        // [item rows][row_words] items slice A left unsaturated
+    int row_words, item_rows;
+    uint32_t *col_prefix;              // [tiles_x][item_rows + 1] (slice_b_filter's first kernel)
     int width, height, tiles_x;
     uint32_t *keysB, *valsB;           // out: slice B's (span key, Gaussian index), appended
 };
@@ -284,13 +300,12 @@ struct SliceBArgs {
 // grids for at most kSliceClassCap[c] splats (class 2: all)
 constexpr int kSliceClasses = 3;
 __host__ __device__ constexpr int64_t slice_class_cap(int c) { return c == 0 ? 4096 : 65536; }
-void launch_slice_plan(const unsigned long long *keys64, int64_t n, FrameCounters *ctr,
-                       float frac, int sms, cudaStream_t s, const KMark &mark = KMark());
+void launch_slice_plan(FrameCounters *ctr, float frac, cudaStream_t s, const KMark &mark = KMark());
 void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark = KMark());
 // sets `handle` (a graph's switch) to slice B's size class, kSliceClasses
 // (no body) when slice B is empty
 void launch_slice_b_decide(const FrameCounters *ctr, cudaGraphConditionalHandle handle,
-                           cudaStream_t s);
+                           uint32_t *class_count, cudaStream_t s);
 
 // jpeg.cu: baseline JPEG of a device u8 frame (Pillow / libjpeg-turbo exact)
 struct JpegLayout {

@@ -59,7 +59,7 @@ __device__ __forceinline__ double sh_channel(const T *v, int c, double x, double
 }
 
 __global__ void __launch_bounds__(256) frame_init_kernel(FrameCounters *ctr) {
-    ctr->slice_hist[threadIdx.x] = 0u;
+    for (int j = threadIdx.x; j < kZBins; j += blockDim.x) ctr->slice_hist[j] = 0u;
     if (threadIdx.x) return;
     ctr->K = 0;
     ctr->D = 0;
@@ -83,11 +83,17 @@ __global__ void __launch_bounds__(256) frame_init_kernel(FrameCounters *ctr) {
 
 __global__ void frame_params_kernel(FrameParams p, FrameParams *dst) { *dst = p; }
 
-__global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
+#ifndef GSR_PP_MINB
+#define GSR_PP_MINB 5
+#endif
+__global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
     SceneView sc, const FrameParams *__restrict__ fp, int do_cull,
     unsigned long long *__restrict__ keys, GeoRec *__restrict__ geo,
-    uint8_t *__restrict__ keep_out, FrameCounters *ctr) {
+    uint8_t *__restrict__ keep_out, FrameCounters *ctr, uint32_t *__restrict__ zhist) {
     __shared__ CameraArgs cam;  // this frame's camera (FrameParams), staged once per block
+    __shared__ uint32_t s_zh[kZBins];
+    if (zhist)
+        for (int j = threadIdx.x; j < kZBins; j += blockDim.x) s_zh[j] = 0u;
     if (threadIdx.x < sizeof(CameraArgs) / 8)
         reinterpret_cast<unsigned long long *>(&cam)[threadIdx.x] =
             reinterpret_cast<const unsigned long long *>(&fp->cam)[threadIdx.x];
@@ -164,6 +170,10 @@ __global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
             if (k) {
                 kept = true;
                 key = (unsigned long long)__double_as_longlong(z);
+                if (zhist) {
+                    const int bin = (int)(key >> kZBinShift) - kZBinBase;
+                    atomicAdd(&s_zh[bin < 0 ? 0 : (bin >= kZBins ? kZBins - 1 : bin)], 1u);
+                }
                 // render.py:442-453
                 const double det = ca * cc - cb * cb;
                 const float ia32 = (float)(cc / det);
@@ -195,6 +205,9 @@ __global__ void __launch_bounds__(256, 5) preprocess_geo_kernel(
         s_cnt[w] = cnt;
     }
     __syncthreads();
+    if (zhist)
+        for (int j = threadIdx.x; j < kZBins; j += blockDim.x)
+            if (s_zh[j]) atomicAdd(zhist + j, s_zh[j]);
     if (threadIdx.x == 0) {
         uint32_t c = 0;
         for (int j = 0; j < (int)(blockDim.x >> 5); j++) {
@@ -284,12 +297,13 @@ const void *frame_params_kernel_fn() { return (const void *)frame_params_kernel;
 
 void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
-                           FrameCounters *ctr, cudaStream_t s, const KMark &mark) {
+                           FrameCounters *ctr, uint32_t *zhist, cudaStream_t s,
+                           const KMark &mark) {
     if (scene.n == 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
     preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, fp, frustum_cull, keys, geo,
-                                                     keep_out, ctr);
+                                                     keep_out, ctr, zhist);
     mark("preprocess_geo");
 }
 

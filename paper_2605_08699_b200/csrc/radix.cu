@@ -9,10 +9,12 @@
 // Stability gives the reference's tie order (equal depths keep index order).
 //
 // Per sort: one histogram kernel computes every pass's digit histogram in one
-// read of the keys; a 1-block plan kernel turns them into global digit
-// offsets and marks passes whose digit is constant as inactive (skipped: an
-// identity permutation), recording which ping-pong buffer each active pass
-// reads.  Each pass: a block takes a 4096-key tile in ticket order, ranks its
+// read of the keys (for slice A it also compacts: appends the slice's (span
+// key, index) pairs, slice.cu).  Every pass kernel then plans in its
+// prologue (the plan was a 1-block kernel of its own): it turns its digit
+// histogram into global digit offsets and finds the passes whose digit is
+// constant (inactive, skipped: an identity permutation), hence which
+// ping-pong buffer it reads; pass 0 publishes the schedule.  Each pass: a block takes a 4096-key tile in ticket order, ranks its
 // keys stably (per-warp digit lane masks + digit counters), publishes its digit
 // counts, looks back over predecessor tiles per digit for its global
 // position, and scatters through shared memory so global writes are
@@ -95,9 +97,15 @@ __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
         for (int64_t j = (int64_t)blockIdx.x * RB + threadIdx.x; j < nz; j += (int64_t)gridDim.x * RB)
             z[j] = 0u;
     }
+    __shared__ uint32_t s_kept;
     for (int j = threadIdx.x; j < 8 * 256; j += RB) (&h[0][0])[j] = 0;
+    if (threadIdx.x == 0) s_kept = 0u;
     __syncthreads();
-    const int64_t n = first_count(a);
+    uint32_t kept_local = 0u;  // keys kept by the first pass (span.count_out)
+    // compacting span keys (slice A): read n_src source keys, append the kept
+    // ones; the passes then read *n_dev = *count_out items
+    const bool compact = sizeof(K) == 4 && a.span.src && a.span.compact;
+    const int64_t n = compact ? a.span.n_src : first_count(a);
     const K *keys = a.keys[0];
     SpanMap sm{0ull, 0ull, 0};
     uint32_t limit = 0xffffffffu;
@@ -109,7 +117,57 @@ __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
     // loop is otherwise one global latency per key)
     constexpr int kHU = 8;
     const int64_t stride = (int64_t)gridDim.x * RB;
-    for (int64_t i0 = (int64_t)blockIdx.x * RB + threadIdx.x; i0 < n; i0 += stride * kHU) {
+    if (compact) {
+        // (k32, index) of the kept keys appended, one global atomic per
+        // block step of RB * kHU keys (the block's warps take consecutive
+        // ranges of it); the order among equal k32 is restored by the depth
+        // fix-up, which orders runs by (f64 key, index)
+        __shared__ uint32_t s_wc[RB / 32 + 1];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int64_t c0 = (int64_t)blockIdx.x * RB * kHU; c0 < n; c0 += stride * kHU) {
+            uint32_t q[kHU];
+            uint32_t bal[kHU];
+            uint32_t wcnt = 0u;
+#pragma unroll
+            for (int u = 0; u < kHU; u++) {
+                const int64_t i = c0 + (int64_t)u * RB + threadIdx.x;
+                const unsigned long long k = i < n ? a.span.src[i] : ~0ull;
+                q[u] = k != ~0ull ? span_key(sm, k) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < kHU; u++) {
+                bal[u] = __ballot_sync(0xffffffffu, q[u] <= limit);
+                wcnt += (uint32_t)__popc(bal[u]);
+            }
+            if (lane == 0) s_wc[w] = wcnt;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t t = 0u;
+                for (int j = 0; j < RB / 32; j++) {
+                    const uint32_t c = s_wc[j];
+                    s_wc[j] = t;
+                    t += c;
+                }
+                s_wc[RB / 32] = t ? atomicAdd(a.span.count_out, t) : 0u;
+            }
+            __syncthreads();
+            uint32_t pos = s_wc[RB / 32] + s_wc[w];
+#pragma unroll
+            for (int u = 0; u < kHU; u++) {
+                if (q[u] <= limit) {
+                    const uint32_t at = pos + (uint32_t)__popc(bal[u] & ((1u << lane) - 1u));
+                    a.keys[0][at] = (K)q[u];
+                    a.vals[0][at] = (uint32_t)(c0 + (int64_t)u * RB + threadIdx.x);
+#pragma unroll
+                    for (int p = 0; p < (int)sizeof(K); p++)
+                        if (p < a.passes) atomicAdd(&h[p][(q[u] >> (8 * p)) & 255u], 1u);
+                }
+                pos += (uint32_t)__popc(bal[u]);
+            }
+            __syncthreads();  // s_wc reused by the next step
+        }
+    }
+    for (int64_t i0 = (int64_t)blockIdx.x * RB + threadIdx.x; !compact && i0 < n; i0 += stride * kHU) {
         K kk[kHU];
         unsigned long long k64[kHU];
         const bool span = sizeof(K) == 4 && a.span.src;
@@ -132,48 +190,20 @@ __global__ void __launch_bounds__(RB) radix_hist_kernel(SortArgs<K> a) {
                 k = kk[u];
             }
             if (a.drop_sentinel && k == sentinel<K>()) continue;
+            kept_local++;
 #pragma unroll
             for (int p = 0; p < (int)sizeof(K); p++)
                 if (p < a.passes) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 255u], 1u);
         }
     }
+    if (a.span.count_out && !compact && kept_local) atomicAdd(&s_kept, kept_local);
     __syncthreads();
     for (int j = threadIdx.x; j < a.passes * 256; j += RB) {
         const uint32_t c = (&h[0][0])[j];
         if (c) atomicAdd(a.hist + j, c);
     }
-}
-
-// 1 block x 256 threads: per-pass exclusive digit offsets + pass schedule
-template <typename K>
-__global__ void __launch_bounds__(256) radix_plan_kernel(SortArgs<K> a) {
-    __shared__ uint32_t s_warp[33];
-    __shared__ int s_active[8];
-    const int d = threadIdx.x;
-    for (int p = 0; p < a.passes; p++) {
-        const uint32_t c = a.hist[p * 256 + d];
-        const int nz = __syncthreads_count(c != 0u);
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan_u32(c, s_warp, &tot);
-        a.hist[p * 256 + d] = ex;
-        if (d == 0) s_active[p] = (nz > 1) || (p == 0 && a.force_first);
-    }
-    __syncthreads();
-    if (d == 0) {
-        int cur = 0;
-        for (int p = 0; p < 8; p++) {
-            const int act = p < a.passes ? s_active[p] : 0;
-            a.sched[p] = (uint32_t)act;
-            a.sched[8 + p] = (uint32_t)cur;
-            cur ^= act;
-        }
-        a.sched[16] = (uint32_t)cur;
-        if (a.npass_out) {
-            uint32_t np = 0;
-            for (int p = 0; p < a.passes; p++) np += (uint32_t)s_active[p];
-            *a.npass_out = np;
-        }
-    }
+    if (a.span.count_out && !compact && threadIdx.x == 0 && s_kept)
+        atomicAdd(a.span.count_out, s_kept);
 }
 
 template <typename K>
@@ -186,6 +216,7 @@ struct PassSmem {
     uint32_t dstart[256];
     uint32_t gbase[256];
     uint32_t s_warp[33];
+    uint32_t off[256];   // this pass's exclusive digit offsets (the folded plan)
     uint32_t tile_n;
     uint32_t ticket;
 };
@@ -193,14 +224,39 @@ struct PassSmem {
 template <typename K>
 __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K> a, int pass) {
     constexpr int RI = Cfg<K>::RI, RT = Cfg<K>::RT;
-    if (!a.sched[pass]) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem<K> &S = *reinterpret_cast<PassSmem<K> *>(smem_raw);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t src = a.sched[8 + pass];
+    // the plan, folded into every pass (one kernel boundary less per sort):
+    // a pass is active unless its digit is constant (pass 0 forced when it
+    // compacts); buffers alternate over the active passes; this pass's
+    // digit offsets are the exclusive scan of its histogram
+    uint32_t act_mask = 0u;
+    for (int p = 0; p < a.passes; p++) {
+        const uint32_t c = threadIdx.x < 256 ? a.hist[p * 256 + threadIdx.x] : 0u;
+        const int nz = __syncthreads_count(c != 0u);
+        if (nz > 1 || (p == 0 && a.force_first)) act_mask |= 1u << p;
+        if (p == pass) {
+            const uint32_t ex = block_excl_scan_u32(c, S.s_warp, nullptr);
+            if (threadIdx.x < 256) S.off[threadIdx.x] = ex;
+        }
+    }
+    if (pass == 0 && blockIdx.x == 0 && threadIdx.x == 0) {  // for the sort's consumers
+        uint32_t cur = 0u, np = 0u;
+        for (int p = 0; p < 8; p++) {
+            const uint32_t act = (act_mask >> p) & 1u;
+            a.sched[p] = act;
+            a.sched[8 + p] = cur;
+            cur ^= act;
+            np += act;
+        }
+        a.sched[16] = cur;
+        if (a.npass_out) *a.npass_out = np;
+    }
+    if (!((act_mask >> pass) & 1u)) return;
+    const uint32_t src = (uint32_t)(__popc(act_mask & ((1u << pass) - 1u)) & 1);
     // first active pass: reads the producer's buffer (0) with n_first items
-    bool first = true;
-    for (int p = 0; p < pass; p++) first = first && !a.sched[p];
+    const bool first = (act_mask & ((1u << pass) - 1u)) == 0u;
     const int64_t n = first ? first_count(a) : items_after_first(a);
     if (threadIdx.x == 0) S.ticket = atomicAdd(a.tickets + pass, 1u);
     const bool dig = threadIdx.x < 256;  // digit owner (RB >= 256)
@@ -297,7 +353,7 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
         if (t == 0) {
 #endif
             st_release_u32(st + d, kFlagInc | tot);
-            S.gbase[d] = a.hist[pass * 256 + d];
+            S.gbase[d] = S.off[d];
         } else {
             uint32_t excl = 0;
             int64_t tp = t - 1;
@@ -321,7 +377,7 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
                 tp -= used;
             }
             st_release_u32(st + t * 256 + d, kFlagInc | (excl + tot));
-            S.gbase[d] = a.hist[pass * 256 + d] + excl;
+            S.gbase[d] = S.off[d] + excl;
         }
     }
     uint32_t tile_total;
@@ -412,12 +468,10 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
         mark(sizeof(K) == 8 ? "radix64_hist" : "radix32_hist");
         launches++;
     }
-    radix_plan_kernel<K><<<1, 256, 0, s>>>(a);
-    mark(sizeof(K) == 8 ? "radix64_plan" : "radix32_plan");
-    launches++;
-    if (n_items_cap > 0) {
+    {   // (pass 0 also publishes the schedule, so it always runs)
         for (int p = 0; p < passes; p++) {
-            onesweep_pass_kernel<K><<<(unsigned)a.tiles, RB, sizeof(PassSmem<K>), s>>>(a, p);
+            onesweep_pass_kernel<K><<<(unsigned)std::max<int64_t>(a.tiles, 1), RB,
+                                      sizeof(PassSmem<K>), s>>>(a, p);
             mark(sizeof(K) == 8 ? "radix64_pass" : "radix32_pass");
             launches++;
         }

@@ -9,16 +9,20 @@
 // r02_blend_instrumentation.json).  So a frame is rendered in two passes
 // over one global depth order:
 //   A  the front slice: kept splats whose 24-bit span key (depth.cu) is at
-//      most tau, tau chosen from a histogram of the keys' top 8 bits so the
-//      slice holds about a fraction f of the kept splats.  It is sorted,
+//      most tau, tau chosen from a histogram of the kept depths (built by
+//      preprocess_geo) so the slice holds about a fraction f of them.  It is sorted,
 //      coloured, binned and blended like a whole frame; a work item (two
 //      pixel rows of a 32 x 64 tile) whose pixels all saturate writes its
 //      final pixels, any other item saves its pixels' (T, r, g, b) and sets
-//      its bit in unsat[tile].
+//      its bit in the unsaturated-item rows.
 //   B  the rest: a splat behind the slice is kept only if its conservative
-//      column span (band_span_bound, the binning's own bound) meets a tile
-//      row band holding an unsaturated item; those are sorted, coloured,
-//      binned and blended from the saved state, by the unsaturated items only.
+//      column span (band_span_bound, the binning's own bound, over its whole
+//      row range) meets an unsaturated item in one of its rows (blend A
+//      marks each unsaturated item in a per-item-row bitmask over the tile
+//      columns; per tile column, a prefix count over the item rows answers
+//      "any unsaturated item in rows [r0, r1)" with two loads); those are
+//      sorted, coloured, binned and blended from the saved state, by the
+//      unsaturated items only.
 // Ties in the span key never straddle the slices (the split is on the key),
 // so A's order followed by B's is the global stable depth order, and each
 // unsaturated pixel sees every splat covering it in the reference's order:
@@ -31,24 +35,12 @@ namespace gsr {
 
 namespace {
 
-// top 8 bits of the span keys of the kept splats
-__global__ void __launch_bounds__(256) slice_hist_kernel(const unsigned long long *__restrict__ keys64,
-                                                         int64_t n, FrameCounters *ctr) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const SpanMap m = span_map(ctr->kmin, ctr->kmax);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = __ldg(keys64 + i);
-        if (k != ~0ull) atomicAdd(&h[span_key(m, k) >> (kSpanKeyBits - 8)], 1u);
-    }
-    __syncthreads();
-    if (h[threadIdx.x]) atomicAdd(&ctr->slice_hist[threadIdx.x], h[threadIdx.x]);
-}
-
-// tau = the end of the smallest top-digit prefix holding >= frac * K splats
-__global__ void __launch_bounds__(256) slice_plan_kernel(FrameCounters *ctr, float frac) {
+// tau: the span key of the end of the smallest prefix of depth bins
+// (preprocess_geo's histogram of the kept depths' f64 bits) holding >= frac
+// * K splats.  Any tau gives the same frame (the split is on the span key,
+// so ties never straddle the slices); it only sets the work split.  The
+// slice's size KA is counted by the depth sort's histogram kernel.
+__global__ void __launch_bounds__(kZBins) slice_plan_kernel(FrameCounters *ctr, float frac) {
     __shared__ uint32_t s_warp[33];
     const uint32_t c = ctr->slice_hist[threadIdx.x];
     uint32_t tot;
@@ -56,15 +48,34 @@ __global__ void __launch_bounds__(256) slice_plan_kernel(FrameCounters *ctr, flo
     const uint32_t inc = ex + c;
     uint32_t target = (uint32_t)ceilf(frac * (float)tot);
     target = target < 1u ? 1u : target;
-    // the first digit whose inclusive prefix reaches the target
-    if (inc >= target && ex < target) {
-        ctr->tau = ((uint32_t)threadIdx.x << (kSpanKeyBits - 8)) |
-                   ((1u << (kSpanKeyBits - 8)) - 1u);
-        ctr->KA = inc;
+    if (inc >= target && ex < target) {  // the first bin whose prefix reaches the target
+        const int b = (int)threadIdx.x;
+        const unsigned long long end =
+            b == kZBins - 1 ? ~0ull - 1ull
+                            : ((unsigned long long)(b + 1 + kZBinBase) << kZBinShift) - 1ull;
+        const unsigned long long kmin = ctr->kmin;
+        ctr->tau = end < kmin ? 0u : span_key(span_map(kmin, ctr->kmax), end);
     }
-    if (tot == 0u && threadIdx.x == 0) {
-        ctr->tau = 0u;
-        ctr->KA = 0u;
+    if (tot == 0u && threadIdx.x == 0) ctr->tau = 0u;
+}
+
+// Per tile column c: col_prefix[c][r] = unsaturated items of column c in
+// item rows < r (from blend A's item-row bitmasks), one warp per column,
+// 32 rows per step (ballot + popc prefix).
+__global__ void __launch_bounds__(256) slice_col_prefix_kernel(SliceBArgs a) {
+    const int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= a.tiles_x || a.ctr->n_unsat == 0u) return;
+    uint32_t *col = a.col_prefix + (int64_t)c * (a.item_rows + 1);
+    if (lane == 0) col[0] = 0u;
+    uint32_t run = 0u;
+    for (int r0 = 0; r0 < a.item_rows; r0 += 32) {
+        const int r = r0 + lane;
+        const bool bit = r < a.item_rows &&
+                         ((__ldg(a.unsat_rows + (int64_t)r * a.row_words + (c >> 5)) >> (c & 31)) & 1u);
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        if (r < a.item_rows) col[r + 1] = run + (uint32_t)__popc(bal & (0xffffffffu >> (31 - lane)));
+        run += (uint32_t)__popc(bal);
     }
 }
 
@@ -86,26 +97,26 @@ __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
                 const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b);
                 int lo, hi;
                 row_range(A.y, B.w, a.height, lo, hi);
-                for (int ty = lo / kTileH; lo < hi && ty <= (hi - 1) / kTileH && !member; ty++) {
-                    const int y0 = max(lo, ty * kTileH), y1 = min(hi, ty * kTileH + kTileH);
-                    // items (pixel-row pairs) of this tile row the splat's rows meet
-                    const int w0 = (y0 - ty * kTileH) / 2, w1 = (y1 - 1 - ty * kTileH) / 2;
-                    const uint32_t im = (w1 >= 31 ? 0xffffffffu : (2u << w1) - 1u) &
-                                        ~((1u << w0) - 1u);
-                    int mn = 0, mx = a.width;
-                    if (!band_span_bound(A.x, A.y, A.z, A.w, B.x, B.y, y0, y1, a.width, mn, mx)) {
-                        mn = 0;  // ill-conditioned: every column (conservative)
-                        mx = a.width;
+                // the conservative column span of the whole row range (one
+                // bound; ill-conditioned splats: every column) against the
+                // unsaturated items' rows: item row r = pixel rows 2r, 2r+1,
+                // bit tx of word tx / 32 = the item of tile column tx
+                int mn = 0, mx = a.width;
+                if (lo < hi &&
+                    !band_span_bound(A.x, A.y, A.z, A.w, B.x, B.y, lo, hi, a.width, mn, mx)) {
+                    mn = 0;
+                    mx = a.width;
+                }
+                mn = max(mn, 0);
+                mx = min(mx, a.width);
+                if (lo < hi && mn < mx) {
+                    // unsaturated items in rows [lo/2, (hi-1)/2] of each
+                    // tile column of the span: two prefix-count loads per column
+                    const int r0 = lo >> 1, r1 = ((hi - 1) >> 1) + 1;
+                    for (int c = mn / kTileW; c <= (mx - 1) / kTileW && !member; c++) {
+                        const uint32_t *col = a.col_prefix + (int64_t)c * (a.item_rows + 1);
+                        member = __ldg(col + r1) != __ldg(col + r0);
                     }
-                    mn = max(mn, 0);
-                    mx = min(mx, a.width);
-                    if (mn >= mx) continue;
-                    const uint32_t *row = a.unsat + (int64_t)ty * a.tiles_x;
-                    for (int tx = mn / kTileW; tx <= (mx - 1) / kTileW; tx++)
-                        if (row[tx] & im) {
-                            member = true;
-                            break;
-                        }
                 }
                 if (member) out = k32;
             }
@@ -125,7 +136,7 @@ __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
 }
 
 __global__ void slice_b_decide_kernel(const FrameCounters *ctr,
-                                      cudaGraphConditionalHandle handle) {
+                                      cudaGraphConditionalHandle handle, uint32_t *class_count) {
     const uint32_t kb = ctr->KB;
     unsigned int v = kSliceClasses;  // no body: slice B is empty
     if (kb > 0) {
@@ -134,30 +145,27 @@ __global__ void slice_b_decide_kernel(const FrameCounters *ctr,
             if ((int64_t)kb <= slice_class_cap(c)) v = (unsigned int)c;
     }
     cudaGraphSetConditional(handle, v);
+    class_count[v] += 1u;  // kernel-launch accounting (single thread)
 }
 
 }  // namespace
 
-void launch_slice_plan(const unsigned long long *keys64, int64_t n, FrameCounters *ctr,
-                       float frac, int sms, cudaStream_t s, const KMark &mark) {
-    int64_t blocks = (n + 255) / 256;
-    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
-    if (blocks < 1) blocks = 1;
-    slice_hist_kernel<<<(unsigned)blocks, 256, 0, s>>>(keys64, n, ctr);
-    mark("slice_hist");
-    slice_plan_kernel<<<1, 256, 0, s>>>(ctr, frac);
+void launch_slice_plan(FrameCounters *ctr, float frac, cudaStream_t s, const KMark &mark) {
+    slice_plan_kernel<<<1, kZBins, 0, s>>>(ctr, frac);
     mark("slice_plan");
 }
 
 void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark) {
     if (a.n <= 0) return;
+    slice_col_prefix_kernel<<<(unsigned)((a.tiles_x + 7) / 8), 256, 0, s>>>(a);
+    mark("slice_col_prefix");
     slice_b_filter_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
     mark("slice_b_filter");
 }
 
 void launch_slice_b_decide(const FrameCounters *ctr, cudaGraphConditionalHandle handle,
-                           cudaStream_t s) {
-    slice_b_decide_kernel<<<1, 1, 0, s>>>(ctr, handle);
+                           uint32_t *class_count, cudaStream_t s) {
+    slice_b_decide_kernel<<<1, 1, 0, s>>>(ctr, handle, class_count);
 }
 
 }  // namespace gsr

@@ -37,7 +37,14 @@ ALPHA_MAX = 0.99
 TRANSMITTANCE_STOP = 1.0 / 255.0
 CUTOFF_SIGMA = 4.5
 TAIL_SAFETY = 32.0
-TILE_W, TILE_H = 32, 64  # tiles of the device's lists (csrc/common.cuh kTileW, kTileH)
+
+
+def tile_size() -> tuple[int, int]:
+    """(columns, rows) of the device's list tiles (csrc/common.cuh kTileW,
+    kTileH), as built into the loaded libgsr.so."""
+    w, h = ctypes.c_int(), ctypes.c_int()
+    _lib.check(_lib.load().gsr_tile_size(ctypes.byref(w), ctypes.byref(h)), "gsr_tile_size")
+    return w.value, h.value
 
 
 class EncodeFailure(RenderError):
@@ -532,7 +539,8 @@ def debug_contract_tiles(width: int, height: int, tile: int = 16, *,
 def debug_tile_ranges(width: int, height: int, *, device: int | None = None) -> np.ndarray:
     dev = _default_device if device is None else device
     ctx = _lib.context(dev)
-    n_tiles = ((width + TILE_W - 1) // TILE_W) * ((height + TILE_H - 1) // TILE_H)
+    tw, th = tile_size()
+    n_tiles = ((width + tw - 1) // tw) * ((height + th - 1) // th)
     ranges = np.empty((n_tiles, 2), dtype=np.int32)
     st = _lib.GsrStats()
     _lib.check(ctx.lib.gsr_debug_tile_lists(ctx.handle, None, None, _lib.ptr(ranges),
@@ -546,4 +554,4 @@ __all__ = ["Framebuffer", "RenderStats", "RenderError", "EncodeFailure", "Device
            "render_view", "framebuffer_to_u8", "encode_jpeg", "encode_png", "decode_image",
            "cutoff_radius_sq", "make_camera", "debug_preprocess", "debug_tile_lists",
            "debug_contract_tiles", "set_slicing",
-           "debug_tile_ranges", "Intrinsics"]
+           "debug_tile_ranges", "tile_size", "Intrinsics"]

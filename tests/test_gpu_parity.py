@@ -63,7 +63,8 @@ def _assert_lists_cover(tt, tr, ot, orr, width, max_inflation=1.05):
     superset only costs blend work: splats outside a pixel's exact interval
     are never composited) -- and at most `max_inflation` times as long as the
     contract mapped onto the device tiles."""
-    from paper_2605_08699_b200.render import TILE_H, TILE_W
+    from paper_2605_08699_b200.render import tile_size
+    TILE_W, TILE_H = tile_size()
     n16, nd = (width + 15) // 16, (width + TILE_W - 1) // TILE_W
     g = tt.astype(np.int64) * (1 << 32) + tr.astype(np.int64)
     dev_tile = (ot // n16) // (TILE_H // 16) * nd + (ot % n16) // (TILE_W // 16)

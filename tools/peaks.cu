@@ -5,8 +5,9 @@
 //         so one instruction = one op) per second
 //   fp64  DADD/DMUL per second
 //   smem  LDS.128 bytes per second
-//   issue warp instructions per second (IADD3 chains), the limit of the
-//         branchy integer/FP mix the binning and blend kernels run
+// (no issue-rate figure: an integer-chain microbenchmark measures what ptxas
+// fuses, not the issue limit; the theoretical 148 SMs x 4 schedulers x clock
+// is the denominator for the issue-bound kernels)
 // Build + run (one GPU):  nvcc -O3 -fmad=false -gencode arch=compute_100a,code=sm_100a
 //   tools/peaks.cu -o tools/_build/peaks && tools/_build/peaks > out.json
 #include <cstdio>
@@ -65,20 +66,6 @@ __global__ void smem_kernel(float *out) {
     if (acc.x + acc.y + acc.z + acc.w == 12345.0f) out[0] = acc.x;
 }
 
-__global__ void issue_kernel(int *out, int a) {
-    int x[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) x[i] = a + threadIdx.x + i;
-    for (int it = 0; it < kIters; it++) {
-#pragma unroll
-        for (int i = 0; i < 8; i++) x[i] = x[i] + (it ^ i);
-    }
-    int s = 0;
-#pragma unroll
-    for (int i = 0; i < 8; i++) s += x[i];
-    if (s == 12345) out[0] = s;
-}
-
 template <typename F>
 float time_ms(F launch) {
     cudaEvent_t e0, e1;
@@ -110,16 +97,14 @@ int main() {
     const float t32 = time_ms([&] { fp32_kernel<<<blocks, threads>>>(f, 1.0f, 0.999f); });
     const float t64 = time_ms([&] { fp64_kernel<<<blocks, threads>>>((double *)f, 1.0, 0.999); });
     const float tsm = time_ms([&] { smem_kernel<<<blocks, threads>>>(f); });
-    const float tis = time_ms([&] { issue_kernel<<<blocks, threads>>>((int *)f, 1); });
     const double fp32 = nthr * kIters * 16 / (t32 * 1e-3);
     const double fp64 = nthr * (kIters / 8) * 16 / (t64 * 1e-3);
     const double smem = nthr * kIters * 16.0 / (tsm * 1e-3);
-    const double issue = nthr / 32.0 * kIters * 8 / (tis * 1e-3);
     std::printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f, \"fp32_tops\": %.2f, \"fp64_tops\": %.2f, "
-                "\"smem_tbs\": %.2f, \"warp_inst_per_s_e12\": %.3f, "
+                "\"smem_tbs\": %.2f, "
                 "\"how\": \"tools/peaks.cu: 148x8 CTAs x 256 thr; fp32/fp64 = FMUL+FADD chains "
-                "(8 independent per thread, no FMA), smem = LDS.128 bytes, issue = IADD3 chains; "
+                "(8 independent per thread, no FMA), smem = LDS.128 bytes; "
                 "best of 5, CUDA events\"}\n",
-                sms, clk / 1000.0, fp32 / 1e12, fp64 / 1e12, smem / 1e12, issue / 1e12);
+                sms, clk / 1000.0, fp32 / 1e12, fp64 / 1e12, smem / 1e12);
     return 0;
 }

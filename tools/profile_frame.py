@@ -3,8 +3,13 @@ range "frame" so captures can select exactly one whole frame:
 
     ncu --nvtx --nvtx-include "frame/" ... python tools/profile_frame.py [n_frames] [workload]
 """
+import os
 import sys
 from pathlib import Path
+
+# ncu cannot profile the kernel nodes of graphs with conditional nodes:
+# direct launches (same kernels, slice B sized on the host)
+os.environ.setdefault("GSR_GRAPHS", "0")
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch  # noqa: E402  (NVTX markers only)
