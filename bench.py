@@ -403,7 +403,8 @@ def kernel_work(name, wl, c):
     sliced = c["KB"] > 0 or c["KA"] < k
     table = {
         # mean/scale/rotation/rsq f64 + opacity f32 in; key for all N; record of kept
-        "preprocess_geo": (n * 92 + n * 8 + k * 32, 0),
+        # (+ the 8 B item box of each kept splat when the frame is sliced)
+        "preprocess_geo": (n * 92 + n * 8 + k * 32 + (k * 8 if sliced else 0), 0),
         # order + mean f64 + SH row (or DC) of each ranked splat in; colour out
         "color_ranked": (ks * (4 + 24 + sh_bytes + 16), 0),
         # one pass: f64 depth key of all N in, span key out; slice A: f64 key
@@ -412,8 +413,8 @@ def kernel_work(name, wl, c):
         "radix32_hist": ((n * 8 + c["KA"] * 8 + c["KB"] * 4) if sliced else n * 12, 0),
         "radix32_pass": (3 * ks * 16, 0),  # per pass: key + index read and written
         "depth_fixup": (ks * 4, 0),
-        # depth key of all N; record of each kept splat behind the front slice
-        "slice_b_filter": (n * 8 + max(k - c["KA"], 0) * 32, 0),
+        # depth key of all N; item box of each kept splat behind the front slice
+        "slice_b_filter": (n * 8 + max(k - c["KA"], 0) * 8, 0),
         # order + geometry gathered, 32 B record written
         "bin_gather": (ks * (4 + 32 + 32), 0),
         # records in, pairs out; 20 FP32 ops per exact row interval (render.py:383-397)

@@ -40,7 +40,13 @@ namespace {
 
 constexpr int BR = 512;          // depth ranks per block (stages 1a, 1c)
 constexpr int kPairCache = 6144; // per-block pair results kept in smem (1c)
-constexpr int kSeg = 1024;       // pairs per segment (stage 2)
+#ifndef GSR_BIN_SEG
+#define GSR_BIN_SEG 256
+#endif
+// pairs per segment (stage 2): 256 gives seg_place ~7k warps of work at
+// config 3 (1024: ~1.7k, 12 warps per SM): 0.049 -> 0.033 ms, one-call
+// device p50 1.005 -> 0.960 ms (512: 0.036 / 0.975)
+constexpr int kSeg = GSR_BIN_SEG;
 constexpr int kRowsMax = kMaxTileRows;
 
 __device__ __forceinline__ bool overflowed(const BinArgs &a) {
@@ -415,19 +421,11 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(BinArgs a) {
 }
 
 // ---------------------------------------------------------------- 2d -------
-__device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64_t nseg,
-                                              uint32_t *cur, int lane) {
-    const int tx_n = a.tiles_x;
-    uint32_t *mask = cur + tx_n;
-    __syncwarp();  // the warp's previous segment is done with cur / mask
-    uint32_t ty, p0, p1;
-    seg_bounds(a, g, nseg, ty, p0, p1);
-    const uint32_t *tstart = a.tile_start + (int64_t)ty * tx_n;
-    for (int t = lane; t < tx_n; t += 32) {
-        cur[t] = tstart[t] + a.seg_cnt[g * tx_n + t];
-        mask[t] = 0;
-    }
-    __syncwarp();
+// One warp places pairs [p0, p1) of one tile row, in rank order: cur[t] is
+// the next free slot of tile column t's list, mask[t] (zeroed) a scratch
+// coverage mask (both warp-private shared memory).
+__device__ __forceinline__ void place_pairs(const BinArgs &a, uint32_t p0, uint32_t p1,
+                                            uint32_t *cur, uint32_t *mask, int lane) {
     const uint32_t lt_mask = (1u << lane) - 1u;
     // software pipeline: the next chunks' pairs are in flight while this
     // chunk is placed (the loop is otherwise bound by that load's latency)
@@ -506,6 +504,143 @@ __device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64
     }
 }
 
+__device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64_t nseg,
+                                              uint32_t *cur, int lane) {
+    const int tx_n = a.tiles_x;
+    uint32_t *mask = cur + tx_n;
+    __syncwarp();  // the warp's previous segment is done with cur / mask
+    uint32_t ty, p0, p1;
+    seg_bounds(a, g, nseg, ty, p0, p1);
+    const uint32_t *tstart = a.tile_start + (int64_t)ty * tx_n;
+    for (int t = lane; t < tx_n; t += 32) {
+        cur[t] = tstart[t] + a.seg_cnt[g * tx_n + t];
+        mask[t] = 0;
+    }
+    __syncwarp();
+    place_pairs(a, p0, p1, cur, mask, lane);
+}
+
+// ------------------------------------------------ small slices: 2a-2d fused --
+// One CTA per tile row builds that row's tile lists from its pairs (a small
+// second slice has few pairs per row, so the segment table, the per-segment
+// counts, the two scans and the placement -- five kernels -- become one):
+// the row's pairs are cut into one contiguous chunk per warp; each warp counts
+// its chunk's keys per tile column (difference array); a prefix over the
+// warps gives each warp its first slot per column; the row's region of the
+// list buffer is taken with one atomicAdd (rows land in any order -- the
+// lists are addressed through ranges -- but each list holds its ranks in
+// increasing order); each warp places its chunk (place_pairs).
+constexpr int kRowWarps = 8;
+// [kRowWarps][tiles_x + 1] counts, [kRowWarps][2][tiles_x] cursors + masks,
+// [tiles_x] column totals -> row starts
+__host__ __device__ inline size_t row_lists_smem_bytes(int tiles_x) {
+    return sizeof(uint32_t) * ((size_t)kRowWarps * (3 * (size_t)tiles_x + 1) + (size_t)tiles_x);
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32) bin_rows_kernel(BinArgs a) {
+    extern __shared__ __align__(16) uint32_t row_smem[];
+    __shared__ uint32_t s_base, s_last;
+    const int tx_n = a.tiles_x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ty = blockIdx.x;
+    uint32_t *cnt = row_smem + w * (tx_n + 1);                   // [w][tx_n + 1]
+    uint32_t *cur = row_smem + kRowWarps * (tx_n + 1) + w * 2 * tx_n;
+    uint32_t *mask = cur + tx_n;
+    const bool ov_p = a.ctr->P > (unsigned long long)a.cap_p;
+    uint32_t p0 = 0, p1 = 0;
+    if (!ov_p) {
+        p0 = a.row_start[ty];
+        p1 = a.row_start[ty + 1];
+    }
+    // warp w's chunk of the row's pairs
+    const uint32_t per = (p1 - p0 + kRowWarps - 1) / kRowWarps;
+    const uint32_t c0 = min(p1, p0 + per * w), c1 = min(p1, c0 + per);
+    for (int t = lane; t <= tx_n; t += 32) cnt[t] = 0;
+    __syncwarp();
+    for (uint32_t p = c0 + lane; p < c1; p += 32) {
+        const uint32_t sp = a.pairs[p].y, c = sp >> 16;
+        if (c) {
+            atomicAdd(&cnt[sp & 0xffffu], 1u);
+            atomicSub(&cnt[(sp & 0xffffu) + c], 1u);
+        }
+    }
+    __syncwarp();
+    {   // difference array -> keys per column of this warp's chunk
+        uint32_t carry = 0;
+        for (int t0 = 0; t0 < tx_n; t0 += 32) {
+            const int t = t0 + lane;
+            const uint32_t inc = warp_incl_scan_u32(t < tx_n ? cnt[t] : 0u) + carry;
+            if (t < tx_n) cnt[t] = inc;
+            carry = __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    __syncthreads();
+    // per column: exclusive prefix over the warps (in place), column totals
+    uint32_t *tot = row_smem + kRowWarps * (tx_n + 1) + 2 * tx_n * kRowWarps;  // [tx_n]
+    for (int t = threadIdx.x; t < tx_n; t += blockDim.x) {
+        uint32_t run = 0;
+        for (int j = 0; j < kRowWarps; j++) {
+            uint32_t *cj = row_smem + j * (tx_n + 1);
+            const uint32_t v = cj[t];
+            cj[t] = run;
+            run += v;
+        }
+        tot[t] = run;
+    }
+    __syncthreads();
+    // column totals -> exclusive prefix across the row (one warp), region
+    if (w == 0) {
+        uint32_t carry = 0;
+        for (int t0 = 0; t0 < tx_n; t0 += 32) {
+            const int t = t0 + lane;
+            const uint32_t v = t < tx_n ? tot[t] : 0u;
+            const uint32_t inc = warp_incl_scan_u32(v) + carry;
+            if (t < tx_n) tot[t] = inc - v;  // exclusive start within the row
+            carry = __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) {
+            s_base = carry ? atomicAdd(&a.ctr->Drow, carry) : 0u;
+            const uint32_t end = s_base + carry;
+            // ranges: empty if the region does not fit (the frame re-renders)
+            const bool fits = (int64_t)end <= a.cap_d;
+            s_last = fits ? 1u : 0u;
+        }
+        __syncwarp();
+        const bool fits = s_last != 0u;
+        const uint32_t base = s_base;
+        for (int t0 = 0; t0 < tx_n; t0 += 32) {
+            const int t = t0 + lane;
+            if (t < tx_n) {
+                const uint32_t st = base + tot[t];
+                const uint32_t en = t + 1 < tx_n ? base + tot[t + 1] : base + carry;
+                a.ranges[(int64_t)ty * tx_n + t] = fits ? make_uint2(st, en) : make_uint2(0u, 0u);
+            }
+        }
+    }
+    __syncthreads();
+    if (s_last && c0 < c1) {
+        const uint32_t *cw = row_smem + w * (tx_n + 1);
+        for (int t = lane; t < tx_n; t += 32) {
+            cur[t] = s_base + tot[t] + cw[t];
+            mask[t] = 0;
+        }
+        __syncwarp();
+        place_pairs(a, c0, c1, cur, mask, lane);
+    }
+    // the last row to finish publishes the pass's list total
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&a.ctr->rows_done, 1u) + 1u == gridDim.x) {
+            const unsigned long long d = atomicAdd(&a.ctr->Drow, 0u);
+            a.ctr->D = (uint32_t)d;
+            a.ctr->Dtot += d;
+            a.ctr->Dmax = d > a.ctr->Dmax ? d : a.ctr->Dmax;
+            if ((int64_t)d > a.cap_d) atomicAdd(a.overflow_sticky, 1u);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
     // per warp: column cursors [tiles_x] and coverage masks [tiles_x]
     extern __shared__ __align__(16) uint32_t place_smem[];
@@ -535,10 +670,13 @@ cudaError_t binning_init_attributes() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(seg_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(8 * 2 * kMaxTilesX * sizeof(uint32_t)));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(bin_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)row_lists_smem_bytes(kMaxTilesX));
     return e;
 }
 
-int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark) {
+int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark, bool rows) {
     if (a.n_blocks <= 0) return 0;
     const unsigned nb = (unsigned)a.n_blocks;
     bin_gather_kernel<<<nb, BR, 0, s>>>(a);
@@ -549,6 +687,11 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark) {
     mark("row_scan");
     bin_pairs_kernel<<<nb, BR, pair_smem_bytes(a.n_rows), s>>>(a);
     mark("bin_pairs");
+    if (rows) {  // small slice: one CTA per tile row builds the row's lists
+        bin_rows_kernel<<<(unsigned)a.n_rows, kRowWarps * 32, row_lists_smem_bytes(a.tiles_x), s>>>(a);
+        mark("bin_rows");
+        return 4;
+    }
     seg_table_kernel<<<1, 1024, 0, s>>>(a);
     mark("seg_table");
     // segment kernels loop over the frame's segments: the grid covers the

@@ -129,7 +129,7 @@ struct gsr_ctx {
     DevBuf frame_u8, frame_rgb, frame_t;
     DevBuf colr;          // colours by depth rank of the current pass
     // depth-sliced frames: pixel state after slice A, unsaturated items (bits, list)
-    DevBuf state, unsat_rows, unsat_items, col_prefix;
+    DevBuf state, unsat_rows, unsat_items, col_prefix, ibox;
     DevBuf params;        // FrameParams of the frame being rendered
     // CUDA graphs of this context's frame configurations (record_frame)
     static constexpr int kMaxGraphs = 32;
@@ -192,7 +192,7 @@ struct gsr_ctx {
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &colr, &state, &unsat_rows, &unsat_items, &col_prefix, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
+                               &geo, &colr, &state, &unsat_rows, &unsat_items, &col_prefix, &ibox, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
@@ -327,8 +327,9 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         ss.unsat_items = c->unsat_items.as<uint32_t>();
     }
     // one depth-ordered pass over *count splats (at most cap): sort, colour, bin
+    // rows: small second slices build their lists with one CTA per tile row
     auto sort_color_bin = [&](cudaStream_t st, uint32_t *count, const uint32_t *limit,
-                              bool keys_given, int64_t cap) {
+                              bool keys_given, int64_t cap, bool rows = false) {
         DepthArgs da;
         for (int i = 0; i < 2; i++) {
             da.keys64[i] = c->keys[i].as<unsigned long long>();
@@ -380,7 +381,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         ba.tile_vals = c->tile_vals.as<uint32_t>();
         ba.cap_d = c->cap_d;
         ba.overflow_sticky = c->dsticky();
-        launches += launch_binning(ba, st, mark);
+        launches += launch_binning(ba, st, mark, rows);
     };
     auto blend_on = [&](cudaStream_t st, int mode, const SliceState &sst) {
         launch_blend(c->srec.as<SplatRec>(), c->colr.as<float4>(), c->tile_vals.as<uint32_t>(),
@@ -404,7 +405,8 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
     if (n > 0) {
         launch_preprocess_geo(sc->view, dfp, cull, c->keys[0].as<unsigned long long>(),
                               c->geo.as<GeoRec>(), want_keep ? c->keep.as<uint8_t>() : nullptr,
-                              ctr, slice ? ctr->slice_hist : nullptr, s, mark);
+                              ctr, slice ? ctr->slice_hist : nullptr,
+                              slice ? c->ibox.as<uint2>() : nullptr, s, mark);
         launches += 1;
         if (slice) {
             launch_slice_plan(ctr, c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac(), s,
@@ -437,6 +439,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         SliceBArgs sb;
         sb.keys64 = c->keys[0].as<unsigned long long>();
         sb.geo = c->geo.as<GeoRec>();
+        sb.ibox = c->ibox.as<uint2>();
         sb.n = n;
         sb.ctr = ctr;
         sb.unsat_rows = c->unsat_rows.as<uint32_t>();
@@ -485,7 +488,8 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
                                                           cudaStreamCaptureModeThreadLocal));
                 const int before = launches;
                 if (k < kSliceClasses)
-                    sort_color_bin(c->cap_stream, &ctr->KB, nullptr, true, class_cap(k));
+                    sort_color_bin(c->cap_stream, &ctr->KB, nullptr, true, class_cap(k),
+                                   k < kSliceClasses - 1);
                 blend_on(c->cap_stream, 2, ss);
                 c->body_launches[k] = launches - before;
                 launches = before;  // counted per frame from the device's class counters
@@ -504,7 +508,8 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
             int k = kSliceClasses - 1;
             for (int j = kSliceClasses - 2; j >= 0; j--)
                 if ((int64_t)kb <= slice_class_cap(j)) k = j;
-            if (kb > 0) sort_color_bin(s, &ctr->KB, nullptr, true, class_cap(k));
+            if (kb > 0)
+                sort_color_bin(s, &ctr->KB, nullptr, true, class_cap(k), k < kSliceClasses - 1);
             blend_on(s, 2, ss);
         }
     }
@@ -631,6 +636,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
         if ((rc = cens(c, c->state, sizeof(float4) * (size_t)W * H))) return rc;
         if ((rc = cens(c, c->unsat_rows, unsat_rows_bytes(W, H)))) return rc;
+        if ((rc = cens(c, c->ibox, sizeof(uint2) * (size_t)std::max<int64_t>(n, 1)))) return rc;
         if ((rc = cens(c, c->col_prefix, sizeof(uint32_t) * (size_t)((W + kTileW - 1) / kTileW) *
                                              (size_t)(unsat_item_rows(H) + 1))))
             return rc;
@@ -991,6 +997,11 @@ int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means
         plane_f(L.dc, colors_dc, k, 3);
     }
     for (int k = 0; k < 4; k++) plane_d(L.rot, rotations, k, 4);
+    {
+        double *m4 = reinterpret_cast<double *>(host.data() + L.mean4);
+        for (int64_t i = 0; i < n; i++)
+            for (int k = 0; k < 3; k++) m4[4 * i + k] = means[i * 3 + k];
+    }
     plane_f(L.opac, opacities, 0, 1);
     plane_d(L.op64, opacities, 0, 1);
     if (rsq) plane_d(L.rsq, rsq, 0, 1);

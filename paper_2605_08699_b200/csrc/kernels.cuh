@@ -34,7 +34,9 @@ struct FrameCounters {
     unsigned long long Rb;      // blend: (splat, pixel row) interval evaluations
     unsigned long long Rp;      // binning: (splat, pixel row) interval evaluations
     uint32_t blend_next;        // blend work queue: next (tile, pixel-row pair) item
-    uint32_t pad2;
+    uint32_t rows_done;         // small-slice binning: tile rows whose lists are built
+    uint32_t Drow;              // small-slice binning: list entries allocated (region cursor)
+    uint32_t pad3;
     // blend instrumentation (counting variant only; gsr_debug_frame_counters)
     unsigned long long b_walked;   // list entries loaded by items (all items of all tiles)
     unsigned long long b_hit;      // ... of which the splat's row range meets the item's rows
@@ -91,6 +93,9 @@ struct SceneView {
                           // coefficient k*3 + c; rows so a gather by depth rank reads
                           // whole sectors (colour only for the splats a pass blends)
     const double *op64;   // [stride]     f64 opacity (rsq, read-back)
+    const double *mean4;  // [stride][4]  (x, y, z, 0): the means again, one 32 B sector per
+                          // Gaussian for the colour kernel's gather by depth rank (three
+                          // planes would cost three 64 B DRAM accesses for 24 B)
     int sh_f32;
 };
 
@@ -126,10 +131,31 @@ void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 // K1a: projection, culling, depth keys, packed geometry (render.py:163-290)
 // zhist (depth-sliced frames, else null): += histogram of the kept depths
 // over kZBins bins of their f64 bits (slice_plan's input)
+// ibox (depth-sliced frames, else null): item_box of every kept splat
 void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
-                           FrameCounters *ctr, uint32_t *zhist, cudaStream_t s,
+                           FrameCounters *ctr, uint32_t *zhist, uint2 *ibox, cudaStream_t s,
                            const KMark &mark = KMark());
+
+// A kept splat's conservative box in work-item units, for the slice-B
+// filter: item rows [r0, r1] (pixel rows 2r, 2r + 1) from the reference's
+// own row range (render.py:329-333, row_range), tile columns [c0, c1] from
+// the whole splat's column extent (splat_x_extent; ill-conditioned: every
+// column).  Packed (r0 | r1 << 16, c0 | c1 << 16); empty: r0 > r1.
+__device__ __forceinline__ uint2 item_box(const GeoRec &g, int width, int height) {
+    int lo, hi;
+    row_range(g.a.y, g.b.w, height, lo, hi);
+    if (lo >= hi || width <= 0) return make_uint2(0xffffu, 0u);
+    int mn = 0, mx = width;
+    float xl, xr;
+    if (splat_x_extent(g.a.x, g.a.z, g.a.w, g.b.x, g.b.y, g.b.w, xl, xr)) {
+        mn = max(__float2int_rd(xl), 0);
+        mx = (int)fminf(ceilf(xr) + 1.0f, (float)width);
+    }
+    if (mn >= mx) return make_uint2(0xffffu, 0u);
+    return make_uint2((uint32_t)(lo >> 1) | ((uint32_t)((hi - 1) >> 1) << 16),
+                      (uint32_t)(mn / kTileW) | ((uint32_t)((mx - 1) / kTileW) << 16));
+}
 // depth histogram bins: bin = clamp((bits(z) >> 47) - kZBinBase, 0, 1023),
 // 32 bins per binade (sign, 11 exponent and 5 mantissa bits) over z in
 // [2^-8, 2^24)
@@ -232,8 +258,12 @@ int64_t bin_blocks(int64_t n_cap);
 int64_t bin_scan_tiles(int64_t n_blocks, int n_rows);
 int64_t bin_segments(int64_t cap_p, int n_rows);
 cudaError_t binning_init_attributes();
-int launch_binning(const BinArgs &a, cudaStream_t s,
-                   const KMark &mark = KMark());  // returns kernels launched
+// rows: the small-slice variant -- one CTA per tile row builds the row's
+// lists (bin_rows_kernel) instead of the segment kernels; the list regions
+// are allocated from FrameCounters.Drow / rows_done (zeroed per frame: one
+// rows pass per frame)
+int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark = KMark(),
+                   bool rows = false);  // returns kernels launched
 
 
 // contract.cu: the exact tile-list contract on tile x tile tiles via
@@ -290,6 +320,7 @@ struct SliceBArgs {
     const GeoRec *geo;                 // records by Gaussian index
     int64_t n;
     FrameCounters *ctr;                // kmin, kmax, tau; KB counted here
+    const uint2 *ibox;                 // item_box of each kept splat (preprocess_geo)
     const uint32_t *unsat_rows;        // [item rows][row_words] items slice A left unsaturated
     int row_words, item_rows;
     uint32_t *col_prefix;              // [tiles_x][item_rows + 1] (slice_b_filter's first kernel)

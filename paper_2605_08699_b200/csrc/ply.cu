@@ -268,6 +268,7 @@ struct PlyCols {
 
 struct PlyOut {
     double *mean, *scale, *rot, *rsq, *op64;
+    double *mean4;  // [stride][4] (x, y, z, 0): the colour kernel's gather copy
     float *opac, *dc, *sh;
     int64_t stride;
 };
@@ -313,12 +314,17 @@ __global__ void __launch_bounds__(kPlyThreads) ply_activate_kernel(
         const int64_t st = o.stride;
         auto at = [&](int c) { return row[cols.c[c]]; };
         // raw attributes (model.py:190-203)
+        double m4[4];
 #pragma unroll
         for (int k = 0; k < 3; k++) {
             const float v = at(k);
             if (!finite32(v)) bad |= kBadMeans;
             o.mean[k * st + g] = (double)v;
+            m4[k] = (double)v;
         }
+        m4[3] = 0.0;
+        reinterpret_cast<double2 *>(o.mean4 + 4 * g)[0] = make_double2(m4[0], m4[1]);
+        reinterpret_cast<double2 *>(o.mean4 + 4 * g)[1] = make_double2(m4[2], m4[3]);
         float ls[3], q[4], dc[3];
 #pragma unroll
         for (int k = 0; k < 3; k++) {
@@ -566,6 +572,7 @@ int scene_create_ply(gsr_scene **out, int device, const uint8_t *data, int64_t l
     unsigned char *d = sc->block.as<unsigned char>();
     PlyOut o;
     o.mean = reinterpret_cast<double *>(d + L.mean);
+    o.mean4 = reinterpret_cast<double *>(d + L.mean4);
     o.scale = reinterpret_cast<double *>(d + L.scale);
     o.rot = reinterpret_cast<double *>(d + L.rot);
     o.rsq = reinterpret_cast<double *>(d + L.rsq);

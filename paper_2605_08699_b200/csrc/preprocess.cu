@@ -74,7 +74,9 @@ __global__ void __launch_bounds__(256) frame_init_kernel(FrameCounters *ctr) {
     ctr->Rb = 0ull;
     ctr->Rp = 0ull;
     ctr->blend_next = 0;
-    ctr->pad2 = 0;
+    ctr->rows_done = 0u;
+    ctr->Drow = 0u;
+    
     ctr->b_walked = ctr->b_hit = ctr->b_batches = ctr->b_iters = ctr->b_lanes = 0ull;
     ctr->b_items = ctr->b_used = 0ull;
     ctr->KA = ctr->KB = ctr->tau = ctr->n_unsat = 0u;
@@ -89,7 +91,8 @@ __global__ void frame_params_kernel(FrameParams p, FrameParams *dst) { *dst = p;
 __global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
     SceneView sc, const FrameParams *__restrict__ fp, int do_cull,
     unsigned long long *__restrict__ keys, GeoRec *__restrict__ geo,
-    uint8_t *__restrict__ keep_out, FrameCounters *ctr, uint32_t *__restrict__ zhist) {
+    uint8_t *__restrict__ keep_out, FrameCounters *ctr, uint32_t *__restrict__ zhist,
+    uint2 *__restrict__ ibox) {
     __shared__ CameraArgs cam;  // this frame's camera (FrameParams), staged once per block
     __shared__ uint32_t s_zh[kZBins];
     if (zhist)
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
                 o.a = make_float4((float)u, (float)v, ia32, (float)(-cb / det));
                 o.b = make_float4((float)(ca / det), (float)rsq, opac, (float)sqrt(cc * rsq));
                 geo[i] = o;
+                if (ibox) ibox[i] = item_box(o, cam.iwidth, cam.iheight);
             }
         }
         keys[i] = key;
@@ -228,8 +232,11 @@ __global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
 // every load before any arithmetic (one memory round trip).  Only the ranks
 // a pass sorted are coloured, so splats behind the front slice that no
 // unsaturated pixel reaches never read their 192 B of SH.
+#ifndef GSR_COLOR_MINB
+#define GSR_COLOR_MINB 1
+#endif
 template <typename ShT, int DEG>
-__global__ void __launch_bounds__(256) color_ranked_kernel(
+__global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
     SceneView sc, const FrameParams *__restrict__ fp, DepthOrder ord,
     const uint32_t *__restrict__ count, float4 *__restrict__ colr) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -266,8 +273,8 @@ __global__ void __launch_bounds__(256) color_ranked_kernel(
 #pragma unroll
             for (int k = 0; k < NC; k++) v[k] = (ShT)((k & 1) ? q[k >> 1].y : q[k >> 1].x);
         }
-        const double mx = __ldg(sc.mean + i), my = __ldg(sc.mean + st + i),
-                     mz = __ldg(sc.mean + 2 * st + i);
+        const double2 m01 = __ldg(reinterpret_cast<const double2 *>(sc.mean4 + 4 * i));
+        const double mx = m01.x, my = m01.y, mz = __ldg(sc.mean4 + 4 * i + 2);
         const double dx = mx - cam.campos[0];
         const double dy = my - cam.campos[1];
         const double dz = mz - cam.campos[2];
@@ -297,13 +304,13 @@ const void *frame_params_kernel_fn() { return (const void *)frame_params_kernel;
 
 void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,
-                           FrameCounters *ctr, uint32_t *zhist, cudaStream_t s,
+                           FrameCounters *ctr, uint32_t *zhist, uint2 *ibox, cudaStream_t s,
                            const KMark &mark) {
     if (scene.n == 0) return;
     const int threads = 256;
     const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
     preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, fp, frustum_cull, keys, geo,
-                                                     keep_out, ctr, zhist);
+                                                     keep_out, ctr, zhist, ibox);
     mark("preprocess_geo");
 }
 

@@ -44,7 +44,7 @@ struct DeviceGuard {
 // Planar scene layout (one device block, 256-B aligned planes of `stride`
 // elements): see SceneView (kernels.cuh) for the plane types.
 struct SceneLayout {
-    size_t mean, scale, rot, rsq, opac, dc, op64, sh, total;
+    size_t mean, scale, rot, rsq, opac, dc, op64, sh, mean4, total;
 };
 
 inline SceneLayout scene_layout(int64_t stride, bool has_sh, bool sh_f32) {
@@ -64,6 +64,7 @@ inline SceneLayout scene_layout(int64_t stride, bool has_sh, bool sh_f32) {
     L.dc = take(3 * st * 4);
     L.op64 = take(st * 8);
     L.sh = take(has_sh ? 48 * st * (sh_f32 ? 4 : 8) : 16);
+    L.mean4 = take(4 * st * 8);
     L.total = off;
     return L;
 }
@@ -93,6 +94,7 @@ struct gsr_scene {
         view.dc = reinterpret_cast<const float *>(d + L.dc);
         view.op64 = reinterpret_cast<const double *>(d + L.op64);
         view.sh = d + L.sh;
+        view.mean4 = reinterpret_cast<const double *>(d + L.mean4);
         view.sh_f32 = sh_f32;
     }
 };

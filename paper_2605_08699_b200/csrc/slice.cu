@@ -16,8 +16,8 @@
 //      final pixels, any other item saves its pixels' (T, r, g, b) and sets
 //      its bit in the unsaturated-item rows.
 //   B  the rest: a splat behind the slice is kept only if its conservative
-//      column span (band_span_bound, the binning's own bound, over its whole
-//      row range) meets an unsaturated item in one of its rows (blend A
+//      box in item rows x tile columns (item_box: the reference's row range,
+//      the whole splat's column extent) meets an unsaturated item (blend A
 //      marks each unsaturated item in a per-item-row bitmask over the tile
 //      columns; per tile column, a prefix count over the item rows answers
 //      "any unsaturated item in rows [r0, r1)" with two loads); those are
@@ -94,30 +94,16 @@ __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
             const SpanMap m = span_map(a.ctr->kmin, a.ctr->kmax);
             const uint32_t k32 = span_key(m, k64);
             if (k32 > a.ctr->tau) {
-                const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b);
-                int lo, hi;
-                row_range(A.y, B.w, a.height, lo, hi);
-                // the conservative column span of the whole row range (one
-                // bound; ill-conditioned splats: every column) against the
-                // unsaturated items' rows: item row r = pixel rows 2r, 2r+1,
-                // bit tx of word tx / 32 = the item of tile column tx
-                int mn = 0, mx = a.width;
-                if (lo < hi &&
-                    !band_span_bound(A.x, A.y, A.z, A.w, B.x, B.y, lo, hi, a.width, mn, mx)) {
-                    mn = 0;
-                    mx = a.width;
-                }
-                mn = max(mn, 0);
-                mx = min(mx, a.width);
-                if (lo < hi && mn < mx) {
-                    // unsaturated items in rows [lo/2, (hi-1)/2] of each
-                    // tile column of the span: two prefix-count loads per column
-                    const int r0 = lo >> 1, r1 = ((hi - 1) >> 1) + 1;
-                    for (int c = mn / kTileW; c <= (mx - 1) / kTileW && !member; c++) {
+                // the splat's box in item rows x tile columns (item_box,
+                // written by preprocess_geo) against the unsaturated items:
+                // per tile column, two loads of the prefix counts over item rows
+                const uint2 bx = __ldg(a.ibox + i);
+                const uint32_t r0 = bx.x & 0xffffu, r1 = (bx.x >> 16) + 1u;
+                if (r0 < r1)
+                    for (uint32_t c = bx.y & 0xffffu; c <= (bx.y >> 16) && !member; c++) {
                         const uint32_t *col = a.col_prefix + (int64_t)c * (a.item_rows + 1);
                         member = __ldg(col + r1) != __ldg(col + r0);
                     }
-                }
                 if (member) out = k32;
             }
         }

@@ -138,4 +138,6 @@ def _scene_bytes(prims) -> int:
     n = int(prims.means.shape[0])
     stride = (max(n, 1) + 31) // 32 * 32
     sh = getattr(prims, "sh_coeffs", None)
-    return stride * (11 * 8 + 4 + 12 + 8 + (192 if sh is not None else 0))
+    # means/scales/rotations/rsq f64, opacity + dc f32, opacity f64, the (x, y, z, 0)
+    # f64 gather copy of the means, f32 SH rows
+    return stride * (11 * 8 + 4 + 12 + 8 + 32 + (192 if sh is not None else 0))

@@ -29,7 +29,7 @@ def main():
     frames = int(sys.argv[2]) if len(sys.argv) > 2 else 10
     wl = bench.WORKLOADS[wl_name]
     from paper_2605_08699_b200 import _lib
-    from paper_2605_08699_b200.render import _bg, device_scene, make_camera
+    from paper_2605_08699_b200.render import _bg, device_scene, make_camera, tile_size
     prims = bench.build_scene(wl)
     intr = bench.intrinsics(wl)
     poses = bench.poses_for(0, frames + 3)
@@ -54,7 +54,8 @@ def main():
                                   None, None, ctypes.byref(st)))
         _lib.check(lib.gsr_debug_frame_counters(ctx.handle, out, 15))
         rows.append([int(x) for x in out])
-        n_items = ((intr.width + 31) // 32) * ((intr.height + 63) // 64) * 32
+        tw, th = tile_size()
+        n_items = ((intr.width + tw - 1) // tw) * ((intr.height + th - 1) // th) * (th // 2)
         info = np.empty(n_items, dtype=np.uint32)
         _lib.check(lib.gsr_debug_blend_items(ctx.handle, info.ctypes.data, n_items))
         items.append(info)
@@ -77,6 +78,9 @@ def main():
         "composites_per_iteration": m["E"] / iters,
         "composites_per_batch": m["E"] / m["batches"],
         "splats_colour_read_fraction_of_K": m["used"] / m["K"],
+        "tile": list(tile_size()),
+        "slices": {"KA": m["KA"], "KB": m["KB"],
+                   "note": "counters sum both slices of a depth-sliced frame"},
     }
     sat = np.concatenate([(x >> 31) == 1 for x in items])
     last = np.concatenate([(x & 0x7fffffff) for x in items]).astype(np.float64)
