@@ -685,7 +685,7 @@ def run_gsr(args, wl):
 
     # the north-star binning design on 16x16 tiles ((tile|rank) keys, radix
     # sort, ranges: contract.cu), timed on the same frames beside the render
-    # path's sort-free 32x64 binning
+    # path's sort-free 32x16 binning
     contract = contract_profile(ctx, lib, sc, cams[W:], wl, bg, min(K, 10))
 
     # config 3's full ABR ladder: base + 3 rungs rendered, upsampled, SSIM-scored
@@ -827,7 +827,7 @@ def contract_profile(ctx, lib, sc, cams, wl, bg, frames):
             "render_path_binning_ms": float(np.mean(binning)),
             "what": "exact 16x16 contract, north-star item (2): (tile|rank) u64 keys, "
                     "Onesweep radix sort, range identification (SURVEY 8d B_sort = 24K + 28D), "
-                    "from the depth-ranked records; the render path's sort-free 32x64 binning "
+                    "from the depth-ranked records; the render path's sort-free 32x16 binning "
                     "stage (gather + pairs + lists) of the same frames beside it"}
 
 

@@ -195,7 +195,7 @@ GSR_API int gsr_ctx_kernel_times(gsr_ctx *ctx, int max, char *names, float *ms, 
 
 /* ---- the hot path: render_framebuffer (render.py:516-524) ----------------
  * project (render.py:163-290) -> stable f64 depth sort (293-302) -> tile
- * lists in depth order (32x64 device tiles) -> front-to-back blend
+ * lists in depth order (32x16 device tiles) -> front-to-back blend
  * (430-473) -> u8 (484-485).  Outputs are optional host buffers:
  *   out_u8   (H,W,3) u8   = framebuffer_to_u8(fb); page-locked memory with
  *                           W % 32 == 0 is written by the blend kernel
@@ -241,7 +241,7 @@ GSR_API int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_
  * interval, render.py:329-333 + 384-397, reaching that tile column) of the
  * last render on ctx, built on the device from 64-bit (tile | rank) keys, a
  * radix sort and per-tile range identification (north_star item 2).  The
- * render path itself blends from conservative 32 x 64 superset lists
+ * render path itself blends from conservative 32 x 16 superset lists
  * (gsr_debug_tile_lists); this entry exists so the contract can be compared
  * bit for bit with the reference's rows.  First call (outputs NULL) builds
  * the lists and returns *out_count = D; later calls for the same frame and
@@ -259,7 +259,7 @@ GSR_API int gsr_debug_tile_lists(gsr_ctx *ctx, int32_t *out_tiles, int32_t *out_
  * need GSR_TIMING_COUNTERS; D and P are summed over the slices. */
 #define GSR_NCOUNTERS 16
 GSR_API int gsr_debug_frame_counters(gsr_ctx *ctx, uint64_t *out, int n);
-/* Per blend work item (tile-major, 32 items of two pixel rows per 32 x 64
+/* Per blend work item (tile-major, 8 items of two pixel rows per 32 x 16
  * tile) of the last frame rendered with GSR_TIMING_COUNTERS: the deepest
  * depth rank it walked, | 1 << 31 if all its pixels saturated (T < 1/255). */
 GSR_API int gsr_debug_blend_items(gsr_ctx *ctx, uint32_t *out, int64_t n);

@@ -1,4 +1,4 @@
-// blend.cu -- K6: per-tile (32x64) front-to-back alpha blending.
+// blend.cu -- K6: per-tile (32x16) front-to-back alpha blending.
 //
 // Restates _composite_kernel's per-pixel arithmetic (render.py:383-427) with
 // its exact f32 operation order and glibc expf, so frames are float-identical
@@ -14,7 +14,7 @@
 // (render.py:423-427), then the u8 conversion of render.py:470+484-485.
 //
 // Layout: a work item is one warp's kSets x 32 pixels, pixel rows of a
-// 32x64 tile (lane = column; rows composited one after the other), taken from a work queue by a persistent grid (see
+// 32x16 tile (lane = column; the two rows composited interleaved), taken from a work queue by a persistent grid (see
 // blend_kernel).  A warp walks the tile list 32 splats at a time: lane j
 // loads splat j's record (128-bit loads), computes its row interval (exact,
 // row_xlr) as a 32-bit pixel-coverage mask and stages the splat's row terms

@@ -11,7 +11,7 @@
 // to the splat's row range (render.py:329-333).
 //
 // The render path's own lists (binning.cu) are a conservative superset on
-// 32 x 64 tiles, built without a key sort; this path emits the contract
+// 32 x 16 tiles, built without a key sort; this path emits the contract
 // itself from the same frame's depth-ranked records, so the lists can be
 // compared bit for bit with the oracle (gsr_debug_contract_tiles) and its
 // cost measured beside the product binning (bench.py).

@@ -227,6 +227,15 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem<K> &S = *reinterpret_cast<PassSmem<K> *>(smem_raw);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // tile ticket first: the grid is sized for the capacity, and tiles past
+    // the items (most of them for a front slice) leave before any set-up
+    if (threadIdx.x == 0) S.ticket = atomicAdd(a.tickets + pass, 1u);
+    __syncthreads();
+    const int64_t t = S.ticket;
+    {
+        const int64_t nf = first_count(a), na = items_after_first(a);
+        if (t > 0 && t * RT >= (nf > na ? nf : na)) return;  // (ticket 0 publishes the plan)
+    }
     // the plan, folded into every pass (one kernel boundary less per sort):
     // a pass is active unless its digit is constant (pass 0 forced when it
     // compacts); buffers alternate over the active passes; this pass's
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
             if (threadIdx.x < 256) S.off[threadIdx.x] = ex;
         }
     }
-    if (pass == 0 && blockIdx.x == 0 && threadIdx.x == 0) {  // for the sort's consumers
+    if (pass == 0 && t == 0 && threadIdx.x == 0) {  // for the sort's consumers
         uint32_t cur = 0u, np = 0u;
         for (int p = 0; p < 8; p++) {
             const uint32_t act = (act_mask >> p) & 1u;
@@ -258,14 +267,12 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
     // first active pass: reads the producer's buffer (0) with n_first items
     const bool first = (act_mask & ((1u << pass) - 1u)) == 0u;
     const int64_t n = first ? first_count(a) : items_after_first(a);
-    if (threadIdx.x == 0) S.ticket = atomicAdd(a.tickets + pass, 1u);
+    if (t * RT >= n) return;
     const bool dig = threadIdx.x < 256;  // digit owner (RB >= 256)
     for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wcnt[0][0])[j] = 0;
     for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wmask[0][0])[j] = 0;
     if (dig) S.hcnt[threadIdx.x] = 0;
     __syncthreads();
-    const int64_t t = S.ticket;
-    if (t * RT >= n) return;
     uint32_t *st = a.status + ((int64_t)pass * a.tiles) * 256;
     // (ternaries, not a.keys[src]: runtime-indexed param arrays go to local memory)
     const K *kin = src ? a.keys[1] : a.keys[0];

@@ -12,7 +12,7 @@
 //      most tau, tau chosen from a histogram of the kept depths (built by
 //      preprocess_geo) so the slice holds about a fraction f of them.  It is sorted,
 //      coloured, binned and blended like a whole frame; a work item (two
-//      pixel rows of a 32 x 64 tile) whose pixels all saturate writes its
+//      pixel rows of a 32 x 16 tile) whose pixels all saturate writes its
 //      final pixels, any other item saves its pixels' (T, r, g, b) and sets
 //      its bit in the unsaturated-item rows.
 //   B  the rest: a splat behind the slice is kept only if its conservative
@@ -83,42 +83,59 @@ __global__ void __launch_bounds__(256) slice_col_prefix_kernel(SliceBArgs a) {
 // (span key, Gaussian index).  The append order depends on scheduling; the
 // sort and the fix-up order by (span key, f64 key, index), so the order of
 // the slice does not.
+constexpr int kFilterItems = 4;  // Gaussians per thread: all loads of a step in flight at once
+
 __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) a.ctr->blend_next = 0u;  // blend A has finished (stream order)
-    bool member = false;
-    uint32_t out = 0xffffffffu;
-    if (i < a.n && a.ctr->n_unsat) {
-        const unsigned long long k64 = __ldg(a.keys64 + i);
-        if (k64 != ~0ull) {
-            const SpanMap m = span_map(a.ctr->kmin, a.ctr->kmax);
-            const uint32_t k32 = span_key(m, k64);
-            if (k32 > a.ctr->tau) {
-                // the splat's box in item rows x tile columns (item_box,
-                // written by preprocess_geo) against the unsaturated items:
-                // per tile column, two loads of the prefix counts over item rows
-                const uint2 bx = __ldg(a.ibox + i);
-                const uint32_t r0 = bx.x & 0xffffu, r1 = (bx.x >> 16) + 1u;
-                if (r0 < r1)
-                    for (uint32_t c = bx.y & 0xffffu; c <= (bx.y >> 16) && !member; c++) {
-                        const uint32_t *col = a.col_prefix + (int64_t)c * (a.item_rows + 1);
-                        member = __ldg(col + r1) != __ldg(col + r0);
-                    }
-                if (member) out = k32;
+    __shared__ uint32_t s_warp[33];
+    __shared__ uint32_t s_base;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctr->blend_next = 0u;  // blend A has finished
+    if (a.ctr->n_unsat == 0u) return;  // (block-uniform)
+    const SpanMap m = span_map(a.ctr->kmin, a.ctr->kmax);
+    const uint32_t tau = a.ctr->tau;
+    const int64_t i0 = (int64_t)blockIdx.x * (256 * kFilterItems) + threadIdx.x;
+    unsigned long long k64[kFilterItems];
+#pragma unroll
+    for (int k = 0; k < kFilterItems; k++) {
+        const int64_t i = i0 + k * 256;
+        k64[k] = i < a.n ? __ldg(a.keys64 + i) : ~0ull;
+    }
+    uint32_t k32[kFilterItems];
+    uint2 bx[kFilterItems];
+#pragma unroll
+    for (int k = 0; k < kFilterItems; k++) {
+        k32[k] = k64[k] != ~0ull ? span_key(m, k64[k]) : 0u;
+        // behind the front slice: its box in item rows x tile columns
+        // (item_box, written by preprocess_geo)
+        bx[k] = (k64[k] != ~0ull && k32[k] > tau) ? __ldg(a.ibox + i0 + k * 256)
+                                                  : make_uint2(0xffffu, 0u);
+    }
+    // member: an unsaturated item in the box -- per tile column, two loads of
+    // the prefix counts over item rows
+    uint32_t memb = 0u;
+#pragma unroll
+    for (int k = 0; k < kFilterItems; k++) {
+        const uint32_t r0 = bx[k].x & 0xffffu, r1 = (bx[k].x >> 16) + 1u;
+        bool member = false;
+        if (r0 < r1)
+            for (uint32_t c = bx[k].y & 0xffffu; c <= (bx[k].y >> 16) && !member; c++) {
+                const uint32_t *col = a.col_prefix + (int64_t)c * (a.item_rows + 1);
+                member = __ldg(col + r1) != __ldg(col + r0);
             }
+        memb |= (uint32_t)member << k;
+    }
+    // block-aggregated append: one atomic per 1024 Gaussians
+    uint32_t tot;
+    uint32_t pos = block_excl_scan_u32((uint32_t)__popc(memb), s_warp, &tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(&a.ctr->KB, tot) : 0u;
+    __syncthreads();
+    pos += s_base;
+#pragma unroll
+    for (int k = 0; k < kFilterItems; k++)
+        if ((memb >> k) & 1u) {
+            a.keysB[pos] = k32[k];
+            a.valsB[pos] = (uint32_t)(i0 + k * 256);
+            pos++;
         }
-    }
-    // warp-aggregated append
-    const uint32_t ballot = __ballot_sync(0xffffffffu, member);
-    const int lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (lane == 0 && ballot) base = atomicAdd(&a.ctr->KB, (uint32_t)__popc(ballot));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (member) {
-        const uint32_t pos = base + __popc(ballot & ((1u << lane) - 1u));
-        a.keysB[pos] = out;
-        a.valsB[pos] = (uint32_t)i;
-    }
 }
 
 __global__ void slice_b_decide_kernel(const FrameCounters *ctr,
@@ -145,7 +162,8 @@ void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mar
     if (a.n <= 0) return;
     slice_col_prefix_kernel<<<(unsigned)((a.tiles_x + 7) / 8), 256, 0, s>>>(a);
     mark("slice_col_prefix");
-    slice_b_filter_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
+    slice_b_filter_kernel<<<(unsigned)((a.n + 256 * kFilterItems - 1) / (256 * kFilterItems)), 256,
+                            0, s>>>(a);
     mark("slice_b_filter");
 }
 

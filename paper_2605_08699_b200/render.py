@@ -3,7 +3,7 @@
 ``render_framebuffer`` / ``render_view`` keep the reference's signatures and
 return types (render.py:516-541); the work runs in libgsr.so (sm_100a CUDA):
 f64 projection + SH + packing, stable f64 radix depth sort, sort-free
-binning into conservative 32x64 tile lists (a superset of the exact 16x16
+binning into conservative 32x16 tile lists (a superset of the exact 16x16
 tile-list contract, which ``debug_contract_tiles`` emits on the device for
 parity), per-tile front-to-back blend, u8 conversion.  Host work is
 only the reference's own pose math (camera.py) and, at scene upload, the
