@@ -58,16 +58,27 @@ __device__ __forceinline__ int64_t seg_count_of(const BinArgs &a) {
     return n < a.cap_seg ? n : a.cap_seg;
 }
 
+// Blocks of BR depth ranks actually used by this pass (>= 1, so the row
+// scan always covers every tile row).  row_blk is [n_rows][blocks_used]:
+// grids are sized for the capacity (a front slice uses a fraction of it),
+// and the kernels loop over the used blocks only.
+__device__ __forceinline__ int64_t blocks_used(const BinArgs &a) {
+    const int64_t k = *a.count;
+    const int64_t nb = (k + BR - 1) / BR;
+    return nb < 1 ? 1 : (nb < a.n_blocks ? nb : a.n_blocks);
+}
+
 // ---------------------------------------------------------------- 1a -------
 __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
     __shared__ uint32_t cnt[kRowsMax];
     const int tid = threadIdx.x;
-    const int64_t b = blockIdx.x;
     const int64_t k = *a.count;
+    const int64_t nbe = blocks_used(a);
+    for (int64_t b = blockIdx.x; b < nbe; b += gridDim.x) {
     const int64_t r = b * BR + tid;
     for (int t = tid; t < a.n_rows; t += BR) cnt[t] = 0;
     __syncthreads();
-    if (b * BR < k && r < k) {
+    if (r < k) {
         const uint32_t *order = a.depth_sched[16] ? a.order1 : a.order0;
         const uint32_t i = __ldg(order + r);
         const float4 A = __ldg(&a.geo[i].a), B = __ldg(&a.geo[i].b);
@@ -81,8 +92,9 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
             for (int ty = lo / kTileH; ty <= (hi - 1) / kTileH; ty++) atomicAdd(&cnt[ty], 1u);
     }
     __syncthreads();
-    const int64_t nb = a.n_blocks;
-    for (int t = tid; t < a.n_rows; t += BR) a.row_blk[(int64_t)t * nb + b] = cnt[t];
+    for (int t = tid; t < a.n_rows; t += BR) a.row_blk[(int64_t)t * nbe + b] = cnt[t];
+    __syncthreads();  // cnt is reused by the block's next b
+    }
 }
 
 // ---------------------------------------------------------------- 1b -------
@@ -99,7 +111,9 @@ __global__ void __launch_bounds__(256) row_scan_kernel(BinArgs a) {
     __syncthreads();
     const int64_t tile = s_ticket;
     unsigned long long *status = a.scan_work + 1;
-    const int64_t n = (int64_t)a.n_rows * a.n_blocks;
+    const int64_t nbe = blocks_used(a);
+    const int64_t n = (int64_t)a.n_rows * nbe;
+    if (tile * kScanTile >= n) return;  // (n >= n_rows >= 1: tile 0 always works)
     const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
     uint32_t v[kScanItems], s = 0;
 #pragma unroll
@@ -121,7 +135,7 @@ __global__ void __launch_bounds__(256) row_scan_kernel(BinArgs a) {
         if (idx < n) {
             const unsigned long long o = pre + ex;
             a.row_blk[idx] = (uint32_t)o;
-            if (idx % a.n_blocks == 0) a.row_start[idx / a.n_blocks] = (uint32_t)o;
+            if (idx % nbe == 0) a.row_start[idx / nbe] = (uint32_t)o;
         }
         ex += v[j];
     }
@@ -169,9 +183,11 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     uint32_t *wpre_all = reinterpret_cast<uint32_t *>(dyn_raw + sizeof(PairSmem));
     uint32_t *rowbase = wpre_all + (BR / 32) * nr;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int64_t b = blockIdx.x;
     const int64_t k = *a.count;
-    if (b * BR >= k || overflowed(a)) return;
+    if (overflowed(a)) return;
+    const int64_t nbe = blocks_used(a);
+    uint32_t n_rows = 0;
+    for (int64_t b = blockIdx.x; b * BR < k; b += gridDim.x) {
     const int64_t r = b * BR + tid;
     uint32_t ntr = 0;
     int lo = 0, hi = 0;
@@ -232,12 +248,11 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
             wpre_all[j * nr + ty] = run;
             run += c;
         }
-        rowbase[ty] = run ? a.row_blk[(int64_t)ty * a.n_blocks + b] : 0u;
+        rowbase[ty] = run ? a.row_blk[(int64_t)ty * nbe + b] : 0u;
     }
     __syncthreads();
     // One thread per pair: tile span (bounded; exact rows for the few
     // ill-conditioned splats), stored at its grouped slot.
-    uint32_t n_rows = 0;
     for (uint32_t q = tid; q < npairs; q += BR) {
         const int j = q < kPairCache ? (int)S.owner[q] : rank_of_pair(S.poff, q);
         const int ty = S.lo[j] / kTileH + (int)(q - S.poff[j]);
@@ -267,6 +282,8 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
             span = tx0 | (((uint32_t)((mx - 1) / kTileW) - tx0 + 1u) << 16);
         }
         if ((int64_t)slot < a.cap_p) a.pairs[slot] = make_uint2((uint32_t)(b * BR + j), span);
+    }
+    __syncthreads();  // shared state is reused by the block's next b
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) n_rows += __shfl_xor_sync(0xffffffffu, n_rows, o);
@@ -520,7 +537,11 @@ __device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64
     place_pairs(a, p0, p1, cur, mask, lane);
 }
 
-// ------------------------------------------------ small slices: 2a-2d fused --
+// ------------------------------------------------ per-row lists: 2a-2d fused --
+// (for slices of ~0.4M splats -- 1.8M pairs, ~26k per tile row -- the
+// row-per-CTA build with 32 warps took 0.107 ms vs 0.066 for the segment
+// kernels: it is kept for small second slices only)
+constexpr int kRowWarpsSmall = 8;
 // One CTA per tile row builds that row's tile lists from its pairs (a small
 // second slice has few pairs per row, so the segment table, the per-segment
 // counts, the two scans and the placement -- five kernels -- become one):
@@ -530,13 +551,13 @@ __device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64
 // list buffer is taken with one atomicAdd (rows land in any order -- the
 // lists are addressed through ranges -- but each list holds its ranks in
 // increasing order); each warp places its chunk (place_pairs).
-constexpr int kRowWarps = 8;
-// [kRowWarps][tiles_x + 1] counts, [kRowWarps][2][tiles_x] cursors + masks,
-// [tiles_x] column totals -> row starts
-__host__ __device__ inline size_t row_lists_smem_bytes(int tiles_x) {
-    return sizeof(uint32_t) * ((size_t)kRowWarps * (3 * (size_t)tiles_x + 1) + (size_t)tiles_x);
+// [NW][tiles_x + 1] counts, [NW][2][tiles_x] cursors + masks, [tiles_x]
+// column totals -> row starts
+__host__ __device__ inline size_t row_lists_smem_bytes(int tiles_x, int nw) {
+    return sizeof(uint32_t) * ((size_t)nw * (3 * (size_t)tiles_x + 1) + (size_t)tiles_x);
 }
 
+template <int kRowWarps>
 __global__ void __launch_bounds__(kRowWarps * 32) bin_rows_kernel(BinArgs a) {
     extern __shared__ __align__(16) uint32_t row_smem[];
     __shared__ uint32_t s_base, s_last;
@@ -637,6 +658,10 @@ __global__ void __launch_bounds__(kRowWarps * 32) bin_rows_kernel(BinArgs a) {
             a.ctr->Dtot += d;
             a.ctr->Dmax = d > a.ctr->Dmax ? d : a.ctr->Dmax;
             if ((int64_t)d > a.cap_d) atomicAdd(a.overflow_sticky, 1u);
+            // every row of this pass has allocated and counted: reset for
+            // the frame's next pass
+            a.ctr->Drow = 0u;
+            a.ctr->rows_done = 0u;
         }
     }
 }
@@ -671,24 +696,30 @@ cudaError_t binning_init_attributes() {
         e = cudaFuncSetAttribute(seg_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(8 * 2 * kMaxTilesX * sizeof(uint32_t)));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(bin_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)row_lists_smem_bytes(kMaxTilesX));
+        e = cudaFuncSetAttribute(bin_rows_kernel<kRowWarpsSmall>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)row_lists_smem_bytes(kMaxTilesX, kRowWarpsSmall));
+
     return e;
 }
 
 int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark, bool rows) {
     if (a.n_blocks <= 0) return 0;
-    const unsigned nb = (unsigned)a.n_blocks;
+    // grids bounded by what the SMs hold at once (the kernels loop over the
+    // blocks of ranks actually used, read from the device count)
+    const unsigned nb = (unsigned)std::min<int64_t>(a.n_blocks, (int64_t)a.sms * 4);
+    const unsigned nbp = (unsigned)std::min<int64_t>(a.n_blocks, (int64_t)a.sms * 2);
     bin_gather_kernel<<<nb, BR, 0, s>>>(a);
     mark("bin_gather");
     const int64_t scan_tiles = bin_scan_tiles(a.n_blocks, a.n_rows);
     cudaMemsetAsync(a.scan_work, 0, sizeof(unsigned long long) * (size_t)(scan_tiles + 1), s);
     row_scan_kernel<<<(unsigned)scan_tiles, 256, 0, s>>>(a);
     mark("row_scan");
-    bin_pairs_kernel<<<nb, BR, pair_smem_bytes(a.n_rows), s>>>(a);
+    bin_pairs_kernel<<<nbp, BR, pair_smem_bytes(a.n_rows), s>>>(a);
     mark("bin_pairs");
-    if (rows) {  // small slice: one CTA per tile row builds the row's lists
-        bin_rows_kernel<<<(unsigned)a.n_rows, kRowWarps * 32, row_lists_smem_bytes(a.tiles_x), s>>>(a);
+    if (rows) {  // one CTA per tile row builds the row's lists
+        bin_rows_kernel<kRowWarpsSmall><<<(unsigned)a.n_rows, kRowWarpsSmall * 32,
+                                          row_lists_smem_bytes(a.tiles_x, kRowWarpsSmall), s>>>(a);
         mark("bin_rows");
         return 4;
     }

@@ -129,7 +129,9 @@ __device__ __forceinline__ float expf_blend(float q, const unsigned long long *t
     const double sc = __hiloint2double((int)(th + (ki << 15)), (int)tl);
 #else
     unsigned long long t;  // tab[ki & 31] through a precomputed shared-window address
-    asm("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(tab_s + ((ki & 31u) << 3)));
+    // (the table is 256-byte aligned: base | (ki << 3 & 0xf8) is one LOP3
+    // after the shift instead of an AND and an add)
+    asm("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(tab_s | ((ki << 3) & 0xf8u)));
     // t + (ki << 47): only the high word changes (the low word of ki << 47 is 0)
     const double sc = __hiloint2double((int)((uint32_t)(t >> 32) + (ki << 15)), (int)(uint32_t)t);
 #endif
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
     const float bg0 = out.fp->bg[0], bg1 = out.fp->bg[1], bg2 = out.fp->bg[2];
     uint8_t *const host = out.fp->host;
     constexpr int kItems = kTileH / kSets;  // items per tile
-    __shared__ unsigned long long s_tab[32];
+    __shared__ __align__(256) unsigned long long s_tab[32];
     __shared__ WarpBatch s_b[kWarps];
 #ifdef GSR_TAB_SPLIT
     if (threadIdx.x < 32) {

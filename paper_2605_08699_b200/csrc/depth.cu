@@ -19,6 +19,8 @@
 //            host sees it when the frame completes and re-renders the frame
 //            with the full 64-bit sort (8 passes over the raw key bits), so
 //            the order is exact for any input at no cost in the common case.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace gsr {
@@ -30,10 +32,17 @@ constexpr int kMaxRun = 16;
 // 0.2 splats on average; the fix-up resolves the resulting short runs.
 constexpr int kSpanBits = kSpanKeyBits;
 
+__device__ __forceinline__ void depth_fixup_one(const DepthArgs &a, int64_t i, int64_t K);
+
+// grid-stride over the ranks (the grid is bounded; K is read on the device)
 __global__ void depth_fixup_kernel(DepthArgs a) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t K = *a.count;
-    if (i >= K) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K;
+         i += (int64_t)gridDim.x * blockDim.x)
+        depth_fixup_one(a, i, K);
+}
+
+__device__ __forceinline__ void depth_fixup_one(const DepthArgs &a, int64_t i, int64_t K) {
     const uint32_t b = a.sched[16];
     const uint32_t *ks = b ? a.keys32[1] : a.keys32[0];
     uint32_t *vs = b ? a.vals[1] : a.vals[0];
@@ -115,7 +124,8 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &
                                                       &a.ctr->npass, sms, s, mark, span);
         }
     }
-    depth_fixup_kernel<<<g, 256, 0, s>>>(a);
+    g = std::min<unsigned>(g, (unsigned)sms * 8u);  // grid-stride (count on the device)
+    depth_fixup_kernel<<<std::max(g, 1u), 256, 0, s>>>(a);
     mark("depth_fixup");
     return launches + 1;
 }

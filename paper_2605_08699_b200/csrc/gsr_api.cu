@@ -366,6 +366,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         ba.n_rows = (H + kTileH - 1) / kTileH;
         ba.ntiles = c->ntiles;
         ba.n_blocks = bin_blocks(cap);
+        ba.sms = c->sms;
         ba.row_blk = c->row_blk.as<uint32_t>();
         ba.row_start = c->row_start.as<uint32_t>();
         ba.scan_work = c->scan_work.as<unsigned long long>();

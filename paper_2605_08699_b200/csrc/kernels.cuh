@@ -238,6 +238,7 @@ struct BinArgs {
     FrameCounters *ctr;
     int width, height, n_rows, tiles_x, ntiles;
     int64_t n_blocks;       // blocks of 512 depth ranks (capacity)
+    int sms = 148;          // grid bound of the block-looping kernels
     uint32_t *row_blk;      // [n_rows][n_blocks] pair counts -> slots
     uint32_t *row_start;    // [n_rows + 1]
     unsigned long long *scan_work;  // [1 + scan tiles]: ticket, look-back status

@@ -16,6 +16,8 @@
 //              packed geometry (u, v, ia, ib | ic, rsq, op, ry)
 //   K1b colour kept Gaussians only: mean + SH planes (216 B) -> (r, g, b)
 // The binning gather (binning.cu) puts the geometry records in depth order.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace gsr {
@@ -239,10 +241,13 @@ template <typename ShT, int DEG>
 __global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
     SceneView sc, const FrameParams *__restrict__ fp, DepthOrder ord,
     const uint32_t *__restrict__ count, float4 *__restrict__ colr) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= (int64_t)*count) return;
+    const int64_t kr = (int64_t)*count;
     const CameraArgs &cam = fp->cam;
     const uint32_t *order = ord.sched[16] ? ord.order1 : ord.order0;
+    // grid-stride over the ranked splats (the grid is bounded; the count is
+    // read on the device)
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < kr;
+         r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = __ldg(order + r);
     const int64_t st = sc.stride;
     float cr, cg, cbl;
@@ -288,6 +293,7 @@ __global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
         cbl = (float)sh_channel<DEG>(v, 2, ux, uy, uz, xx, yy, zz, xy, yz, xz);
     }
     colr[r] = make_float4(cr, cg, cbl, 0.0f);
+    }
 }
 
 }  // namespace
@@ -319,7 +325,15 @@ void launch_color_ranked(const SceneView &scene, const FrameParams *fp, int sh_d
                          cudaStream_t s, const KMark &mark) {
     if (cap <= 0) return;
     const int threads = 256;
-    const unsigned blocks = (unsigned)((cap + threads - 1) / threads);
+    static int sms = 0;  // (one device model per process)
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const unsigned blocks = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((cap + threads - 1) / threads, (int64_t)sms * 8));
 #define GSR_COLOR(T, D)                                                                   \
     color_ranked_kernel<T, D><<<blocks, threads, 0, s>>>(scene, fp, ord, count, colr)
     if (sh_degree == 0) GSR_COLOR(float, 0);
