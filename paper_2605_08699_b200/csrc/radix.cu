@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
     // the items (most of them for a front slice) leave before any set-up
     if (threadIdx.x == 0) S.ticket = atomicAdd(a.tickets + pass, 1u);
     __syncthreads();
-    const int64_t t = S.ticket;
+    int64_t t = S.ticket;
     {
         const int64_t nf = first_count(a), na = items_after_first(a);
         if (t > 0 && t * RT >= (nf > na ? nf : na)) return;  // (ticket 0 publishes the plan)
@@ -267,6 +267,10 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
     // first active pass: reads the producer's buffer (0) with n_first items
     const bool first = (act_mask & ((1u << pass) - 1u)) == 0u;
     const int64_t n = first ? first_count(a) : items_after_first(a);
+    // persistent: the grid is bounded (SMs x 2), each CTA takes tiles in
+    // ticket order until none is left (a tile only waits on lower tickets,
+    // all held by running CTAs, so the look-back always progresses)
+    for (;; ) {
     if (t * RT >= n) return;
     const bool dig = threadIdx.x < 256;  // digit owner (RB >= 256)
     for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wcnt[0][0])[j] = 0;
@@ -411,6 +415,11 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
         kout[o] = k;
         vout[o] = S.vals[i];
     }
+    __syncthreads();  // shared state is reused by the next tile
+    if (threadIdx.x == 0) S.ticket = atomicAdd(a.tickets + pass, 1u);
+    __syncthreads();
+    t = S.ticket;
+    }
 }
 
 }  // namespace
@@ -477,8 +486,9 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
     }
     {   // (pass 0 also publishes the schedule, so it always runs)
         for (int p = 0; p < passes; p++) {
-            onesweep_pass_kernel<K><<<(unsigned)std::max<int64_t>(a.tiles, 1), RB,
-                                      sizeof(PassSmem<K>), s>>>(a, p);
+            onesweep_pass_kernel<K><<<(unsigned)std::max<int64_t>(
+                                          1, std::min<int64_t>(a.tiles, (int64_t)sms * 2)),
+                                      RB, sizeof(PassSmem<K>), s>>>(a, p);
             mark(sizeof(K) == 8 ? "radix64_pass" : "radix32_pass");
             launches++;
         }

@@ -303,20 +303,21 @@ def render_u8(prims, pose, intr, background=(0.0, 0.0, 0.0), sh_degree: int = 0,
 
 
 class RenderPipeline:
-    """Frames in flight for serving: `depth` device contexts (streams) used
-    round-robin; each `submit` enqueues a render plus the device->host copy of
-    its u8 frame into a pinned slot (gsr_render_enqueue) and returns, so the
-    copy and launch gaps of one frame overlap the kernels of the next.  Once
-    `depth` frames are in flight, `submit` first completes the oldest and
-    returns it as (tag, frame); `drain` completes the rest.  A returned frame
-    is a view of a pinned slot (depth + 1 slots rotate, so the frame enqueued
-    by the same `submit` never lands in the slot it returns); its contents
-    stay valid until the next `submit` (copy it to keep them), and its memory
-    stays allocated as long as the array lives, even after close().  Every
-    frame in flight holds a reference to its scene, so a caller (or the
-    registry's eviction) dropping the primitives cannot free the scene under
-    a frame that may still be re-rendered.  Results are the same frames
-    render_u8 returns, in submission order."""
+    """Frames in flight for serving: `depth` + 1 device contexts (streams)
+    used round-robin; each `submit` enqueues a render plus the device->host
+    copy of its u8 frame into a pinned slot (gsr_render_enqueue) on a free
+    context, and once more than `depth` frames are in flight completes the
+    oldest and returns it as (tag, frame) -- so `depth` frames stay queued on
+    the device even while the host waits for the oldest (no bubble between a
+    completion and the next enqueue); `drain` completes the rest.  A returned
+    frame is a view of a pinned slot (depth + 2 slots rotate, so no frame in
+    flight lands in the slot a submit returns); its contents stay valid
+    until the next `submit` (copy it to keep them), and its memory stays
+    allocated as long as the array lives, even after close().  Every frame in
+    flight holds a reference to its scene, so a caller (or the registry's
+    eviction) dropping the primitives cannot free the scene under a frame
+    that may still be re-rendered.  Results are the same frames render_u8
+    returns, in submission order."""
 
     def __init__(self, intr, sh_degree: int = 0, background=(0.0, 0.0, 0.0), depth: int = 2,
                  device: int | None = None, record_stats: bool = False):
@@ -326,11 +327,12 @@ class RenderPipeline:
         self.intr = intr
         self.sh_degree = int(sh_degree)
         self.bg = _bg(background)
-        self.ctxs = [_lib.Context(self.device) for _ in range(max(1, int(depth)))]
+        self.depth = max(1, int(depth))
+        self.ctxs = [_lib.Context(self.device) for _ in range(self.depth + 1)]
         shape = (int(intr.height), int(intr.width), 3)
         d = len(self.ctxs)
         self.slots = [self.ctxs[k % d].pinned(f"pipeline{k // d}", shape, np.uint8)
-                      for k in range(d + 1)]
+                      for k in range(self.depth + 2)]
         self.inflight = []  # (ctx index, slot index, tag, scene), oldest first
         self.next = 0
         self.next_slot = 0
@@ -347,10 +349,7 @@ class RenderPipeline:
         return self.slots[j]
 
     def submit(self, prims, pose, tag=None):
-        done = None
-        if len(self.inflight) == len(self.ctxs):
-            i, j, t, _sc = self.inflight.pop(0)
-            done = (t, self._finish(i, j))
+        # enqueue on the free context first, then complete the oldest
         i, j = self.next, self.next_slot
         self.next = (self.next + 1) % len(self.ctxs)
         self.next_slot = (self.next_slot + 1) % len(self.slots)
@@ -362,7 +361,10 @@ class RenderPipeline:
                                               self.sh_degree, 1, _lib.ptr(self.slots[j])),
                    "gsr_render_enqueue")
         self.inflight.append((i, j, tag, sc))  # sc stays alive until the frame completes
-        return done
+        if len(self.inflight) > self.depth:
+            i, j, t, _sc = self.inflight.pop(0)
+            return (t, self._finish(i, j))
+        return None
 
     def drain(self):
         out = []
