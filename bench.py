@@ -168,6 +168,14 @@ class Dist:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.dry else "cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        return float(t.item())
+
     def gather(self, obj):
         if self.world == 1:
             return [obj]
@@ -611,6 +619,7 @@ def run_gsr(args, wl):
         torch.cuda.synchronize()
     pipe_ms = d.max(max(ev0.elapsed_time(e) for e in ends))
     value = world * K / (pipe_ms / 1000.0)
+    launches = int(d.sum(launches))  # kernels all ranks ran in the timed region
 
     # ---- per-call latency (>= --latency-calls calls, independent of --steps)
     # and e2e through the public API (pinned host frame) ----
@@ -884,6 +893,7 @@ def run_config5(args, wl):
             pipe.submit(scenes[s.scene], traces[s.index][t])
     pipe.drain()
     pipe.frame_ms.clear()
+    pipe.kernel_launches = 0
     t_sub = {}
     lat = []
     d.barrier()
@@ -899,6 +909,7 @@ def run_config5(args, wl):
         wall = time.perf_counter() - t0
     wall = d.max(wall)
     dev_ms = list(pipe.frame_ms)
+    launches5 = int(d.sum(pipe.kernel_launches))  # kernels of the timed frames, all ranks
     pipe.close()
 
     # ---- ABR-mixed: the server's per-request work at the ABR's rung ----
@@ -978,7 +989,7 @@ def run_config5(args, wl):
                                  "threads, one context each",
                           "levels_from": "tests/golden/abr_sequence.json (reference LatencyAbr "
                                          "+ TokenBucketShaper, virtual time)"},
-            "gpu_launches": None,
+            "gpu_launches": launches5,
             "clocks": clocks.summary(),
         }
         if parity is not None:

@@ -324,6 +324,7 @@ class RenderPipeline:
         self.device = _default_device if device is None else device
         # record_stats: device time (ms, CUDA events) of every completed frame
         self.frame_ms = [] if record_stats else None
+        self.kernel_launches = 0  # kernels the completed frames ran (record_stats only)
         self.intr = intr
         self.sh_degree = int(sh_degree)
         self.bg = _bg(background)
@@ -346,6 +347,7 @@ class RenderPipeline:
             _lib.check(ctx.lib.gsr_ctx_finish(ctx.handle, None, ctypes.byref(st)),
                        "gsr_ctx_finish")
             self.frame_ms.append(float(st.ms_device))
+            self.kernel_launches += int(st.kernel_launches)
         return self.slots[j]
 
     def submit(self, prims, pose, tag=None):
