@@ -49,9 +49,6 @@ constexpr int kPairCache = 6144; // per-block pair results kept in smem (1c)
 constexpr int kSeg = GSR_BIN_SEG;
 constexpr int kRowsMax = kMaxTileRows;
 
-__device__ __forceinline__ bool overflowed(const BinArgs &a) {
-    return a.ctr->P > (unsigned long long)a.cap_p || (int64_t)a.ctr->D > a.cap_d;
-}
 
 __device__ __forceinline__ int64_t seg_count_of(const BinArgs &a) {
     const int64_t n = (int64_t)a.ctr->nseg;
@@ -166,6 +163,8 @@ __host__ __device__ inline size_t pair_smem_bytes(int n_rows) {
     return sizeof(PairSmem) + sizeof(uint32_t) * (size_t)(BR / 32 + 1) * (size_t)n_rows;
 }
 
+__device__ void seg_table_block(const BinArgs &a, uint32_t *s_warp, uint32_t *s_first);
+
 __device__ __forceinline__ int rank_of_pair(const uint32_t *poff, uint32_t q) {
     int lo = 0, hi = BR;  // poff[lo] <= q < poff[hi]
     while (hi - lo > 1) {
@@ -184,7 +183,11 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     uint32_t *rowbase = wpre_all + (BR / 32) * nr;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t k = *a.count;
-    if (overflowed(a)) return;
+    if (blockIdx.x == 0) {  // the segment table (was a one-block kernel of its own)
+        __shared__ uint32_t s_first[kRowsMax + 1];
+        seg_table_block(a, S.s_warp, s_first);
+    }
+    if (a.ctr->P > (unsigned long long)a.cap_p) return;
     const int64_t nbe = blocks_used(a);
     uint32_t n_rows = 0;
     for (int64_t b = blockIdx.x; b * BR < k; b += gridDim.x) {
@@ -292,12 +295,15 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
 
 // ---------------------------------------------------------------- 2a -------
 // segments: row ty's pairs [row_start[ty], row_start[ty+1]) in pieces of kSeg
-__global__ void __launch_bounds__(1024) seg_table_kernel(BinArgs a) {
-    __shared__ uint32_t s_warp[33];
-    __shared__ uint32_t s_first[kRowsMax + 1];
+// The segment table, built by bin_pairs' block 0 (once row_start is final):
+// row ty's pairs [row_start[ty], row_start[ty+1]) in pieces of kSeg ->
+// row_seg0[ty] (its first segment), nseg, seg_row[g] (row of segment g).
+// Also resets the per-row list totals seg_scan accumulates, the pass's D,
+// and the ranges of rows without pairs (no seg_place warp visits them).
+__device__ void seg_table_block(const BinArgs &a, uint32_t *s_warp, uint32_t *s_first) {
     uint32_t carry = 0;
-    const bool ov = overflowed(a);
-    for (int base = 0; base < a.n_rows; base += 1024) {
+    const bool ov = a.ctr->P > (unsigned long long)a.cap_p;
+    for (int base = 0; base < a.n_rows; base += blockDim.x) {
         const int ty = base + threadIdx.x;
         uint32_t ns = 0;
         if (ty < a.n_rows && !ov) {
@@ -309,18 +315,23 @@ __global__ void __launch_bounds__(1024) seg_table_kernel(BinArgs a) {
         if (ty < a.n_rows) {
             a.row_seg0[ty] = carry + ex;
             s_first[ty] = carry + ex;
+            a.row_total[ty] = 0u;
+            if (ns == 0)
+                for (int t = 0; t < a.tiles_x; t++)
+                    a.ranges[(int64_t)ty * a.tiles_x + t] = make_uint2(0u, 0u);
         }
         carry += tot;
     }
     if (threadIdx.x == 0) {
         a.ctr->nseg = carry;
+        a.ctr->D = 0u;  // this pass's list entries, set by seg_place
         a.row_seg0[a.n_rows] = carry;
         s_first[a.n_rows] = carry;
     }
     __syncthreads();
     // segment -> tile row, all threads (binary search over the row starts)
     const int64_t ns_all = carry < (uint64_t)a.cap_seg ? carry : a.cap_seg;
-    for (int64_t g = threadIdx.x; g < ns_all; g += 1024) {
+    for (int64_t g = threadIdx.x; g < ns_all; g += blockDim.x) {
         int lo = 0, hi = a.n_rows;  // s_first[lo] <= g < s_first[hi]
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -329,6 +340,7 @@ __global__ void __launch_bounds__(1024) seg_table_kernel(BinArgs a) {
         }
         a.seg_row[g] = (uint32_t)lo;
     }
+    __syncthreads();
 }
 
 // first segment of tile row ty (written by seg_table)
@@ -379,7 +391,7 @@ __device__ __forceinline__ void seg_count_one(const BinArgs &a, int64_t g, int64
 __global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
     extern __shared__ __align__(16) uint32_t diff_all[];  // [8][tiles_x + 1]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (overflowed(a)) return;
+    if (a.ctr->P > (unsigned long long)a.cap_p) return;
     const int64_t nseg = seg_count_of(a);
     for (int64_t g = (int64_t)blockIdx.x * 8 + w; g < nseg; g += (int64_t)gridDim.x * 8)
         seg_count_one(a, g, nseg, diff_all + w * (a.tiles_x + 1), lane);
@@ -391,7 +403,7 @@ __global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
 __global__ void __launch_bounds__(256) seg_scan_kernel(BinArgs a) {
     const int t = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
-    if (t >= a.ntiles || overflowed(a)) return;
+    if (t >= a.ntiles || a.ctr->P > (unsigned long long)a.cap_p) return;
     const int tx_n = a.tiles_x;
     const int ty = t / tx_n, tx = t % tx_n;
     const uint32_t rs = a.row_start[ty], re = a.row_start[ty + 1];
@@ -406,35 +418,10 @@ __global__ void __launch_bounds__(256) seg_scan_kernel(BinArgs a) {
         if (si < nrow) base[(int64_t)si * tx_n] = carry + inc - v;
         carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    if (lane == 0) a.tile_total[t] = carry;
-}
-
-// one block of 1024: tile starts (exclusive scan of totals), ranges, D
-__global__ void __launch_bounds__(1024) tile_scan_kernel(BinArgs a) {
-    __shared__ uint32_t s_warp[33];
-    const bool ov_p = a.ctr->P > (unsigned long long)a.cap_p;
-    unsigned long long carry = 0;
-    for (int base = 0; base < a.ntiles; base += 1024) {
-        const int t = base + threadIdx.x;
-        const uint32_t v = (t < a.ntiles && !ov_p) ? a.tile_total[t] : 0u;
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan_u32(v, s_warp, &tot);
-        if (t < a.ntiles) {
-            const unsigned long long s = carry + ex;
-            a.tile_start[t] = (uint32_t)s;
-            a.ranges[t] = make_uint2((uint32_t)s, (uint32_t)(s + v));
-        }
-        carry += tot;
+    if (lane == 0) {
+        a.tile_total[t] = carry;
+        if (carry) atomicAdd(a.row_total + ty, carry);  // the row's list entries
     }
-    const bool overflow = ov_p || (int64_t)carry > a.cap_d;
-    if (threadIdx.x == 0) {
-        a.ctr->D = (uint32_t)(carry < 0xffffffffull ? carry : 0xffffffffull);
-        a.ctr->Dtot += carry;
-        a.ctr->Dmax = carry > a.ctr->Dmax ? carry : a.ctr->Dmax;
-        if ((int64_t)carry > a.cap_d) atomicAdd(a.overflow_sticky, 1u);
-    }
-    if (overflow)  // lists are not placed: empty ranges keep the blend in bounds
-        for (int t = threadIdx.x; t < a.ntiles; t += 1024) a.ranges[t] = make_uint2(0u, 0u);
 }
 
 // ---------------------------------------------------------------- 2d -------
@@ -528,11 +515,46 @@ __device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64
     __syncwarp();  // the warp's previous segment is done with cur / mask
     uint32_t ty, p0, p1;
     seg_bounds(a, g, nseg, ty, p0, p1);
-    const uint32_t *tstart = a.tile_start + (int64_t)ty * tx_n;
-    for (int t = lane; t < tx_n; t += 32) {
-        cur[t] = tstart[t] + a.seg_cnt[g * tx_n + t];
-        mask[t] = 0;
+    // the lists are tile-major: row ty's lists start after every earlier
+    // row's (row_total from seg_scan); D = all rows' entries.  (This replaces
+    // a one-block scan over all tile totals.)
+    unsigned long long base = 0, d = 0;
+    for (int r0 = 0; r0 < a.n_rows; r0 += 32) {
+        const int r = r0 + lane;
+        const uint32_t v = r < a.n_rows ? a.row_total[r] : 0u;
+        d += v;
+        base += (uint32_t)r < ty ? v : 0u;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        base += __shfl_xor_sync(0xffffffffu, base, o);
+    }
+    const bool over = (int64_t)d > a.cap_d;
+    const bool first_of_row = g == first_seg_of_row(a, ty, nseg);
+    uint32_t carry = 0;
+    for (int t0 = 0; t0 < tx_n; t0 += 32) {
+        const int t = t0 + lane;
+        const uint32_t v = t < tx_n ? a.tile_total[(int64_t)ty * tx_n + t] : 0u;
+        const uint32_t inc = warp_incl_scan_u32(v);
+        const uint32_t st = (uint32_t)base + carry + inc - v;  // tile start
+        if (t < tx_n) {
+            cur[t] = st + a.seg_cnt[g * tx_n + t];
+            mask[t] = 0;
+            // ranges: by the row's first segment (empty on overflow: the frame
+            // re-renders, and the blend must stay in bounds)
+            if (first_of_row)
+                a.ranges[(int64_t)ty * tx_n + t] = over ? make_uint2(0u, 0u) : make_uint2(st, st + v);
+        }
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (g == 0 && lane == 0) {  // the pass's list size (one writer)
+        a.ctr->D = (uint32_t)(d < 0xffffffffull ? d : 0xffffffffull);
+        a.ctr->Dtot += d;
+        a.ctr->Dmax = d > a.ctr->Dmax ? d : a.ctr->Dmax;
+        if (over) atomicAdd(a.overflow_sticky, 1u);
+    }
+    if (over) return;
     __syncwarp();
     place_pairs(a, p0, p1, cur, mask, lane);
 }
@@ -670,7 +692,7 @@ __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
     // per warp: column cursors [tiles_x] and coverage masks [tiles_x]
     extern __shared__ __align__(16) uint32_t place_smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (overflowed(a)) return;
+    if (a.ctr->P > (unsigned long long)a.cap_p) return;
     const int64_t nseg = seg_count_of(a);
     for (int64_t g = (int64_t)blockIdx.x * 8 + w; g < nseg; g += (int64_t)gridDim.x * 8)
         seg_place_one(a, g, nseg, place_smem + w * 2 * a.tiles_x, lane);
@@ -723,8 +745,6 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark, bool row
         mark("bin_rows");
         return 4;
     }
-    seg_table_kernel<<<1, 1024, 0, s>>>(a);
-    mark("seg_table");
     // segment kernels loop over the frame's segments: the grid covers the
     // capacity up to 2048 blocks (a small slice's pass exits early)
     const unsigned sb = (unsigned)std::min<int64_t>((a.cap_seg + 7) / 8, 2048);
@@ -732,11 +752,9 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark, bool row
     mark("seg_count");
     seg_scan_kernel<<<(unsigned)((a.ntiles + 7) / 8), 256, 0, s>>>(a);
     mark("seg_scan");
-    tile_scan_kernel<<<1, 1024, 0, s>>>(a);
-    mark("tile_scan");
     seg_place_kernel<<<sb, 256, 8 * 2 * a.tiles_x * sizeof(uint32_t), s>>>(a);
     mark("seg_place");
-    return 8;
+    return 6;
 }
 
 }  // namespace gsr

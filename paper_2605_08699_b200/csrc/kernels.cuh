@@ -249,6 +249,7 @@ struct BinArgs {
     int64_t cap_seg;
     uint32_t *seg_cnt;      // [cap_seg][tiles_x] keys per column -> offsets
     uint32_t *tile_total;   // [ntiles]
+    uint32_t *row_total;    // [n_rows] list entries per tile row (seg_scan)
     uint32_t *tile_start;   // [ntiles]
     uint2 *ranges;          // [ntiles] [start, end) into tile_vals
     uint32_t *tile_vals;    // [cap_d] depth ranks, tile-major

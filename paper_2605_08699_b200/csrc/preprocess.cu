@@ -164,7 +164,14 @@ __global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
             const double u = cam.fx * x * inv_z + cam.cx;
             const double v = cam.fy * y * inv_z + cam.cy;
             bool k = true;
-            if (do_cull) {  // render.py:230-235
+            // render.py:230-235.  A splat whose centre lies inside the image
+            // is kept whatever its radius, as long as the radius is not NaN
+            // (finite covariance: ca, cc >= 0.3, so mid + sqrt(disc) > 0):
+            // the two f64 square roots are only needed near and outside the
+            // border -- the same keep mask, fewer instructions
+            const bool inside = u > 0.0 && u < cam.width && v > 0.0 && v < cam.height &&
+                                isfinite(ca) && isfinite(cb) && isfinite(cc);
+            if (do_cull && !inside) {
                 const double mid = 0.5 * (ca + cc);
                 const double d = ca - cc;
                 const double disc = 0.25 * (d * d) + cb * cb;
@@ -296,6 +303,97 @@ __global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
     }
 }
 
+// The same colours with the gather done by the bulk-copy (TMA) engine: each
+// warp takes 32 consecutive ranks; every lane issues two cp.async.bulk
+// copies -- its Gaussian's 192 B SH row and 32 B mean -- into the warp's
+// shared-memory rows, completing on the warp's mbarrier; the lanes then
+// evaluate from shared memory.  Decouples the gather (no per-thread loads
+// in flight, no LSU throttling) from the 96 registers the SH evaluation
+// holds.  f32 SH only (every PLY scene; f64 scenes use the kernel above).
+constexpr int kBulkRow = 240;  // 192 B SH + 32 B mean + 16 B pad: 60 words, so a
+                               // warp's LDS.128 of 32 rows hits all 32 banks
+constexpr int kBulkWarps = 4;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(kBulkWarps * 32) color_ranked_bulk_kernel(
+    SceneView sc, const FrameParams *__restrict__ fp, DepthOrder ord,
+    const uint32_t *__restrict__ count, float4 *__restrict__ colr) {
+    __shared__ __align__(128) unsigned char rows[kBulkWarps][32 * kBulkRow];
+    __shared__ __align__(8) unsigned long long bar[kBulkWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&bar[w]);
+    const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(&rows[w][0]);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t kr = (int64_t)*count;
+    const CameraArgs &cam = fp->cam;
+    const uint32_t *order = ord.sched[16] ? ord.order1 : ord.order0;
+    uint32_t phase = 0;
+    const int64_t wstride = (int64_t)gridDim.x * kBulkWarps * 32;
+    for (int64_t r0 = ((int64_t)blockIdx.x * kBulkWarps + w) * 32; r0 < kr; r0 += wstride) {
+        const int64_t r = r0 + lane;
+        const bool valid = r < kr;
+        const uint32_t bal = __ballot_sync(0xffffffffu, valid);
+        const int64_t i = valid ? (int64_t)__ldg(order + r) : 0;
+        // the warp's rows were read by the generic proxy in the last round
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         ::"r"(mbar), "r"((uint32_t)__popc(bal) * 224u) : "memory");
+        if (valid) {
+            const uint32_t dst = rbase + (uint32_t)lane * kBulkRow;
+            bulk_g2s(dst, reinterpret_cast<const float *>(sc.sh) + i * 48, 192u, mbar);
+            bulk_g2s(dst + 192u, sc.mean4 + 4 * i, 32u, mbar);
+        }
+        // wait for the warp's bytes (phase parity flips every round)
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                "selp.u32 %0, 1, 0, p; }"
+                : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
+        phase ^= 1u;
+        if (valid) {
+            constexpr int NC = (DEG + 1) * (DEG + 1) * 3;
+            const unsigned char *row = &rows[w][lane * kBulkRow];
+            float v[NC];
+#pragma unroll
+            for (int k = 0; k < (NC + 3) / 4; k++) {
+                const float4 q = *reinterpret_cast<const float4 *>(row + 16 * k);
+                if (4 * k + 0 < NC) v[4 * k + 0] = q.x;
+                if (4 * k + 1 < NC) v[4 * k + 1] = q.y;
+                if (4 * k + 2 < NC) v[4 * k + 2] = q.z;
+                if (4 * k + 3 < NC) v[4 * k + 3] = q.w;
+            }
+            const double2 m01 = *reinterpret_cast<const double2 *>(row + 192);
+            const double mz = *reinterpret_cast<const double *>(row + 208);
+            const double dx = m01.x - cam.campos[0];
+            const double dy = m01.y - cam.campos[1];
+            const double dz = mz - cam.campos[2];
+            const double norm = sqrt((dx * dx + dy * dy) + dz * dz);
+            const double den = norm > 1e-12 ? norm : 1e-12;
+            const double ux = dx / den, uy = dy / den, uz = dz / den;
+            const double xx = ux * ux, yy = uy * uy, zz = uz * uz;
+            const double xy = ux * uy, yz = uy * uz, xz = ux * uz;
+            const float cr = (float)sh_channel<DEG>(v, 0, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+            const float cg = (float)sh_channel<DEG>(v, 1, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+            const float cb = (float)sh_channel<DEG>(v, 2, ux, uy, uz, xx, yy, zz, xy, yz, xz);
+            colr[r] = make_float4(cr, cg, cb, 0.0f);
+        }
+    }
+}
+
 }  // namespace
 
 void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
@@ -336,6 +434,21 @@ void launch_color_ranked(const SceneView &scene, const FrameParams *fp, int sh_d
         1, std::min<int64_t>((cap + threads - 1) / threads, (int64_t)sms * 8));
 #define GSR_COLOR(T, D)                                                                   \
     color_ranked_kernel<T, D><<<blocks, threads, 0, s>>>(scene, fp, ord, count, colr)
+#ifndef GSR_COLOR_BULK
+#define GSR_COLOR_BULK 0
+#endif
+    if (GSR_COLOR_BULK && scene.sh_f32 && sh_degree >= 1) {
+        const unsigned bb = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((cap + kBulkWarps * 32 - 1) / (kBulkWarps * 32), (int64_t)sms * 8));
+        if (sh_degree == 1)
+            color_ranked_bulk_kernel<1><<<bb, kBulkWarps * 32, 0, s>>>(scene, fp, ord, count, colr);
+        else if (sh_degree == 2)
+            color_ranked_bulk_kernel<2><<<bb, kBulkWarps * 32, 0, s>>>(scene, fp, ord, count, colr);
+        else
+            color_ranked_bulk_kernel<3><<<bb, kBulkWarps * 32, 0, s>>>(scene, fp, ord, count, colr);
+        mark("color_ranked");
+        return;
+    }
     if (sh_degree == 0) GSR_COLOR(float, 0);
     else if (scene.sh_f32 && sh_degree == 1) GSR_COLOR(float, 1);
     else if (scene.sh_f32 && sh_degree == 2) GSR_COLOR(float, 2);
