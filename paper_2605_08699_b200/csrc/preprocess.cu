@@ -435,7 +435,7 @@ void launch_color_ranked(const SceneView &scene, const FrameParams *fp, int sh_d
 #define GSR_COLOR(T, D)                                                                   \
     color_ranked_kernel<T, D><<<blocks, threads, 0, s>>>(scene, fp, ord, count, colr)
 #ifndef GSR_COLOR_BULK
-#define GSR_COLOR_BULK 0
+#define GSR_COLOR_BULK 1
 #endif
     if (GSR_COLOR_BULK && scene.sh_f32 && sh_degree >= 1) {
         const unsigned bb = (unsigned)std::max<int64_t>(
