@@ -144,10 +144,32 @@ __device__ __forceinline__ float expf_blend(float q, const unsigned long long *t
 }
 
 
+// Records of the next batch staged by cp.async (LDGSTS) while the current
+// one composites (ranks fetched two batches ahead): blend A 0.3160-0.3167 ->
+// 0.3147-0.3151 ms at config 3 (GSR_BLEND_ASYNC=0 restores plain loads).
+#ifndef GSR_BLEND_ASYNC
+#define GSR_BLEND_ASYNC 1
+#endif
+#if !GSR_BLEND_ASYNC
+#undef GSR_BLEND_ASYNC
+#endif
+
 struct WarpBatch {         // one warp's current 32 splats, splat j in slot 32 - j; slot 0: null
     float4 geo[2][33];     // per pixel row of the item: (u, ia, (2*ib)*dy, (ic*dy)*dy)
     float4 col[33];        // (op, r, g, b)
+#ifdef GSR_BLEND_ASYNC
+    float4 rec[2][32][2];  // records of the next batch, staged by cp.async (double buffer)
+#endif
 };
+
+#ifdef GSR_BLEND_ASYNC
+// cp.async 16 B global -> shared (L1-bypassing .cg), one group per batch
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+#endif
 
 // Each lane walks its own covering splats of the batch in depth order
 // (render.py:405-421, reference operation order).  The body is branch-free:
@@ -275,7 +297,7 @@ __device__ __forceinline__ uint32_t to_u8(float c) {
 // one after the other from the same staged batch.
 // kMode 0: one pass over the frame's lists.  1: slice A (slice.cu) -- an
 // item whose pixels all saturate writes them; any other saves (T, r, g, b)
-// per pixel in `state`, sets its bit in unsat_rows and lists itself in
+// per pixel in `state`, sets its bit in unsat_cols and lists itself in
 // unsat_items.  2: slice B -- only the listed items, continuing from `state`.
 template <int kSets, bool kPairLoop, bool kCount, int kMode>
 // 7 CTAs (28 warps) per SM: 71 registers keep the exp constants in registers
@@ -369,6 +391,21 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
         const uint2 rg = (kMode == 2 && ctr->KB == 0u) ? make_uint2(0u, 0u) : ranges[tile];
         uint32_t last_r = 0;  // instrumentation: deepest rank this item walked
 
+#ifdef GSR_BLEND_ASYNC
+        // records staged one batch ahead by cp.async, ranks two batches ahead
+        uint32_t r_cur = 0u, r_nxt = 0u, buf = 0u;
+        {
+            const uint32_t j0 = rg.x + lane, j1 = rg.x + 32u + lane;
+            r_cur = j0 < rg.y ? __ldg(tile_vals + j0) : 0u;
+            r_nxt = j1 < rg.y ? __ldg(tile_vals + j1) : 0u;
+            if (j0 < rg.y) {
+                const uint32_t d = (uint32_t)__cvta_generic_to_shared(&B_.rec[0][lane][0]);
+                cp_async16(d, &srec[r_cur].a);
+                cp_async16(d + 16u, &srec[r_cur].b);
+            }
+            cp_async_commit();
+        }
+#endif
         for (uint32_t c = rg.x; c < rg.y; c += 32) {
             bool all_done = true;
 #pragma unroll
@@ -380,11 +417,36 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
 #pragma unroll
             for (int h = 0; h < kSets; h++) mask[h] = 0u;
             bool safe = true;
+#ifdef GSR_BLEND_ASYNC
+            cp_async_wait_all();
+            __syncwarp();
+            const uint32_t r_this = r_cur;
+            const float4 A_s = B_.rec[buf][lane][0], B_s = B_.rec[buf][lane][1];
+            {   // stage the next batch's records, fetch the ranks after it
+                const uint32_t jn = c + 32u + lane, jn2 = c + 64u + lane;
+                if (jn < rg.y) {
+                    const uint32_t d = (uint32_t)__cvta_generic_to_shared(&B_.rec[buf ^ 1u][lane][0]);
+                    cp_async16(d, &srec[r_nxt].a);
+                    cp_async16(d + 16u, &srec[r_nxt].b);
+                }
+                cp_async_commit();
+                r_cur = r_nxt;
+                r_nxt = jn2 < rg.y ? __ldg(tile_vals + jn2) : 0u;
+                buf ^= 1u;
+            }
+#endif
             if (j < rg.y) {
+#ifdef GSR_BLEND_ASYNC
+                const uint32_t r = r_this;
+                if (kCount) last_r = max(last_r, r);
+                const float4 A = A_s;
+                const float4 B = B_s;
+#else
                 const uint32_t r = __ldg(tile_vals + j);  // depth rank
                 if (kCount) last_r = max(last_r, r);
                 const float4 A = __ldg(&srec[r].a);
                 const float4 B = __ldg(&srec[r].b);
+#endif
                 int lo, hi;  // precomputed per frame by bin_gather (SplatRec.b.w)
                 bool fast, esafe;
                 unpack_rows(B.w, lo, hi, fast, esafe);
@@ -445,6 +507,10 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
             }
             __syncwarp();
         }
+#ifdef GSR_BLEND_ASYNC
+        cp_async_wait_all();  // the staging buffers are reused by the next item
+        __syncwarp();
+#endif
         if (kCount && out.item_info) {
             bool sat = true;
 #pragma unroll
@@ -465,8 +531,9 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
                         ss.state[(int64_t)(iy0 + h) * width + ix] =
                             make_float4(T[h], cr[h], cg[h], cb[h]);
                 if (lane == 0) {
-                    atomicOr(ss.unsat_rows + (int64_t)(iy0 >> 1) * ss.row_words + (tx >> 5),
-                             1u << (tx & 31));
+                    // column-major: tile column tx, bit (item row & 31) of word item row / 32
+                    atomicOr(ss.unsat_cols + (int64_t)tx * ss.col_words + ((iy0 >> 1) >> 5),
+                             1u << ((iy0 >> 1) & 31));
                     ss.unsat_items[atomicAdd(&ctr->n_unsat, 1u)] = (uint32_t)item;
                 }
                 continue;

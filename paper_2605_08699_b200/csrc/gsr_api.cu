@@ -52,10 +52,10 @@ int ensure(DevBuf &b, size_t bytes) {
 // holding about GSR_SLICE_FRAC (default 0.15) of the kept splats.
 // depth-sliced frames: unsaturated items after slice A, one bit per tile
 // column in each item row (two pixel rows; tile rows are whole item rows)
-int unsat_row_words(int W) { return ((W + kTileW - 1) / kTileW + 31) / 32; }
 int unsat_item_rows(int H) { return ((H + kTileH - 1) / kTileH) * (kTileH / 2); }
-size_t unsat_rows_bytes(int W, int H) {
-    return sizeof(uint32_t) * (size_t)unsat_item_rows(H) * (size_t)unsat_row_words(W);
+int unsat_col_words(int H) { return (unsat_item_rows(H) + 31) / 32; }
+size_t unsat_cols_bytes(int W, int H) {
+    return sizeof(uint32_t) * (size_t)((W + kTileW - 1) / kTileW) * (size_t)unsat_col_words(H);
 }
 
 int64_t slice_min() {
@@ -129,7 +129,7 @@ struct gsr_ctx {
     DevBuf frame_u8, frame_rgb, frame_t;
     DevBuf colr;          // colours by depth rank of the current pass
     // depth-sliced frames: pixel state after slice A, unsaturated items (bits, list)
-    DevBuf state, unsat_rows, unsat_items, col_prefix, ibox;
+    DevBuf state, unsat_cols, unsat_items, ibox;
     DevBuf params;        // FrameParams of the frame being rendered
     // CUDA graphs of this context's frame configurations (record_frame)
     static constexpr int kMaxGraphs = 32;
@@ -192,7 +192,7 @@ struct gsr_ctx {
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &colr, &state, &unsat_rows, &unsat_items, &col_prefix, &ibox, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row, &rowtot,
+                               &geo, &colr, &state, &unsat_cols, &unsat_items, &ibox, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row, &rowtot,
                                &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
@@ -307,7 +307,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
     const int64_t n = sc->n;
     uint32_t *dsched = c->sched.as<uint32_t>();
     const unsigned evflags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
-    int launches = 2;  // frame params + frame init
+    int launches = 1;  // frame_start
 
     KMark mark;
     if (c->ktime && !graph) {
@@ -323,8 +323,8 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
     SliceState ss;
     if (slice) {
         ss.state = c->state.as<float4>();
-        ss.unsat_rows = c->unsat_rows.as<uint32_t>();
-        ss.row_words = unsat_row_words(W);
+        ss.unsat_cols = c->unsat_cols.as<uint32_t>();
+        ss.col_words = unsat_col_words(H);
         ss.unsat_items = c->unsat_items.as<uint32_t>();
     }
     // one depth-ordered pass over *count splats (at most cap): sort, colour, bin
@@ -396,9 +396,8 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
 
     cudaEventRecordWithFlags(c->ev[0], s, evflags);
     if (c->ktime && !graph) cudaEventRecord(c->kev[0], s);
-    launch_frame_params(fp, dfp, s);
-    launch_frame_init(ctr, s);
-    mark("frame_init");
+    launch_frame_start(fp, dfp, ctr, s);
+    mark("frame_start");
     if (c->kcount &&
         ensure(c->used, sizeof(uint32_t) * ((size_t)c->cap_n + n_items)) == GSR_OK) {
         cudaMemsetAsync(c->used.p, 0, sizeof(uint32_t) * ((size_t)c->cap_n + n_items), s);
@@ -435,7 +434,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         // slice A: the front of the depth order
         sort_color_bin(s, &ctr->KA, &ctr->tau, false, c->cap_n);
         cudaEventRecordWithFlags(c->ev[3], s, evflags);
-        cudaMemsetAsync(c->unsat_rows.p, 0, unsat_rows_bytes(W, H), s);
+        cudaMemsetAsync(c->unsat_cols.p, 0, unsat_cols_bytes(W, H), s);
         blend(1);
         cudaEventRecordWithFlags(c->ev[4], s, evflags);
         // slice B: the splats behind it that can reach an unsaturated item
@@ -445,17 +444,15 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         sb.ibox = c->ibox.as<uint2>();
         sb.n = n;
         sb.ctr = ctr;
-        sb.unsat_rows = c->unsat_rows.as<uint32_t>();
-        sb.row_words = unsat_row_words(W);
-        sb.item_rows = unsat_item_rows(H);
-        sb.col_prefix = c->col_prefix.as<uint32_t>();
+        sb.unsat_cols = c->unsat_cols.as<uint32_t>();
+        sb.col_words = unsat_col_words(H);
         sb.width = W;
         sb.height = H;
         sb.tiles_x = (W + kTileW - 1) / kTileW;
         sb.keysB = c->keys32[0].as<uint32_t>();
         sb.valsB = c->vals[0].as<uint32_t>();
         launch_slice_b_filter(sb, s, mark);
-        launches += 2;
+        launches += 1;
         auto class_cap = [&](int k) {
             return k < kSliceClasses - 1 ? std::min<int64_t>(slice_class_cap(k), c->cap_n)
                                          : c->cap_n;
@@ -584,7 +581,7 @@ int frame_graph(gsr_ctx *c, const FrameKey &key, const gsr_scene *sc, const Fram
         if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
         cudaKernelNodeParams kp{};
         if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
-            kp.func == frame_params_kernel_fn()) {
+            kp.func == frame_start_kernel_fn()) {
             fg.params_node = nd;
             break;
         }
@@ -638,11 +635,8 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     if (slice) {
         const size_t n_items = (size_t)c->ntiles * (kTileH / 2);
         if ((rc = cens(c, c->state, sizeof(float4) * (size_t)W * H))) return rc;
-        if ((rc = cens(c, c->unsat_rows, unsat_rows_bytes(W, H)))) return rc;
+        if ((rc = cens(c, c->unsat_cols, unsat_cols_bytes(W, H)))) return rc;
         if ((rc = cens(c, c->ibox, sizeof(uint2) * (size_t)std::max<int64_t>(n, 1)))) return rc;
-        if ((rc = cens(c, c->col_prefix, sizeof(uint32_t) * (size_t)((W + kTileW - 1) / kTileW) *
-                                             (size_t)(unsat_item_rows(H) + 1))))
-            return rc;
         if ((rc = cens(c, c->unsat_items, sizeof(uint32_t) * n_items))) return rc;
     }
     FrameParams fp;
@@ -672,10 +666,11 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
             return rc;
         cudaKernelNodeParams kp{};
         FrameParams *dfp = c->params.as<FrameParams>();
-        void *args[2] = {&fp, &dfp};
-        kp.func = const_cast<void *>(frame_params_kernel_fn());
+        FrameCounters *dctr = c->ctr.as<FrameCounters>();
+        void *args[3] = {&fp, &dfp, &dctr};
+        kp.func = const_cast<void *>(frame_start_kernel_fn());
         kp.gridDim = dim3(1);
-        kp.blockDim = dim3(1);
+        kp.blockDim = dim3(kFrameStartThreads);
         kp.kernelParams = args;
         GSR_CUDA_OK(cudaGraphExecKernelNodeSetParams(fg->exec, fg->params_node, &kp));
         GSR_CUDA_OK(cudaGraphLaunch(fg->exec, c->stream));

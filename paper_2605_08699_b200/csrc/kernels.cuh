@@ -18,7 +18,7 @@ struct KMark {
     }
 };
 
-// Per-frame device counters (one struct, reset by frame_init_kernel).
+// Per-frame device counters (one struct, reset by frame_start_kernel).
 struct FrameCounters {
     uint32_t K;                 // kept splats
     uint32_t D;                 // tile keys under the contract (may exceed capacity)
@@ -122,12 +122,14 @@ struct FrameParams {
     float bg[3];
     uint8_t *host;  // device view of a mapped pinned (H,W,3) frame (zero copy), or null
 };
-void launch_frame_params(const FrameParams &p, FrameParams *dst, cudaStream_t s);
-const void *frame_params_kernel_fn();  // its function (graph node updates)
+// the frame's first kernel: FrameParams into device memory + counters reset
+constexpr int kFrameStartThreads = 256;
+void launch_frame_start(const FrameParams &p, FrameParams *dst, FrameCounters *ctr,
+                        cudaStream_t s);
+const void *frame_start_kernel_fn();  // its function (graph node updates)
 
 // preprocess.cu (2 kernels)
 using GeoRec = SplatRec;  // by Gaussian index (preprocess), by depth rank (gather)
-void launch_frame_init(FrameCounters *ctr, cudaStream_t s);
 // K1a: projection, culling, depth keys, packed geometry (render.py:163-290)
 // zhist (depth-sliced frames, else null): += histogram of the kept depths
 // over kZBins bins of their f64 bits (slice_plan's input)
@@ -303,12 +305,13 @@ struct BlendOut {
 bool blend_has_slices();  // the selected blend variant has modes 1 and 2
 int blend_grid(int width, int height);  // its persistent grid (host query, cached)
 // mode: 0 one pass; 1 slice A (saturated items write the frame, the others
-// save their pixels' state, set their bit in unsat_rows and are listed in
+// save their pixels' state, set their bit in unsat_cols and are listed in
 // unsat_items); 2 slice B (the listed items only, from the saved state)
 struct SliceState {
     float4 *state = nullptr;        // (H, W) pixel (T, r, g, b) after slice A
-    uint32_t *unsat_rows = nullptr; // [item rows][row_words]: bit tx = item of tile column tx
-    int row_words = 0;              // words per item row: (tiles_x + 31) / 32
+    uint32_t *unsat_cols = nullptr; // [tiles_x][col_words]: bit r of tile column tx's bitmask =
+                                    // the item (tx, item row r) is unsaturated
+    int col_words = 0;              // words per tile column: (item rows + 31) / 32
     uint32_t *unsat_items = nullptr;  // [n_items] their ids; count in FrameCounters.n_unsat
 };
 void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
@@ -323,9 +326,8 @@ struct SliceBArgs {
     int64_t n;
     FrameCounters *ctr;                // kmin, kmax, tau; KB counted here
     const uint2 *ibox;                 // item_box of each kept splat (preprocess_geo)
-    const uint32_t *unsat_rows;        // [item rows][row_words] items slice A left unsaturated
-    int row_words, item_rows;
-    uint32_t *col_prefix;              // [tiles_x][item_rows + 1] (slice_b_filter's first kernel)
+    const uint32_t *unsat_cols;        // [tiles_x][col_words] items slice A left unsaturated
+    int col_words;
     int width, height, tiles_x;
     uint32_t *keysB, *valsB;           // out: slice B's (span key, Gaussian index), appended
 };

@@ -60,9 +60,14 @@ __device__ __forceinline__ double sh_channel(const T *v, int c, double x, double
     return r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);  // np.clip(result + 0.5, 0, 1)
 }
 
-__global__ void __launch_bounds__(256) frame_init_kernel(FrameCounters *ctr) {
+// The frame's first kernel: its parameters (camera, background, mapped host
+// frame) into device memory -- the CUDA graph's one updated node -- and the
+// per-frame counters reset.
+__global__ void __launch_bounds__(256) frame_start_kernel(FrameParams p, FrameParams *dst,
+                                                          FrameCounters *ctr) {
     for (int j = threadIdx.x; j < kZBins; j += blockDim.x) ctr->slice_hist[j] = 0u;
     if (threadIdx.x) return;
+    *dst = p;
     ctr->K = 0;
     ctr->D = 0;
     ctr->npass = 0;
@@ -85,7 +90,6 @@ __global__ void __launch_bounds__(256) frame_init_kernel(FrameCounters *ctr) {
     ctr->Dtot = ctr->Ptot = ctr->Dmax = ctr->Pmax = 0ull;
 }
 
-__global__ void frame_params_kernel(FrameParams p, FrameParams *dst) { *dst = p; }
 
 #ifndef GSR_PP_MINB
 #define GSR_PP_MINB 5
@@ -396,15 +400,14 @@ __global__ void __launch_bounds__(kBulkWarps * 32) color_ranked_bulk_kernel(
 
 }  // namespace
 
-void launch_frame_init(FrameCounters *ctr, cudaStream_t s) {
-    frame_init_kernel<<<1, 256, 0, s>>>(ctr);
+
+
+void launch_frame_start(const FrameParams &p, FrameParams *dst, FrameCounters *ctr,
+                        cudaStream_t s) {
+    frame_start_kernel<<<1, kFrameStartThreads, 0, s>>>(p, dst, ctr);
 }
 
-void launch_frame_params(const FrameParams &p, FrameParams *dst, cudaStream_t s) {
-    frame_params_kernel<<<1, 1, 0, s>>>(p, dst);
-}
-
-const void *frame_params_kernel_fn() { return (const void *)frame_params_kernel; }
+const void *frame_start_kernel_fn() { return (const void *)frame_start_kernel; }
 
 void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int frustum_cull,
                            unsigned long long *keys, GeoRec *geo, uint8_t *keep_out,

@@ -14,15 +14,14 @@
 //      coloured, binned and blended like a whole frame; a work item (two
 //      pixel rows of a 32 x 16 tile) whose pixels all saturate writes its
 //      final pixels, any other item saves its pixels' (T, r, g, b) and sets
-//      its bit in the unsaturated-item rows.
+//      its bit in the unsaturated-item bitmask.
 //   B  the rest: a splat behind the slice is kept only if its conservative
 //      box in item rows x tile columns (item_box: the reference's row range,
 //      the whole splat's column extent) meets an unsaturated item (blend A
-//      marks each unsaturated item in a per-item-row bitmask over the tile
-//      columns; per tile column, a prefix count over the item rows answers
-//      "any unsaturated item in rows [r0, r1)" with two loads); those are
-//      sorted, coloured, binned and blended from the saved state, by the
-//      unsaturated items only.
+//      sets its bit in a column-major bitmask -- per tile column, one bit per
+//      item row -- so a box's rows in a column are one or two masked words);
+//      those are sorted, coloured, binned and blended from the saved state,
+//      by the unsaturated items only.
 // Ties in the span key never straddle the slices (the split is on the key),
 // so A's order followed by B's is the global stable depth order, and each
 // unsaturated pixel sees every splat covering it in the reference's order:
@@ -59,26 +58,6 @@ __global__ void __launch_bounds__(kZBins) slice_plan_kernel(FrameCounters *ctr, 
     if (tot == 0u && threadIdx.x == 0) ctr->tau = 0u;
 }
 
-// Per tile column c: col_prefix[c][r] = unsaturated items of column c in
-// item rows < r (from blend A's item-row bitmasks), one warp per column,
-// 32 rows per step (ballot + popc prefix).
-__global__ void __launch_bounds__(256) slice_col_prefix_kernel(SliceBArgs a) {
-    const int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (c >= a.tiles_x || a.ctr->n_unsat == 0u) return;
-    uint32_t *col = a.col_prefix + (int64_t)c * (a.item_rows + 1);
-    if (lane == 0) col[0] = 0u;
-    uint32_t run = 0u;
-    for (int r0 = 0; r0 < a.item_rows; r0 += 32) {
-        const int r = r0 + lane;
-        const bool bit = r < a.item_rows &&
-                         ((__ldg(a.unsat_rows + (int64_t)r * a.row_words + (c >> 5)) >> (c & 31)) & 1u);
-        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-        if (r < a.item_rows) col[r + 1] = run + (uint32_t)__popc(bal & (0xffffffffu >> (31 - lane)));
-        run += (uint32_t)__popc(bal);
-    }
-}
-
 // Splats behind the slice that may reach an unsaturated item, appended as
 // (span key, Gaussian index).  The append order depends on scheduling; the
 // sort and the fix-up order by (span key, f64 key, index), so the order of
@@ -109,17 +88,23 @@ __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
         bx[k] = (k64[k] != ~0ull && k32[k] > tau) ? __ldg(a.ibox + i0 + k * 256)
                                                   : make_uint2(0xffffu, 0u);
     }
-    // member: an unsaturated item in the box -- per tile column, two loads of
-    // the prefix counts over item rows
+    // member: an unsaturated item in the box -- per tile column, the words of
+    // its item-row bitmask the box's rows [r0, r1] span (one or two for all
+    // but tall splats), masked to the rows
     uint32_t memb = 0u;
 #pragma unroll
     for (int k = 0; k < kFilterItems; k++) {
-        const uint32_t r0 = bx[k].x & 0xffffu, r1 = (bx[k].x >> 16) + 1u;
+        const uint32_t r0 = bx[k].x & 0xffffu, r1 = bx[k].x >> 16;
         bool member = false;
-        if (r0 < r1)
+        if (r0 <= r1)
             for (uint32_t c = bx[k].y & 0xffffu; c <= (bx[k].y >> 16) && !member; c++) {
-                const uint32_t *col = a.col_prefix + (int64_t)c * (a.item_rows + 1);
-                member = __ldg(col + r1) != __ldg(col + r0);
+                const uint32_t *col = a.unsat_cols + (int64_t)c * a.col_words;
+                for (uint32_t wd = r0 >> 5; wd <= (r1 >> 5) && !member; wd++) {
+                    uint32_t m = __ldg(col + wd);
+                    if (wd == (r0 >> 5)) m &= ~0u << (r0 & 31);
+                    if (wd == (r1 >> 5)) m &= ~0u >> (31 - (r1 & 31));
+                    member = m != 0u;
+                }
             }
         memb |= (uint32_t)member << k;
     }
@@ -160,8 +145,6 @@ void launch_slice_plan(FrameCounters *ctr, float frac, cudaStream_t s, const KMa
 
 void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark) {
     if (a.n <= 0) return;
-    slice_col_prefix_kernel<<<(unsigned)((a.tiles_x + 7) / 8), 256, 0, s>>>(a);
-    mark("slice_col_prefix");
     slice_b_filter_kernel<<<(unsigned)((a.n + 256 * kFilterItems - 1) / (256 * kFilterItems)), 256,
                             0, s>>>(a);
     mark("slice_b_filter");

@@ -115,3 +115,36 @@ def test_config3_ladder_3m_vs_reference(gsr, oracle, scene3):
                                sh_degree=3)
     assert np.allclose(fused, [r["ssim"] for r in lad["rungs"]], atol=SSIM_TOL, rtol=0)
     assert all(a > b for a, b in zip(scores, scores[1:]))
+
+
+def test_config3_bench_trace_vs_oracle(gsr, oracle):
+    """The bench's own config-3 workload (bench.build_scene: 3M Gaussians,
+    SH3, 1080p, the reference generator's scale range R(N)) at six poses of
+    the bench trace, through the serving paths the bench times -- render_u8
+    (one CUDA graph per frame, depth-sliced) and RenderPipeline (4 frames in
+    flight) -- frame for frame equal to the oracle (u8 bit-exact)."""
+    import bench
+    wl = bench.WORKLOADS["config3"]
+    prims = bench.build_scene(wl)
+    intr = bench.intrinsics(wl)
+    poses = bench.poses_for(0, 40)[::7][:6]
+    want = []
+    for p in poses:
+        rot, w2c = oracle.world_to_camera(p.azimuth, p.elevation, p.translation)
+        fr = oracle.render(prims.means, prims.scales, prims.rotations, prims.opacities,
+                           prims.colors_dc, prims.sh_coeffs, w2c, rot, intr.fx, intr.fy,
+                           intr.cx, intr.cy, intr.width, intr.height, (0.0, 0.0, 0.0), 3)
+        want.append(fr.u8)
+    for p, w in zip(poses, want):
+        assert np.array_equal(gsr.render_u8(prims, p, intr, sh_degree=3), w)
+    pipe = gsr.RenderPipeline(intr, sh_degree=3, depth=4)
+    got = {}
+    for i, p in enumerate(poses):
+        r = pipe.submit(prims, p, tag=i)
+        if r is not None:
+            got[r[0]] = r[1].copy()
+    for t, f in pipe.drain():
+        got[t] = f.copy()
+    pipe.close()
+    for i, w in enumerate(want):
+        assert np.array_equal(got[i], w), i

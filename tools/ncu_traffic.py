@@ -21,7 +21,7 @@ MAP = [(r"preprocess_geo_kernel", "preprocess_geo"),
        (r"radix_hist_kernel<unsigned long long>", "radix64_hist"),
        (r"radix_plan_kernel<unsigned long long>", "radix64_plan"),
        (r"onesweep_pass_kernel<unsigned long long>", "radix64_pass"),
-       (r"frame_init_kernel", "frame_init"), (r"frame_params_kernel", "frame_params"),
+       (r"frame_start_kernel", "frame_start"),
        (r"color_ranked_kernel", "color_ranked"), (r"blend_kernel", "blend")]
 for k in ["bin_gather", "row_scan", "bin_pairs", "seg_table", "seg_count", "seg_scan",
           "tile_scan", "seg_place", "bin_rows", "slice_plan", "slice_col_prefix",
