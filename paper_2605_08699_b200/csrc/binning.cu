@@ -50,10 +50,6 @@ constexpr int kSeg = GSR_BIN_SEG;
 constexpr int kRowsMax = kMaxTileRows;
 
 
-__device__ __forceinline__ int64_t seg_count_of(const BinArgs &a) {
-    const int64_t n = (int64_t)a.ctr->nseg;
-    return n < a.cap_seg ? n : a.cap_seg;
-}
 
 // Blocks of BR depth ranks actually used by this pass (>= 1, so the row
 // scan always covers every tile row).  row_blk is [n_rows][blocks_used]:
@@ -137,6 +133,10 @@ __global__ void __launch_bounds__(256) row_scan_kernel(BinArgs a) {
         ex += v[j];
     }
     if (threadIdx.x == 255 && (tile + 1) * kScanTile >= n) {  // last tile: totals
+        // (and this pass's per-row list totals and D, accumulated / set by
+        // seg_scan / seg_place)
+        for (int r = 0; r < a.n_rows; r++) a.row_total[r] = 0u;
+        a.ctr->D = 0u;
         const unsigned long long p = pre + ex;
         a.ctr->P = p;
         a.ctr->Ptot += p;  // one thread of one block per pass
@@ -163,8 +163,6 @@ __host__ __device__ inline size_t pair_smem_bytes(int n_rows) {
     return sizeof(PairSmem) + sizeof(uint32_t) * (size_t)(BR / 32 + 1) * (size_t)n_rows;
 }
 
-__device__ void seg_table_block(const BinArgs &a, uint32_t *s_warp, uint32_t *s_first);
-
 __device__ __forceinline__ int rank_of_pair(const uint32_t *poff, uint32_t q) {
     int lo = 0, hi = BR;  // poff[lo] <= q < poff[hi]
     while (hi - lo > 1) {
@@ -183,10 +181,6 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
     uint32_t *rowbase = wpre_all + (BR / 32) * nr;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t k = *a.count;
-    if (blockIdx.x == 0) {  // the segment table (was a one-block kernel of its own)
-        __shared__ uint32_t s_first[kRowsMax + 1];
-        seg_table_block(a, S.s_warp, s_first);
-    }
     if (a.ctr->P > (unsigned long long)a.cap_p) return;
     const int64_t nbe = blocks_used(a);
     uint32_t n_rows = 0;
@@ -295,12 +289,16 @@ __global__ void __launch_bounds__(BR) bin_pairs_kernel(BinArgs a) {
 
 // ---------------------------------------------------------------- 2a -------
 // segments: row ty's pairs [row_start[ty], row_start[ty+1]) in pieces of kSeg
-// The segment table, built by bin_pairs' block 0 (once row_start is final):
-// row ty's pairs [row_start[ty], row_start[ty+1]) in pieces of kSeg ->
-// row_seg0[ty] (its first segment), nseg, seg_row[g] (row of segment g).
-// Also resets the per-row list totals seg_scan accumulates, the pass's D,
-// and the ranges of rows without pairs (no seg_place warp visits them).
-__device__ void seg_table_block(const BinArgs &a, uint32_t *s_warp, uint32_t *s_first) {
+// The segment table -- row ty's pairs [row_start[ty], row_start[ty+1]) in
+// pieces of kSeg; s_first[ty] = its first segment, s_first[n_rows] = all --
+// rebuilt in shared memory by every CTA of the segment kernels (a block scan
+// over <= 512 rows: cheaper than a one-block kernel and its launch).
+struct SegTable {
+    uint32_t first[kRowsMax + 1];
+    uint32_t warp[33];
+};
+
+__device__ __forceinline__ void seg_table(const BinArgs &a, SegTable &T) {
     uint32_t carry = 0;
     const bool ov = a.ctr->P > (unsigned long long)a.cap_p;
     for (int base = 0; base < a.n_rows; base += blockDim.x) {
@@ -311,62 +309,50 @@ __device__ void seg_table_block(const BinArgs &a, uint32_t *s_warp, uint32_t *s_
             ns = (len + kSeg - 1) / kSeg;
         }
         uint32_t tot;
-        const uint32_t ex = block_excl_scan_u32(ns, s_warp, &tot);
-        if (ty < a.n_rows) {
-            a.row_seg0[ty] = carry + ex;
-            s_first[ty] = carry + ex;
-            a.row_total[ty] = 0u;
-            if (ns == 0)
-                for (int t = 0; t < a.tiles_x; t++)
-                    a.ranges[(int64_t)ty * a.tiles_x + t] = make_uint2(0u, 0u);
-        }
+        const uint32_t ex = block_excl_scan_u32(ns, T.warp, &tot);
+        if (ty < a.n_rows) T.first[ty] = carry + ex;
         carry += tot;
     }
-    if (threadIdx.x == 0) {
-        a.ctr->nseg = carry;
-        a.ctr->D = 0u;  // this pass's list entries, set by seg_place
-        a.row_seg0[a.n_rows] = carry;
-        s_first[a.n_rows] = carry;
-    }
-    __syncthreads();
-    // segment -> tile row, all threads (binary search over the row starts)
-    const int64_t ns_all = carry < (uint64_t)a.cap_seg ? carry : a.cap_seg;
-    for (int64_t g = threadIdx.x; g < ns_all; g += blockDim.x) {
-        int lo = 0, hi = a.n_rows;  // s_first[lo] <= g < s_first[hi]
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_first[mid] <= (uint32_t)g) lo = mid;
-            else hi = mid;
-        }
-        a.seg_row[g] = (uint32_t)lo;
-    }
+    if (threadIdx.x == 0) T.first[a.n_rows] = carry;
     __syncthreads();
 }
 
-// first segment of tile row ty (written by seg_table)
-__device__ __forceinline__ int64_t first_seg_of_row(const BinArgs &a, uint32_t ty, int64_t nseg) {
-    const int64_t f = (int64_t)a.row_seg0[ty];
+__device__ __forceinline__ int64_t seg_total(const BinArgs &a, const SegTable &T) {
+    const int64_t n = (int64_t)T.first[a.n_rows];
+    return n < a.cap_seg ? n : a.cap_seg;
+}
+
+// first segment of tile row ty
+__device__ __forceinline__ int64_t first_seg_of_row(const SegTable &T, uint32_t ty, int64_t nseg) {
+    const int64_t f = (int64_t)T.first[ty];
     return f < nseg ? f : nseg;
 }
 
-__device__ __forceinline__ void seg_bounds(const BinArgs &a, int64_t g, int64_t nseg,
-                                           uint32_t &ty, uint32_t &p0, uint32_t &p1) {
-    ty = a.seg_row[g];
-    const int64_t first = first_seg_of_row(a, ty, nseg);
+__device__ __forceinline__ void seg_bounds(const BinArgs &a, const SegTable &T, int64_t g,
+                                           int64_t nseg, uint32_t &ty, uint32_t &p0,
+                                           uint32_t &p1) {
+    int lo = 0, hi = a.n_rows;  // first[lo] <= g < first[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (T.first[mid] <= (uint32_t)g) lo = mid;
+        else hi = mid;
+    }
+    ty = (uint32_t)lo;
+    const int64_t first = first_seg_of_row(T, ty, nseg);
     const uint32_t rs = a.row_start[ty], re = a.row_start[ty + 1];
     p0 = rs + (uint32_t)(g - first) * kSeg;
     p1 = min(re, p0 + kSeg);
 }
 
 // ---------------------------------------------------------------- 2b -------
-__device__ __forceinline__ void seg_count_one(const BinArgs &a, int64_t g, int64_t nseg,
-                                              uint32_t *diff, int lane) {
+__device__ __forceinline__ void seg_count_one(const BinArgs &a, const SegTable &T, int64_t g,
+                                              int64_t nseg, uint32_t *diff, int lane) {
     const int tx_n = a.tiles_x;
     __syncwarp();  // the warp's previous segment is done with diff
     for (int t = lane; t <= tx_n; t += 32) diff[t] = 0;
     __syncwarp();
     uint32_t ty, p0, p1;
-    seg_bounds(a, g, nseg, ty, p0, p1);
+    seg_bounds(a, T, g, nseg, ty, p0, p1);
     for (uint32_t p = p0 + lane; p < p1; p += 32) {
         const uint32_t sp = a.pairs[p].y;
         const uint32_t c = sp >> 16;
@@ -390,25 +376,35 @@ __device__ __forceinline__ void seg_count_one(const BinArgs &a, int64_t g, int64
 // one warp per segment: keys per tile column via a difference array
 __global__ void __launch_bounds__(256) seg_count_kernel(BinArgs a) {
     extern __shared__ __align__(16) uint32_t diff_all[];  // [8][tiles_x + 1]
+    __shared__ SegTable T;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (a.ctr->P > (unsigned long long)a.cap_p) return;
-    const int64_t nseg = seg_count_of(a);
+    seg_table(a, T);
+    const int64_t nseg = seg_total(a, T);
     for (int64_t g = (int64_t)blockIdx.x * 8 + w; g < nseg; g += (int64_t)gridDim.x * 8)
-        seg_count_one(a, g, nseg, diff_all + w * (a.tiles_x + 1), lane);
+        seg_count_one(a, T, g, nseg, diff_all + w * (a.tiles_x + 1), lane);
 }
 
 // ---------------------------------------------------------------- 2c -------
 // warp per tile: exclusive prefix over its row's segments (32 at a time,
 // warp scan), tile total
 __global__ void __launch_bounds__(256) seg_scan_kernel(BinArgs a) {
+    __shared__ SegTable T;
     const int t = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
-    if (t >= a.ntiles || a.ctr->P > (unsigned long long)a.cap_p) return;
+    if (a.ctr->P > (unsigned long long)a.cap_p) {
+        // the pairs overflowed: no lists this pass (the frame re-renders with
+        // larger buffers), but the blend still runs -- empty every range
+        if (t < a.ntiles && lane == 0) a.ranges[t] = make_uint2(0u, 0u);
+        return;
+    }
+    seg_table(a, T);
+    if (t >= a.ntiles) return;
     const int tx_n = a.tiles_x;
     const int ty = t / tx_n, tx = t % tx_n;
     const uint32_t rs = a.row_start[ty], re = a.row_start[ty + 1];
     const uint32_t nrow = (re - rs + kSeg - 1) / kSeg;
-    const int64_t lo = first_seg_of_row(a, (uint32_t)ty, seg_count_of(a));
+    const int64_t lo = first_seg_of_row(T, (uint32_t)ty, seg_total(a, T));
     uint32_t *base = a.seg_cnt + lo * tx_n + tx;
     uint32_t carry = 0;
     for (uint32_t s0 = 0; s0 < nrow; s0 += 32) {
@@ -421,6 +417,9 @@ __global__ void __launch_bounds__(256) seg_scan_kernel(BinArgs a) {
     if (lane == 0) {
         a.tile_total[t] = carry;
         if (carry) atomicAdd(a.row_total + ty, carry);  // the row's list entries
+        // an empty list (tiles of rows without pairs have no seg_place warp;
+        // seg_place overwrites the others)
+        else a.ranges[t] = make_uint2(0u, 0u);
     }
 }
 
@@ -508,13 +507,13 @@ __device__ __forceinline__ void place_pairs(const BinArgs &a, uint32_t p0, uint3
     }
 }
 
-__device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64_t nseg,
-                                              uint32_t *cur, int lane) {
+__device__ __forceinline__ void seg_place_one(const BinArgs &a, const SegTable &T, int64_t g,
+                                              int64_t nseg, uint32_t *cur, int lane) {
     const int tx_n = a.tiles_x;
     uint32_t *mask = cur + tx_n;
     __syncwarp();  // the warp's previous segment is done with cur / mask
     uint32_t ty, p0, p1;
-    seg_bounds(a, g, nseg, ty, p0, p1);
+    seg_bounds(a, T, g, nseg, ty, p0, p1);
     // the lists are tile-major: row ty's lists start after every earlier
     // row's (row_total from seg_scan); D = all rows' entries.  (This replaces
     // a one-block scan over all tile totals.)
@@ -531,7 +530,7 @@ __device__ __forceinline__ void seg_place_one(const BinArgs &a, int64_t g, int64
         base += __shfl_xor_sync(0xffffffffu, base, o);
     }
     const bool over = (int64_t)d > a.cap_d;
-    const bool first_of_row = g == first_seg_of_row(a, ty, nseg);
+    const bool first_of_row = g == first_seg_of_row(T, ty, nseg);
     uint32_t carry = 0;
     for (int t0 = 0; t0 < tx_n; t0 += 32) {
         const int t = t0 + lane;
@@ -691,11 +690,13 @@ __global__ void __launch_bounds__(kRowWarps * 32) bin_rows_kernel(BinArgs a) {
 __global__ void __launch_bounds__(256) seg_place_kernel(BinArgs a) {
     // per warp: column cursors [tiles_x] and coverage masks [tiles_x]
     extern __shared__ __align__(16) uint32_t place_smem[];
+    __shared__ SegTable T;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (a.ctr->P > (unsigned long long)a.cap_p) return;
-    const int64_t nseg = seg_count_of(a);
+    seg_table(a, T);
+    const int64_t nseg = seg_total(a, T);
     for (int64_t g = (int64_t)blockIdx.x * 8 + w; g < nseg; g += (int64_t)gridDim.x * 8)
-        seg_place_one(a, g, nseg, place_smem + w * 2 * a.tiles_x, lane);
+        seg_place_one(a, T, g, nseg, place_smem + w * 2 * a.tiles_x, lane);
 }
 
 

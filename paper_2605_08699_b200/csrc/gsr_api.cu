@@ -1312,12 +1312,16 @@ int ensure_one_pass(gsr_ctx *c) {
     if (rc || !c->last_sliced) return rc;
     SavedCall sv = c->saved;
     if (!sv.scene) return fail(GSR_E_INVALID, "the last frame's scene is gone");
+    // one pass through completion: a re-render complete_frame does after a
+    // buffer overflow must stay one-pass too (it used to slice again, so a
+    // caller sizing its buffers from the first call's counts could be handed
+    // a different frame's lists)
     c->force_full = true;
     rc = enqueue_frame(c, sv.scene, &sv.cam, sv.bg, sv.sh_degree, sv.cull, sv.want_rgb,
                        sv.want_keep);
+    if (!rc) rc = complete_frame(c);
     c->force_full = false;
-    if (rc) return rc;
-    return complete_frame(c);
+    return rc;
 }
 }  // namespace
 

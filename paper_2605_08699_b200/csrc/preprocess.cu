@@ -208,12 +208,16 @@ __global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
     __shared__ uint32_t s_cnt[8];
     unsigned long long kmn = kept ? key : ~0ull, kmx = kept ? key : 0ull;
     uint32_t cnt = __popc(__ballot_sync(0xffffffffu, kept));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long a = __shfl_xor_sync(0xffffffffu, kmn, o);
-        unsigned long long b = __shfl_xor_sync(0xffffffffu, kmx, o);
-        kmn = a < kmn ? a : kmn;
-        kmx = b > kmx ? b : kmx;
+    {   // warp min / max of the 64-bit keys with 32-bit REDUX: the high words,
+        // then the low words among the lanes holding the extreme high word
+        const uint32_t hmn = __reduce_min_sync(0xffffffffu, (uint32_t)(kmn >> 32));
+        const uint32_t lmn = __reduce_min_sync(
+            0xffffffffu, (uint32_t)(kmn >> 32) == hmn ? (uint32_t)kmn : 0xffffffffu);
+        const uint32_t hmx = __reduce_max_sync(0xffffffffu, (uint32_t)(kmx >> 32));
+        const uint32_t lmx =
+            __reduce_max_sync(0xffffffffu, (uint32_t)(kmx >> 32) == hmx ? (uint32_t)kmx : 0u);
+        kmn = ((unsigned long long)hmn << 32) | lmn;
+        kmx = ((unsigned long long)hmx << 32) | lmx;
     }
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {

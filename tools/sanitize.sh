@@ -1,12 +1,16 @@
 # compute-sanitizer over a small render (config-1-like), the ladder, JPEG and
-# the depth-tie / overflow paths: memcheck (device memory errors) and
+# the depth-tie / overflow paths, depth-sliced frames (forced on the small
+# scene) through render_u8 / render_framebuffer / fresh pipeline contexts:
+# memcheck (device memory errors) and
 # racecheck / synccheck (shared-memory hazards, barrier misuse).
 mkdir -p gpurun_out
 rm -f gpurun_out/sanitizer_summary.txt
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 cat > /tmp/san_case.py <<'PY'
+import os
 import sys
 sys.path.insert(0, ".")
+os.environ["GSR_SLICE_MIN"] = "1"  # every context slices (the pipeline's too)
 import numpy as np
 import paper_2605_08699_b200 as g
 from paper_2605_08699_b200.synth import synthetic_scene
@@ -28,6 +32,20 @@ from paper_2605_08699_b200.synth import make_synthetic_set, serialize_ply
 dp = g.load_ply(serialize_ply(make_synthetic_set(count=5000, seed=4, include_rest=True)))
 g.render_u8(dp, g.CameraPose(0.0, 0.0), intr, sh_degree=3)
 _ = dp.scales, dp.colors_dc, dp.sh_coeffs
+# depth-sliced frames on this small scene (forced): front slices of 15 % and
+# 2 % (a larger second slice), render_u8 + render_framebuffer + a pipeline of
+# fresh contexts (first frames overflow their buffers and re-render)
+for frac in (0.15, 0.02):
+    g.set_slicing(1, frac)
+    for i in range(2):
+        g.render_u8(prims, g.CameraPose(0.03 * i, 0.01, (0.0, 0.0, 0.05)), intr, sh_degree=3)
+    g.render_framebuffer(prims, g.CameraPose(-0.02, 0.0), intr, sh_degree=3)
+    pipe = g.RenderPipeline(intr, sh_degree=3, depth=2)
+    for i in range(3):
+        pipe.submit(prims, g.CameraPose(0.01 * i, 0.0))
+    pipe.drain()
+    pipe.close()
+g.set_slicing(-1, 0.0)
 print("case ok", len(jp), round(s, 6))
 PY
 for tool in memcheck racecheck synccheck; do
