@@ -22,8 +22,9 @@ prims = bench.build_scene(wl)
 intr = bench.intrinsics(wl)
 poses = bench.poses_for(0, int(sys.argv[1]) if len(sys.argv) > 1 else 3)
 st = g.RenderStats()
+mark_all = len(sys.argv) > 3 and sys.argv[3] == "all"  # every frame in the NVTX range
 for i, p in enumerate(poses):
-    last = i == len(poses) - 1
+    last = mark_all or i == len(poses) - 1
     if last:
         torch.cuda.nvtx.range_push("frame")
     g.render_u8(prims, p, intr, sh_degree=wl["sh"], stats=st)
