@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
 // holds.  f32 SH only (every PLY scene; f64 scenes use the kernel above).
 constexpr int kBulkRow = 240;  // 192 B SH + 32 B mean + 16 B pad: 60 words, so a
                                // warp's LDS.128 of 32 rows hits all 32 banks
-constexpr int kBulkWarps = 4;
+constexpr int kBulkWarps = 3;  // two 7.5 KB row buffers per warp: 46 KB per CTA
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
                                          uint32_t mbar) {
@@ -329,52 +329,75 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
         ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
 }
 
+// A warp's chunk of 32 ranks: their Gaussian indices (the order read),
+// then lane 0 arms the chunk buffer's mbarrier with the bytes and every valid
+// lane issues its two bulk copies.
+__device__ __forceinline__ void bulk_issue(const SceneView &sc, const uint32_t *order,
+                                           int64_t r0, int64_t kr, int lane, uint32_t rbase,
+                                           uint32_t mbar) {
+    const int64_t r = r0 + lane;
+    const bool valid = r < kr;
+    const uint32_t bal = __ballot_sync(0xffffffffu, valid);
+    const int64_t i = valid ? (int64_t)__ldg(order + r) : 0;
+    if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     ::"r"(mbar), "r"((uint32_t)__popc(bal) * 224u) : "memory");
+    if (valid) {
+        const uint32_t dst = rbase + (uint32_t)lane * kBulkRow;
+        bulk_g2s(dst, reinterpret_cast<const float *>(sc.sh) + i * 48, 192u, mbar);
+        bulk_g2s(dst + 192u, sc.mean4 + 4 * i, 32u, mbar);
+    }
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
+}
+
+// Double-buffered per warp: chunk k + 1's copies are in flight while chunk k
+// is evaluated.
 template <int DEG>
 __global__ void __launch_bounds__(kBulkWarps * 32) color_ranked_bulk_kernel(
     SceneView sc, const FrameParams *__restrict__ fp, DepthOrder ord,
     const uint32_t *__restrict__ count, float4 *__restrict__ colr) {
-    __shared__ __align__(128) unsigned char rows[kBulkWarps][32 * kBulkRow];
-    __shared__ __align__(8) unsigned long long bar[kBulkWarps];
+    __shared__ __align__(128) unsigned char rows[kBulkWarps][2][32 * kBulkRow];
+    __shared__ __align__(8) unsigned long long bar[kBulkWarps][2];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&bar[w]);
-    const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(&rows[w][0]);
+    // (scalars and selects, not arrays indexed by the buffer: those go to
+    // local memory)
+    const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&bar[w][0]);
+    const uint32_t mbar1 = (uint32_t)__cvta_generic_to_shared(&bar[w][1]);
+    const uint32_t rbase0 = (uint32_t)__cvta_generic_to_shared(&rows[w][0][0]);
+    const uint32_t rbase1 = (uint32_t)__cvta_generic_to_shared(&rows[w][1][0]);
     if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar1) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
     const int64_t kr = (int64_t)*count;
     const CameraArgs &cam = fp->cam;
     const uint32_t *order = ord.sched[16] ? ord.order1 : ord.order0;
-    uint32_t phase = 0;
+    uint32_t phases = 0u;  // bit k: the parity buffer k waits for next
     const int64_t wstride = (int64_t)gridDim.x * kBulkWarps * 32;
-    for (int64_t r0 = ((int64_t)blockIdx.x * kBulkWarps + w) * 32; r0 < kr; r0 += wstride) {
-        const int64_t r = r0 + lane;
-        const bool valid = r < kr;
-        const uint32_t bal = __ballot_sync(0xffffffffu, valid);
-        const int64_t i = valid ? (int64_t)__ldg(order + r) : 0;
-        // the warp's rows were read by the generic proxy in the last round
+    int64_t r0 = ((int64_t)blockIdx.x * kBulkWarps + w) * 32;
+    if (r0 < kr) bulk_issue(sc, order, r0, kr, lane, rbase0, mbar0);
+    for (int b = 0; r0 < kr; r0 += wstride, b ^= 1) {
+        // the other buffer was read by the generic proxy two chunks ago
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                         ::"r"(mbar), "r"((uint32_t)__popc(bal) * 224u) : "memory");
-        if (valid) {
-            const uint32_t dst = rbase + (uint32_t)lane * kBulkRow;
-            bulk_g2s(dst, reinterpret_cast<const float *>(sc.sh) + i * 48, 192u, mbar);
-            bulk_g2s(dst + 192u, sc.mean4 + 4 * i, 32u, mbar);
-        }
-        // wait for the warp's bytes (phase parity flips every round)
-        uint32_t done = 0;
-        while (!done)
-            asm volatile(
-                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-                "selp.u32 %0, 1, 0, p; }"
-                : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
-        phase ^= 1u;
-        if (valid) {
+        if (r0 + wstride < kr)
+            bulk_issue(sc, order, r0 + wstride, kr, lane, b ? rbase0 : rbase1, b ? mbar0 : mbar1);
+        mbar_wait(b ? mbar1 : mbar0, (phases >> b) & 1u);
+        phases ^= 1u << b;
+        const int64_t r = r0 + lane;
+        if (r < kr) {
             constexpr int NC = (DEG + 1) * (DEG + 1) * 3;
-            const unsigned char *row = &rows[w][lane * kBulkRow];
+            const unsigned char *row = &rows[w][b][lane * kBulkRow];
             float v[NC];
 #pragma unroll
             for (int k = 0; k < (NC + 3) / 4; k++) {
@@ -403,8 +426,6 @@ __global__ void __launch_bounds__(kBulkWarps * 32) color_ranked_bulk_kernel(
 }
 
 }  // namespace
-
-
 
 void launch_frame_start(const FrameParams &p, FrameParams *dst, FrameCounters *ctr,
                         cudaStream_t s) {

@@ -356,7 +356,10 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
     // time (independent loads in flight), summing aggregates until it meets
     // an inclusive prefix.
     if (dig) {
-        constexpr int kLbWindow = 8;
+#ifndef GSR_LB_WINDOW
+#define GSR_LB_WINDOW 8
+#endif
+        constexpr int kLbWindow = GSR_LB_WINDOW;
         const int d = threadIdx.x;
 #ifdef GSR_RADIX_NO_LOOKBACK  // microbenchmark only (tools/radix_bench.cu): wrong output
         if (true) {
