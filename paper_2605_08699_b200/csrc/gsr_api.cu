@@ -124,7 +124,7 @@ struct gsr_ctx {
     DevBuf depth_work, depth_work32, sched;  // depth-sort scratch; sched[16] = result buffer
     uint32_t *hsched = nullptr;   // pinned host copy of sched
     // tile-list buffers (binning.cu)
-    DevBuf row_blk, row_start, scan_work, pairs, seg_row, seg_cnt, ttotal, tstart, rowtot, tile_vals;
+    DevBuf row_blk, row_start, scan_work, pairs, seg_cnt, ttotal, rowtot, tile_vals;
     DevBuf ranges;
     DevBuf frame_u8, frame_rgb, frame_t;
     DevBuf colr;          // colours by depth rank of the current pass
@@ -192,8 +192,8 @@ struct gsr_ctx {
     int64_t bytes() const {
         int64_t s = 0;
         const DevBuf *all[] = {&keys[0], &keys[1], &vals[0], &vals[1], &keys32[0], &keys32[1],
-                               &geo, &colr, &state, &unsat_cols, &unsat_items, &ibox, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &seg_row, &rowtot,
-                               &seg_cnt, &ttotal, &tstart, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
+                               &geo, &colr, &state, &unsat_cols, &unsat_items, &ibox, &params, &srec, &keep, &depth_work, &depth_work32, &sched, &row_blk, &row_start, &scan_work, &pairs, &rowtot,
+                               &seg_cnt, &ttotal, &tile_vals, &ranges, &frame_u8, &frame_rgb, &frame_t,
                                &ctr, &base_u8, &up_u8, &tmp_u8, &src_u8, &dst_u8, &coefs,
                                &ssim_part, &ssim_misc, &ssim_w, &jpeg_ws, &ckeys[0], &ckeys[1],
                                &cvals[0], &cvals[1], &cwork, &csched, &cranges, &cdcount, &used};
@@ -268,7 +268,6 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
     const int ntiles = tiles_x * n_rows;
     if ((rc = cens(c, c->ranges, sizeof(uint2) * (size_t)ntiles))) return rc;
     if ((rc = cens(c, c->ttotal, sizeof(uint32_t) * (size_t)ntiles))) return rc;
-    if ((rc = cens(c, c->tstart, sizeof(uint32_t) * (size_t)ntiles))) return rc;
     if ((rc = cens(c, c->rowtot, sizeof(uint32_t) * (size_t)(n_rows + 1)))) return rc;
     if ((rc = cens(c, c->row_blk, sizeof(uint32_t) * (size_t)n_rows * bin_blocks(c->cap_n))))
         return rc;
@@ -277,7 +276,6 @@ int ensure_capacity(gsr_ctx *c, int64_t n, int W, int H, bool want_rgb, bool wan
                                        (size_t)(bin_scan_tiles(bin_blocks(c->cap_n), n_rows) + 1))))
         return rc;
     const int64_t cap_seg = bin_segments(c->cap_p, n_rows);
-    if ((rc = cens(c, c->seg_row, sizeof(uint32_t) * (size_t)(cap_seg + n_rows + 2)))) return rc;
     if ((rc = cens(c, c->seg_cnt, sizeof(uint32_t) * (size_t)cap_seg * tiles_x))) return rc;
     const int64_t px = (int64_t)W * H;
     if ((rc = cens(c, c->frame_u8, (size_t)px * 3))) return rc;
@@ -373,12 +371,9 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         ba.scan_work = c->scan_work.as<unsigned long long>();
         ba.pairs = c->pairs.as<uint2>();
         ba.cap_p = c->cap_p;
-        ba.seg_row = c->seg_row.as<uint32_t>();
         ba.cap_seg = bin_segments(c->cap_p, ba.n_rows);
-        ba.row_seg0 = ba.seg_row + ba.cap_seg;
         ba.seg_cnt = c->seg_cnt.as<uint32_t>();
         ba.tile_total = c->ttotal.as<uint32_t>();
-        ba.tile_start = c->tstart.as<uint32_t>();
         ba.row_total = c->rowtot.as<uint32_t>();
         ba.ranges = c->ranges.as<uint2>();
         ba.tile_vals = c->tile_vals.as<uint32_t>();

@@ -246,13 +246,10 @@ struct BinArgs {
     unsigned long long *scan_work;  // [1 + scan tiles]: ticket, look-back status
     uint2 *pairs;           // [cap_p] (rank, tx0 | count << 16), grouped by tile row
     int64_t cap_p;
-    uint32_t *seg_row;      // [cap_seg] tile row of each segment
-    uint32_t *row_seg0;     // [n_rows + 1] first segment of each tile row
     int64_t cap_seg;
     uint32_t *seg_cnt;      // [cap_seg][tiles_x] keys per column -> offsets
     uint32_t *tile_total;   // [ntiles]
     uint32_t *row_total;    // [n_rows] list entries per tile row (seg_scan)
-    uint32_t *tile_start;   // [ntiles]
     uint2 *ranges;          // [ntiles] [start, end) into tile_vals
     uint32_t *tile_vals;    // [cap_d] depth ranks, tile-major
     int64_t cap_d;

@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(kZBins) slice_plan_kernel(FrameCounters *ctr, 
 // (span key, Gaussian index).  The append order depends on scheduling; the
 // sort and the fix-up order by (span key, f64 key, index), so the order of
 // the slice does not.
-constexpr int kFilterItems = 4;  // Gaussians per thread: all loads of a step in flight at once
+#ifndef GSR_FILTER_ITEMS
+#define GSR_FILTER_ITEMS 4
+#endif
+constexpr int kFilterItems = GSR_FILTER_ITEMS;  // Gaussians per thread: all loads in flight at once
 
 __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
     __shared__ uint32_t s_warp[33];
@@ -72,21 +75,24 @@ __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
     const SpanMap m = span_map(a.ctr->kmin, a.ctr->kmax);
     const uint32_t tau = a.ctr->tau;
     const int64_t i0 = (int64_t)blockIdx.x * (256 * kFilterItems) + threadIdx.x;
+    // keys and item boxes in one round of loads (a box is only used when its
+    // splat lies behind the front slice; culled splats' boxes are never read
+    // as members)
     unsigned long long k64[kFilterItems];
+    uint2 bx[kFilterItems];
 #pragma unroll
     for (int k = 0; k < kFilterItems; k++) {
         const int64_t i = i0 + k * 256;
         k64[k] = i < a.n ? __ldg(a.keys64 + i) : ~0ull;
+        bx[k] = i < a.n ? __ldg(a.ibox + i) : make_uint2(0xffffu, 0u);
     }
     uint32_t k32[kFilterItems];
-    uint2 bx[kFilterItems];
 #pragma unroll
     for (int k = 0; k < kFilterItems; k++) {
         k32[k] = k64[k] != ~0ull ? span_key(m, k64[k]) : 0u;
         // behind the front slice: its box in item rows x tile columns
         // (item_box, written by preprocess_geo)
-        bx[k] = (k64[k] != ~0ull && k32[k] > tau) ? __ldg(a.ibox + i0 + k * 256)
-                                                  : make_uint2(0xffffu, 0u);
+        if (!(k64[k] != ~0ull && k32[k] > tau)) bx[k] = make_uint2(0xffffu, 0u);
     }
     // member: an unsaturated item in the box -- per tile column, the words of
     // its item-row bitmask the box's rows [r0, r1] span (one or two for all
