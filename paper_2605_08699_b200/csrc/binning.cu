@@ -561,8 +561,12 @@ __device__ __forceinline__ void seg_place_one(const BinArgs &a, const SegTable &
 // ------------------------------------------------ per-row lists: 2a-2d fused --
 // (for slices of ~0.4M splats -- 1.8M pairs, ~26k per tile row -- the
 // row-per-CTA build with 32 warps took 0.107 ms vs 0.066 for the segment
-// kernels: it is kept for small second slices only)
-constexpr int kRowWarpsSmall = 8;
+// kernels: it is kept for small second slices only, where 32 warps per row
+// beat 16 and 8: 16.9 / 17.8 / 23.3 us per frame at config 3)
+#ifndef GSR_ROW_WARPS
+#define GSR_ROW_WARPS 32
+#endif
+constexpr int kRowWarpsSmall = GSR_ROW_WARPS;
 // One CTA per tile row builds that row's tile lists from its pairs (a small
 // second slice has few pairs per row, so the segment table, the per-segment
 // counts, the two scans and the placement -- five kernels -- become one):

@@ -286,6 +286,69 @@ __device__ __forceinline__ uint32_t to_u8(float c) {
     return (uint32_t)(int)q;
 }
 
+// render.py:423-427 (rgb += T * bg) and the frame stores of one pixel p of
+// a warp's row (lane = column): f32 planes when asked, u8 -- when the row is
+// packed, the warp's 32 pixels are 96 contiguous bytes: lane l < 24 stores
+// bytes 4l..4l+3 (pixels 4l/3 and (4l+3)/3) as one word, so a row is three
+// full 32 B sectors (full-sector writes also to mapped host memory).
+__device__ __forceinline__ void store_pixel(const BlendOut &out, uint8_t *host, int64_t p,
+                                            int lane, float T, float cr, float cg, float cb,
+                                            float bg0, float bg1, float bg2) {
+    const float rr = cr + T * bg0, gg = cg + T * bg1, bb = cb + T * bg2;
+    if (out.rgb) {
+        out.rgb[3 * p + 0] = rr;
+        out.rgb[3 * p + 1] = gg;
+        out.rgb[3 * p + 2] = bb;
+    }
+    if (out.trans) out.trans[p] = T;
+    const uint32_t px = to_u8(rr) | (to_u8(gg) << 8) | (to_u8(bb) << 16);
+    if (out.packed) {
+        const int a = (4 * lane) / 3, b = min((4 * lane + 3) / 3, 31);
+        const uint32_t pa = __shfl_sync(0xffffffffu, px, a);
+        const uint32_t pb = __shfl_sync(0xffffffffu, px, b);
+        const unsigned long long both = (unsigned long long)pa | ((unsigned long long)pb << 24);
+        const uint32_t word = (uint32_t)(both >> (8 * (lane % 3)));
+        const int64_t wofs = (3 * (p - lane)) / 4 + lane;
+        if (lane < 24) {
+            reinterpret_cast<uint32_t *>(out.u8)[wofs] = word;
+            if (host) reinterpret_cast<uint32_t *>(host)[wofs] = word;
+        }
+    } else {
+        out.u8[3 * p + 0] = (uint8_t)(px & 0xffu);
+        out.u8[3 * p + 1] = (uint8_t)((px >> 8) & 0xffu);
+        out.u8[3 * p + 2] = (uint8_t)(px >> 16);
+    }
+}
+
+// Slice B empty: the items slice A left unsaturated only finish from their
+// saved state (nothing behind the front slice reaches them), so instead of
+// the blend's persistent grid a plain warp per listed item stores its pixels.
+__global__ void __launch_bounds__(128) finish_items_kernel(int width, int height, BlendOut out,
+                                                           const FrameCounters *__restrict__ ctr,
+                                                           SliceState ss) {
+    const float bg0 = out.fp->bg[0], bg1 = out.fp->bg[1], bg2 = out.fp->bg[2];
+    uint8_t *const host = out.fp->host;
+    constexpr int kItems = kTileH / 2;
+    const int tiles_x = (width + kTileW - 1) / kTileW;
+    const int lane = lane_id();
+    const int n = (int)ctr->n_unsat;
+    for (int q = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < n;
+         q += (int)((gridDim.x * blockDim.x) >> 5)) {
+        const int item = (int)__ldg(ss.unsat_items + q);
+        const int tile = item / kItems, wr = item % kItems;
+        const int tx = tile % tiles_x, ty = tile / tiles_x;
+        const int ix = tx * kTileW + lane, iy0 = ty * kTileH + 2 * wr;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            // (warp-uniform when out.packed: W % 32 == 0, so every lane is inside)
+            if (iy0 + h >= height || ix >= width) continue;
+            const int64_t p = (int64_t)(iy0 + h) * width + ix;
+            const float4 st = ss.state[p];
+            store_pixel(out, host, p, lane, st.x, st.y, st.z, st.w, bg0, bg1, bg2);
+        }
+    }
+}
+
 // Persistent kernel: the work items are (tile, pixel-row pair) = one warp's
 // 2x32 pixels; warps take items from a frame-global queue (ctr->blend_next)
 // until it is empty.  Item lengths vary by orders of magnitude (a warp leaves
@@ -542,35 +605,8 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
 #pragma unroll
         for (int h = 0; h < kSets; h++) {
             if (!inside[h]) continue;  // warp-uniform when out.packed
-            const float rr = cr[h] + T[h] * bg0, gg = cg[h] + T[h] * bg1, bb = cb[h] + T[h] * bg2;
-            const int64_t p = (int64_t)(iy0 + h) * width + ix;
-            if (out.rgb) {
-                out.rgb[3 * p + 0] = rr;
-                out.rgb[3 * p + 1] = gg;
-                out.rgb[3 * p + 2] = bb;
-            }
-            if (out.trans) out.trans[p] = T[h];
-            const uint32_t px = to_u8(rr) | (to_u8(gg) << 8) | (to_u8(bb) << 16);
-            if (out.packed) {
-                // the warp's 32 pixels are 96 contiguous bytes: lane l < 24
-                // stores bytes 4l..4l+3 (pixels 4l/3 and (4l+3)/3) as one word,
-                // so a row is three full 32 B sectors (and full-sector writes
-                // when the copy goes to mapped host memory)
-                const int a = (4 * lane) / 3, b = min((4 * lane + 3) / 3, 31);
-                const uint32_t pa = __shfl_sync(0xffffffffu, px, a);
-                const uint32_t pb = __shfl_sync(0xffffffffu, px, b);
-                const unsigned long long both = (unsigned long long)pa | ((unsigned long long)pb << 24);
-                const uint32_t word = (uint32_t)(both >> (8 * (lane % 3)));
-                const int64_t wofs = (3 * (p - lane)) / 4 + lane;
-                if (lane < 24) {
-                    reinterpret_cast<uint32_t *>(out.u8)[wofs] = word;
-                    if (host) reinterpret_cast<uint32_t *>(host)[wofs] = word;
-                }
-            } else {
-                out.u8[3 * p + 0] = (uint8_t)(px & 0xffu);
-                out.u8[3 * p + 1] = (uint8_t)((px >> 8) & 0xffu);
-                out.u8[3 * p + 2] = (uint8_t)(px >> 16);
-            }
+            store_pixel(out, host, (int64_t)(iy0 + h) * width + ix, lane, T[h], cr[h], cg[h],
+                        cb[h], bg0, bg1, bg2);
         }
     }
     if (kCount) {
@@ -633,6 +669,14 @@ int blend_grid(int width, int height) {
     }
     const int tiles = ((width + kTileW - 1) / kTileW) * ((height + kTileH - 1) / kTileH);
     return std::max(1, std::min(g_blend_grid, tiles * kTileH));
+}
+
+void launch_finish_items(int width, int height, BlendOut out, const FrameCounters *ctr,
+                         SliceState ss, int max_items, cudaStream_t s, const KMark &mark) {
+    const int sms_x8 = 148 * 8;
+    const int blocks = std::max(1, std::min((max_items + 3) / 4, sms_x8));
+    finish_items_kernel<<<blocks, 128, 0, s>>>(width, height, out, ctr, ss);
+    mark("finish_items");
 }
 
 void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,

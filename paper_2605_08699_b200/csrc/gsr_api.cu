@@ -67,6 +67,13 @@ int64_t slice_min() {
     }();
     return v;
 }
+// slice-B classes whose lists are built one CTA per tile row (bin_rows):
+// classes below GSR_ROWS_CLASSES (default: all but the last)
+#ifndef GSR_ROWS_CLASSES
+#define GSR_ROWS_CLASSES (kSliceClasses - 1)
+#endif
+inline bool rows_class(int k) { return k < GSR_ROWS_CLASSES; }
+
 float slice_frac() {
     static const float v = [] {
         const char *e = getenv("GSR_SLICE_FRAC");
@@ -482,10 +489,14 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
                                                           nullptr, nullptr, 0,
                                                           cudaStreamCaptureModeThreadLocal));
                 const int before = launches;
-                if (k < kSliceClasses)
+                if (k < kSliceClasses) {
                     sort_color_bin(c->cap_stream, &ctr->KB, nullptr, true, class_cap(k),
-                                   k < kSliceClasses - 1);
-                blend_on(c->cap_stream, 2, ss);
+                                   rows_class(k));
+                    blend_on(c->cap_stream, 2, ss);
+                } else {  // slice B empty: the unsaturated items only finish
+                    launch_finish_items(W, H, out, ctr, ss, (int)n_items, c->cap_stream, mark);
+                    launches += 1;
+                }
                 c->body_launches[k] = launches - before;
                 launches = before;  // counted per frame from the device's class counters
                 cudaGraph_t body = nullptr;
@@ -503,9 +514,13 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
             int k = kSliceClasses - 1;
             for (int j = kSliceClasses - 2; j >= 0; j--)
                 if ((int64_t)kb <= slice_class_cap(j)) k = j;
-            if (kb > 0)
-                sort_color_bin(s, &ctr->KB, nullptr, true, class_cap(k), k < kSliceClasses - 1);
-            blend_on(s, 2, ss);
+            if (kb > 0) {
+                sort_color_bin(s, &ctr->KB, nullptr, true, class_cap(k), rows_class(k));
+                blend_on(s, 2, ss);
+            } else {
+                launch_finish_items(W, H, out, ctr, ss, (int)n_items, s, mark);
+                launches += 1;
+            }
         }
     }
     cudaEventRecordWithFlags(c->ev[5], s, evflags);

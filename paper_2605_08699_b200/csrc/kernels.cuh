@@ -311,6 +311,9 @@ struct SliceState {
     int col_words = 0;              // words per tile column: (item rows + 31) / 32
     uint32_t *unsat_items = nullptr;  // [n_items] their ids; count in FrameCounters.n_unsat
 };
+// slice B empty: the listed unsaturated items' pixels from their saved state
+void launch_finish_items(int width, int height, BlendOut out, const FrameCounters *ctr,
+                         SliceState ss, int max_items, cudaStream_t s, const KMark &mark = KMark());
 void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile_vals,
                   const uint2 *ranges, int width, int height, BlendOut out, FrameCounters *ctr,
                   cudaStream_t s, const KMark &mark = KMark(), bool count = true, int mode = 0,

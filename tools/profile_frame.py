@@ -20,7 +20,9 @@ import paper_2605_08699_b200 as g  # noqa: E402
 wl = bench.WORKLOADS[sys.argv[2] if len(sys.argv) > 2 else "config3"]
 prims = bench.build_scene(wl)
 intr = bench.intrinsics(wl)
-poses = bench.poses_for(0, int(sys.argv[1]) if len(sys.argv) > 1 else 3)
+nf = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+first = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # first pose of the bench trace
+poses = bench.poses_for(0, first + nf)[first:]
 st = g.RenderStats()
 mark_all = len(sys.argv) > 3 and sys.argv[3] == "all"  # every frame in the NVTX range
 for i, p in enumerate(poses):
