@@ -639,8 +639,8 @@ def run_gsr(args, wl):
     # pipelined e2e: RenderPipeline keeps S frames in flight; every step still
     # uploads its camera and copies its u8 frame to pinned host memory
     pipe = g.RenderPipeline(intr, sh_degree=wl["sh"], depth=S, device=local_rank)
-    for i in range(W):
-        pipe.submit(prims, poses[i])
+    for i in range(max(W, len(pipe.ctxs))):  # every context captures its graph here
+        pipe.submit(prims, poses[i % len(poses)])
     pipe.drain()
     checksum = 0
     d.barrier()
@@ -888,9 +888,14 @@ def run_config5(args, wl):
 
     # ---- all-1080p through RenderPipeline ----
     pipe = g.RenderPipeline(intr, sh_degree=3, depth=S, device=local_rank, record_stats=True)
-    for s in mine:  # upload every scene + warm every context
-        for t in range(W):
-            pipe.submit(scenes[s.scene], traces[s.index][t])
+    # upload every scene and warm every (context, scene) pair: a context
+    # captures one CUDA graph per scene configuration on its first frame of
+    # it, which must not land in the timed region (the pipeline's contexts
+    # rotate per submit, so each scene is submitted once per context)
+    nctx = len(pipe.ctxs)
+    for s in mine:
+        for t in range(max(W, nctx)):
+            pipe.submit(scenes[s.scene], traces[s.index][t % 300])
     pipe.drain()
     pipe.frame_ms.clear()
     pipe.kernel_launches = 0
