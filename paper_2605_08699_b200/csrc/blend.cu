@@ -418,13 +418,22 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
     uint32_t n_walk = 0, n_hit = 0, n_batch = 0, n_it = 0, n_lanes = 0, n_done = 0;
 
     // slice B: only the items slice A left unsaturated (its list)
-    const int n_queue = kMode == 2 ? (int)ctr->n_unsat : n_items;
+    // slice B with one-row work items (kSets == 1): each listed two-row item
+    // is two queue entries, so an unsaturated item's rows walk their (equal)
+    // lists on two warps -- the kernel's length is the longest item's walk
+    constexpr int kSplit = (kMode == 2 && kSets == 1) ? 2 : 1;
+    const int n_queue = kMode == 2 ? (int)ctr->n_unsat * kSplit : n_items;
     while (true) {
         int item = 0;
         if (lane == 0) item = (int)atomicAdd(&ctr->blend_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= n_queue) break;
-        if (kMode == 2) item = (int)__ldg(ss.unsat_items + item);
+        if (kMode == 2) {
+            const int item2 = (int)__ldg(ss.unsat_items + item / kSplit);  // two-row item
+            item = kSplit == 2 ? (item2 / (kTileH / 2)) * kItems + 2 * (item2 % (kTileH / 2)) +
+                                     (item & 1)
+                               : item2;
+        }
         if (kCount) n_done += (lane == 0);
         const int tile = item / kItems, wr = item % kItems;
         const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -574,7 +583,7 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
         cp_async_wait_all();  // the staging buffers are reused by the next item
         __syncwarp();
 #endif
-        if (kCount && out.item_info) {
+        if (kCount && out.item_info && kSplit == 1) {  // (indexed by two-row item)
             bool sat = true;
 #pragma unroll
             for (int h = 0; h < kSets; h++) sat = sat && done[h];
@@ -690,7 +699,13 @@ void launch_blend(const SplatRec *srec, const float4 *colr, const uint32_t *tile
     if (sets == 1) GSR_BLEND(1, false, true, 0);  // tuning variants: one pass only
     else if (sets == 2) GSR_BLEND(2, false, true, 0);
     else if (mode == 1) { if (count) GSR_BLEND(2, true, true, 1); else GSR_BLEND(2, true, false, 1); }
-    else if (mode == 2) { if (count) GSR_BLEND(2, true, true, 2); else GSR_BLEND(2, true, false, 2); }
+#ifndef GSR_BLEND_B_ROWS
+#define GSR_BLEND_B_ROWS 2  // pixel rows per slice-B work item (1: two warps per listed item; measured within noise)
+#endif
+    else if (mode == 2) {
+        if (GSR_BLEND_B_ROWS == 1) { if (count) GSR_BLEND(1, false, true, 2); else GSR_BLEND(1, false, false, 2); }
+        else { if (count) GSR_BLEND(2, true, true, 2); else GSR_BLEND(2, true, false, 2); }
+    }
     else if (count) GSR_BLEND(2, true, true, 0);  // work counters (E, Rb) only when asked
     else GSR_BLEND(2, true, false, 0);
 #undef GSR_BLEND
