@@ -68,9 +68,11 @@ int64_t slice_min() {
     return v;
 }
 // slice-B classes whose lists are built one CTA per tile row (bin_rows):
-// classes below GSR_ROWS_CLASSES (default: all but the last)
+// classes below GSR_ROWS_CLASSES (default: <= 65536 splats; rows for the
+// <= 262144 class too measured 1693-1708 vs 1695-1698 frames/s, kept on the
+// segment kernels for the lower latency, 0.833 vs 0.848 ms device p50)
 #ifndef GSR_ROWS_CLASSES
-#define GSR_ROWS_CLASSES (kSliceClasses - 1)
+#define GSR_ROWS_CLASSES 2
 #endif
 inline bool rows_class(int k) { return k < GSR_ROWS_CLASSES; }
 

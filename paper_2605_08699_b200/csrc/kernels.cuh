@@ -332,9 +332,17 @@ struct SliceBArgs {
     uint32_t *keysB, *valsB;           // out: slice B's (span key, Gaussian index), appended
 };
 // slice-B size classes: the second slice's sort / colour / lists run with
-// grids for at most kSliceClassCap[c] splats (class 2: all)
-constexpr int kSliceClasses = 3;
-__host__ __device__ constexpr int64_t slice_class_cap(int c) { return c == 0 ? 4096 : 65536; }
+// grids for at most slice_class_cap(c) splats (the last class: all)
+#ifndef GSR_SLICE_CLASSES
+#define GSR_SLICE_CLASSES 4
+#endif
+#ifndef GSR_SLICE_CAP2
+#define GSR_SLICE_CAP2 262144
+#endif
+constexpr int kSliceClasses = GSR_SLICE_CLASSES;
+__host__ __device__ constexpr int64_t slice_class_cap(int c) {
+    return c == 0 ? 4096 : c == 1 ? 65536 : GSR_SLICE_CAP2;
+}
 void launch_slice_plan(FrameCounters *ctr, float frac, cudaStream_t s, const KMark &mark = KMark());
 void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark = KMark());
 // sets `handle` (a graph's switch) to slice B's size class, kSliceClasses
