@@ -363,11 +363,16 @@ __global__ void __launch_bounds__(128) finish_items_kernel(int width, int height
 // per pixel in `state`, sets its bit in unsat_cols and lists itself in
 // unsat_items.  2: slice B -- only the listed items, continuing from `state`.
 template <int kSets, bool kPairLoop, bool kCount, int kMode>
-// 7 CTAs (28 warps) per SM: 71 registers keep the exp constants in registers
-// (at 8 CTAs / 64 registers ptxas reloads four of them from constant memory
-// in every composite iteration); one-call device p50 1.011 -> 1.005 ms
+// 6 CTAs (24 warps) per SM, 80 registers, with the expf constants read from
+// shared memory (below): the composite-pair iteration is 84 instructions with
+// no constant reloads (88 with four LDC.64 at 7 CTAs / 72 registers); blend
+// 0.3445 -> 0.3408-0.3423 ms, one-call device p50 0.831-0.834 -> 0.824 ms at
+// config 3 (8 CTAs: 0.349-0.351 ms)
 #ifndef GSR_BLEND_MINB
-#define GSR_BLEND_MINB 7
+#define GSR_BLEND_MINB 6
+#endif
+#ifndef GSR_EXPK_CONST
+#define GSR_EXPK_SMEM 1
 #endif
 __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB) blend_kernel(
     const SplatRec *__restrict__ srec, const float4 *__restrict__ colr,
@@ -385,6 +390,10 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
     }
 #else
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+#endif
+#ifdef GSR_EXPK_SMEM
+    __shared__ double s_ek[4];
+    if (threadIdx.x < 4) s_ek[threadIdx.x] = kExpK[threadIdx.x];
 #endif
     {   // zero records (the null slot is never written afterwards)
         float4 *z = reinterpret_cast<float4 *>(s_b);
@@ -410,10 +419,22 @@ __global__ void __launch_bounds__(kBlendThreads, kSets == 1 ? 9 : GSR_BLEND_MINB
     asm volatile("mov.u32 %0, %1;" : "=r"(tab_s) : "r"((uint32_t)__cvta_generic_to_shared(s_tab)));
     // pinned in registers (opaque to rematerialisation by constant reloads)
     ExpK ek;
+#ifdef GSR_EXPK_SMEM
+    // from shared memory: ptxas cannot rematerialise a shared load, so the
+    // four constants stay in registers instead of four LDC.64 per iteration
+    {
+        const uint32_t a = (uint32_t)__cvta_generic_to_shared(s_ek);
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(ek.inv_ln2n) : "r"(a));
+        asm volatile("ld.shared.f64 %0, [%1+8];" : "=d"(ek.c0) : "r"(a));
+        asm volatile("ld.shared.f64 %0, [%1+16];" : "=d"(ek.c1) : "r"(a));
+        asm volatile("ld.shared.f64 %0, [%1+24];" : "=d"(ek.c2) : "r"(a));
+    }
+#else
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.inv_ln2n) : "d"(kExpK[0]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c0) : "d"(kExpK[1]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c1) : "d"(kExpK[2]));
     asm volatile("mov.b64 %0, %1;" : "=d"(ek.c2) : "d"(kExpK[3]));
+#endif
     uint32_t n_comp = 0, n_rows = 0;  // work counters (roofline)
     uint32_t n_walk = 0, n_hit = 0, n_batch = 0, n_it = 0, n_lanes = 0, n_done = 0;
 
