@@ -91,123 +91,127 @@ __global__ void __launch_bounds__(256) frame_start_kernel(FrameParams p, FramePa
 }
 
 
-#ifndef GSR_PP_MINB
-#define GSR_PP_MINB 4  // 64 registers, no spill: 0.1124 -> 0.1075 ms at config 3 (5: 51 registers + 94 B spilled)
-#endif
-__global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
-    SceneView sc, const FrameParams *__restrict__ fp, int do_cull,
-    unsigned long long *__restrict__ keys, GeoRec *__restrict__ geo,
-    uint8_t *__restrict__ keep_out, FrameCounters *ctr, uint32_t *__restrict__ zhist,
-    uint2 *__restrict__ ibox) {
-    __shared__ CameraArgs cam;  // this frame's camera (FrameParams), staged once per block
-    __shared__ uint32_t s_zh[kZBins];
-    if (zhist)
-        for (int j = threadIdx.x; j < kZBins; j += blockDim.x) s_zh[j] = 0u;
-    if (threadIdx.x < sizeof(CameraArgs) / 8)
-        reinterpret_cast<unsigned long long *>(&cam)[threadIdx.x] =
-            reinterpret_cast<const unsigned long long *>(&fp->cam)[threadIdx.x];
-    __syncthreads();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t st = sc.stride;
-    bool kept = false;
-    unsigned long long key = ~0ull;
-    if (i < sc.n) {
-        const double r00 = cam.r[0], r01 = cam.r[1], r02 = cam.r[2];
-        const double r10 = cam.r[3], r11 = cam.r[4], r12 = cam.r[5];
-        const double r20 = cam.r[6], r21 = cam.r[7], r22 = cam.r[8];
-        // every load first (one memory round trip), then the f64 math
-        const double mx = __ldg(sc.mean + i), my = __ldg(sc.mean + st + i),
-                     mz = __ldg(sc.mean + 2 * st + i);
-        const double qw = __ldg(sc.rot + i), qx = __ldg(sc.rot + st + i),
-                     qy = __ldg(sc.rot + 2 * st + i), qz = __ldg(sc.rot + 3 * st + i);
-        const double sx = __ldg(sc.scale + i), sy = __ldg(sc.scale + st + i),
-                     sz = __ldg(sc.scale + 2 * st + i);
-        const double rsq = __ldg(sc.rsq + i);
-        const float opac = __ldg(sc.opac + i);
-        // render.py:174-176
-        const double x = r00 * mx + r01 * my + r02 * mz + cam.t[0];
-        const double y = r10 * mx + r11 * my + r12 * mz + cam.t[1];
-        const double z = r20 * mx + r21 * my + r22 * mz + cam.t[2];
-        if (!(z <= kZNear)) {
-            // render.py:185-193
-            const double m00 = (1.0 - 2.0 * (qy * qy + qz * qz)) * sx;
-            const double m01 = (2.0 * (qx * qy - qw * qz)) * sy;
-            const double m02 = (2.0 * (qx * qz + qw * qy)) * sz;
-            const double m10 = (2.0 * (qx * qy + qw * qz)) * sx;
-            const double m11 = (1.0 - 2.0 * (qx * qx + qz * qz)) * sy;
-            const double m12 = (2.0 * (qy * qz - qw * qx)) * sz;
-            const double m20 = (2.0 * (qx * qz - qw * qy)) * sx;
-            const double m21 = (2.0 * (qy * qz + qw * qx)) * sy;
-            const double m22 = (1.0 - 2.0 * (qx * qx + qy * qy)) * sz;
-            // render.py:196-204
-            const double a00 = r00 * m00 + r01 * m10 + r02 * m20;
-            const double a01 = r00 * m01 + r01 * m11 + r02 * m21;
-            const double a02 = r00 * m02 + r01 * m12 + r02 * m22;
-            const double a10 = r10 * m00 + r11 * m10 + r12 * m20;
-            const double a11 = r10 * m01 + r11 * m11 + r12 * m21;
-            const double a12 = r10 * m02 + r11 * m12 + r12 * m22;
-            const double a20 = r20 * m00 + r21 * m10 + r22 * m20;
-            const double a21 = r20 * m01 + r21 * m11 + r22 * m21;
-            const double a22 = r20 * m02 + r21 * m12 + r22 * m22;
-            // render.py:206-220
-            const double inv_z = 1.0 / z;
-            const double jx = cam.fx * inv_z;
-            const double jy = cam.fy * inv_z;
-            const double gx = -cam.fx * x * inv_z * inv_z;
-            const double gy = -cam.fy * y * inv_z * inv_z;
-            const double p0 = jx * a00 + gx * a20;
-            const double p1 = jx * a01 + gx * a21;
-            const double p2 = jx * a02 + gx * a22;
-            const double q0 = jy * a10 + gy * a20;
-            const double q1 = jy * a11 + gy * a21;
-            const double q2 = jy * a12 + gy * a22;
-            const double ca = p0 * p0 + p1 * p1 + p2 * p2 + kCovFloor;
-            const double cb = p0 * q0 + p1 * q1 + p2 * q2;
-            const double cc = q0 * q0 + q1 * q1 + q2 * q2 + kCovFloor;
-            // render.py:222-223
-            const double u = cam.fx * x * inv_z + cam.cx;
-            const double v = cam.fy * y * inv_z + cam.cy;
-            bool k = true;
-            // render.py:230-235.  A splat whose centre lies inside the image
-            // is kept whatever its radius, as long as the radius is not NaN
-            // (finite covariance: ca, cc >= 0.3, so mid + sqrt(disc) > 0):
-            // the two f64 square roots are only needed near and outside the
-            // border -- the same keep mask, fewer instructions
-            const bool inside = u > 0.0 && u < cam.width && v > 0.0 && v < cam.height &&
-                                isfinite(ca) && isfinite(cb) && isfinite(cc);
-            if (do_cull && !inside) {
-                const double mid = 0.5 * (ca + cc);
-                const double d = ca - cc;
-                const double disc = 0.25 * (d * d) + cb * cb;
-                const double radius = kCutoffSigma * sqrt(mid + sqrt(disc));
-                k = (u + radius > 0.0 && u - radius < cam.width && v + radius > 0.0 &&
-                     v - radius < cam.height);
-            }
-            if (k) {
-                kept = true;
-                key = (unsigned long long)__double_as_longlong(z);
-                if (zhist) {
-                    const int bin = (int)(key >> kZBinShift) - kZBinBase;
-                    atomicAdd(&s_zh[bin < 0 ? 0 : (bin >= kZBins ? kZBins - 1 : bin)], 1u);
-                }
-                // render.py:442-453
-                const double det = ca * cc - cb * cb;
-                const float ia32 = (float)(cc / det);
-                GeoRec o;
-                o.a = make_float4((float)u, (float)v, ia32, (float)(-cb / det));
-                o.b = make_float4((float)(ca / det), (float)rsq, opac, (float)sqrt(cc * rsq));
-                geo[i] = o;
-                if (ibox) ibox[i] = item_box(o, cam.iwidth, cam.iheight);
-            }
-        }
-        keys[i] = key;
-        if (keep_out) keep_out[i] = kept ? 1 : 0;
+// cp.async.bulk global -> shared, completing on an mbarrier (tx bytes)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
+}
+
+// One Gaussian's inputs (SoA planes), loaded by the caller -- from global
+// memory, or from a shared-memory stage filled by the bulk-copy engine.
+struct PPIn {
+    double mx, my, mz, qw, qx, qy, qz, sx, sy, sz, rsq;
+    float opac;
+};
+
+// Projection, cull and packing of Gaussian i (render.py:174-235, 442-453):
+// writes geo[i] / ibox[i] and the depth histogram when kept; returns kept and
+// sets key (the f64 bits of z, ~0 when culled).
+__device__ __forceinline__ bool pp_one(const CameraArgs &cam, int do_cull, int64_t i,
+                                       const PPIn &in, GeoRec *__restrict__ geo,
+                                       uint2 *__restrict__ ibox, uint32_t *s_zh,
+                                       unsigned long long &key) {
+    const double r00 = cam.r[0], r01 = cam.r[1], r02 = cam.r[2];
+    const double r10 = cam.r[3], r11 = cam.r[4], r12 = cam.r[5];
+    const double r20 = cam.r[6], r21 = cam.r[7], r22 = cam.r[8];
+    const double mx = in.mx, my = in.my, mz = in.mz;
+    const double qw = in.qw, qx = in.qx, qy = in.qy, qz = in.qz;
+    const double sx = in.sx, sy = in.sy, sz = in.sz;
+    key = ~0ull;
+    // render.py:174-176
+    const double x = r00 * mx + r01 * my + r02 * mz + cam.t[0];
+    const double y = r10 * mx + r11 * my + r12 * mz + cam.t[1];
+    const double z = r20 * mx + r21 * my + r22 * mz + cam.t[2];
+    if (z <= kZNear) return false;
+    // render.py:185-193
+    const double m00 = (1.0 - 2.0 * (qy * qy + qz * qz)) * sx;
+    const double m01 = (2.0 * (qx * qy - qw * qz)) * sy;
+    const double m02 = (2.0 * (qx * qz + qw * qy)) * sz;
+    const double m10 = (2.0 * (qx * qy + qw * qz)) * sx;
+    const double m11 = (1.0 - 2.0 * (qx * qx + qz * qz)) * sy;
+    const double m12 = (2.0 * (qy * qz - qw * qx)) * sz;
+    const double m20 = (2.0 * (qx * qz - qw * qy)) * sx;
+    const double m21 = (2.0 * (qy * qz + qw * qx)) * sy;
+    const double m22 = (1.0 - 2.0 * (qx * qx + qy * qy)) * sz;
+    // render.py:196-204
+    const double a00 = r00 * m00 + r01 * m10 + r02 * m20;
+    const double a01 = r00 * m01 + r01 * m11 + r02 * m21;
+    const double a02 = r00 * m02 + r01 * m12 + r02 * m22;
+    const double a10 = r10 * m00 + r11 * m10 + r12 * m20;
+    const double a11 = r10 * m01 + r11 * m11 + r12 * m21;
+    const double a12 = r10 * m02 + r11 * m12 + r12 * m22;
+    const double a20 = r20 * m00 + r21 * m10 + r22 * m20;
+    const double a21 = r20 * m01 + r21 * m11 + r22 * m21;
+    const double a22 = r20 * m02 + r21 * m12 + r22 * m22;
+    // render.py:206-220
+    const double inv_z = 1.0 / z;
+    const double jx = cam.fx * inv_z;
+    const double jy = cam.fy * inv_z;
+    const double gx = -cam.fx * x * inv_z * inv_z;
+    const double gy = -cam.fy * y * inv_z * inv_z;
+    const double p0 = jx * a00 + gx * a20;
+    const double p1 = jx * a01 + gx * a21;
+    const double p2 = jx * a02 + gx * a22;
+    const double q0 = jy * a10 + gy * a20;
+    const double q1 = jy * a11 + gy * a21;
+    const double q2 = jy * a12 + gy * a22;
+    const double ca = p0 * p0 + p1 * p1 + p2 * p2 + kCovFloor;
+    const double cb = p0 * q0 + p1 * q1 + p2 * q2;
+    const double cc = q0 * q0 + q1 * q1 + q2 * q2 + kCovFloor;
+    // render.py:222-223
+    const double u = cam.fx * x * inv_z + cam.cx;
+    const double v = cam.fy * y * inv_z + cam.cy;
+    // render.py:230-235.  A splat whose centre lies inside the image is kept
+    // whatever its radius, as long as the radius is not NaN (finite
+    // covariance: ca, cc >= 0.3, so mid + sqrt(disc) > 0): the two f64 square
+    // roots are only needed near and outside the border -- the same keep
+    // mask, fewer instructions
+    const bool inside = u > 0.0 && u < cam.width && v > 0.0 && v < cam.height &&
+                        isfinite(ca) && isfinite(cb) && isfinite(cc);
+    if (do_cull && !inside) {
+        const double mid = 0.5 * (ca + cc);
+        const double d = ca - cc;
+        const double disc = 0.25 * (d * d) + cb * cb;
+        const double radius = kCutoffSigma * sqrt(mid + sqrt(disc));
+        if (!(u + radius > 0.0 && u - radius < cam.width && v + radius > 0.0 &&
+              v - radius < cam.height))
+            return false;
     }
-    // block reduction of K and of the kept key range (radix pass trimming)
+    key = (unsigned long long)__double_as_longlong(z);
+    if (s_zh) {
+        const int bin = (int)(key >> kZBinShift) - kZBinBase;
+        atomicAdd(&s_zh[bin < 0 ? 0 : (bin >= kZBins ? kZBins - 1 : bin)], 1u);
+    }
+    // render.py:442-453
+    const double det = ca * cc - cb * cb;
+    const float ia32 = (float)(cc / det);
+    GeoRec o;
+    o.a = make_float4((float)u, (float)v, ia32, (float)(-cb / det));
+    o.b = make_float4((float)(ca / det), (float)in.rsq, in.opac, (float)sqrt(cc * in.rsq));
+    geo[i] = o;
+    if (ibox) ibox[i] = item_box(o, cam.iwidth, cam.iheight);
+    return true;
+}
+
+// Block reduction of K and of the kept key range (radix pass trimming), and
+// the block's depth histogram into the frame's.
+__device__ __forceinline__ void pp_reduce(uint32_t cnt, unsigned long long kmn,
+                                          unsigned long long kmx, const uint32_t *s_zh,
+                                          uint32_t *zhist, FrameCounters *ctr) {
     __shared__ unsigned long long s_min[8], s_max[8];
     __shared__ uint32_t s_cnt[8];
-    unsigned long long kmn = kept ? key : ~0ull, kmx = kept ? key : 0ull;
-    uint32_t cnt = __popc(__ballot_sync(0xffffffffu, kept));
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
     {   // warp min / max of the 64-bit keys with 32-bit REDUX: the high words,
         // then the low words among the lanes holding the extreme high word
         const uint32_t hmn = __reduce_min_sync(0xffffffffu, (uint32_t)(kmn >> 32));
@@ -242,6 +246,159 @@ __global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
             atomicMax(&ctr->kmax, kmx);
         }
     }
+}
+
+#ifndef GSR_PP_MINB
+#define GSR_PP_MINB 4  // 64 registers, no spill: 0.1124 -> 0.1075 ms at config 3 (5: 51 registers + 94 B spilled)
+#endif
+// One Gaussian per thread, its 92 B loaded from global memory first (one
+// memory round trip), then the f64 math.
+__global__ void __launch_bounds__(256, GSR_PP_MINB) preprocess_geo_kernel(
+    SceneView sc, const FrameParams *__restrict__ fp, int do_cull,
+    unsigned long long *__restrict__ keys, GeoRec *__restrict__ geo,
+    uint8_t *__restrict__ keep_out, FrameCounters *ctr, uint32_t *__restrict__ zhist,
+    uint2 *__restrict__ ibox) {
+    __shared__ CameraArgs cam;  // this frame's camera (FrameParams), staged once per block
+    __shared__ uint32_t s_zh[kZBins];
+    if (zhist)
+        for (int j = threadIdx.x; j < kZBins; j += blockDim.x) s_zh[j] = 0u;
+    if (threadIdx.x < sizeof(CameraArgs) / 8)
+        reinterpret_cast<unsigned long long *>(&cam)[threadIdx.x] =
+            reinterpret_cast<const unsigned long long *>(&fp->cam)[threadIdx.x];
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t st = sc.stride;
+    bool kept = false;
+    unsigned long long key = ~0ull;
+    if (i < sc.n) {
+        PPIn in;
+        in.mx = __ldg(sc.mean + i);
+        in.my = __ldg(sc.mean + st + i);
+        in.mz = __ldg(sc.mean + 2 * st + i);
+        in.qw = __ldg(sc.rot + i);
+        in.qx = __ldg(sc.rot + st + i);
+        in.qy = __ldg(sc.rot + 2 * st + i);
+        in.qz = __ldg(sc.rot + 3 * st + i);
+        in.sx = __ldg(sc.scale + i);
+        in.sy = __ldg(sc.scale + st + i);
+        in.sz = __ldg(sc.scale + 2 * st + i);
+        in.rsq = __ldg(sc.rsq + i);
+        in.opac = __ldg(sc.opac + i);
+        kept = pp_one(cam, do_cull, i, in, geo, ibox, zhist ? s_zh : nullptr, key);
+        keys[i] = key;
+        if (keep_out) keep_out[i] = kept ? 1 : 0;
+    }
+    pp_reduce(kept ? 1u : 0u, kept ? key : ~0ull, kept ? key : 0ull, s_zh, zhist, ctr);
+}
+
+// The same per-Gaussian work with the inputs brought in by the bulk-copy
+// (TMA) engine: a persistent CTA takes tiles of 256 Gaussians; one thread
+// issues the tile's twelve plane chunks (11 x 2 KB f64 + 1 KB f32, contiguous
+// in the SoA planes) as cp.async.bulk copies into one of two shared stages,
+// completing on the stage's mbarrier, so tile k + 1's 23.5 KB are in flight
+// while tile k computes.  (The one-shot kernel above issues its loads once
+// per thread and then computes for ~800 instructions: CTAs of a wave load
+// and compute in phase, and HBM idles during the compute.)
+constexpr int kPPTile = 256;
+struct PPStage {
+    double m[3][kPPTile];
+    double q[4][kPPTile];
+    double s[3][kPPTile];
+    double rsq[kPPTile];
+    float op[kPPTile];
+};
+#ifndef GSR_PPB_MINB
+#define GSR_PPB_MINB 4
+#endif
+__device__ __forceinline__ void pp_issue(const SceneView &sc, int64_t t, uint32_t stage,
+                                         uint32_t mbar) {
+    const int64_t st = sc.stride;
+    const int64_t i0 = t * kPPTile;
+    const int64_t cnt = st - i0 < kPPTile ? st - i0 : kPPTile;  // multiple of 32
+    const uint32_t b64 = (uint32_t)cnt * 8u, b32 = (uint32_t)cnt * 4u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(mbar), "r"(11u * b64 + b32) : "memory");
+    constexpr uint32_t P = kPPTile * 8;  // one f64 plane chunk in the stage
+#pragma unroll
+    for (int k = 0; k < 3; k++) bulk_g2s(stage + k * P, sc.mean + k * st + i0, b64, mbar);
+#pragma unroll
+    for (int k = 0; k < 4; k++) bulk_g2s(stage + (3 + k) * P, sc.rot + k * st + i0, b64, mbar);
+#pragma unroll
+    for (int k = 0; k < 3; k++) bulk_g2s(stage + (7 + k) * P, sc.scale + k * st + i0, b64, mbar);
+    bulk_g2s(stage + 10 * P, sc.rsq + i0, b64, mbar);
+    bulk_g2s(stage + 11 * P, sc.opac + i0, b32, mbar);
+}
+
+__global__ void __launch_bounds__(kPPTile, GSR_PPB_MINB) preprocess_geo_bulk_kernel(
+    SceneView sc, const FrameParams *__restrict__ fp, int do_cull,
+    unsigned long long *__restrict__ keys, GeoRec *__restrict__ geo,
+    uint8_t *__restrict__ keep_out, FrameCounters *ctr, uint32_t *__restrict__ zhist,
+    uint2 *__restrict__ ibox) {
+    extern __shared__ __align__(128) unsigned char pp_smem[];
+    PPStage *stg = reinterpret_cast<PPStage *>(pp_smem);  // [2]
+    __shared__ CameraArgs cam;
+    __shared__ uint32_t s_zh[kZBins];
+    __shared__ __align__(8) unsigned long long bar[2];
+    const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
+    const uint32_t mbar1 = (uint32_t)__cvta_generic_to_shared(&bar[1]);
+    const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&stg[0]);
+    const uint32_t stage1 = (uint32_t)__cvta_generic_to_shared(&stg[1]);
+    const int64_t n_tiles = (sc.n + kPPTile - 1) / kPPTile;
+    if (zhist)
+        for (int j = threadIdx.x; j < kZBins; j += blockDim.x) s_zh[j] = 0u;
+    if (threadIdx.x < sizeof(CameraArgs) / 8)
+        reinterpret_cast<unsigned long long *>(&cam)[threadIdx.x] =
+            reinterpret_cast<const unsigned long long *>(&fp->cam)[threadIdx.x];
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if ((int64_t)blockIdx.x < n_tiles) pp_issue(sc, blockIdx.x, stage0, mbar0);
+    }
+    __syncthreads();
+    uint32_t cnt = 0u;
+    unsigned long long kmn = ~0ull, kmx = 0ull;
+    uint32_t phases = 0u;  // bit b: the parity stage b waits for next
+    int b = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, b ^= 1) {
+        if (threadIdx.x == 0 && t + gridDim.x < n_tiles) {
+            // the other stage was last read (generic proxy) before the
+            // __syncthreads ending the previous tile
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            pp_issue(sc, t + gridDim.x, b ? stage0 : stage1, b ? mbar0 : mbar1);
+        }
+        mbar_wait(b ? mbar1 : mbar0, (phases >> b) & 1u);
+        phases ^= 1u << b;
+        const int64_t i = t * kPPTile + threadIdx.x;
+        if (i < sc.n) {
+            const PPStage &S = stg[b];
+            const int j = threadIdx.x;
+            PPIn in;
+            in.mx = S.m[0][j];
+            in.my = S.m[1][j];
+            in.mz = S.m[2][j];
+            in.qw = S.q[0][j];
+            in.qx = S.q[1][j];
+            in.qy = S.q[2][j];
+            in.qz = S.q[3][j];
+            in.sx = S.s[0][j];
+            in.sy = S.s[1][j];
+            in.sz = S.s[2][j];
+            in.rsq = S.rsq[j];
+            in.opac = S.op[j];
+            unsigned long long key;
+            const bool kept = pp_one(cam, do_cull, i, in, geo, ibox, zhist ? s_zh : nullptr, key);
+            keys[i] = key;
+            if (keep_out) keep_out[i] = kept ? 1 : 0;
+            if (kept) {
+                cnt++;
+                kmn = key < kmn ? key : kmn;
+                kmx = key > kmx ? key : kmx;
+            }
+        }
+        __syncthreads();  // stage b is refilled by the tile after next
+    }
+    pp_reduce(cnt, kmn, kmx, s_zh, zhist, ctr);
 }
 
 // Colour of the splat at depth rank r of a pass (order[r] = Gaussian index):
@@ -322,13 +479,6 @@ constexpr int kBulkRow = 240;  // 192 B SH + 32 B mean + 16 B pad: 60 words, so 
                                // warp's LDS.128 of 32 rows hits all 32 banks
 constexpr int kBulkWarps = 3;  // two 7.5 KB row buffers per warp: 46 KB per CTA
 
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
-                                         uint32_t mbar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
-}
-
 // A warp's chunk of 32 ranks: their Gaussian indices (the order read),
 // then lane 0 arms the chunk buffer's mbarrier with the bytes and every valid
 // lane issues its two bulk copies.
@@ -347,15 +497,6 @@ __device__ __forceinline__ void bulk_issue(const SceneView &sc, const uint32_t *
         bulk_g2s(dst, reinterpret_cast<const float *>(sc.sh) + i * 48, 192u, mbar);
         bulk_g2s(dst + 192u, sc.mean4 + 4 * i, 32u, mbar);
     }
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
-    uint32_t done = 0;
-    while (!done)
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-            "selp.u32 %0, 1, 0, p; }"
-            : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
 }
 
 // Double-buffered per warp: chunk k + 1's copies are in flight while chunk k
@@ -439,10 +580,35 @@ void launch_preprocess_geo(const SceneView &scene, const FrameParams *fp, int fr
                            FrameCounters *ctr, uint32_t *zhist, uint2 *ibox, cudaStream_t s,
                            const KMark &mark) {
     if (scene.n == 0) return;
-    const int threads = 256;
-    const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
-    preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, fp, frustum_cull, keys, geo,
-                                                     keep_out, ctr, zhist, ibox);
+#ifndef GSR_PP_BULK
+#define GSR_PP_BULK 1
+#endif
+    if (GSR_PP_BULK) {
+        static int sms = 0;  // (one device model per process)
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+            // the largest shared carveout: GSR_PPB_MINB CTAs of ~52 KB per SM
+            cudaFuncSetAttribute(preprocess_geo_bulk_kernel,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            // (the default dynamic limit is 48 KB minus the static 5.5 KB)
+            cudaFuncSetAttribute(preprocess_geo_bulk_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(2 * sizeof(PPStage)));
+        }
+        const int64_t tiles = (scene.n + kPPTile - 1) / kPPTile;
+        const unsigned blocks =
+            (unsigned)std::min<int64_t>(tiles, (int64_t)sms * GSR_PPB_MINB);
+        preprocess_geo_bulk_kernel<<<blocks, kPPTile, 2 * sizeof(PPStage), s>>>(
+            scene, fp, frustum_cull, keys, geo, keep_out, ctr, zhist, ibox);
+    } else {
+        const int threads = 256;
+        const unsigned blocks = (unsigned)((scene.n + threads - 1) / threads);
+        preprocess_geo_kernel<<<blocks, threads, 0, s>>>(scene, fp, frustum_cull, keys, geo,
+                                                         keep_out, ctr, zhist, ibox);
+    }
     mark("preprocess_geo");
 }
 
