@@ -27,6 +27,8 @@
 // unsaturated pixel sees every splat covering it in the reference's order:
 // frames are bit-identical to the one-pass render (tests/test_gpu_parity.py
 // compares both paths and the oracle).
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "scan.cuh"
 
@@ -66,67 +68,92 @@ __global__ void __launch_bounds__(kZBins) slice_plan_kernel(FrameCounters *ctr, 
 #define GSR_FILTER_ITEMS 4
 #endif
 constexpr int kFilterItems = GSR_FILTER_ITEMS;  // Gaussians per thread: all loads in flight at once
+constexpr int kFilterSmemWords = 12288;         // bitmask staged in shared memory up to 48 KB
 
+// Membership of one box in the unsaturated-item bitmask `cols` ([tiles_x]
+// [col_words], column-major): per tile column c0..c1, the box's rows
+// [r0, r1] are words w0..w1 (one for all but tall splats), masked at both
+// ends.  The words are OR-ed without an early exit, so the loads are
+// independent (most splats behind the slice are not members: the whole box
+// is read either way).
+__device__ __forceinline__ bool box_member(const uint32_t *cols, int col_words, uint2 bx) {
+    const uint32_t r0 = bx.x & 0xffffu, r1 = bx.x >> 16;
+    const uint32_t c0 = bx.y & 0xffffu, c1 = bx.y >> 16;
+    if (r0 > r1 || c0 > c1) return false;
+    const uint32_t w0 = r0 >> 5, w1 = r1 >> 5;
+    const uint32_t mlo = ~0u << (r0 & 31), mhi = ~0u >> (31 - (r1 & 31));
+    uint32_t acc = 0u;
+    const uint32_t *p = cols + c0 * (uint32_t)col_words + w0;
+    if (w0 == w1) {
+        const uint32_t mm = mlo & mhi;
+        for (uint32_t c = c0; c <= c1; c++, p += col_words) acc |= *p & mm;
+    } else {
+        for (uint32_t c = c0; c <= c1; c++, p += col_words) {
+            acc |= p[0] & mlo;
+            for (uint32_t w = 1; w < w1 - w0; w++) acc |= p[w];
+            acc |= p[w1 - w0] & mhi;
+        }
+    }
+    return acc != 0u;
+}
+
+// Persistent: each CTA stages the bitmask in shared memory once (4 KB at
+// 1080p), then takes blocks of 256 x kFilterItems Gaussians.
+template <bool kSmem>
 __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
+    extern __shared__ uint32_t s_cols[];
     __shared__ uint32_t s_warp[33];
     __shared__ uint32_t s_base;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.ctr->blend_next = 0u;  // blend A has finished
     if (a.ctr->n_unsat == 0u) return;  // (block-uniform)
+    const uint32_t *cols = a.unsat_cols;
+    if (kSmem) {
+        const int nw = a.tiles_x * a.col_words;
+        for (int j = threadIdx.x; j < nw; j += blockDim.x) s_cols[j] = __ldg(a.unsat_cols + j);
+        __syncthreads();
+        cols = s_cols;
+    }
     const SpanMap m = span_map(a.ctr->kmin, a.ctr->kmax);
     const uint32_t tau = a.ctr->tau;
-    const int64_t i0 = (int64_t)blockIdx.x * (256 * kFilterItems) + threadIdx.x;
-    // keys and item boxes in one round of loads (a box is only used when its
-    // splat lies behind the front slice; culled splats' boxes are never read
-    // as members)
-    unsigned long long k64[kFilterItems];
-    uint2 bx[kFilterItems];
+    const int64_t step = (int64_t)gridDim.x * (256 * kFilterItems);
+    for (int64_t i0 = (int64_t)blockIdx.x * (256 * kFilterItems) + threadIdx.x;
+         i0 - threadIdx.x < a.n; i0 += step) {
+        // keys and item boxes in one round of loads (a box is only used when
+        // its splat lies behind the front slice; culled splats' boxes are
+        // never read as members)
+        unsigned long long k64[kFilterItems];
+        uint2 bx[kFilterItems];
 #pragma unroll
-    for (int k = 0; k < kFilterItems; k++) {
-        const int64_t i = i0 + k * 256;
-        k64[k] = i < a.n ? __ldg(a.keys64 + i) : ~0ull;
-        bx[k] = i < a.n ? __ldg(a.ibox + i) : make_uint2(0xffffu, 0u);
-    }
-    uint32_t k32[kFilterItems];
-#pragma unroll
-    for (int k = 0; k < kFilterItems; k++) {
-        k32[k] = k64[k] != ~0ull ? span_key(m, k64[k]) : 0u;
-        // behind the front slice: its box in item rows x tile columns
-        // (item_box, written by preprocess_geo)
-        if (!(k64[k] != ~0ull && k32[k] > tau)) bx[k] = make_uint2(0xffffu, 0u);
-    }
-    // member: an unsaturated item in the box -- per tile column, the words of
-    // its item-row bitmask the box's rows [r0, r1] span (one or two for all
-    // but tall splats), masked to the rows
-    uint32_t memb = 0u;
-#pragma unroll
-    for (int k = 0; k < kFilterItems; k++) {
-        const uint32_t r0 = bx[k].x & 0xffffu, r1 = bx[k].x >> 16;
-        bool member = false;
-        if (r0 <= r1)
-            for (uint32_t c = bx[k].y & 0xffffu; c <= (bx[k].y >> 16) && !member; c++) {
-                const uint32_t *col = a.unsat_cols + (int64_t)c * a.col_words;
-                for (uint32_t wd = r0 >> 5; wd <= (r1 >> 5) && !member; wd++) {
-                    uint32_t m = __ldg(col + wd);
-                    if (wd == (r0 >> 5)) m &= ~0u << (r0 & 31);
-                    if (wd == (r1 >> 5)) m &= ~0u >> (31 - (r1 & 31));
-                    member = m != 0u;
-                }
-            }
-        memb |= (uint32_t)member << k;
-    }
-    // block-aggregated append: one atomic per 1024 Gaussians
-    uint32_t tot;
-    uint32_t pos = block_excl_scan_u32((uint32_t)__popc(memb), s_warp, &tot);
-    if (threadIdx.x == 0) s_base = tot ? atomicAdd(&a.ctr->KB, tot) : 0u;
-    __syncthreads();
-    pos += s_base;
-#pragma unroll
-    for (int k = 0; k < kFilterItems; k++)
-        if ((memb >> k) & 1u) {
-            a.keysB[pos] = k32[k];
-            a.valsB[pos] = (uint32_t)(i0 + k * 256);
-            pos++;
+        for (int k = 0; k < kFilterItems; k++) {
+            const int64_t i = i0 + k * 256;
+            k64[k] = i < a.n ? __ldg(a.keys64 + i) : ~0ull;
+            bx[k] = i < a.n ? __ldg(a.ibox + i) : make_uint2(0xffffu, 0u);
         }
+        uint32_t k32[kFilterItems];
+        uint32_t memb = 0u;
+#pragma unroll
+        for (int k = 0; k < kFilterItems; k++) {
+            k32[k] = k64[k] != ~0ull ? span_key(m, k64[k]) : 0u;
+            // behind the front slice, and its box (item_box, written by
+            // preprocess_geo) meets an unsaturated item
+            if (k64[k] != ~0ull && k32[k] > tau && box_member(cols, a.col_words, bx[k]))
+                memb |= 1u << k;
+        }
+        // block-aggregated append: one atomic per 1024 Gaussians
+        uint32_t tot;
+        uint32_t pos = block_excl_scan_u32((uint32_t)__popc(memb), s_warp, &tot);
+        if (threadIdx.x == 0) s_base = tot ? atomicAdd(&a.ctr->KB, tot) : 0u;
+        __syncthreads();
+        pos += s_base;
+#pragma unroll
+        for (int k = 0; k < kFilterItems; k++)
+            if ((memb >> k) & 1u) {
+                a.keysB[pos] = k32[k];
+                a.valsB[pos] = (uint32_t)(i0 + k * 256);
+                pos++;
+            }
+        __syncthreads();  // s_base / s_warp reused by the next block step
+    }
 }
 
 __global__ void slice_b_decide_kernel(const FrameCounters *ctr,
@@ -151,8 +178,26 @@ void launch_slice_plan(FrameCounters *ctr, float frac, cudaStream_t s, const KMa
 
 void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark) {
     if (a.n <= 0) return;
-    slice_b_filter_kernel<<<(unsigned)((a.n + 256 * kFilterItems - 1) / (256 * kFilterItems)), 256,
-                            0, s>>>(a);
+    static int sms = 0;  // (one device model per process)
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+        cudaFuncSetAttribute(slice_b_filter_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kFilterSmemWords * sizeof(uint32_t)));
+    }
+#ifndef GSR_FILTER_CTAS
+#define GSR_FILTER_CTAS 16
+#endif
+    const unsigned blocks = (unsigned)std::min<int64_t>(
+        (a.n + 256 * kFilterItems - 1) / (256 * kFilterItems), (int64_t)sms * GSR_FILTER_CTAS);
+    const int64_t words = (int64_t)a.tiles_x * a.col_words;
+    if (words <= kFilterSmemWords)
+        slice_b_filter_kernel<true><<<blocks, 256, words * sizeof(uint32_t), s>>>(a);
+    else
+        slice_b_filter_kernel<false><<<blocks, 256, 0, s>>>(a);
     mark("slice_b_filter");
 }
 
