@@ -1010,7 +1010,7 @@ int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means
     {
         double *m4 = reinterpret_cast<double *>(host.data() + L.mean4);
         for (int64_t i = 0; i < n; i++)
-            for (int k = 0; k < 3; k++) m4[4 * i + k] = means[i * 3 + k];
+            for (int k = 0; k < 3; k++) m4[(size_t)L.m4_row * i + k] = means[i * 3 + k];
     }
     plane_f(L.opac, opacities, 0, 1);
     plane_d(L.op64, opacities, 0, 1);
@@ -1018,7 +1018,9 @@ int gsr_scene_create(gsr_scene **out, int device, int64_t n, const double *means
     if (sc->has_sh) {  // rows of 48 coefficients (SceneView.sh)
         if (sc->sh_f32) {
             float *d = reinterpret_cast<float *>(host.data() + L.sh);
-            for (int64_t i = 0; i < n * 48; i++) d[i] = (float)sh_coeffs[i];
+            for (int64_t i = 0; i < n; i++)
+                for (int j = 0; j < 48; j++)
+                    d[(size_t)L.sh_row * i + j] = (float)sh_coeffs[i * 48 + j];
         } else {
             std::memcpy(host.data() + L.sh, sh_coeffs, sizeof(double) * (size_t)(n * 48));
         }

@@ -97,6 +97,9 @@ struct SceneView {
                           // Gaussian for the colour kernel's gather by depth rank (three
                           // planes would cost three 64 B DRAM accesses for 24 B)
     int sh_f32;
+    int sh_row;           // floats per f32 SH row: 48, or 56 when the row carries the mean
+                          // (f32 SH scenes: SH row + mean4 in one 224 B record, one gather)
+    int m4_row;           // doubles between consecutive mean4 entries (4, or 28 inside the rows)
 };
 
 struct CameraArgs {

@@ -271,6 +271,7 @@ struct PlyOut {
     double *mean4;  // [stride][4] (x, y, z, 0): the colour kernel's gather copy
     float *opac, *dc, *sh;
     int64_t stride;
+    int sh_row, m4_row;  // floats per SH row, doubles per mean4 entry (SceneView)
 };
 
 // failure bits, in the reference's check order (model.py:199-203, 239-243)
@@ -323,8 +324,8 @@ __global__ void __launch_bounds__(kPlyThreads) ply_activate_kernel(
             m4[k] = (double)v;
         }
         m4[3] = 0.0;
-        reinterpret_cast<double2 *>(o.mean4 + 4 * g)[0] = make_double2(m4[0], m4[1]);
-        reinterpret_cast<double2 *>(o.mean4 + 4 * g)[1] = make_double2(m4[2], m4[3]);
+        reinterpret_cast<double2 *>(o.mean4 + (int64_t)o.m4_row * g)[0] = make_double2(m4[0], m4[1]);
+        reinterpret_cast<double2 *>(o.mean4 + (int64_t)o.m4_row * g)[1] = make_double2(m4[2], m4[3]);
         float ls[3], q[4], dc[3];
 #pragma unroll
         for (int k = 0; k < 3; k++) {
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kPlyThreads) ply_activate_kernel(
         for (int k = 0; k < 3; k++) {
             dc[k] = at(11 + k);
             if (!finite32(dc[k])) bad |= kBadSh;
-            o.sh[g * 48 + k] = dc[k];  // sh[:, 0, c] (model.py:193)
+            o.sh[g * o.sh_row + k] = dc[k];  // sh[:, 0, c] (model.py:193)
         }
         // sh[:, 1 + i, c] = f_rest_{15 c + i} (channel-major on disk, model.py:197-198)
 #pragma unroll 5
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kPlyThreads) ply_activate_kernel(
                     v = at(kRequired + 15 * c + i);
                     if (!finite32(v)) bad |= kBadSh;
                 }
-                o.sh[g * 48 + 3 * (1 + i) + c] = v;
+                o.sh[g * o.sh_row + 3 * (1 + i) + c] = v;
             }
         }
         // activation (model.py:211-252)
@@ -581,6 +582,8 @@ int scene_create_ply(gsr_scene **out, int device, const uint8_t *data, int64_t l
     o.dc = reinterpret_cast<float *>(d + L.dc);
     o.sh = reinterpret_cast<float *>(d + L.sh);
     o.stride = sc->stride;
+    o.sh_row = L.sh_row;
+    o.m4_row = L.m4_row;
     PlyCols cols;
     for (int c = 0; c < GSR_PLY_NCOLS; c++) cols.c[c] = info.col[c];
 
@@ -701,11 +704,11 @@ int scene_read(const gsr_scene *sc, int attr, double *host) {
         case GSR_ATTR_COLORS_DC:
             if (!sc->from_ply)
                 return fail(GSR_E_INVALID, "colors_dc is stored as f32 only for this scene");
-            plane = v.sh; comps = 3; f32 = 1; colors = 1; row_width = 48;
+            plane = v.sh; comps = 3; f32 = 1; colors = 1; row_width = v.sh_row;
             break;
         case GSR_ATTR_SH:
             if (!sc->has_sh) return fail(GSR_E_INVALID, "scene has no SH coefficients");
-            plane = v.sh; comps = 48; f32 = sc->sh_f32; row_width = 48;
+            plane = v.sh; comps = 48; f32 = sc->sh_f32; row_width = sc->sh_f32 ? v.sh_row : 48;
             break;
         case GSR_ATTR_RSQ: plane = v.rsq; comps = 1; break;
         default: return fail(GSR_E_INVALID, "unknown attribute");

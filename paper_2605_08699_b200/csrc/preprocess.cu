@@ -430,9 +430,10 @@ __global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
     } else {  // render.py:134-160
         constexpr int NC = (DEG + 1) * (DEG + 1) * 3;
         ShT v[NC];
-        if (sizeof(ShT) == 4) {  // f32 rows: 192 B, 16 B aligned
+        if (sizeof(ShT) == 4) {  // f32 rows: 192 B (224 B records with the mean), 16 B aligned
             constexpr int N4 = (NC + 3) / 4;
-            const float4 *row = reinterpret_cast<const float4 *>(sc.sh) + i * 12;
+            const float4 *row =
+                reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(sc.sh) + i * sc.sh_row);
             float4 q[N4];
 #pragma unroll
             for (int k = 0; k < N4; k++) q[k] = __ldg(row + k);
@@ -450,8 +451,9 @@ __global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
 #pragma unroll
             for (int k = 0; k < NC; k++) v[k] = (ShT)((k & 1) ? q[k >> 1].y : q[k >> 1].x);
         }
-        const double2 m01 = __ldg(reinterpret_cast<const double2 *>(sc.mean4 + 4 * i));
-        const double mx = m01.x, my = m01.y, mz = __ldg(sc.mean4 + 4 * i + 2);
+        const double *m4 = sc.mean4 + (int64_t)sc.m4_row * i;
+        const double2 m01 = __ldg(reinterpret_cast<const double2 *>(m4));
+        const double mx = m01.x, my = m01.y, mz = __ldg(m4 + 2);
         const double dx = mx - cam.campos[0];
         const double dy = my - cam.campos[1];
         const double dz = mz - cam.campos[2];
@@ -469,19 +471,22 @@ __global__ void __launch_bounds__(256, GSR_COLOR_MINB) color_ranked_kernel(
 }
 
 // The same colours with the gather done by the bulk-copy (TMA) engine: each
-// warp takes 32 consecutive ranks; every lane issues two cp.async.bulk
-// copies -- its Gaussian's 192 B SH row and 32 B mean -- into the warp's
-// shared-memory rows, completing on the warp's mbarrier; the lanes then
+// warp takes 32 consecutive ranks; every lane issues one cp.async.bulk copy
+// of its Gaussian's 224 B colour record -- 192 B SH row and 32 B mean,
+// adjacent in the scene (scene.cuh) -- into the warp's shared-memory rows,
+// completing on the warp's mbarrier (two copies: 0.0572 ms per frame at
+// config 3, the bulk-copy issue rate bound it); the lanes then
 // evaluate from shared memory.  Decouples the gather (no per-thread loads
 // in flight, no LSU throttling) from the 96 registers the SH evaluation
 // holds.  f32 SH only (every PLY scene; f64 scenes use the kernel above).
 constexpr int kBulkRow = 240;  // 192 B SH + 32 B mean + 16 B pad: 60 words, so a
                                // warp's LDS.128 of 32 rows hits all 32 banks
+constexpr uint32_t kBulkTx = 224u;  // bytes per splat either way
 constexpr int kBulkWarps = 3;  // two 7.5 KB row buffers per warp: 46 KB per CTA
 
 // A warp's chunk of 32 ranks: their Gaussian indices (the order read),
 // then lane 0 arms the chunk buffer's mbarrier with the bytes and every valid
-// lane issues its two bulk copies.
+// lane issues its copy.
 __device__ __forceinline__ void bulk_issue(const SceneView &sc, const uint32_t *order,
                                            int64_t r0, int64_t kr, int lane, uint32_t rbase,
                                            uint32_t mbar) {
@@ -491,11 +496,15 @@ __device__ __forceinline__ void bulk_issue(const SceneView &sc, const uint32_t *
     const int64_t i = valid ? (int64_t)__ldg(order + r) : 0;
     if (lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                     ::"r"(mbar), "r"((uint32_t)__popc(bal) * 224u) : "memory");
+                     ::"r"(mbar), "r"((uint32_t)__popc(bal) * kBulkTx) : "memory");
     if (valid) {
         const uint32_t dst = rbase + (uint32_t)lane * kBulkRow;
-        bulk_g2s(dst, reinterpret_cast<const float *>(sc.sh) + i * 48, 192u, mbar);
-        bulk_g2s(dst + 192u, sc.mean4 + 4 * i, 32u, mbar);
+        if (sc.m4_row == 28) {  // one 224 B record: SH row then mean (scene.cuh)
+            bulk_g2s(dst, reinterpret_cast<const float *>(sc.sh) + i * 56, 224u, mbar);
+        } else {
+            bulk_g2s(dst, reinterpret_cast<const float *>(sc.sh) + i * sc.sh_row, 192u, mbar);
+            bulk_g2s(dst + 192u, sc.mean4 + (int64_t)sc.m4_row * i, 32u, mbar);
+        }
     }
 }
 

@@ -45,6 +45,7 @@ struct DeviceGuard {
 // elements): see SceneView (kernels.cuh) for the plane types.
 struct SceneLayout {
     size_t mean, scale, rot, rsq, opac, dc, op64, sh, mean4, total;
+    int sh_row, m4_row;  // see SceneView
 };
 
 inline SceneLayout scene_layout(int64_t stride, bool has_sh, bool sh_f32) {
@@ -63,8 +64,20 @@ inline SceneLayout scene_layout(int64_t stride, bool has_sh, bool sh_f32) {
     L.opac = take(st * 4);
     L.dc = take(3 * st * 4);
     L.op64 = take(st * 8);
-    L.sh = take(has_sh ? 48 * st * (sh_f32 ? 4 : 8) : 16);
-    L.mean4 = take(4 * st * 8);
+    if (has_sh && sh_f32) {
+        // colour records: 48 f32 SH coefficients then the mean (x, y, z, 0)
+        // in f64 -- 224 B, 32-B aligned -- so the colour kernel's gather by
+        // depth rank is one bulk copy per splat
+        L.sh = take(224 * st);
+        L.mean4 = L.sh + 192;
+        L.sh_row = 56;
+        L.m4_row = 28;
+    } else {
+        L.sh = take(has_sh ? 48 * st * (sh_f32 ? 4 : 8) : 16);
+        L.mean4 = take(4 * st * 8);
+        L.sh_row = 48;
+        L.m4_row = 4;
+    }
     L.total = off;
     return L;
 }
@@ -96,5 +109,7 @@ struct gsr_scene {
         view.sh = d + L.sh;
         view.mean4 = reinterpret_cast<const double *>(d + L.mean4);
         view.sh_f32 = sh_f32;
+        view.sh_row = L.sh_row;
+        view.m4_row = L.m4_row;
     }
 };
