@@ -219,6 +219,7 @@ struct PassSmem {
     uint32_t off[256];   // this pass's exclusive digit offsets (the folded plan)
     uint32_t tile_n;
     uint32_t ticket;
+    int64_t nf, na;      // items read by the first active pass / by the others
 };
 
 template <typename K>
@@ -227,22 +228,32 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem<K> &S = *reinterpret_cast<PassSmem<K> *>(smem_raw);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // tile ticket first: the grid is sized for the capacity, and tiles past
-    // the items (most of them for a front slice) leave before any set-up
+    // the prologue's global reads in one round trip: the tile ticket (the
+    // grid is sized for the capacity, and tiles past the items -- most of
+    // them for a front slice -- leave before any set-up), the item counts and
+    // every pass's digit histogram (the plan below)
+    uint32_t hc[sizeof(K)];
+#pragma unroll
+    for (int p = 0; p < (int)sizeof(K); p++)
+        hc[p] = (p < a.passes && threadIdx.x < 256) ? a.hist[p * 256 + threadIdx.x] : 0u;
     if (threadIdx.x == 0) S.ticket = atomicAdd(a.tickets + pass, 1u);
+    if (threadIdx.x == 32) {
+        S.nf = first_count(a);
+        S.na = items_after_first(a);
+    }
     __syncthreads();
     int64_t t = S.ticket;
-    {
-        const int64_t nf = first_count(a), na = items_after_first(a);
-        if (t > 0 && t * RT >= (nf > na ? nf : na)) return;  // (ticket 0 publishes the plan)
-    }
+    const int64_t nf = S.nf, na = S.na;
+    if (t > 0 && t * RT >= (nf > na ? nf : na)) return;  // (ticket 0 publishes the plan)
     // the plan, folded into every pass (one kernel boundary less per sort):
     // a pass is active unless its digit is constant (pass 0 forced when it
     // compacts); buffers alternate over the active passes; this pass's
     // digit offsets are the exclusive scan of its histogram
     uint32_t act_mask = 0u;
-    for (int p = 0; p < a.passes; p++) {
-        const uint32_t c = threadIdx.x < 256 ? a.hist[p * 256 + threadIdx.x] : 0u;
+#pragma unroll
+    for (int p = 0; p < (int)sizeof(K); p++) {
+        if (p >= a.passes) break;
+        const uint32_t c = hc[p];
         const int nz = __syncthreads_count(c != 0u);
         if (nz > 1 || (p == 0 && a.force_first)) act_mask |= 1u << p;
         if (p == pass) {
@@ -266,17 +277,13 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
     const uint32_t src = (uint32_t)(__popc(act_mask & ((1u << pass) - 1u)) & 1);
     // first active pass: reads the producer's buffer (0) with n_first items
     const bool first = (act_mask & ((1u << pass) - 1u)) == 0u;
-    const int64_t n = first ? first_count(a) : items_after_first(a);
+    const int64_t n = first ? nf : na;
     // persistent: the grid is bounded (SMs x 2), each CTA takes tiles in
     // ticket order until none is left (a tile only waits on lower tickets,
     // all held by running CTAs, so the look-back always progresses)
     for (;; ) {
     if (t * RT >= n) return;
     const bool dig = threadIdx.x < 256;  // digit owner (RB >= 256)
-    for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wcnt[0][0])[j] = 0;
-    for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wmask[0][0])[j] = 0;
-    if (dig) S.hcnt[threadIdx.x] = 0;
-    __syncthreads();
     uint32_t *st = a.status + ((int64_t)pass * a.tiles) * 256;
     // (ternaries, not a.keys[src]: runtime-indexed param arrays go to local memory)
     const K *kin = src ? a.keys[1] : a.keys[0];
@@ -301,6 +308,11 @@ __global__ void __launch_bounds__(RB, 1024 / RB) onesweep_pass_kernel(SortArgs<K
         vals[r] = idx < n ? (vin ? __ldg(vin + idx) : (uint32_t)idx) : 0u;
         if (idx < n && !(drop && keys[r] == sentinel<K>())) valid_bits |= 1u << r;
     }
+    // (the counters are cleared while the loads are in flight)
+    for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wcnt[0][0])[j] = 0;
+    for (int j = threadIdx.x; j < RW * 256; j += RB) (&S.wmask[0][0])[j] = 0;
+    if (dig) S.hcnt[threadIdx.x] = 0;
+    __syncthreads();
     // tile digit counts first, published as aggregates before the (slower)
     // stable ranking so successors' look-back can proceed meanwhile
 #pragma unroll
