@@ -47,6 +47,15 @@ for frac in (0.15, 0.02):
     pipe.drain()
     pipe.close()
 set_slicing(-1, 0.0)
+# a scene large enough that every persistent preprocess CTA takes several
+# 256-Gaussian tiles (its two bulk-copy stages are refilled), one-pass and
+# sliced, on a small image
+big = synthetic_scene(400000, seed=5, sh_degree=3)
+small = g.Intrinsics(fx=60.0, fy=60.0, cx=32.0, cy=32.0, width=64, height=64)
+for mn, frac in ((10 ** 12, 0.0), (1, 0.15)):  # one-pass, then sliced
+    set_slicing(mn, frac)
+    g.render_u8(big, g.CameraPose(0.0, 0.0), small, sh_degree=3)
+set_slicing(-1, 0.0)
 print("case ok", len(jp), round(s, 6))
 PY
 for tool in memcheck racecheck synccheck; do
