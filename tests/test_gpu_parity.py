@@ -273,6 +273,36 @@ def _oracle_frame(oracle, prims, pose, intr, sh, bg=(0.0, 0.0, 0.0)):
                          intr.cy, intr.width, intr.height, bg, sh)
 
 
+def test_f64_sh_scene_vs_oracle(gsr, oracle):
+    """SH coefficients that are not f32-exact stay f64 on the device (384 B
+    rows, means in a separate gather copy -- the other scenes' 224 B colour
+    records put the f32 SH row and the mean side by side): frames exact vs
+    the oracle, one-pass and depth-sliced, SH degrees 1-3."""
+    from paper_2605_08699_b200.render import DeviceScene, set_slicing
+    from paper_2605_08699_b200.synth import ActivatedPrimitives
+    base = golden_scene((6000, 7, (0.02, 0.12), 3))
+    rng = np.random.default_rng(11)
+    sh = base.sh_coeffs + rng.uniform(-1e-9, 1e-9, base.sh_coeffs.shape)
+    prims = ActivatedPrimitives(base.means, base.scales, base.rotations, base.opacities,
+                                base.colors_dc, sh)
+    ds = DeviceScene(prims)
+    assert ds.lib.gsr_scene_sh_is_f32(ds.handle) == 0
+    ds.close()
+    intr = gsr.Intrinsics(fx=200.0, fy=200.0, cx=96.0, cy=64.0, width=192, height=128)
+    pose = gsr.CameraPose(0.04, -0.02, (0.0, 0.0, 0.1))
+    try:
+        for mn, frac in ((10 ** 12, 0.0), (1, 0.15)):  # one pass, then sliced
+            set_slicing(mn, frac)
+            for deg in (1, 3):
+                fb = gsr.render_framebuffer(prims, pose, intr, sh_degree=deg)
+                fr = _oracle_frame(oracle, prims, pose, intr, deg)
+                assert np.array_equal(fb._rgb32, fr.rgb32)
+                assert np.array_equal(fb._t32, fr.trans32)
+                assert np.array_equal(fb.u8, fr.u8)
+    finally:
+        set_slicing(-1, 0.0)
+
+
 def test_config2_500k_720p_trace_vs_oracle(gsr, oracle):
     """Config 2 (500k, SH3, 1280x720, pose trace): frames, order, tile lists exact."""
     from paper_2605_08699_b200.render import debug_tile_lists
