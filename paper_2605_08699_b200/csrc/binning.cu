@@ -61,10 +61,18 @@ __device__ __forceinline__ int64_t blocks_used(const BinArgs &a) {
     return nb < 1 ? 1 : (nb < a.n_blocks ? nb : a.n_blocks);
 }
 
+constexpr int kScanItems = 8;  // row_scan: items per thread, 2048-element tiles
+constexpr int kScanTile = 256 * kScanItems;
+
 // ---------------------------------------------------------------- 1a -------
 __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
     __shared__ uint32_t cnt[kRowsMax];
     const int tid = threadIdx.x;
+    {   // row_scan's look-back words (no memset node in the frame graph)
+        const int64_t nz = (a.n_blocks * a.n_rows + kScanTile - 1) / kScanTile + 1;
+        for (int64_t j = (int64_t)blockIdx.x * BR + tid; j < nz; j += (int64_t)gridDim.x * BR)
+            a.scan_work[j] = 0ull;
+    }
     const int64_t k = *a.count;
     const int64_t nbe = blocks_used(a);
     for (int64_t b = blockIdx.x; b < nbe; b += gridDim.x) {
@@ -93,8 +101,7 @@ __global__ void __launch_bounds__(BR) bin_gather_kernel(BinArgs a) {
 // ---------------------------------------------------------------- 1b -------
 // exclusive scan of row_blk (n_rows x n_blocks, row major) in place:
 // 2048-element tiles in ticket order, decoupled look-back between tiles
-constexpr int kScanItems = 8;
-constexpr int kScanTile = 256 * kScanItems;
+// (kScanTile above)
 
 __global__ void __launch_bounds__(256) row_scan_kernel(BinArgs a) {
     __shared__ uint32_t s_warp[33];
@@ -738,8 +745,7 @@ int launch_binning(const BinArgs &a, cudaStream_t s, const KMark &mark, bool row
     const unsigned nbp = (unsigned)std::min<int64_t>(a.n_blocks, (int64_t)a.sms * 2);
     bin_gather_kernel<<<nb, BR, 0, s>>>(a);
     mark("bin_gather");
-    const int64_t scan_tiles = bin_scan_tiles(a.n_blocks, a.n_rows);
-    cudaMemsetAsync(a.scan_work, 0, sizeof(unsigned long long) * (size_t)(scan_tiles + 1), s);
+    const int64_t scan_tiles = bin_scan_tiles(a.n_blocks, a.n_rows);  // (zeroed by bin_gather)
     row_scan_kernel<<<(unsigned)scan_tiles, 256, 0, s>>>(a);
     mark("row_scan");
     bin_pairs_kernel<<<nbp, BR, pair_smem_bytes(a.n_rows), s>>>(a);

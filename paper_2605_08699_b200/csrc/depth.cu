@@ -95,14 +95,17 @@ int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s, const KMark &
     unsigned g;
     if (a.keys_given) {  // slice B: appended (span key, index) pairs, no sentinels
         g = (unsigned)((a.cap + 255) / 256);
+        SpanKeys opts;
+        opts.hist_zeroed = a.hist_zeroed;
         launches = launch_onesweep_sort<uint32_t>(a.keys32[0], a.keys32[1], a.vals[0], a.vals[1],
                                                   false, false, a.count, -1, a.cap,
                                                   kSpanBits / 8, false, a.work32, a.sched,
-                                                  &a.ctr->npass, sms, s, mark);
+                                                  &a.ctr->npass, sms, s, mark, opts);
     } else {
         g = (unsigned)((a.n + 255) / 256);
         SpanKeys span;  // the histogram kernel writes the span keys (step 1)
         span.src = a.keys64[0];
+        span.hist_zeroed = a.hist_zeroed;
         span.kmin = &a.ctr->kmin;
         span.kmax = &a.ctr->kmax;
         span.bits = kSpanBits;

@@ -355,6 +355,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         da.limit = limit;
         da.keys_given = keys_given;
         da.cap = cap;
+        da.hist_zeroed = slice;  // by slice_plan (slice A) / slice_b_filter (slice B)
         launches += launch_depth_sort(da, c->sms, st, mark);
         launch_color_ranked(sc->view, dfp, sh_degree, ord, count, cap, c->colr.as<float4>(), st,
                             mark);
@@ -415,8 +416,12 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
                               slice ? c->ibox.as<uint2>() : nullptr, s, mark);
         launches += 1;
         if (slice) {
-            launch_slice_plan(ctr, c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac(), s,
-                              mark);
+            // (also clears the unsaturated-item bitmask and slice A's sort
+            // histograms: no memset nodes)
+            launch_slice_plan(ctr, c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac(),
+                              c->unsat_cols.as<uint32_t>(), (int)(unsat_cols_bytes(W, H) / 4),
+                              reinterpret_cast<uint32_t *>(c->depth_work32.p), kDepthHistWords,
+                              s, mark);
             launches += 1;
         }
     }
@@ -438,7 +443,6 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         // slice A: the front of the depth order
         sort_color_bin(s, &ctr->KA, &ctr->tau, false, c->cap_n);
         cudaEventRecordWithFlags(c->ev[3], s, evflags);
-        cudaMemsetAsync(c->unsat_cols.p, 0, unsat_cols_bytes(W, H), s);
         blend(1);
         cudaEventRecordWithFlags(c->ev[4], s, evflags);
         // slice B: the splats behind it that can reach an unsaturated item
@@ -455,6 +459,8 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         sb.tiles_x = (W + kTileW - 1) / kTileW;
         sb.keysB = c->keys32[0].as<uint32_t>();
         sb.valsB = c->vals[0].as<uint32_t>();
+        sb.zero = reinterpret_cast<uint32_t *>(c->depth_work32.p);  // slice B's sort histograms
+        sb.zero_words = kDepthHistWords;
         launch_slice_b_filter(sb, s, mark);
         launches += 1;
         auto class_cap = [&](int k) {

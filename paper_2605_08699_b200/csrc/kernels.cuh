@@ -196,6 +196,8 @@ struct SpanKeys {
     uint32_t *count_out = nullptr;    // += keys the first pass keeps (slice A's KA; zeroed per frame)
     bool compact = false;             // append the kept (key, index) pairs to keys[0]/vals[0]
     int64_t n_src = 0;                // (compact) source keys read
+    bool hist_zeroed = false;         // the digit histograms were zeroed by an earlier kernel
+                                      // of the frame (no memset node before the sort)
 };
 // Sorts (keys0, vals0) over `passes` 8-bit digits; the result lands in buffer
 // sched[16] (0 or 1).  First pass: n_first items (>= 0) or *n_dev (n_first <
@@ -225,7 +227,9 @@ struct DepthArgs {
     bool keys_given = false;  // slice B: keys32[0] / vals[0] hold *count appended
                               // (span key, Gaussian index) pairs, at most `cap` of them
     int64_t cap = 0;
+    bool hist_zeroed = false;  // 32-bit sorts: work32's histograms already zeroed (slice.cu)
 };
+constexpr int kDepthHistWords = 4 * 256;  // zeroed ahead of a 32-bit depth sort (<= 4 passes)
 size_t depth_work32_bytes(int64_t n_cap);
 size_t depth_work64_bytes(int64_t n_cap);
 int launch_depth_sort(const DepthArgs &a, int sms, cudaStream_t s,
@@ -333,6 +337,8 @@ struct SliceBArgs {
     int col_words;
     int width, height, tiles_x;
     uint32_t *keysB, *valsB;           // out: slice B's (span key, Gaussian index), appended
+    uint32_t *zero = nullptr;          // cleared by block 0 (slice B's sort histograms)
+    int zero_words = 0;
 };
 // slice-B size classes: the second slice's sort / colour / lists run with
 // grids for at most slice_class_cap(c) splats (the last class: all)
@@ -346,7 +352,8 @@ constexpr int kSliceClasses = GSR_SLICE_CLASSES;
 __host__ __device__ constexpr int64_t slice_class_cap(int c) {
     return c == 0 ? 4096 : c == 1 ? 65536 : GSR_SLICE_CAP2;
 }
-void launch_slice_plan(FrameCounters *ctr, float frac, cudaStream_t s, const KMark &mark = KMark());
+void launch_slice_plan(FrameCounters *ctr, float frac, uint32_t *zero0, int n0, uint32_t *zero1,
+                       int n1, cudaStream_t s, const KMark &mark = KMark());
 void launch_slice_b_filter(const SliceBArgs &a, cudaStream_t s, const KMark &mark = KMark());
 // sets `handle` (a graph's switch) to slice B's size class, kSliceClasses
 // (no body) when slice B is empty

@@ -489,7 +489,8 @@ int launch_onesweep_sort(K *keys0, K *keys1, uint32_t *vals0, uint32_t *vals1,
     a.tickets = a.status + (size_t)passes * a.tiles * 256;
     a.sched = sched;
     a.npass_out = npass_out;
-    cudaMemsetAsync(work, 0, sizeof(uint32_t) * (size_t)passes * 256, s);  // hist only
+    if (!span.hist_zeroed)
+        cudaMemsetAsync(work, 0, sizeof(uint32_t) * (size_t)passes * 256, s);  // hist only
     int launches = 0;
     if (n_items_cap > 0) {
         int64_t hb = (n_items_cap + RB * 16 - 1) / (RB * 16);

@@ -41,8 +41,14 @@ namespace {
 // * K splats.  Any tau gives the same frame (the split is on the span key,
 // so ties never straddle the slices); it only sets the work split.  The
 // slice's size KA is counted by the depth sort's histogram kernel.
-__global__ void __launch_bounds__(kZBins) slice_plan_kernel(FrameCounters *ctr, float frac) {
+__global__ void __launch_bounds__(kZBins) slice_plan_kernel(FrameCounters *ctr, float frac,
+                                                            uint32_t *zero0, int n0,
+                                                            uint32_t *zero1, int n1) {
     __shared__ uint32_t s_warp[33];
+    // buffers the frame's next kernels need cleared (the unsaturated-item
+    // bitmask, slice A's sort histograms): no memset nodes in the graph
+    for (int j = threadIdx.x; j < n0; j += blockDim.x) zero0[j] = 0u;
+    for (int j = threadIdx.x; j < n1; j += blockDim.x) zero1[j] = 0u;
     const uint32_t c = ctr->slice_hist[threadIdx.x];
     uint32_t tot;
     const uint32_t ex = block_excl_scan_u32(c, s_warp, &tot);
@@ -104,7 +110,11 @@ __global__ void __launch_bounds__(256) slice_b_filter_kernel(SliceBArgs a) {
     extern __shared__ uint32_t s_cols[];
     __shared__ uint32_t s_warp[33];
     __shared__ uint32_t s_base;
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctr->blend_next = 0u;  // blend A has finished
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) a.ctr->blend_next = 0u;  // blend A has finished
+        // slice B's sort histograms (slice A's sort is long done)
+        for (int j = threadIdx.x; j < a.zero_words; j += blockDim.x) a.zero[j] = 0u;
+    }
     if (a.ctr->n_unsat == 0u) return;  // (block-uniform)
     const uint32_t *cols = a.unsat_cols;
     if (kSmem) {
@@ -171,8 +181,9 @@ __global__ void slice_b_decide_kernel(const FrameCounters *ctr,
 
 }  // namespace
 
-void launch_slice_plan(FrameCounters *ctr, float frac, cudaStream_t s, const KMark &mark) {
-    slice_plan_kernel<<<1, kZBins, 0, s>>>(ctr, frac);
+void launch_slice_plan(FrameCounters *ctr, float frac, uint32_t *zero0, int n0, uint32_t *zero1,
+                       int n1, cudaStream_t s, const KMark &mark) {
+    slice_plan_kernel<<<1, kZBins, 0, s>>>(ctr, frac, zero0, n0, zero1, n1);
     mark("slice_plan");
 }
 
