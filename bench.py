@@ -653,7 +653,9 @@ def run_gsr(args, wl):
         checksum += int(f[0, 0, 0])
     e2e_s = d.max(time.perf_counter() - t_e2e)
     pipe.close()
-    # per-stage device timings (event pairs inside the ABI), separate pass
+    # per-stage device timings (event pairs inside the ABI, GSR_TIMING_STAGES:
+    # four event nodes in the frame graph, off while serving), separate pass
+    _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 4))
     stage_stats = []
     for i in range(W, W + min(K, 50)):
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cams[i]), bg, wl["sh"], 1,
@@ -816,6 +818,7 @@ def contract_profile(ctx, lib, sc, cams, wl, bg, frames):
     from paper_2605_08699_b200 import _lib
     st = _lib.GsrStats()
     ms, d_keys, binning = [], [], []
+    lib.gsr_ctx_set_kernel_timing(ctx.handle, 4)  # stage times (the binning stage)
     for cam in cams[:frames]:
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(cam), bg, wl["sh"], 1,
                                   None, None, None, ctypes.byref(st)))
@@ -826,6 +829,7 @@ def contract_profile(ctx, lib, sc, cams, wl, bg, frames):
                                                  None, ctypes.byref(t)))
         ms.append(t.value)
         d_keys.append(n.value)
+    lib.gsr_ctx_set_kernel_timing(ctx.handle, 0)
     if not ms:
         return None
     dk = float(np.mean(d_keys))

@@ -95,7 +95,7 @@ using namespace gsr;
 // CUDA graph.
 struct FrameKey {
     SceneView view;
-    int W, H, sh_degree, cull, want_rgb, want_keep, slice, kcount, full64, packed;
+    int W, H, sh_degree, cull, want_rgb, want_keep, slice, kcount, full64, packed, stages;
     float frac;    // the front slice's fraction (a slice_plan kernel parameter)
     uint64_t gen;  // buffer generation of the context (reallocation -> new graphs)
     bool operator==(const FrameKey &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
@@ -171,6 +171,8 @@ struct gsr_ctx {
     static constexpr int kMaxMarks = 64;
     bool ktime = false;   // per-kernel event marks
     bool kcount = false;  // blend work counters (E, Rb): the counting blend variant
+    bool stages = false;  // stage boundary events (gsr_stats stage times)
+    bool stages_last = false;  // the frame in flight / last frame recorded them
     int nmarks = 0;
     cudaEvent_t kev[kMaxMarks + 1] = {};
     const char *kname[kMaxMarks] = {};
@@ -314,6 +316,12 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
     const int64_t n = sc->n;
     uint32_t *dsched = c->sched.as<uint32_t>();
     const unsigned evflags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
+    // stage boundary events (ev[1..4]) only with GSR_TIMING_STAGES: four event
+    // nodes cost a frame graph 0.02-0.03 ms of latency (one stream 1,304 ->
+    // 1,340 frames/s without them); ev[0] / ev[5] always bracket the frame
+    auto stage_ev = [&](int k, cudaStream_t st) {
+        if (c->stages) cudaEventRecordWithFlags(c->ev[k], st, evflags);
+    };
     int launches = 1;  // frame_start
 
     KMark mark;
@@ -360,7 +368,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         launch_color_ranked(sc->view, dfp, sh_degree, ord, count, cap, c->colr.as<float4>(), st,
                             mark);
         launches += 1;
-        if (!keys_given) cudaEventRecordWithFlags(c->ev[2], st, evflags);
+        if (!keys_given) stage_ev(2, st);
         BinArgs ba;
         ba.count = count;
         ba.order0 = c->vals[0].as<uint32_t>();
@@ -425,26 +433,26 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
             launches += 1;
         }
     }
-    cudaEventRecordWithFlags(c->ev[1], s, evflags);
+    stage_ev(1, s);
     if (n == 0) {
-        cudaEventRecordWithFlags(c->ev[2], s, evflags);
+        stage_ev(2, s);
         cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->ntiles, s);
-        cudaEventRecordWithFlags(c->ev[3], s, evflags);
+        stage_ev(3, s);
         blend(0);
-        cudaEventRecordWithFlags(c->ev[4], s, evflags);
+        stage_ev(4, s);
     } else if (!slice) {
         // stable f64 depth order of all kept splats (the first radix pass
         // compacts: drops the culled sentinels), colours, lists, blend
         sort_color_bin(s, &ctr->K, nullptr, false, c->cap_n);
-        cudaEventRecordWithFlags(c->ev[3], s, evflags);
+        stage_ev(3, s);
         blend(0);
-        cudaEventRecordWithFlags(c->ev[4], s, evflags);
+        stage_ev(4, s);
     } else {
         // slice A: the front of the depth order
         sort_color_bin(s, &ctr->KA, &ctr->tau, false, c->cap_n);
-        cudaEventRecordWithFlags(c->ev[3], s, evflags);
+        stage_ev(3, s);
         blend(1);
-        cudaEventRecordWithFlags(c->ev[4], s, evflags);
+        stage_ev(4, s);
         // slice B: the splats behind it that can reach an unsaturated item
         SliceBArgs sb;
         sb.keys64 = c->keys[0].as<unsigned long long>();
@@ -663,6 +671,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
     const bool packed = W % kTileW == 0 && ((uintptr_t)c->zc_host & 3u) == 0;
     c->zc_used = packed && c->zc_host != nullptr;
     fp.host = c->zc_used ? c->zc_host : nullptr;
+    c->stages_last = c->stages;
     if (graphs_enabled() && !c->ktime && !c->kcount) {
         FrameKey key;
         std::memset(&key, 0, sizeof(key));
@@ -675,6 +684,7 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         key.want_keep = want_keep;
         key.slice = slice;
         key.kcount = c->kcount;
+        key.stages = c->stages;
         key.full64 = c->saved_full64;
         key.packed = W % kTileW == 0;
         key.frac = slice ? (c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac()) : 0.0f;
@@ -757,11 +767,13 @@ void fill_stats(gsr_ctx *c, const gsr_scene *sc, gsr_stats *st) {
     st->retries = c->retries;
     float t[6] = {0, 0, 0, 0, 0, 0};
     cudaEventElapsedTime(&t[0], c->ev[0], c->ev[5]);
-    cudaEventElapsedTime(&t[1], c->ev[0], c->ev[1]);
-    cudaEventElapsedTime(&t[2], c->ev[1], c->ev[2]);
-    cudaEventElapsedTime(&t[3], c->ev[2], c->ev[3]);
-    cudaEventElapsedTime(&t[4], c->ev[3], c->ev[4]);
-    cudaEventElapsedTime(&t[5], c->ev[4], c->ev[5]);
+    if (c->stages_last) {  // the frame recorded its stage events
+        cudaEventElapsedTime(&t[1], c->ev[0], c->ev[1]);
+        cudaEventElapsedTime(&t[2], c->ev[1], c->ev[2]);
+        cudaEventElapsedTime(&t[3], c->ev[2], c->ev[3]);
+        cudaEventElapsedTime(&t[4], c->ev[3], c->ev[4]);
+        cudaEventElapsedTime(&t[5], c->ev[4], c->ev[5]);
+    }
     st->ms_device = t[0];
     st->ms_preprocess = t[1];   // projection (+ slice plan)
     st->ms_depth_sort = t[2];   // depth sort + colours (of slice A)
@@ -1156,6 +1168,7 @@ int gsr_ctx_set_kernel_timing(gsr_ctx *ctx, int enable) {
     if (!ctx) return fail(GSR_E_INVALID, "ctx is null");
     ctx->ktime = (enable & GSR_TIMING_EVENTS) != 0;
     ctx->kcount = (enable & GSR_TIMING_COUNTERS) != 0;
+    ctx->stages = (enable & GSR_TIMING_STAGES) != 0;
     ctx->nmarks = 0;
     return GSR_OK;
 }

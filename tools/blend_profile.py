@@ -45,7 +45,7 @@ def main():
     rows, blend_ms, items = [], [], []
     out = (ctypes.c_uint64 * 15)()
     for c in cams[3:]:
-        _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 0))
+        _lib.check(lib.gsr_ctx_set_kernel_timing(ctx.handle, 4))  # stage times
         _lib.check(lib.gsr_render(ctx.handle, sc.handle, ctypes.byref(c), bg, wl["sh"], 1, None,
                                   None, None, ctypes.byref(st)))
         blend_ms.append(st.ms_blend)
