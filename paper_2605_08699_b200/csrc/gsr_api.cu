@@ -159,6 +159,11 @@ struct gsr_ctx {
     // overflowed, [1] frames needing the 64-bit sort, [2 + k] graph frames
     // whose slice B ran conditional body k (kernel-launch accounting)
     static constexpr int kSticky = 2 + kSliceClasses + 1;
+    // the depth sort's schedule (64 words) follows the counters in the same
+    // buffer, so a frame ends with ONE device->host copy of both
+    static constexpr size_t kSchedOff =
+        (sizeof(FrameCounters) + kSticky * sizeof(uint32_t) + 15) / 16 * 16;
+    static constexpr size_t kCtrBytes = kSchedOff + 64 * sizeof(uint32_t);
     uint32_t sticky_seen[kSticky] = {};  // sticky values reported by the last fill_stats
     // kernels per graph frame outside the conditional bodies, and per body
     // (recorded at capture; a graph launch counts its kernels, not 1)
@@ -314,7 +319,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
     FrameParams *dfp = c->params.as<FrameParams>();
     const int W = c->W, H = c->H;
     const int64_t n = sc->n;
-    uint32_t *dsched = c->sched.as<uint32_t>();
+    uint32_t *dsched = reinterpret_cast<uint32_t *>(c->ctr.as<unsigned char>() + gsr_ctx::kSchedOff);
     const unsigned evflags = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
     // stage boundary events (ev[1..4]) only with GSR_TIMING_STAGES: four event
     // nodes cost a frame graph 0.02-0.03 ms of latency (one stream 1,304 ->
@@ -540,9 +545,7 @@ int record_frame(gsr_ctx *c, const gsr_scene *sc, const FrameParams &fp, int sh_
         }
     }
     cudaEventRecordWithFlags(c->ev[5], s, evflags);
-    cudaMemcpyAsync(c->hctr, ctr, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t),
-                    cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(c->hsched, dsched, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(c->hctr, ctr, gsr_ctx::kCtrBytes, cudaMemcpyDeviceToHost, s);  // + sched
     GSR_CUDA_OK(cudaGetLastError());
     c->launches += launches;
     return GSR_OK;
@@ -1096,23 +1099,22 @@ int gsr_ctx_create(gsr_ctx **out, int device) {
     for (int i = 0; i < 8 && e == cudaSuccess; i++) e = cudaEventCreate(&c->ev[i]);
     for (int i = 0; i <= gsr_ctx::kMaxMarks && e == cudaSuccess; i++) e = cudaEventCreate(&c->kev[i]);
     if (e == cudaSuccess)
-        e = cudaMallocHost((void **)&c->hctr, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t));
+        e = cudaMallocHost((void **)&c->hctr, gsr_ctx::kCtrBytes);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hssim, sizeof(double) * 64);
-    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hsched, sizeof(uint32_t) * 64);
+    if (e == cudaSuccess)
+        c->hsched = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(c->hctr) +
+                                                 gsr_ctx::kSchedOff);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->hjpeg, sizeof(uint32_t) * 4);
     if (e != cudaSuccess) {
         int rc = fail_cuda(e, "context setup");
         gsr_ctx_destroy(c);
         return rc;
     }
-    int rc = ensure(c->ctr, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t));
+    int rc = ensure(c->ctr, gsr_ctx::kCtrBytes);  // counters, sticky counters, sort schedule
     if (!rc) rc = ensure(c->params, sizeof(FrameParams));
-    if (!rc) rc = ensure(c->sched, 64 * sizeof(uint32_t));
-    if (!rc && cudaMemset(c->sched.p, 0, 64 * sizeof(uint32_t)) != cudaSuccess)
-        rc = fail(GSR_E_CUDA, "memset");
     if (!rc && cudaMemset(c->ctr.p, 0, c->ctr.bytes) != cudaSuccess)
         rc = fail(GSR_E_CUDA, "memset");
-    if (!rc) std::memset(c->hctr, 0, sizeof(FrameCounters) + gsr_ctx::kSticky * sizeof(uint32_t));
+    if (!rc) std::memset(c->hctr, 0, gsr_ctx::kCtrBytes);
     if (!rc) rc = ensure(c->ssim_misc, 64);
     if (!rc) rc = ensure(c->ssim_w, sizeof(double) * 11);
     if (rc) {
@@ -1147,7 +1149,6 @@ int gsr_ctx_destroy(gsr_ctx *ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->hctr) cudaFreeHost(ctx->hctr);
     if (ctx->hssim) cudaFreeHost(ctx->hssim);
-    if (ctx->hsched) cudaFreeHost(ctx->hsched);
     if (ctx->hjpeg) cudaFreeHost(ctx->hjpeg);
     for (auto &fg : ctx->graphs) destroy_graph(fg);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
