@@ -98,6 +98,11 @@ struct FrameKey {
     int W, H, sh_degree, cull, want_rgb, want_keep, slice, kcount, full64, packed, stages;
     float frac;    // the front slice's fraction (a slice_plan kernel parameter)
     uint64_t gen;  // buffer generation of the context (reallocation -> new graphs)
+    // capacities baked into the captured kernels' arguments (overflow checks,
+    // grids): a capacity can grow inside an existing allocation (no new
+    // generation), and a graph replayed with a stale one would overflow
+    // again while the host saw the frame fit (an empty frame)
+    int64_t cap_n, cap_p, cap_d;
     bool operator==(const FrameKey &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
@@ -692,6 +697,9 @@ int enqueue_frame(gsr_ctx *c, const gsr_scene *sc, const gsr_camera *cam, const 
         key.packed = W % kTileW == 0;
         key.frac = slice ? (c->slice_frac_v > 0.0f ? c->slice_frac_v : slice_frac()) : 0.0f;
         key.gen = c->gen;
+        key.cap_n = c->cap_n;
+        key.cap_p = c->cap_p;
+        key.cap_d = c->cap_d;
         FrameGraph *fg = nullptr;
         if ((rc = frame_graph(c, key, sc, fp, sh_degree, cull, want_rgb, want_keep, slice, &fg)))
             return rc;
@@ -740,7 +748,9 @@ int complete_frame(gsr_ctx *c) {
         if (!ov_p && !ov_d && !long_runs) break;
         if (round == 3) return fail(GSR_E_OOM, "tile list buffer overflow");
         if (ov_p) c->cap_p = round_up(p + p / 4 + (1 << 20), 4096);
-        if (ov_p || ov_d) c->cap_d = round_up(std::max(d, 3 * p) + std::max(d, 3 * p) / 4 + (1 << 20), 4096);
+        if (ov_p || ov_d)  // (never below the current capacity)
+            c->cap_d = std::max(c->cap_d, round_up(std::max(d, 3 * p) + std::max(d, 3 * p) / 4 +
+                                                       (1 << 20), 4096));
         if (c->cap_d >= (int64_t(1) << 32) || c->cap_p >= (int64_t(1) << 32))
             return fail(GSR_E_OOM, "tile list exceeds 2^32 entries");
         if (long_runs) c->saved_full64 = true;

@@ -40,12 +40,27 @@ def _case(g, synth, rng):
 
 
 def test_random_frames_bit_exact(oracle):
+    _soak(oracle, int(os.environ.get("GSR_SOAK_CASES", "24")),
+          int(os.environ.get("GSR_SOAK_SEED", "20261017")))
+
+
+def test_capacity_history_regression(oracle):
+    """Seed 777's first 111 cases in one process: case 110 (150k large
+    splats, 7M tile keys at 320x241) needs a tile-key capacity that an
+    earlier case's allocation already holds, so the capacity grows without a
+    new buffer generation.  Its frame graph was keyed by the generation only
+    and replayed with the old capacity baked in: the lists overflowed again
+    while the host saw the frame fit, and the frame came back empty.  The
+    graph key now includes the capacities."""
+    _soak(oracle, 111, 777)
+
+
+def _soak(oracle, cases, seed):
     import paper_2605_08699_b200 as g
     from paper_2605_08699_b200 import _lib, synth
     if _lib.device_count() == 0:
         pytest.fail("no CUDA device visible to libgsr")
-    cases = int(os.environ.get("GSR_SOAK_CASES", "24"))
-    rng = np.random.default_rng(int(os.environ.get("GSR_SOAK_SEED", "20261017")))
+    rng = np.random.default_rng(seed)
     px = evals = 0
     only = os.environ.get("GSR_SOAK_ONLY")  # debugging: render just this case index
     for k in range(cases):
