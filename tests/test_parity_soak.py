@@ -45,14 +45,20 @@ def test_random_frames_bit_exact(oracle):
 
 
 def test_capacity_history_regression(oracle):
-    """Seed 777's first 111 cases in one process: case 110 (150k large
-    splats, 7M tile keys at 320x241) needs a tile-key capacity that an
-    earlier case's allocation already holds, so the capacity grows without a
-    new buffer generation.  Its frame graph was keyed by the generation only
-    and replayed with the old capacity baked in: the lists overflowed again
-    while the host saw the frame fit, and the frame came back empty.  The
-    graph key now includes the capacities."""
-    _soak(oracle, 111, 777)
+    """Seed 777's cases 0..109 rendered in a fresh process, then case 110
+    (150k large splats, 7M tile keys at 320x241) compared with the oracle.
+    With that history case 110's tile-key capacity grew inside an existing
+    allocation (no new buffer generation), and its frame graph, keyed by the
+    generation only, was replayed with the old capacity baked in: the lists
+    overflowed again while the host saw the frame fit, and the frame came back
+    empty.  The graph key now includes the capacities.  (A fresh process:
+    the allocation history is what triggers it.)"""
+    import subprocess
+    import sys
+    root = os.path.join(os.path.dirname(__file__), "..")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "debug_soak_case.py"),
+                        "777", "110", "0"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def _soak(oracle, cases, seed):
@@ -85,3 +91,48 @@ def _soak(oracle, cases, seed):
         g.evict(prims)
     print(f"soak: {cases} random frames bit-exact vs the oracle "
           f"({px / 1e6:.1f} Mpx, {evals} splats drawn)")
+
+
+def test_pipeline_random_scenes_bit_exact(oracle):
+    """RenderPipeline (3 frames in flight, contexts rotating) over a random
+    mix of scenes -- small, large, and 150k large splats whose first frames
+    overflow the tile-key buffers and re-render while other frames are in
+    flight -- every returned frame bit-exact (u8) vs the oracle."""
+    import paper_2605_08699_b200 as g
+    from paper_2605_08699_b200 import synth
+    rng = np.random.default_rng(31)
+    intr = g.Intrinsics(fx=300.0, fy=320.0, cx=160.0, cy=120.5, width=320, height=241)
+    specs = [(500, None), (2_000, None), (40_000, None), (150_000, (0.001, 0.4)),
+             (80_000, None), (150_000, None)]
+    scenes = []
+    for k, (n, sr) in enumerate(specs):
+        raw = synth.make_synthetic_set(count=n, seed=100 + k,
+                                       scale_range=sr or synth.scale_range_for(n),
+                                       include_rest=True)
+        scenes.append(synth.activate(synth.ply_round_trip(raw)))
+    jobs = {}
+    pipe = g.RenderPipeline(intr, sh_degree=3, depth=3)
+
+    def check(tag, frame):
+        k, pose = jobs.pop(tag)
+        p = scenes[k]
+        rot, w2c = oracle.world_to_camera(pose.azimuth, pose.elevation, pose.translation)
+        ref = oracle.render(p.means, p.scales, p.rotations, p.opacities, p.colors_dc,
+                            p.sh_coeffs, w2c, rot, intr.fx, intr.fy, intr.cx, intr.cy,
+                            intr.width, intr.height, (0.0, 0.0, 0.0), 3)
+        assert np.array_equal(frame, ref.u8), (tag, k)
+
+    try:
+        for t in range(30):
+            k = int(rng.integers(len(scenes)))
+            pose = g.pose_from_degrees(float(rng.uniform(-40, 40)), float(rng.uniform(-20, 20)),
+                                       tuple(float(x) for x in rng.uniform(-0.3, 0.3, 3)))
+            jobs[t] = (k, pose)
+            r = pipe.submit(scenes[k], pose, tag=t)
+            if r is not None:
+                check(r[0], r[1].copy())
+        for tag, frame in pipe.drain():
+            check(tag, frame.copy())
+    finally:
+        pipe.close()
+    assert not jobs

@@ -44,7 +44,8 @@ def main(seed, k, start=None):
         print("tiles (32x16):", sorted(set(zip((ys // 16).tolist(), (xs // 32).tolist())))[:40])
         y, x = bad[0]
         print("first", (y, x), "gpu", fb._rgb32[y, x], fb._t32[y, x], "ref", ref.rgb32[y, x], ref.trans32[y, x])
+    return 0 if (not len(bad) and not dr.any() and not dt.any()) else 1
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else None)
+    sys.exit(main(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else None))
